@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark: Toeplitz-extraction raw Gbit/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one
+batch: the one-shot C-ABI call qrng_toeplitz_extract_async on the rank's
+blocks (seed preparation, output clear, extraction kernel, tail fix-up), with
+raw bits and seed already resident in HBM.  The default workload is
+BASELINE.json configs[1] (n = 8192, m = 5734, 16384 blocks).
+
+Multi-GPU (torchrun, one process per GPU, NCCL): blocks are independent, so
+each rank extracts its own batch of the config's size ("scaling": "weak"); the
+seed is broadcast once from rank 0 (NCCL), nothing is exchanged in the timed
+loop, and the time is the max over ranks of the summed CUDA-event step times.
+L2 is flushed (256 MiB write) between timed steps, outside the events.
+
+Also reported: the dominant kernel's roofline (CUDA events on its own stream
+inside libqrng), the end-to-end number through the host-buffer C-ABI call,
+the CPU oracle as cpu_baseline (rank 0, N=1), clocks sampled during the timed
+region, and the number of libqrng kernel launches in the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import qrng_synth as S  # noqa: E402
+
+METRIC = "Toeplitz extraction raw Gbit/s (1/2/4/8 B200), fraction of roofline"
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def workload(cfg: int) -> S.Workload:
+    if cfg in S.CONFIGS:
+        return S.CONFIGS[cfg]
+    if cfg >= 10:  # sweep point: --config 10..22 means config 5 at n = 2^cfg
+        return S.sweep_workload(cfg)
+    raise SystemExit(f"unknown config {cfg}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx, self.rows, self.proc = gpu_index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool):
+    """Roofline numerators, per launch of the main kernel."""
+    import paper_2011_04130_b200 as q
+    if path == q.PATH_GEMM:
+        return 2.0 * w.m * w.n * n_blocks, "tensor", "TOPS"  # int8 ops of D = T X
+    L = w.n + w.m - 1
+    P = 1 << max(5, math.ceil(math.log2(L)))
+    transforms = (n_blocks + 1) // 2 if pack else n_blocks
+    bfly = transforms * (P * math.log2(P) + P)  # fwd + inv radix-2 butterflies (P/2 log P each) + P products
+    return bfly, "alu", "Gbutterfly/s"
+
+
+def alu_peak_gbfly(pk):
+    # 148 SMs x 4 SMSP x 32 lanes issue per clock at the max SM clock, over the
+    # 7 integer instructions of one lazy Shoup butterfly.
+    return 148 * 128 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 7 / 1e9
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2011_04130_b200 as q
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    q.load_library()
+    w = workload(args.config)
+    B = w.n_blocks
+    # rank r owns blocks [r*B, (r+1)*B) of a world*B-block stream (weak scaling)
+    raw_np = S.adc_samples(w.key, B * w.n // 8, w.mu, w.sigma, start=rank * B * w.n // 8)
+    seed = torch.empty((w.seed_bits + 7) // 8, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        seed.copy_(torch.from_numpy(S.workload_inputs(w, 0, 1)[1]))
+    if world > 1:
+        dist.broadcast(seed, 0)  # N1: the one collective, outside the timed loop
+    raw = torch.from_numpy(raw_np).cuda()
+    out = torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8, device="cuda")
+    if args.path != "auto":
+        q.set_debug_path({"gemm": q.PATH_GEMM, "ntt": q.PATH_NTT}[args.path])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        q.toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    with q.Plan(w.n, w.m, seed) as pl:
+        path = pl.path
+    pack = w.n <= (1 << 14)
+    # timed region
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    q.kernel_timing(True)
+    q.kernel_time_ms()  # clear
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = q.launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the events
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = q.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_total = sum(ms_steps)
+    kern_ms, kern_n = q.kernel_time_ms()
+    q.kernel_timing(False)
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    bits_all = float(w.raw_bits) * world * args.steps
+    value = bits_all / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer C-ABI call (pinned buffers) ----
+    e2e = None
+    if not args.no_e2e:
+        h_raw = torch.from_numpy(raw_np).pin_memory()
+        h_seed = seed.cpu().pin_memory()
+        h_out = torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8).pin_memory()
+        hr, hs, ho = h_raw.numpy(), h_seed.numpy(), h_out.numpy()
+        for _ in range(2):
+            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, ho, stream=stream)
+        if world > 1:
+            dist.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for a, b in ev:
+            flush.zero_()
+            a.record(stream)
+            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, ho, stream=stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": bits_all / (float(e_ms.item()) * 1e-3) / 1e9, "unit": "Gbit/s",
+               "h2d_bytes_per_step": int(h_raw.numel() + h_seed.numel()),
+               "d2h_bytes_per_step": int(h_out.numel()),
+               "api": "qrng_toeplitz_extract_host (pinned host buffers)"}
+
+    # ---- roofline of the dominant kernel ----
+    pk, pk_kind = peaks()
+    work, bound, unit = algorithmic_work(path, w, B, pack)
+    roof = None
+    if kern_n:
+        per_launch_s = kern_ms / kern_n * 1e-3
+        if bound == "tensor":
+            achieved = work / per_launch_s / 1e12
+            peak = pk["bf16_tflops"] * 2.0  # int8 dense = 2x bf16 (guide's nominal ratio)
+            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
+                    "peak_kind": f"{pk_kind} bf16 x 2 (int8 nominal ratio)"}
+        else:
+            achieved = work / per_launch_s / 1e9
+            peak = alu_peak_gbfly(pk)
+            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
+                    "peak_kind": "derived: 148 SM x 128 int32 lanes/clk x sm_max_mhz / 7 instr per butterfly"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["kernel_ms"] = kern_ms / kern_n
+        roof["kernel_share_of_step"] = (kern_ms / kern_n) / (ms_total / args.steps)
+        hbm_bytes = B * w.n / 8 + B * w.m / 8
+        roof["hbm_gbs_algorithmic"] = hbm_bytes / per_launch_s / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8 bits; int32 mod-p NTT" if path == 2 else "u8 bits; int8 x int8 -> int32 tensor core",
+        "data": "synthetic: uint8 ADC samples clip(rint(N(128,sigma^2))) from PCG64 (qrng_synth); seeded uniform seed",
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_per_gpu": B, "seed_bits": w.seed_bits,
+                   "raw_bits_per_gpu": w.raw_bits, "path": {1: "gemm", 2: "ntt"}[path],
+                   "two_blocks_per_transform": bool(pack and path == 2),
+                   "l2": "flushed between timed steps (256 MiB write, outside events)",
+                   "step": "one-shot qrng_toeplitz_extract_async (seed prep + clear + extract)",
+                   "parallelism": f"block-sharded x{world}"},
+        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0):
+    """The oracle as it stands (word mode, OpenMP over blocks) on a bounded
+    sample of the same workload: consecutive blocks until ~budget_s."""
+    import oracle
+    oracle.build()
+    cores = oracle.max_threads() if threads == 0 else threads
+    sample_blocks = min(w.n_blocks, 4096)
+    raw, seed = S.workload_inputs(w, 0, sample_blocks)
+    blocks_done, t_total, nb, pos = 0, 0.0, max(1, min(cores, sample_blocks)), 0
+    while t_total < budget_s:
+        if pos + nb > sample_blocks:  # cycle over the sample
+            pos = 0
+        chunk = raw[pos * w.n // 8:(pos + nb) * w.n // 8]
+        t0 = time.perf_counter()
+        oracle.extract(chunk, nb, w.n, w.m, seed, "words", threads)
+        t_total += time.perf_counter() - t0
+        blocks_done += nb
+        pos += nb
+        if t_total < budget_s / 8:
+            nb = min(nb * 2, sample_blocks)
+    return {"value": blocks_done * w.n / t_total / 1e9, "unit": "Gbit/s", "cores": cores,
+            "kind": "oracle", "sample": f"{blocks_done} blocks (cycling over the first {sample_blocks} of "
+                                        f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, word-parallel "
+                                        f"mode, OpenMP over blocks"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    w = workload(args.config)
+    cores = oracle.max_threads()
+    per_step_blocks = max(cores, min(w.n_blocks, int(os.environ.get("QRNG_REF_BLOCKS", "0")) or
+                                     _ref_blocks(w, cores)))
+    raw, seed = S.workload_inputs(w, 0, per_step_blocks)
+    for _ in range(args.warmup):
+        oracle.extract(raw[:cores * w.n // 8], cores, w.n, w.m, seed)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.extract(raw, per_step_blocks, w.n, w.m, seed)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    value = per_step_blocks * w.n * args.steps / total / 1e9
+    sample = f"{per_step_blocks} of {w.n_blocks} blocks of {w.name} per step (word-parallel oracle, OpenMP)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 bit words",
+        "data": "synthetic (qrng_synth)", "config": {"workload": w.name, "n": w.n, "m": w.m,
+                                                     "blocks_per_step": per_step_blocks},
+        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def _ref_blocks(w: S.Workload, cores: int) -> int:
+    # ~ m*n/64 word ops per block at ~1e9 word-ops/s per core; aim for ~5 s per step
+    per_block_s = w.m * w.n / 64 / 1.0e9
+    return int(max(1, min(w.n_blocks, 5.0 * cores / per_block_s)))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--path", choices=["auto", "gemm", "ntt"], default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * qrng.h -- C ABI of libqrng.so: B200 (sm_100a) Toeplitz-hashing randomness
+ * extraction and min-entropy sizing, after arXiv 2011.04130 (Zhao, Ma, Zhou,
+ * "Performance Optimization on Practical Quantum Random Number Generators").
+ *
+ * Citations: PAPER.md:<line> is the paper text, SPEC.md:<line> the derived CPU
+ * spec (interfaces / error split only).  Conventions C1-C4 are fixed in
+ * DESIGN.md "Readings of the paper" (from BASELINE.json and SURVEY.md Sec. 0).
+ *
+ *  C1  y = T x mod 2 with T[i][j] = s[i - j + n - 1], 0 <= i < m, 0 <= j < n:
+ *      the m x n Toeplitz matrix displayed at PAPER.md:193 (row 1 = a_n..a_1,
+ *      last row = a_{n+m-1}..a_m, a_k = s[k-1]), equivalently outputs
+ *      k_n..k_{n+m-1} of the circulant product.
+ *  C2  Every bit buffer is MSB-first: bit k is (buf[k >> 3] >> (7 - (k & 7))) & 1.
+ *      An array of 8-bit ADC samples therefore IS the packed raw bit stream.
+ *  C3  Block b is raw bits [b*n, (b+1)*n)  (block segmentation, Fig. 5).
+ *  C4  Output: block b's y_i is output bit b*m + i; ceil(n_blocks*m/8) bytes;
+ *      pad bits of the last byte are written as 0.
+ *
+ * Pointers named d_* are CUDA device pointers, h_* host pointers.  The caller
+ * owns every buffer it passes; the library owns only plans and their
+ * workspace.  Results never depend on the path taken, the stream or the
+ * number of GPUs the caller shards blocks over (blocks are independent).
+ * There is no CPU fallback: without a usable sm_100 device every entry point
+ * that touches data returns QRNG_E_CUDA.
+ */
+#ifndef QRNG_H_
+#define QRNG_H_
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#if defined(__GNUC__)
+#define QRNG_API __attribute__((visibility("default")))
+#else
+#define QRNG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    QRNG_OK            = 0,
+    QRNG_E_INVALID     = 1, /* argument violates a precondition ("validation error") */
+    QRNG_E_UNSUPPORTED = 2, /* valid for the method, outside this build's limits */
+    QRNG_E_NO_OUTPUT   = 3, /* derived m <= 0: block too short for the security parameter */
+    QRNG_E_CUDA        = 4, /* a CUDA call failed or no sm_100 device ("runtime error") */
+    QRNG_E_NOMEM       = 5  /* device or host allocation failed */
+} qrng_status;
+
+/* Extraction path.  AUTO picks by n (crossover measured on B200). */
+typedef enum { QRNG_PATH_AUTO = 0, QRNG_PATH_GEMM = 1, QRNG_PATH_NTT = 2 } qrng_path;
+
+/* Ideal ADC model: Gaussian N(mu, sigma^2) discretised on bins [k-1/2, k+1/2),
+ * edge bins absorbing the tails (reading A10).  sigma > 0. */
+typedef struct { double mu, sigma; } qrng_gauss;
+
+typedef struct {
+    uint64_t counts[256];   /* histogram of the samples (bins >= 2^bit_depth are 0)   */
+    uint64_t n_samples;
+    uint32_t bit_depth;     /* N */
+    uint32_t reserved;
+    double   mu, sigma;     /* model used: fitted (population sigma) or supplied       */
+    double   h_min_hist;    /* -log2(max_x counts[x] / n_samples)   PAPER.md:59 on P'  */
+    double   h_min_ideal;   /* -log2 max P(x) of the model          PAPER.md:59 on P   */
+    double   stat_dist;     /* d_U(P', P) = 1/2 sum |P' - P|, U = all 2^N bins */
+    double   delta_h_m;     /* log2(d_U / 2^(-N-1) + 1)       */
+    double   h_min_mod;     /* max(0, h_min_ideal - delta_h_m)       */
+    int64_t  m;             /* floor(n * h_min_mod / N) - s       */
+} qrng_entropy_report;
+
+typedef struct qrng_plan qrng_plan;
+
+/* ---------------------------------------------------------------------------
+ * Min-entropy and output length.
+ *
+ * qrng_minentropy: histogram of n_samples uint8 ADC samples on the device,
+ * then the host finalises in double precision: H_min of the histogram, the
+ * model P (supplied, or N(mu, sigma^2) fitted from the histogram when model is
+ * NULL), d_U(P', P), Delta H_m, H_min^modify and m = floor(n*H_mod/N) - s, where
+ * s = 2 log2(1/eps) is passed as an integer (reading A7).  Synchronous on
+ * `stream` (one 2 KiB device-to-host copy).  rep is a host pointer and is
+ * filled even when QRNG_E_NO_OUTPUT is returned.
+ * Errors: E_INVALID if d_samples or rep is NULL, n_samples == 0, bit_depth
+ * outside [1, 8], a sample >= 2^bit_depth, or model->sigma <= 0;
+ * E_NO_OUTPUT if the derived m <= 0.
+ */
+QRNG_API qrng_status qrng_minentropy(const uint8_t *d_samples, uint64_t n_samples, uint32_t bit_depth,
+                            const qrng_gauss *model, uint64_t n, uint32_t s,
+                            qrng_entropy_report *rep, cudaStream_t stream);
+
+/* Building blocks of qrng_minentropy for sharded samples (one process per
+ * GPU): each rank ACCUMULATES its shard's counts into d_counts (uint64[256],
+ * device, caller-zeroed) asynchronously, the caller all-reduces the 256
+ * counts, then any rank finalises on the host.  h_counts is a host pointer. */
+QRNG_API qrng_status qrng_hist256_async(const uint8_t *d_samples, uint64_t n_samples,
+                               uint64_t *d_counts, cudaStream_t stream);
+QRNG_API qrng_status qrng_entropy_from_counts(const uint64_t *h_counts, uint32_t bit_depth,
+                                     const qrng_gauss *model, uint64_t n, uint32_t s,
+                                     qrng_entropy_report *rep);
+
+/* ---------------------------------------------------------------------------
+ * Toeplitz extraction y = T x mod 2 of every block (C1-C4).
+ *
+ * d_raw_bits : n_blocks*n bits (C2, C3), ceil(n_blocks*n/8) bytes, 16-byte aligned.
+ * d_seed     : L = n+m-1 seed bits a_1..a_L (C2), ceil(L/8) bytes, 16-byte aligned;
+ *              bits past L are ignored.  One seed serves every block.
+ * d_out      : ceil(n_blocks*m/8) bytes, 16-byte aligned, written completely (C4).
+ * Errors: E_INVALID if a pointer is NULL or not 16-byte aligned, n == 0, m == 0,
+ *         m >= n, n_blocks == 0, or d_out overlaps d_raw_bits or d_seed;
+ *         E_UNSUPPORTED if n % 32 != 0 or L > 2^23 (2-adic limit of the NTT prime
+ *         p = 119*2^23 + 1);  E_CUDA / E_NOMEM on device failures.
+ * The one-shot calls build a temporary plan (seed preparation included) and
+ * release it stream-ordered; _async returns once the work is enqueued.
+ */
+QRNG_API qrng_status qrng_toeplitz_extract(const uint8_t *d_raw_bits, uint64_t n_blocks, uint64_t n,
+                                  uint64_t m, const uint8_t *d_seed, uint8_t *d_out);
+QRNG_API qrng_status qrng_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks, uint64_t n,
+                                        uint64_t m, const uint8_t *d_seed, uint8_t *d_out,
+                                        cudaStream_t stream);
+
+/* End-to-end form with HOST buffers (h_raw_bits / h_seed / h_out, pinned
+ * memory recommended): copies in, extracts and copies the key back on
+ * `stream`, then synchronises it.  Same layouts and errors as above except
+ * that host pointers need no particular alignment. */
+QRNG_API qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blocks, uint64_t n,
+                                       uint64_t m, const uint8_t *h_seed, uint8_t *h_out,
+                                       cudaStream_t stream);
+
+/* Plans: seed preparation (a3) once per (seed, n, m), reused over many batches.
+ * qrng_plan_create reads d_seed on `stream` (the seed may be freed once that
+ * stream has passed the call).  qrng_plan_extract has the layouts of
+ * qrng_toeplitz_extract for n_blocks blocks of the plan's n.  A plan may be
+ * used from several streams at once; destroy it only after its work is done. */
+QRNG_API qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed,
+                             cudaStream_t stream, qrng_plan **plan);
+QRNG_API qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits,
+                              uint64_t n_blocks, uint8_t *d_out, cudaStream_t stream);
+QRNG_API void        qrng_plan_destroy(qrng_plan *plan);
+/* Path the plan runs (QRNG_PATH_GEMM or QRNG_PATH_NTT); -1 for NULL. */
+QRNG_API int         qrng_plan_path(const qrng_plan *plan);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+QRNG_API const char *qrng_last_error(void);
+/* Library version string, e.g. "qrng-b200 0.1 sm_100a". */
+QRNG_API const char *qrng_version(void);
+
+/* TEST ONLY: force the path of plans created afterwards on this process
+ * (QRNG_PATH_AUTO restores the measured crossover).  Used to cross-check the
+ * two independent GPU paths and to measure the crossover; not a backend switch. */
+QRNG_API void        qrng_debug_set_path(int path);
+
+/* BENCH / TEST ONLY instrumentation.
+ * qrng_debug_launch_count: number of kernels this library has launched in the
+ * process so far (plan preparation and extraction kernels alike).
+ * qrng_debug_kernel_timing(1) makes every subsequent main extraction-kernel
+ * launch record CUDA events on its own stream; qrng_debug_kernel_time_ms
+ * synchronises those events, returns the summed device time in ms, stores the
+ * number of timed launches in *launches (if not NULL) and clears the record. */
+QRNG_API uint64_t    qrng_debug_launch_count(void);
+QRNG_API void        qrng_debug_kernel_timing(int enable);
+QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QRNG_H_ */

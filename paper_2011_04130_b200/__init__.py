@@ -1,0 +1,278 @@
+"""Python binding of libqrng.so (include/qrng.h) -- argument marshalling only.
+
+B200-native Toeplitz-hashing randomness extraction after arXiv 2011.04130:
+every step of the hot path runs in the CUDA kernels of ``csrc/``; this module
+only turns torch tensors (device memory, streams) into pointers and status
+codes into exceptions.  There is no CPU fallback: if ``libqrng.so`` is
+missing or the device is not sm_100, calls raise.
+
+Names follow the paper: n (block length, bits), m (output bits per block),
+seed a = s (n+m-1 bits), raw r = x, key k = y.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqrng.so")
+
+QRNG_OK, QRNG_E_INVALID, QRNG_E_UNSUPPORTED, QRNG_E_NO_OUTPUT, QRNG_E_CUDA, QRNG_E_NOMEM = range(6)
+PATH_AUTO, PATH_GEMM, PATH_NTT = 0, 1, 2
+STATUS_NAMES = {0: "QRNG_OK", 1: "QRNG_E_INVALID", 2: "QRNG_E_UNSUPPORTED", 3: "QRNG_E_NO_OUTPUT",
+                4: "QRNG_E_CUDA", 5: "QRNG_E_NOMEM"}
+
+# Every symbol include/qrng.h declares (checked by tests/test_abi.py).
+EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
+           "qrng_toeplitz_extract", "qrng_toeplitz_extract_async", "qrng_toeplitz_extract_host",
+           "qrng_plan_create", "qrng_plan_extract", "qrng_plan_destroy", "qrng_plan_path",
+           "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
+           "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms"]
+
+
+class QrngError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Gauss(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_double), ("sigma", ctypes.c_double)]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("counts", ctypes.c_uint64 * 256), ("n_samples", ctypes.c_uint64),
+                ("bit_depth", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("mu", ctypes.c_double), ("sigma", ctypes.c_double),
+                ("h_min_hist", ctypes.c_double), ("h_min_ideal", ctypes.c_double),
+                ("stat_dist", ctypes.c_double), ("delta_h_m", ctypes.c_double),
+                ("h_min_mod", ctypes.c_double), ("m", ctypes.c_int64)]
+
+
+@dataclasses.dataclass
+class EntropyReport:
+    counts: np.ndarray
+    n_samples: int
+    bit_depth: int
+    mu: float
+    sigma: float
+    h_min_hist: float
+    h_min_ideal: float
+    stat_dist: float
+    delta_h_m: float
+    h_min_mod: float
+    m: int
+    status: int
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libqrng.so (build it with ``python -m paper_2011_04130_b200.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_2011_04130_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, u64, u32, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
+    sig = {
+        "qrng_minentropy": ([vp, u64, u32, vp, u64, u32, vp, vp], i32),
+        "qrng_hist256_async": ([vp, u64, vp, vp], i32),
+        "qrng_entropy_from_counts": ([vp, u32, vp, u64, u32, vp], i32),
+        "qrng_toeplitz_extract": ([vp, u64, u64, u64, vp, vp], i32),
+        "qrng_toeplitz_extract_async": ([vp, u64, u64, u64, vp, vp, vp], i32),
+        "qrng_toeplitz_extract_host": ([vp, u64, u64, u64, vp, vp, vp], i32),
+        "qrng_plan_create": ([u64, u64, vp, vp, ctypes.POINTER(vp)], i32),
+        "qrng_plan_extract": ([vp, vp, u64, vp, vp], i32),
+        "qrng_plan_destroy": ([vp], None),
+        "qrng_plan_path": ([vp], i32),
+        "qrng_last_error": ([], ctypes.c_char_p),
+        "qrng_version": ([], ctypes.c_char_p),
+        "qrng_debug_set_path": ([i32], None),
+        "qrng_debug_launch_count": ([], u64),
+        "qrng_debug_kernel_timing": ([i32], None),
+        "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != QRNG_OK:
+        raise QrngError(status, load_library().qrng_last_error().decode())
+
+
+def _stream_handle(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _need_cuda_u8(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.dtype != torch.uint8 \
+            or not t.is_contiguous():
+        raise TypeError(f"{name} must be a contiguous uint8 CUDA tensor")
+
+
+def out_bytes(n_blocks: int, m: int) -> int:
+    return (n_blocks * m + 7) // 8
+
+
+def version() -> str:
+    return load_library().qrng_version().decode()
+
+
+def last_error() -> str:
+    return load_library().qrng_last_error().decode()
+
+
+def set_debug_path(path: int) -> None:
+    """TEST ONLY: force QRNG_PATH_GEMM / QRNG_PATH_NTT for plans created afterwards."""
+    load_library().qrng_debug_set_path(int(path))
+
+
+def launch_count() -> int:
+    """Kernels launched by libqrng.so in this process (bench/test instrumentation)."""
+    return int(load_library().qrng_debug_launch_count())
+
+
+def kernel_timing(enable: bool) -> None:
+    load_library().qrng_debug_kernel_timing(1 if enable else 0)
+
+
+def kernel_time_ms() -> tuple[float, int]:
+    """(summed device ms, launches) of the main extraction kernel since the last read."""
+    n = ctypes.c_uint64()
+    ms = load_library().qrng_debug_kernel_time_ms(ctypes.byref(n))
+    return float(ms), int(n.value)
+
+
+def toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=None):
+    """Key bytes (C4) of n_blocks blocks: qrng_toeplitz_extract_async on `stream`."""
+    import torch
+    _need_cuda_u8(raw, "raw")
+    _need_cuda_u8(seed, "seed")
+    if out is None:
+        out = torch.empty(out_bytes(n_blocks, m), dtype=torch.uint8, device=raw.device)
+    _need_cuda_u8(out, "out")
+    _check(load_library().qrng_toeplitz_extract_async(_ptr(raw), n_blocks, n, m, _ptr(seed), _ptr(out),
+                                                      _stream_handle(stream)))
+    return out
+
+
+def toeplitz_extract_host(raw: np.ndarray, n_blocks: int, n: int, m: int, seed: np.ndarray,
+                          out: np.ndarray, stream=None) -> np.ndarray:
+    """End-to-end call with HOST buffers (numpy views; pinned memory recommended)."""
+    for a in (raw, seed, out):
+        if not (isinstance(a, np.ndarray) and a.dtype == np.uint8 and a.flags.c_contiguous):
+            raise TypeError("host buffers must be contiguous uint8 numpy arrays")
+    if out.size < out_bytes(n_blocks, m):
+        raise ValueError("out too small")
+    _check(load_library().qrng_toeplitz_extract_host(raw.ctypes.data, n_blocks, n, m, seed.ctypes.data,
+                                                     out.ctypes.data, _stream_handle(stream)))
+    return out
+
+
+class Plan:
+    """Seed preparation once per (seed, n, m); extract many batches."""
+
+    def __init__(self, n: int, m: int, seed, stream=None):
+        _need_cuda_u8(seed, "seed")
+        self.n, self.m = n, m
+        h = ctypes.c_void_p()
+        _check(load_library().qrng_plan_create(n, m, _ptr(seed), _stream_handle(stream), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def path(self) -> int:
+        return load_library().qrng_plan_path(self._h)
+
+    def extract(self, raw, n_blocks: int, out=None, stream=None):
+        import torch
+        _need_cuda_u8(raw, "raw")
+        if out is None:
+            out = torch.empty(out_bytes(n_blocks, self.m), dtype=torch.uint8, device=raw.device)
+        _need_cuda_u8(out, "out")
+        _check(load_library().qrng_plan_extract(self._h, _ptr(raw), n_blocks, _ptr(out),
+                                                _stream_handle(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().qrng_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def _report(rep: _Report, status: int) -> EntropyReport:
+    return EntropyReport(np.array(rep.counts[:], dtype=np.uint64), rep.n_samples, rep.bit_depth, rep.mu,
+                         rep.sigma, rep.h_min_hist, rep.h_min_ideal, rep.stat_dist, rep.delta_h_m,
+                         rep.h_min_mod, rep.m, status)
+
+
+def minentropy(samples, bit_depth: int = 8, n: int = 0, s: int = 0, model=None, stream=None,
+               allow_no_output: bool = False) -> EntropyReport:
+    """qrng_minentropy: device histogram + host H_min / Delta H_m / m (synchronous)."""
+    _need_cuda_u8(samples, "samples")
+    rep = _Report()
+    g = _Gauss(*model) if model is not None else None
+    st = load_library().qrng_minentropy(_ptr(samples), samples.numel(), bit_depth,
+                                        ctypes.byref(g) if g is not None else None, n, s,
+                                        ctypes.byref(rep), _stream_handle(stream))
+    if not (st == QRNG_OK or (allow_no_output and st == QRNG_E_NO_OUTPUT)):
+        _check(st)
+    return _report(rep, st)
+
+
+def hist256_async(samples, counts, stream=None):
+    """Accumulate the shard's histogram into counts (uint64[256] CUDA tensor, caller-zeroed)."""
+    import torch
+    _need_cuda_u8(samples, "samples")
+    if counts.dtype not in (torch.int64, torch.uint64) or counts.numel() != 256 or counts.device.type != "cuda":
+        raise TypeError("counts must be a 256-element 64-bit CUDA tensor")
+    _check(load_library().qrng_hist256_async(_ptr(samples), samples.numel(), _ptr(counts),
+                                             _stream_handle(stream)))
+    return counts
+
+
+def entropy_from_counts(counts: np.ndarray, bit_depth: int = 8, n: int = 0, s: int = 0, model=None,
+                        allow_no_output: bool = False) -> EntropyReport:
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
+    if c.size != 256:
+        raise ValueError("counts must have 256 entries")
+    rep = _Report()
+    g = _Gauss(*model) if model is not None else None
+    st = load_library().qrng_entropy_from_counts(c.ctypes.data, bit_depth,
+                                                 ctypes.byref(g) if g is not None else None, n, s,
+                                                 ctypes.byref(rep))
+    if not (st == QRNG_OK or (allow_no_output and st == QRNG_E_NO_OUTPUT)):
+        _check(st)
+    return _report(rep, st)

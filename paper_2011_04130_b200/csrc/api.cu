@@ -1,0 +1,356 @@
+// api.cu -- the C ABI of libqrng.so (include/qrng.h): argument validation,
+// plans and the block scheduler that picks the extraction path, and the
+// host-side finalisation of the min-entropy chain.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <vector>
+#include "qrng_internal.cuh"
+
+namespace qrng {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+// ---- instrumentation (qrng_debug_*) ----
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_timing{0};
+static std::mutex g_tmu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+KernelTimer::KernelTimer(cudaStream_t st) : s(st) {
+    count_launch();
+    if (!g_timing.load()) return;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
+    cudaEventRecord(a, s);
+}
+void KernelTimer::stop() {
+    if (!a) return;
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_events.emplace_back(a, b);
+}
+
+// Measured GEMM/NTT crossover in n; GEMM for n <= this.
+static uint64_t g_gemm_max_n = 0;
+static int g_debug_path = QRNG_PATH_AUTO;
+
+// One-time device check: sm_100 required (no CPU fallback), stream-ordered
+// pool kept warm so per-call workspace allocation is cheap.
+static qrng_status device_ready() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        set_error("no CUDA device: %s", cudaGetErrorString(e));
+        return QRNG_E_CUDA;
+    }
+    static std::mutex mu;
+    static bool ready[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && ready[dev]) return QRNG_OK;
+    int major = 0, minor = 0;
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    if (major != 10 || minor != 0) {
+        set_error("libqrng is built for sm_100a (B200); device %d is sm_%d%d", dev, major, minor);
+        return QRNG_E_CUDA;
+    }
+    cudaMemPool_t pool;
+    QRNG_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thresh = UINT64_MAX;
+    QRNG_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    if (dev < 64) ready[dev] = true;
+    return QRNG_OK;
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+static bool overlap(const void *a, uint64_t na, const void *b, uint64_t nb) {
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+static qrng_status check_nm(uint64_t n, uint64_t m) {
+    if (n == 0 || m == 0 || m >= n) {
+        set_error("need 0 < m < n (got n=%llu, m=%llu)", (unsigned long long)n, (unsigned long long)m);
+        return QRNG_E_INVALID;
+    }
+    if (n % 32 != 0) {
+        set_error("n must be a multiple of 32 (got %llu)", (unsigned long long)n);
+        return QRNG_E_UNSUPPORTED;
+    }
+    if (n + m - 1 > (1ull << ntt::kMaxLogP)) {
+        set_error("seed length n+m-1 = %llu exceeds 2^23", (unsigned long long)(n + m - 1));
+        return QRNG_E_UNSUPPORTED;
+    }
+    return QRNG_OK;
+}
+
+}  // namespace qrng
+
+using namespace qrng;
+
+struct qrng_plan {
+    uint64_t n = 0, m = 0;
+    int path = QRNG_PATH_NTT;
+    ntt::Plan ntt;
+    gemm::Plan gemm;
+    uint32_t *tail = nullptr;  // scratch word for a final partial output word
+};
+
+static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
+    if (!p) return;
+    auto fr = [&](void *ptr) {
+        if (!ptr) return;
+        if (async) cudaFreeAsync(ptr, s);
+        else cudaFree(ptr);
+    };
+    fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.work);
+    fr(p->gemm.seed_words);
+    fr(p->tail);
+    delete p;
+}
+
+extern "C" {
+
+const char *qrng_last_error(void) { return g_err; }
+const char *qrng_version(void) { return "qrng-b200 0.1 sm_100a"; }
+void qrng_debug_set_path(int path) { g_debug_path = path; }
+uint64_t qrng_debug_launch_count(void) { return g_launches.load(); }
+void qrng_debug_kernel_timing(int enable) { g_timing.store(enable ? 1 : 0); }
+double qrng_debug_kernel_time_ms(uint64_t *launches) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    double total = 0;
+    for (auto &e : g_events) {
+        float ms = 0;
+        if (cudaEventSynchronize(e.second) == cudaSuccess && cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess)
+            total += ms;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    if (launches) *launches = g_events.size();
+    g_events.clear();
+    return total;
+}
+
+int qrng_plan_path(const qrng_plan *plan) { return plan ? plan->path : -1; }
+
+qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
+                             qrng_plan **plan) {
+    if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
+    *plan = nullptr;
+    qrng_status st = check_nm(n, m);
+    if (st != QRNG_OK) return st;
+    if (!d_seed || !aligned16(d_seed)) { set_error("d_seed is NULL or not 16-byte aligned"); return QRNG_E_INVALID; }
+    if ((st = device_ready()) != QRNG_OK) return st;
+    qrng_plan *p = new (std::nothrow) qrng_plan;
+    if (!p) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
+    p->n = n;
+    p->m = m;
+    int want = g_debug_path;
+    if (want == QRNG_PATH_AUTO) want = (gemm::supported(n, m) && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
+    if (want == QRNG_PATH_GEMM && !gemm::supported(n, m)) {
+        set_error("GEMM path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
+        delete p;
+        return QRNG_E_UNSUPPORTED;
+    }
+    p->path = want;
+    cudaError_t e = cudaMallocAsync(&p->tail, 4, stream);
+    if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); delete p; return QRNG_E_NOMEM; }
+    st = (want == QRNG_PATH_GEMM) ? gemm::plan_init(p->gemm, n, m, d_seed, stream)
+                                  : ntt::plan_init(p->ntt, n, m, d_seed, stream);
+    if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
+    *plan = p;
+    return QRNG_OK;
+}
+
+void qrng_plan_destroy(qrng_plan *plan) { plan_release(plan, 0, false); }
+
+qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, uint64_t n_blocks,
+                              uint8_t *d_out, cudaStream_t stream) {
+    if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
+    const uint64_t n = plan->n, m = plan->m;
+    if (n_blocks == 0) { set_error("n_blocks must be > 0"); return QRNG_E_INVALID; }
+    if (!d_raw_bits || !d_out) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    if (!aligned16(d_raw_bits) || !aligned16(d_out)) { set_error("buffers must be 16-byte aligned"); return QRNG_E_INVALID; }
+    if (n_blocks > (UINT64_MAX / n)) { set_error("n_blocks * n overflows"); return QRNG_E_INVALID; }
+    const uint64_t raw_bytes = n_blocks * n / 8, out_bits = n_blocks * m, out_bytes = (out_bits + 7) / 8;
+    if (overlap(d_raw_bits, raw_bytes, d_out, out_bytes)) { set_error("d_out overlaps d_raw_bits"); return QRNG_E_INVALID; }
+    OutStream o;
+    o.words = reinterpret_cast<uint32_t *>(d_out);
+    o.total_bits = out_bits;
+    o.full_words = out_bytes / 4;
+    o.tail = plan->tail;
+    QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
+    if (out_bytes % 4) QRNG_CUDA_TRY(cudaMemsetAsync(plan->tail, 0, 4, stream));
+    qrng_status st = (plan->path == QRNG_PATH_GEMM) ? gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
+                                                    : ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream);
+    if (st != QRNG_OK) return st;
+    if (out_bytes % 4)
+        QRNG_CUDA_TRY(cudaMemcpyAsync(d_out + (out_bytes / 4) * 4, plan->tail, out_bytes % 4,
+                                      cudaMemcpyDeviceToDevice, stream));
+    return QRNG_OK;
+}
+
+qrng_status qrng_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks, uint64_t n, uint64_t m,
+                                        const uint8_t *d_seed, uint8_t *d_out, cudaStream_t stream) {
+    qrng_status st = check_nm(n, m);
+    if (st != QRNG_OK) return st;
+    if (!d_raw_bits || !d_seed || !d_out) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    if (n_blocks == 0) { set_error("n_blocks must be > 0"); return QRNG_E_INVALID; }
+    if (d_out && d_seed && n_blocks <= UINT64_MAX / m &&
+        overlap(d_seed, (n + m - 1 + 7) / 8, d_out, (n_blocks * m + 7) / 8)) {
+        set_error("d_out overlaps d_seed");
+        return QRNG_E_INVALID;
+    }
+    qrng_plan *p = nullptr;
+    if ((st = qrng_plan_create(n, m, d_seed, stream, &p)) != QRNG_OK) return st;
+    st = qrng_plan_extract(p, d_raw_bits, n_blocks, d_out, stream);
+    plan_release(p, stream, true);
+    return st;
+}
+
+qrng_status qrng_toeplitz_extract(const uint8_t *d_raw_bits, uint64_t n_blocks, uint64_t n, uint64_t m,
+                                  const uint8_t *d_seed, uint8_t *d_out) {
+    qrng_status st = qrng_toeplitz_extract_async(d_raw_bits, n_blocks, n, m, d_seed, d_out, 0);
+    if (st != QRNG_OK) return st;
+    QRNG_CUDA_TRY(cudaStreamSynchronize(0));
+    return QRNG_OK;
+}
+
+qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blocks, uint64_t n, uint64_t m,
+                                       const uint8_t *h_seed, uint8_t *h_out, cudaStream_t stream) {
+    qrng_status st = check_nm(n, m);
+    if (st != QRNG_OK) return st;
+    if (!h_raw_bits || !h_seed || !h_out) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    if (n_blocks == 0 || n_blocks > UINT64_MAX / n) { set_error("bad n_blocks"); return QRNG_E_INVALID; }
+    if ((st = device_ready()) != QRNG_OK) return st;
+    const uint64_t raw_bytes = n_blocks * n / 8, seed_bytes = (n + m - 1 + 7) / 8,
+                   out_bytes = (n_blocks * m + 7) / 8;
+    uint8_t *d_raw = nullptr, *d_seed = nullptr, *d_out = nullptr;
+    QRNG_CUDA_TRY(cudaMallocAsync(&d_raw, raw_bytes, stream));
+    QRNG_CUDA_TRY(cudaMallocAsync(&d_seed, seed_bytes, stream));
+    QRNG_CUDA_TRY(cudaMallocAsync(&d_out, out_bytes, stream));
+    QRNG_CUDA_TRY(cudaMemcpyAsync(d_raw, h_raw_bits, raw_bytes, cudaMemcpyHostToDevice, stream));
+    QRNG_CUDA_TRY(cudaMemcpyAsync(d_seed, h_seed, seed_bytes, cudaMemcpyHostToDevice, stream));
+    st = qrng_toeplitz_extract_async(d_raw, n_blocks, n, m, d_seed, d_out, stream);
+    if (st == QRNG_OK)
+        QRNG_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, stream));
+    cudaFreeAsync(d_raw, stream);
+    cudaFreeAsync(d_seed, stream);
+    cudaFreeAsync(d_out, stream);
+    QRNG_CUDA_TRY(cudaStreamSynchronize(stream));
+    return st;
+}
+
+// ---- min-entropy ------------------------
+
+qrng_status qrng_hist256_async(const uint8_t *d_samples, uint64_t n_samples, uint64_t *d_counts,
+                               cudaStream_t stream) {
+    if (!d_samples || !d_counts) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    if (n_samples == 0) { set_error("n_samples must be > 0"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    return hist256_launch(d_samples, n_samples, reinterpret_cast<unsigned long long *>(d_counts), stream);
+}
+
+static double std_normal_cdf(double z) { return 0.5 * (1.0 + erf(z / sqrt(2.0))); }
+
+qrng_status qrng_entropy_from_counts(const uint64_t *h_counts, uint32_t bit_depth, const qrng_gauss *model,
+                                     uint64_t n, uint32_t s, qrng_entropy_report *rep) {
+    if (!h_counts || !rep) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    if (bit_depth < 1 || bit_depth > 8) { set_error("bit_depth must be in [1, 8]"); return QRNG_E_INVALID; }
+    memset(rep, 0, sizeof *rep);
+    const int K = 1 << bit_depth;
+    uint64_t total = 0, cmax = 0;
+    for (int k = 0; k < 256; ++k) {
+        rep->counts[k] = h_counts[k];
+        total += h_counts[k];
+        if (k >= K && h_counts[k]) {
+            set_error("sample value %d >= 2^bit_depth", k);
+            return QRNG_E_INVALID;
+        }
+        if (h_counts[k] > cmax) cmax = h_counts[k];
+    }
+    rep->n_samples = total;
+    rep->bit_depth = bit_depth;
+    if (total == 0) { set_error("empty histogram"); return QRNG_E_INVALID; }
+    const double T = (double)total;
+    // H_min of the empirical distribution P'(x) = counts / T
+    rep->h_min_hist = -log2((double)cmax / T);
+    double mu, sigma;
+    if (model) {
+        mu = model->mu;
+        sigma = model->sigma;
+    } else {  // reading A10: moments of the histogram, population sigma
+        double s1 = 0, s2 = 0;
+        for (int k = 0; k < K; ++k) {
+            s1 += (double)k * (double)h_counts[k];
+            s2 += (double)k * (double)k * (double)h_counts[k];
+        }
+        mu = s1 / T;
+        double var = s2 / T - mu * mu;
+        sigma = sqrt(var > 0 ? var : 0);
+    }
+    rep->mu = mu;
+    rep->sigma = sigma;
+    if (!(sigma > 0)) { set_error("model sigma must be > 0"); return QRNG_E_INVALID; }
+    // ideal model P: N(mu, sigma^2) on bins [k-1/2, k+1/2), tails in the edge bins
+    double pmax = 0, d = 0, prev = 0;
+    for (int k = 0; k < K; ++k) {
+        double cdf = (k == K - 1) ? 1.0 : std_normal_cdf(((double)k + 0.5 - mu) / sigma);
+        double pk = cdf - prev;
+        prev = cdf;
+        if (pk > pmax) pmax = pk;
+        d += fabs((double)h_counts[k] / T - pk);
+    }
+    d *= 0.5;                                                     // d_U
+    rep->h_min_ideal = -log2(pmax);
+    rep->stat_dist = d;
+    rep->delta_h_m = log2(d / pow(2.0, -(double)bit_depth - 1.0) + 1.0);
+    double hm = rep->h_min_ideal - rep->delta_h_m;
+    rep->h_min_mod = hm > 0 ? hm : 0.0;
+    rep->m = (int64_t)floor((double)n * rep->h_min_mod / (double)bit_depth) - (int64_t)s;
+    if (rep->m <= 0) {
+        set_error("derived m = %lld <= 0", (long long)rep->m);
+        return QRNG_E_NO_OUTPUT;
+    }
+    return QRNG_OK;
+}
+
+qrng_status qrng_minentropy(const uint8_t *d_samples, uint64_t n_samples, uint32_t bit_depth,
+                            const qrng_gauss *model, uint64_t n, uint32_t s, qrng_entropy_report *rep,
+                            cudaStream_t stream) {
+    if (!d_samples || !rep) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    if (n_samples == 0) { set_error("n_samples must be > 0"); return QRNG_E_INVALID; }
+    if (bit_depth < 1 || bit_depth > 8) { set_error("bit_depth must be in [1, 8]"); return QRNG_E_INVALID; }
+    if (model && !(model->sigma > 0)) { set_error("model sigma must be > 0"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    uint64_t *d_counts = nullptr;
+    uint64_t h[256];
+    QRNG_CUDA_TRY(cudaMallocAsync(&d_counts, 256 * sizeof(uint64_t), stream));
+    QRNG_CUDA_TRY(cudaMemsetAsync(d_counts, 0, 256 * sizeof(uint64_t), stream));
+    st = hist256_launch(d_samples, n_samples, reinterpret_cast<unsigned long long *>(d_counts), stream);
+    if (st == QRNG_OK) {
+        cudaError_t e = cudaMemcpyAsync(h, d_counts, sizeof h, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) { set_error("histogram copy: %s", cudaGetErrorString(e)); st = QRNG_E_CUDA; }
+    }
+    cudaFreeAsync(d_counts, stream);
+    if (st != QRNG_OK) return st;
+    return qrng_entropy_from_counts(h, bit_depth, model, n, s, rep);
+}
+
+}  // extern "C"

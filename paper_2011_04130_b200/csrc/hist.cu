@@ -1,0 +1,69 @@
+// hist.cu -- exact 256-bin histogram of 8-bit ADC samples (HBM-bound).
+//
+// Feeds the empirical distribution P'(x) of PAPER.md:141-155 (Sec. II.C) and
+// the max-probability H_min of PAPER.md:59.  B200 design: grid-stride over
+// 16-byte vectors (one LDG.128 per thread per iteration), per-warp private
+// sub-histograms in shared memory (Gaussian ADC data concentrates on a few
+// bins, so a single CTA histogram would serialise on the hot bins), then one
+// 64-bit global atomic per bin per CTA.  Counts are exact (uint32 in smem per
+// CTA chunk, uint64 in HBM).
+#include "qrng_internal.cuh"
+
+namespace qrng {
+
+namespace {
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ void add4(uint32_t *h, uint32_t w) {
+    atomicAdd(&h[w & 0xFF], 1u);
+    atomicAdd(&h[(w >> 8) & 0xFF], 1u);
+    atomicAdd(&h[(w >> 16) & 0xFF], 1u);
+    atomicAdd(&h[w >> 24], 1u);
+}
+
+__global__ void __launch_bounds__(kThreads) hist256_kernel(const uint8_t *__restrict__ x, uint64_t n,
+                                                           unsigned long long *__restrict__ counts) {
+    __shared__ uint32_t h[kWarps][256];
+    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t *mine = h[threadIdx.x >> 5];
+    const uint64_t nvec = n / 16;
+    const uint4 *v = reinterpret_cast<const uint4 *>(x);
+    const uint64_t tid = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
+    const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = tid; i < nvec; i += nthr) {
+        uint4 q = __ldcs(v + i);  // streamed once
+        add4(mine, q.x);
+        add4(mine, q.y);
+        add4(mine, q.z);
+        add4(mine, q.w);
+    }
+    for (uint64_t i = nvec * 16 + tid; i < n; i += nthr) atomicAdd(&mine[x[i]], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += kThreads) {
+        uint32_t s = 0;
+        for (int w = 0; w < kWarps; ++w) s += h[w][b];
+        if (s) atomicAdd(counts + b, (unsigned long long)s);
+    }
+}
+}  // namespace
+
+qrng_status hist256_launch(const uint8_t *d_samples, uint64_t n, unsigned long long *d_counts,
+                           cudaStream_t s) {
+    int dev = 0, sms = 148;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // <= 2^31 samples per CTA keeps every per-CTA smem count below 2^32
+    uint64_t want = (n / 16 + kThreads - 1) / kThreads;
+    uint64_t grid = want < (uint64_t)sms * 4 ? want : (uint64_t)sms * 4;
+    uint64_t min_grid = n / (1ull << 31) + 1;
+    if (grid < min_grid) grid = min_grid;
+    if (grid == 0) grid = 1;
+    count_launch();
+    hist256_kernel<<<(unsigned)grid, kThreads, 0, s>>>(d_samples, n, d_counts);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+}  // namespace qrng

@@ -1,0 +1,513 @@
+// ntt.cu -- exact number-theoretic-transform path of the Toeplitz extractor.
+//
+// Method (Sec. III.B, Def. 1-2, Thm. 1-2): embed T in the
+// circulant of the seed, so that the key is a window of a cyclic convolution:
+//     y_i = c[n-1+i],   c = s * x   (linear convolution).
+// The paper computes it with a floating-point FFT followed by round and mod 2
+// (Listing 2).  Here the transform is an NTT modulo the prime
+// p = 119*2^23 + 1 over a cyclic length P = 2^ceil(log2(n+m-1)) (A20,
+// PAPER.md:251): every window value c_t <= n < p, and P >= L rules out
+// wrap-around inside the window, so z_t mod p == c_t EXACTLY and y_i is its
+// parity (reading A16: no rounding, zero tolerance).
+//
+// B200 design: one CTA owns one transform of length
+// P <= 2^15 in shared memory (padded 1 word per 32 against bank conflicts).
+// The transform is a mixed-radix (2^3..2^5) Cooley-Tukey decomposition: each
+// pass runs a register-resident radix-2^r DIF sub-DFT with compile-time roots
+// in the constant bank (Shoup multiplication), then the inter-pass twiddles
+// (Montgomery, powers generated in registers from one table word per thread).
+// The deepest pass fuses forward DFT -> pointwise product with the prepared
+// seed spectrum -> inverse DFT, so the spectrum never leaves registers.
+// For n <= 2^14 two blocks share one transform as x1 + 2^k x2 (2^k > n and
+// n (2^k + 1) < p keeps both convolutions exact and separable: parity of c1
+// is bit 0, parity of c2 is bit k).  Values are kept lazily in [0, 2p); the
+// final residue is made canonical before its parity is taken.
+#include <cstdio>
+#include "qrng_internal.cuh"
+
+namespace qrng {
+namespace ntt {
+
+constexpr uint32_t P = kP;
+constexpr uint32_t P2 = 2u * kP;
+constexpr uint32_t PINV = 3296722945u;  // p^-1 mod 2^32
+constexpr uint32_t R1 = 301989884u;     // 2^32 mod p
+
+constexpr uint64_t powmod_c(uint64_t b, uint64_t e) {
+    uint64_t r = 1;
+    b %= P;
+    while (e) {
+        if (e & 1) r = r * b % P;
+        b = b * b % P;
+        e >>= 1;
+    }
+    return r;
+}
+
+struct RootTab {
+    uint32_t w[64], wp[64], iw[64], iwp[64];  // w_64^e, Shoup companions, inverses
+};
+constexpr RootTab make_roots() {
+    RootTab t{};
+    uint64_t w64 = powmod_c(3, (P - 1) / 64), iw64 = powmod_c(w64, P - 2);
+    uint64_t a = 1, b = 1;
+    for (int e = 0; e < 64; ++e) {
+        t.w[e] = (uint32_t)a;
+        t.wp[e] = (uint32_t)((a << 32) / P);
+        t.iw[e] = (uint32_t)b;
+        t.iwp[e] = (uint32_t)((b << 32) / P);
+        a = a * w64 % P;
+        b = b * iw64 % P;
+    }
+    return t;
+}
+__constant__ RootTab c_roots = make_roots();
+
+// ---- modular arithmetic on lazy residues in [0, 2p) ------------------------
+__device__ __forceinline__ uint32_t red2(uint32_t x) { return min(x, x - P2); }  // [0,4p)->[0,2p)
+__device__ __forceinline__ uint32_t shoup(uint32_t a, uint32_t w, uint32_t wp) {
+    uint32_t q = __umulhi(a, wp);
+    return a * w - q * P;  // a*w mod p in [0, 2p), any 32-bit a
+}
+__device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b) {  // a*b/2^32 mod p, a,b < 2p
+    uint32_t lo = a * b, hi = __umulhi(a, b);
+    uint32_t q = lo * PINV;
+    return hi - __umulhi(q, P) + P;  // in (0, 2p)
+}
+
+__host__ __device__ constexpr int brev(int x, int bits) {
+    int r = 0;
+    for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
+    return r;
+}
+
+// Radix-2^R DIF on registers: natural order in, bit-reversed order out.
+template <int R>
+__device__ __forceinline__ void dft_fwd(uint32_t (&x)[1 << R]) {
+    constexpr int N = 1 << R;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int half = N >> (t + 1);
+        const int step = 64 / (2 * half);
+#pragma unroll
+        for (int i0 = 0; i0 < N; i0 += 2 * half)
+#pragma unroll
+            for (int e = 0; e < half; ++e) {
+                uint32_t a = x[i0 + e], b = x[i0 + e + half];
+                uint32_t v = a - b + P2;
+                x[i0 + e] = red2(a + b);
+                x[i0 + e + half] = (e == 0) ? red2(v) : shoup(v, c_roots.w[e * step], c_roots.wp[e * step]);
+            }
+    }
+}
+
+// Radix-2^R DIT with inverse roots: bit-reversed order in, natural order out
+// (unscaled: returns N times the inverse DFT).
+template <int R>
+__device__ __forceinline__ void dft_inv(uint32_t (&x)[1 << R]) {
+    constexpr int N = 1 << R;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int half = 1 << t;
+        const int step = 64 / (2 * half);
+#pragma unroll
+        for (int i0 = 0; i0 < N; i0 += 2 * half)
+#pragma unroll
+            for (int e = 0; e < half; ++e) {
+                uint32_t a = x[i0 + e], b = x[i0 + e + half];
+                uint32_t tb = (e == 0) ? b : shoup(b, c_roots.iw[e * step], c_roots.iwp[e * step]);
+                x[i0 + e] = red2(a + tb);
+                x[i0 + e + half] = red2(a - tb + P2);
+            }
+    }
+}
+
+// Register q holds spectrum index k1 = brev(q): multiply it by tau^k1
+// (tauM = tau * 2^32 mod p, Montgomery form).
+template <int R>
+__device__ __forceinline__ void twiddle(uint32_t (&x)[1 << R], uint32_t tauM) {
+    constexpr int N = 1 << R;
+    uint32_t pw = tauM;
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+        if (k > 1) pw = mont(pw, tauM);
+        x[brev(k, R)] = mont(x[brev(k, R)], pw);
+    }
+}
+
+// ---- pass schedule ---------------------------------------------------------
+__host__ __device__ constexpr int np_of(int logP) { return (logP + 4) / 5; }
+__host__ __device__ constexpr int radix_of(int logP, int lv) {
+    return logP / np_of(logP) + (lv < logP % np_of(logP) ? 1 : 0);
+}
+__host__ __device__ constexpr int prefix_of(int logP, int lv) {
+    int s = 0;
+    for (int i = 0; i < lv; ++i) s += radix_of(logP, i);
+    return s;
+}
+__host__ __device__ constexpr int threads_of(int logP) {
+    return (1 << logP) / 32 < 32 ? 32 : ((1 << logP) / 32 > 1024 ? 1024 : (1 << logP) / 32);
+}
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 5); }
+
+struct FusedArgs {
+    const uint32_t *raw;      // raw stream as 32-bit words (MSB-first bytes)
+    uint64_t n_blocks;
+    uint32_t n, m;
+    int shift;                // pack shift (PACK only)
+    const uint32_t *shat, *tw, *itw;
+    OutStream out;
+    uint32_t stage_words;     // per-CTA staging words
+};
+
+// bit idx of block b (idx < n), stream MSB-first; n % 32 == 0
+__device__ __forceinline__ uint32_t raw_bit(const uint32_t *raw, uint64_t b, uint32_t n, uint32_t idx) {
+    uint32_t w = __ldg(raw + b * (n >> 5) + (idx >> 5));
+    return (bswap32(w) >> (31 - (idx & 31))) & 1u;
+}
+
+template <int LOGP, int LV, bool PACK>
+struct Level {
+    static constexpr int R = radix_of(LOGP, LV);
+    static constexpr int S = prefix_of(LOGP, LV);
+    static constexpr int NPASS = np_of(LOGP);
+    static constexpr int N1 = 1 << R;
+    static constexpr int STRIDE = (1 << LOGP) >> (S + R);
+    static constexpr int NSEG = (1 << LOGP) >> S;
+    static constexpr int NSUB = (1 << LOGP) >> R;
+    static constexpr bool LAST = (LV == NPASS - 1);
+    static constexpr int T = threads_of(LOGP);
+
+    __device__ static __forceinline__ int addr(int u, int q) {
+        return (u / STRIDE) * NSEG + q * STRIDE + (u % STRIDE);
+    }
+
+    __device__ static __forceinline__ void load(uint32_t (&x)[N1], int u, uint32_t *data,
+                                                const FusedArgs &a, uint64_t b0, int nb) {
+        if (LV == 0) {  // level 0 has one segment: idx = q*STRIDE + u
+#pragma unroll
+            for (int q = 0; q < N1; ++q) {
+                uint32_t idx = (uint32_t)(q * STRIDE + u), v = 0;
+                if (idx < a.n) {
+                    v = raw_bit(a.raw, b0, a.n, idx);
+                    if (PACK && nb > 1) v |= raw_bit(a.raw, b0 + 1, a.n, idx) << a.shift;
+                }
+                x[q] = v;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
+        }
+    }
+
+    // Final inverse output at level 0: element q is z_t, t = q*STRIDE + u.
+    __device__ static __forceinline__ void emit(uint32_t (&x)[N1], int u, uint32_t *stage,
+                                                const FusedArgs &a, uint64_t b0, int nb,
+                                                uint64_t wfirst) {
+#pragma unroll
+        for (int q = 0; q < N1; ++q) {
+            int64_t i = (int64_t)(q * STRIDE + u) - (int64_t)(a.n - 1);
+            if (i >= 0 && i < (int64_t)a.m) {
+                uint32_t z = x[q] >= P ? x[q] - P : x[q];  // canonical residue
+                if (z & 1u) {
+                    uint64_t g = b0 * a.m + (uint64_t)i;
+                    atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
+                }
+                if (PACK && nb > 1 && ((z >> a.shift) & 1u)) {
+                    uint64_t g = (b0 + 1) * a.m + (uint64_t)i;
+                    atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
+                }
+            }
+        }
+    }
+
+    __device__ static __forceinline__ void fwd(uint32_t *data, uint32_t *stage, const FusedArgs &a,
+                                               uint64_t b0, int nb, uint64_t wfirst) {
+        for (int u = threadIdx.x; u < NSUB; u += T) {
+            uint32_t x[N1];
+            load(x, u, data, a, b0, nb);
+            dft_fwd<R>(x);
+            if (!LAST) {
+                const int n2 = u % STRIDE;
+                if (n2) twiddle<R>(x, __ldg(a.tw + (n2 << S)));
+#pragma unroll
+                for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+            } else {
+                // pointwise product with the seed spectrum (DIF order: position u*N1+q)
+                const uint4 *sh = reinterpret_cast<const uint4 *>(a.shat + (size_t)u * N1);
+#pragma unroll
+                for (int q4 = 0; q4 < N1 / 4; ++q4) {
+                    uint4 s4 = __ldg(sh + q4);
+                    x[4 * q4 + 0] = mont(x[4 * q4 + 0], s4.x);
+                    x[4 * q4 + 1] = mont(x[4 * q4 + 1], s4.y);
+                    x[4 * q4 + 2] = mont(x[4 * q4 + 2], s4.z);
+                    x[4 * q4 + 3] = mont(x[4 * q4 + 3], s4.w);
+                }
+                dft_inv<R>(x);
+                if (LV == 0) emit(x, u, stage, a, b0, nb, wfirst);
+                else {
+#pragma unroll
+                    for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    __device__ static __forceinline__ void inv(uint32_t *data, uint32_t *stage, const FusedArgs &a,
+                                               uint64_t b0, int nb, uint64_t wfirst) {
+        for (int u = threadIdx.x; u < NSUB; u += T) {
+            uint32_t x[N1];
+#pragma unroll
+            for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
+            const int n2 = u % STRIDE;
+            if (n2) twiddle<R>(x, __ldg(a.itw + (n2 << S)));
+            dft_inv<R>(x);
+            if (LV == 0) emit(x, u, stage, a, b0, nb, wfirst);
+            else {
+#pragma unroll
+                for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+            }
+        }
+        __syncthreads();
+    }
+};
+
+template <int LOGP, int LV, bool PACK>
+__device__ __forceinline__ void run_levels(uint32_t *data, uint32_t *stage, const FusedArgs &a,
+                                           uint64_t b0, int nb, uint64_t wfirst) {
+    using L = Level<LOGP, LV, PACK>;
+    L::fwd(data, stage, a, b0, nb, wfirst);
+    if constexpr (!L::LAST) {
+        run_levels<LOGP, LV + 1, PACK>(data, stage, a, b0, nb, wfirst);
+        L::inv(data, stage, a, b0, nb, wfirst);
+    }
+}
+
+template <int LOGP, bool PACK>
+__global__ void __launch_bounds__(threads_of(LOGP)) ntt_fused_kernel(FusedArgs a) {
+    extern __shared__ uint32_t smem[];
+    constexpr int PP = 1 << LOGP;
+    uint32_t *data = smem;
+    uint32_t *stage = smem + PP + PP / 32;
+    const int per = PACK ? 2 : 1;
+    const uint64_t b0 = (uint64_t)blockIdx.x * per;
+    const int nb = (int)min((uint64_t)per, a.n_blocks - b0);
+    const uint64_t g_lo = b0 * a.m, g_hi = (b0 + nb) * a.m;  // [g_lo, g_hi)
+    const uint64_t wfirst = g_lo >> 5, wlast = (g_hi - 1) >> 5;
+    for (uint32_t i = threadIdx.x; i < a.stage_words; i += blockDim.x) stage[i] = 0;
+    __syncthreads();
+    run_levels<LOGP, 0, PACK>(data, stage, a, b0, nb, wfirst);
+    for (uint64_t w = wfirst + threadIdx.x; w <= wlast; w += blockDim.x) {
+        bool excl = (w << 5) >= g_lo && ((w << 5) + 31) < g_hi;
+        emit_word(a.out, w, stage[w - wfirst], excl);
+    }
+}
+
+// ---- plan preparation kernels ----------------------------------------------
+__device__ uint32_t powmod_d(uint64_t b, uint64_t e) {
+    uint64_t r = 1;
+    b %= P;
+    while (e) {
+        if (e & 1) r = r * b % P;
+        b = b * b % P;
+        e >>= 1;
+    }
+    return (uint32_t)r;
+}
+
+// tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P.
+__global__ void twiddle_table_kernel(uint32_t *tw, uint32_t *itw, uint32_t Pn, uint32_t w, uint32_t iw) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < Pn; e += gridDim.x * blockDim.x) {
+        tw[e] = (uint32_t)(((uint64_t)powmod_d(w, e) << 32) % P);
+        itw[e] = (uint32_t)(((uint64_t)powmod_d(iw, e) << 32) % P);
+    }
+}
+
+// Seed spectrum, fused single-CTA version (P <= 2^15): forward passes only.
+template <int LOGP, int LV>
+__device__ __forceinline__ void seed_levels(uint32_t *data, const uint32_t *seed_words, uint32_t L,
+                                            const uint32_t *tw, uint32_t *shat, uint32_t scaleM) {
+    constexpr int R = radix_of(LOGP, LV), S = prefix_of(LOGP, LV), N1 = 1 << R;
+    constexpr int STRIDE = (1 << LOGP) >> (S + R), NSEG = (1 << LOGP) >> S, NSUB = (1 << LOGP) >> R;
+    constexpr bool LAST = (LV == np_of(LOGP) - 1);
+    for (int u = threadIdx.x; u < NSUB; u += blockDim.x) {
+        uint32_t x[N1];
+        const int seg = u / STRIDE, n2 = u % STRIDE;
+#pragma unroll
+        for (int q = 0; q < N1; ++q) {
+            int idx = seg * NSEG + q * STRIDE + n2;
+            if (LV == 0) {
+                uint32_t v = 0;
+                if ((uint32_t)idx < L) v = (seed_words[idx >> 5] >> (31 - (idx & 31))) & 1u;
+                x[q] = v;
+            } else {
+                x[q] = data[pidx(idx)];
+            }
+        }
+        dft_fwd<R>(x);
+        if (!LAST) {
+            if (n2) twiddle<R>(x, tw[n2 << S]);
+#pragma unroll
+            for (int q = 0; q < N1; ++q) data[pidx(seg * NSEG + q * STRIDE + n2)] = x[q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < N1; ++q) shat[u * N1 + q] = mont(x[q], scaleM);  // * P^-1 * 2^32
+        }
+    }
+    __syncthreads();
+    if constexpr (!LAST) seed_levels<LOGP, LV + 1>(data, seed_words, L, tw, shat, scaleM);
+}
+
+template <int LOGP>
+__global__ void __launch_bounds__(threads_of(LOGP)) seed_fused_kernel(const uint32_t *seed_words, uint32_t L,
+                                                                      const uint32_t *tw, uint32_t *shat,
+                                                                      uint32_t scaleM) {
+    extern __shared__ uint32_t smem[];
+    seed_levels<LOGP, 0>(smem, seed_words, L, tw, shat, scaleM);
+}
+
+// Seed bytes (MSB-first) -> logical big-endian words (bit k at 31-(k&31)), zero padded.
+__global__ void seed_words_kernel(const uint8_t *seed, uint64_t L, uint32_t *words, uint64_t nwords) {
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int k = 0; k < 4; ++k) {
+            uint64_t byte = w * 4 + k;
+            uint32_t bv = (byte * 8 < L) ? seed[byte] : 0u;
+            v |= bv << (24 - 8 * k);
+        }
+        uint64_t lo = w * 32;  // mask bits >= L
+        if (lo + 32 > L) v &= (L > lo) ? (0xFFFFFFFFu << (32 - (L - lo))) : 0u;
+        words[w] = v;
+    }
+}
+
+// ---- host side -------------------------------------------------------------
+int choose_pack_shift(uint64_t n, int logP) {
+    (void)logP;
+    int shift = 0;
+    while ((1ull << shift) <= n) ++shift;  // 2^shift > n >= any window sum
+    if ((unsigned __int128)n * ((1ull << shift) + 1) >= P) return 0;
+    return shift;
+}
+
+template <int LOGP, bool PACK>
+static qrng_status launch_fused(const FusedArgs &a, cudaStream_t s) {
+    const int per = PACK ? 2 : 1;
+    const size_t smem = ((size_t)(1 << LOGP) + (1 << LOGP) / 32 + a.stage_words) * 4;
+    static bool attr = false;
+    if (!attr) {
+        QRNG_CUDA_TRY(cudaFuncSetAttribute(ntt_fused_kernel<LOGP, PACK>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    uint64_t grid = (a.n_blocks + per - 1) / per;
+    KernelTimer t(s);
+    ntt_fused_kernel<LOGP, PACK><<<(unsigned)grid, threads_of(LOGP), smem, s>>>(a);
+    t.stop();
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+template <int LOGP>
+static qrng_status launch_seed(const uint32_t *seed_words, uint32_t L, const uint32_t *tw,
+                               uint32_t *shat, uint32_t scaleM, cudaStream_t s) {
+    const size_t smem = ((size_t)(1 << LOGP) + (1 << LOGP) / 32) * 4;
+    static bool attr = false;
+    if (!attr) {
+        QRNG_CUDA_TRY(cudaFuncSetAttribute(seed_fused_kernel<LOGP>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    count_launch();
+    seed_fused_kernel<LOGP><<<1, threads_of(LOGP), smem, s>>>(seed_words, L, tw, shat, scaleM);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+#define QRNG_LOGP_CASES(X) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)
+
+static uint64_t powmod_h(uint64_t b, uint64_t e) { return powmod_c(b, e); }
+
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s) {
+    const uint64_t L = n + m - 1;
+    int logP = 0;
+    while ((1ull << logP) < L) ++logP;
+    if (logP < 5) logP = 5;
+    if (logP > kMaxLogP) {
+        set_error("NTT path: L = %llu exceeds 2^23", (unsigned long long)L);
+        return QRNG_E_UNSUPPORTED;
+    }
+    if (logP > kMaxFusedLogP) {
+        set_error("NTT path: P = 2^%d not implemented yet (fused kernel limit 2^15)", logP);
+        return QRNG_E_UNSUPPORTED;
+    }
+    pl.logP = logP;
+    pl.pack_shift = choose_pack_shift(n, logP);
+    const uint64_t Pn = 1ull << logP;
+    const uint64_t nwords = (L + 31) / 32 + 1;
+    uint32_t *seed_words = nullptr;
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.shat, Pn * 4, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.tw, Pn * 4, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.itw, Pn * 4, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(&seed_words, nwords * 4, s));
+    const uint64_t w = powmod_h(3, (P - 1) >> logP), iw = powmod_h(w, P - 2);
+    count_launch();
+    twiddle_table_kernel<<<(unsigned)((Pn + 255) / 256 < 1024 ? (Pn + 255) / 256 : 1024), 256, 0, s>>>(
+        pl.tw, pl.itw, (uint32_t)Pn, (uint32_t)w, (uint32_t)iw);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    count_launch();
+    seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_words, nwords);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    // scale = P^-1 * 2^64 mod p, so mont(v, scale) = v * P^-1 * 2^32 (Montgomery form for the pointwise product)
+    const uint64_t pinvP = powmod_h(Pn % P, P - 2);
+    const uint64_t r2 = (uint64_t)(((unsigned __int128)1 << 64) % P);
+    const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * r2 % P);
+    qrng_status st = QRNG_E_UNSUPPORTED;
+    switch (logP) {
+#define X(LP) case LP: st = launch_seed<LP>(seed_words, (uint32_t)L, pl.tw, pl.shat, scaleM, s); break;
+        QRNG_LOGP_CASES(X)
+#undef X
+        default: break;
+    }
+    cudaFreeAsync(seed_words, s);
+    return st;
+}
+
+void plan_free(Plan &pl) {
+    if (pl.shat) cudaFree(pl.shat);
+    if (pl.tw) cudaFree(pl.tw);
+    if (pl.itw) cudaFree(pl.itw);
+    if (pl.work) cudaFree(pl.work);
+    pl = Plan{};
+}
+
+qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                    const OutStream &out, cudaStream_t s) {
+    FusedArgs a;
+    a.raw = reinterpret_cast<const uint32_t *>(d_raw);
+    a.n_blocks = n_blocks;
+    a.n = (uint32_t)n;
+    a.m = (uint32_t)m;
+    a.shift = pl.pack_shift;
+    a.shat = pl.shat;
+    a.tw = pl.tw;
+    a.itw = pl.itw;
+    a.out = out;
+    const int per = pl.pack_shift ? 2 : 1;
+    a.stage_words = (uint32_t)((per * m + 31) / 32 + 2);
+    switch (pl.logP) {
+#define X(LP)                                                               \
+    case LP:                                                                \
+        return pl.pack_shift ? launch_fused<LP, true>(a, s) : launch_fused<LP, false>(a, s);
+        QRNG_LOGP_CASES(X)
+#undef X
+        default:
+            set_error("NTT path: unsupported P = 2^%d", pl.logP);
+            return QRNG_E_UNSUPPORTED;
+    }
+}
+
+}  // namespace ntt
+}  // namespace qrng

@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+bit-exact (integer/bit work: zero tolerance), on seeded synthetic inputs.
+
+Run on a B200:  python -m pytest tests -m gpu
+"""
+import numpy as np
+import pytest
+
+import qrng_synth as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2011_04130_b200 as q
+    from paper_2011_04130_b200 import build
+    build.build()
+    q.load_library()
+    yield q
+    q.set_debug_path(q.PATH_AUTO)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint8)).cuda()
+
+
+def gpu_extract(q, raw, B, n, m, seed, path=None):
+    if path is not None:
+        q.set_debug_path(path)
+    try:
+        out = q.toeplitz_extract(dev(raw), B, n, m, dev(seed))
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+    finally:
+        if path is not None:
+            q.set_debug_path(q.PATH_AUTO)
+
+
+def assert_same(got, ref, m):
+    if not np.array_equal(got, ref):
+        gb, rb = np.unpackbits(got), np.unpackbits(ref)
+        bad = np.nonzero(gb != rb)[0]
+        raise AssertionError(f"{bad.size} bits differ; first at bit {bad[0]} "
+                             f"(block {bad[0] // m}, i {bad[0] % m})")
+
+
+PATHS = ["ntt"]
+
+
+def path_id(q, name):
+    return {"ntt": q.PATH_NTT, "gemm": q.PATH_GEMM}[name]
+
+
+SMALL_CASES = [
+    (32, 1, 1), (32, 31, 3), (64, 7, 5), (96, 50, 7), (128, 127, 2), (256, 200, 9),
+    (512, 300, 33), (1024, 716, 17), (1024, 1, 4), (2048, 1433, 10), (4096, 2867, 5),
+    (8192, 5734, 7), (16384, 11468, 3), (16384, 16383, 2), (12288, 8000, 5),
+]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("n,m,B", SMALL_CASES)
+def test_random_small(q, oracle_mod, path, n, m, B):
+    key = n * 7919 + m
+    raw = S.random_bytes(key, B * n // 8)
+    seed = S.random_bytes(key, (n + m - 1 + 7) // 8, tag=2)
+    ref = oracle_mod.extract(raw, B, n, m, seed)
+    assert_same(gpu_extract(q, raw, B, n, m, seed, path_id(q, path)), ref, m)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("n,m,B", [(1024, 716, 3), (8192, 5734, 3), (16384, 11468, 2), (96, 95, 5)])
+def test_all_ones_max_window(q, oracle_mod, path, n, m, B):
+    """Every window sum equals n (the maximum): exercises p > n and the
+    two-blocks-per-transform separation at its worst case."""
+    raw = np.full(B * n // 8, 0xFF, np.uint8)
+    seed = np.full((n + m - 1 + 7) // 8, 0xFF, np.uint8)
+    ref = oracle_mod.extract(raw, B, n, m, seed)
+    assert_same(gpu_extract(q, raw, B, n, m, seed, path_id(q, path)), ref, m)
+    alt = np.full(B * n // 8, 0xAA, np.uint8)
+    assert_same(gpu_extract(q, alt, B, n, m, seed, path_id(q, path)),
+                oracle_mod.extract(alt, B, n, m, seed), m)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_config_full(q, oracle_mod, cfg):
+    """BASELINE configs 1 and 2, every block, in the launch configuration bench.py times."""
+    w = S.CONFIGS[cfg]
+    raw, seed = S.workload_inputs(w)
+    ref = oracle_mod.extract(raw, w.n_blocks, w.n, w.m, seed)
+    assert_same(gpu_extract(q, raw, w.n_blocks, w.n, w.m, seed), ref, w.m)
+
+
+def test_plan_reuse_and_block_slices(q, oracle_mod):
+    w = S.CONFIGS[1]
+    raw, seed = S.workload_inputs(w)
+    ref = oracle_mod.extract(raw, w.n_blocks, w.n, w.m, seed)
+    with q.Plan(w.n, w.m, dev(seed)) as plan:
+        assert plan.path in (q.PATH_NTT, q.PATH_GEMM)
+        draw = dev(raw)
+        for _ in range(2):
+            out = plan.extract(draw, w.n_blocks).cpu().numpy()
+            assert_same(out, ref, w.m)
+        # a shard of 32 blocks starting at block 64 is word aligned (32*m % 32 == 0)
+        sub = plan.extract(draw[64 * w.n // 8:96 * w.n // 8], 32).cpu().numpy()
+        assert np.array_equal(sub, ref[64 * w.m // 8:96 * w.m // 8])
+
+
+def test_host_buffers_api(q, oracle_mod):
+    w = S.CONFIGS[1]
+    raw, seed = S.workload_inputs(w, 0, 40)
+    out = np.zeros(q.out_bytes(40, w.m), np.uint8)
+    q.toeplitz_extract_host(raw, 40, w.n, w.m, seed, out)
+    assert_same(out, oracle_mod.extract(raw, 40, w.n, w.m, seed), w.m)
+
+
+def test_partial_tail_word_and_pad_bits(q, oracle_mod):
+    n, m, B = 64, 13, 3  # 39 output bits: 5 bytes, final 32-bit word partial
+    raw = S.random_bytes(5, B * n // 8)
+    seed = S.random_bytes(5, (n + m - 1 + 7) // 8, tag=3)
+    ref = oracle_mod.extract(raw, B, n, m, seed)
+    d_out = torch.full((16,), 0xEE, dtype=torch.uint8, device="cuda")
+    q.toeplitz_extract(dev(raw), B, n, m, dev(seed), out=d_out[:5])
+    got = d_out.cpu().numpy()
+    assert np.array_equal(got[:5], ref)
+    assert (got[5:] == 0xEE).all()  # nothing written past ceil(B*m/8)
+
+
+def test_rejects_misaligned_and_overlap(q):
+    buf = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+    seed = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(q.QrngError) as ei:
+        q.toeplitz_extract(buf[1:129], 1, 1024, 716, seed, out=buf[1024:1200])
+    assert ei.value.status == q.QRNG_E_INVALID
+    with pytest.raises(q.QrngError) as ei:
+        q.toeplitz_extract(buf[:128], 1, 1024, 716, seed, out=buf[64:256])
+    assert ei.value.status == q.QRNG_E_INVALID
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_minentropy_matches_oracle(q, cfg):
+    from oracle import entropy as E
+    import oracle
+    w = S.CONFIGS[cfg]
+    raw, _ = S.workload_inputs(w)
+    rep = q.minentropy(dev(raw), 8, w.n, 0)
+    assert np.array_equal(rep.counts, oracle.hist256(raw))
+    ref = E.report(raw, 8, w.n, 0)
+    for f in ("mu", "sigma", "h_min_hist", "h_min_ideal", "stat_dist", "delta_h_m", "h_min_mod"):
+        assert getattr(rep, f) == pytest.approx(getattr(ref, f), rel=1e-12, abs=1e-12), f
+    assert rep.m == ref.m
+
+
+def test_hist_sharded_accumulate(q):
+    import oracle
+    x = S.adc_samples(9, (1 << 20) + 13, 128, 12)
+    counts = torch.zeros(256, dtype=torch.int64, device="cuda")
+    half = x.size // 2
+    q.hist256_async(dev(x[:half]), counts)
+    q.hist256_async(dev(x[half:]), counts)
+    assert np.array_equal(counts.cpu().numpy().astype(np.uint64), oracle.hist256(x))
