@@ -159,6 +159,12 @@ QRNG_API void        qrng_debug_set_path(int path);
  * synchronises those events, returns the summed device time in ms, stores the
  * number of timed launches in *launches (if not NULL) and clears the record. */
 QRNG_API uint64_t    qrng_debug_launch_count(void);
+/* TEST ONLY: one-CTA probe of the tcgen05 operand layouts used by the GEMM
+ * path: D (128 x N int32, row-major, device) = A (128 x K uint8 0/1 or any
+ * u8, row-major, device) times B^T with the Hankel B[i][k] = h[i + k]
+ * (h: N+K bytes, device).  N in [16, 256] multiple of 16, K multiple of 128. */
+QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D,
+                                           int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);
 

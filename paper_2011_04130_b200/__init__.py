@@ -31,7 +31,7 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_toeplitz_extract", "qrng_toeplitz_extract_async", "qrng_toeplitz_extract_host",
            "qrng_plan_create", "qrng_plan_extract", "qrng_plan_destroy", "qrng_plan_path",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
-           "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms"]
+           "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe"]
 
 
 class QrngError(RuntimeError):
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_version": ([], ctypes.c_char_p),
         "qrng_debug_set_path": ([i32], None),
         "qrng_debug_launch_count": ([], u64),
+        "qrng_debug_umma_probe": ([vp, vp, vp, i32, i32, vp], i32),
         "qrng_debug_kernel_timing": ([i32], None),
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
     }
@@ -162,6 +163,16 @@ def kernel_time_ms() -> tuple[float, int]:
     n = ctypes.c_uint64()
     ms = load_library().qrng_debug_kernel_time_ms(ctypes.byref(n))
     return float(ms), int(n.value)
+
+
+def umma_probe(A, h, N: int, K: int, stream=None):
+    """TEST ONLY: D = A @ B^T on the tcgen05 path, B[i][k] = h[i + k] (see qrng.h)."""
+    import torch
+    _need_cuda_u8(A, "A")
+    _need_cuda_u8(h, "h")
+    D = torch.empty((128, N), dtype=torch.int32, device=A.device)
+    _check(load_library().qrng_debug_umma_probe(_ptr(A), _ptr(h), _ptr(D), N, K, _stream_handle(stream)))
+    return D
 
 
 def toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=None):

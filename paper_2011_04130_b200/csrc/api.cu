@@ -43,7 +43,7 @@ void KernelTimer::stop() {
 }
 
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
-static uint64_t g_gemm_max_n = 0;
+static uint64_t g_gemm_max_n = 1ull << 16;
 static int g_debug_path = QRNG_PATH_AUTO;
 
 // One-time device check: sm_100 required (no CPU fallback), stream-ordered
@@ -128,6 +128,13 @@ const char *qrng_last_error(void) { return g_err; }
 const char *qrng_version(void) { return "qrng-b200 0.1 sm_100a"; }
 void qrng_debug_set_path(int path) { g_debug_path = path; }
 uint64_t qrng_debug_launch_count(void) { return g_launches.load(); }
+qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D, int N, int K,
+                                  cudaStream_t stream) {
+    if (!d_A || !d_h || !d_D) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    return gemm::probe(d_A, d_h, d_D, N, K, stream);
+}
 void qrng_debug_kernel_timing(int enable) { g_timing.store(enable ? 1 : 0); }
 double qrng_debug_kernel_time_ms(uint64_t *launches) {
     std::lock_guard<std::mutex> lk(g_tmu);

@@ -1,15 +1,450 @@
 // gemm_tc.cu -- batched dense Toeplitz product on tcgen05 int8 tensor cores.
-// (placeholder: the tcgen05 kernel lands in the next milestone)
+//
+// Method: the direct O(mn) product k = T r of PAPER.md:189-197 (Listing 1 at
+// PAPER.md:388-400) for ALL blocks at once.  Every block shares the seed, so
+// the blocks form the columns of one matrix and the extraction is one dense
+// contraction  D[b][i] = sum_j T[i][j] x_b[j]  (exact int32, max value n),
+// followed by parity: y_i = D[b][i] & 1 (C1).
+//
+// B200 design:
+//  * Rewritten as a Hankel product with the K index reversed, j'' = n-1-j:
+//        T[i][j] = s[i + j'']            A[b][j''] = x_b[n-1-j'']
+//    so the B operand (rows i, K j'') is a sliding window of the seed with
+//    positive unit strides in both directions.
+//  * B operand (N = 192 output rows) in shared memory, generated on chip from
+//    the packed seed, never read from HBM/L2: in the K-major no-swizzle
+//    canonical layout a core matrix (8 rows x 16 K-bytes) at (row group g,
+//    K chunk q) only depends on g + 2q, so ONE linear array of core matrices
+//    with SBO = 128 B (row-group stride) and LBO = 256 B (K-chunk stride)
+//    describes every B tile; the MMA simply reads overlapping windows of it.
+//  * A operand (M = 128 blocks) in TMEM: "transform" warps load 16 packed
+//    bytes per block and K-stage, expand bits to int8 0/1 in registers and
+//    tcgen05.st them (32 columns = 128 K per stage, 4-stage ring).
+//  * tcgen05.mma.cta_group::1.kind::i8 M128 N192 K32, S32 accumulators in
+//    TMEM, two accumulators so the epilogue overlaps the next tile.
+//  * Epilogue warps tcgen05.ld the accumulators, take parity, pack 32 outputs
+//    per word MSB-first and store them at bit b*m + i (C4).
+//  * Persistent grid (one CTA per SM), warp-specialised, mbarrier pipelines.
 #include "qrng_internal.cuh"
 
 namespace qrng {
 namespace gemm {
 
-bool supported(uint64_t, uint64_t) { return false; }
+constexpr int BM = 128;        // blocks per tile (TMEM lanes)
+constexpr int BN = 192;        // output rows per tile
+constexpr int KS = 128;        // K per A stage
+constexpr int A_STAGES = 4;
+constexpr int KC = 1024;       // K per B chunk
+constexpr int SPC = KC / KS;   // A stages per B chunk
+constexpr int B_SLOTS = 3;
+constexpr int CM_PER_CHUNK = KC / 8 + BN / 8 - 1;  // core matrices per chunk
+constexpr int CHUNK_BYTES = CM_PER_CHUNK * 128;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 128)
+constexpr uint32_t ACC_COL0 = 128;  // accumulators: [128, 320) and [320, 512)
+constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, W_EPI0 = 8;
+constexpr int NTHREADS = 12 * 32;
+constexpr int MAX_N = 1 << 16;
 
-qrng_status plan_init(Plan &, uint64_t, uint64_t, const uint8_t *, cudaStream_t) {
-    set_error("GEMM path not built yet");
-    return QRNG_E_UNSUPPORTED;
+// ---- PTX helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_alloc(uint32_t *slot, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, int8 x int8 -> s32, M128, N from idesc, K32
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+#define QRNG_R8(i) "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3]), "r"(v[i + 4]), "r"(v[i + 5]), "r"(v[i + 6]), "r"(v[i + 7])
+#define QRNG_W8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+
+// Each thread writes 32 consecutive 32-bit columns of its own TMEM lane.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        QRNG_R8(0), QRNG_R8(8), QRNG_R8(16), QRNG_R8(24)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : QRNG_W8(0), QRNG_W8(8), QRNG_W8(16), QRNG_W8(24)
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, K-major, no swizzle (canonical layout:
+// 8x16-byte core matrices; LBO = K-direction stride, SBO = 8-row-group stride).
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;  // descriptor version for sm_100
+    return d;         // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+
+// kind::i8 instruction descriptor: S32 accumulate, U8 x U8, both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// 4 bits (LSB = first element) -> 4 int8 0/1 bytes (little endian).
+__device__ __forceinline__ uint32_t expand4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+// ---- the extraction kernel -----------------------------------------------------
+struct Args {
+    const uint32_t *raw;       // packed raw stream (MSB-first bytes) as words
+    uint64_t n_blocks;
+    uint32_t n, m;
+    uint32_t kst;              // K stages per tile = n / 128
+    uint32_t nchunks;          // B chunks per tile = ceil(kst / SPC)
+    uint32_t n_mtiles, n_ntiles;
+    const uint32_t *seed_words;  // logical big-endian seed words, zero padded
+    uint32_t seed_words_n;
+    OutStream out;
+};
+
+__device__ __forceinline__ void xform_stage(uint32_t taddr, uint4 w) {
+    // elements c = 32*g4 + c' of this stage come from logical word q = 3 - g4, bit c'
+    uint32_t L[4] = {bswap32(w.x), bswap32(w.y), bswap32(w.z), bswap32(w.w)};
+    uint32_t v[32];
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[8 * g4 + e] = expand4((L[3 - g4] >> (4 * e)) & 0xFu);
+    tmem_st32(taddr, v);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *chunks = smem;
+    uint32_t *seed_s = reinterpret_cast<uint32_t *>(smem + B_SLOTS * CHUNK_BYTES);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((a.seed_words_n + 3) & ~3u));
+    uint64_t *a_full = bars, *a_empty = bars + 4, *b_full = bars + 8, *b_empty = bars + 11;
+    uint64_t *acc_full = bars + 14, *acc_empty = bars + 16;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 18);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t i = threadIdx.x; i < a.seed_words_n; i += NTHREADS) seed_s[i] = a.seed_words[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], 4); mbar_init(&a_empty[s], 1); }
+        for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], N_BGEN); mbar_init(&b_empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W_MMA) tmem_alloc(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t ntiles = a.n_mtiles * a.n_ntiles;
+
+    if (warp == W_MMA) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_i8(BM, BN);
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const uint32_t acc = it & 1, accph = (it >> 1) & 1;
+                mbar_wait(&acc_empty[acc], accph ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + ACC_COL0 + acc * BN;
+                for (uint32_t ks = 0; ks < a.kst; ++ks) {
+                    const uint32_t kin = ks % SPC;
+                    if (kin == 0) {
+                        mbar_wait(&b_full[bs], bph);
+                        tc_fence_after();
+                    }
+                    mbar_wait(&a_full[as], aph);
+                    tc_fence_after();
+                    const uint32_t a_tmem = tmem + A_COL0 + as * 32;
+                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < 4; ++kk) {
+                        const uint32_t koff = kin * KS + kk * 32;  // K offset inside the chunk
+                        const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
+                        mma_i8_ts(d_tmem, a_tmem + kk * 8, bdesc, idesc, (ks | kk) != 0);
+                    }
+                    mma_commit(&a_empty[as]);
+                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    if (kin == SPC - 1 || ks == a.kst - 1) {
+                        mma_commit(&b_empty[bs]);
+                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                    }
+                }
+                mma_commit(&acc_full[acc]);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= W_BGEN0 && warp < W_BGEN0 + N_BGEN) {
+        // B generators: core matrix tau of chunk (n0, k0): row r' holds seed bits
+        // s[n0 + k0 + 8 tau + r' + c], c = 0..15, as int8 0/1.
+        const int tb = (warp - W_BGEN0) * 32 + lane;
+        uint32_t bs = 0, bph = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const uint32_t n0 = (t / a.n_mtiles) * BN;
+            for (uint32_t c = 0; c < a.nchunks; ++c) {
+                const uint32_t base = n0 + c * KC;
+                mbar_wait(&b_empty[bs], bph ^ 1);
+                uint8_t *cb = chunks + bs * CHUNK_BYTES;
+                for (int r = tb; r < CM_PER_CHUNK * 8; r += N_BGEN * 32) {
+                    const uint32_t p = base + 8 * (r >> 3) + (r & 7);
+                    const uint32_t v = __funnelshift_l(seed_s[(p >> 5) + 1], seed_s[p >> 5], p & 31);
+                    const uint32_t rv = __brev(v);  // element c at bit c
+                    uint4 o;
+                    o.x = expand4(rv & 0xFu);
+                    o.y = expand4((rv >> 4) & 0xFu);
+                    o.z = expand4((rv >> 8) & 0xFu);
+                    o.w = expand4((rv >> 12) & 0xFu);
+                    *reinterpret_cast<uint4 *>(cb + (r >> 3) * 128 + (r & 7) * 16) = o;
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&b_full[bs]);
+                if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+            }
+        }
+    } else if (warp >= W_XFORM0 && warp < W_XFORM0 + 4) {
+        // A transform: lane row = block, 128 K per stage, 4-stage register prefetch.
+        const uint32_t row = (warp - W_XFORM0) * 32 + lane;
+        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16);
+        const uint32_t wpb = a.n >> 5;  // words per block
+        uint32_t as = 0, aph = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const uint64_t b = (uint64_t)(t % a.n_mtiles) * BM + row;
+            const bool valid = b < a.n_blocks;
+            const uint4 *blk = reinterpret_cast<const uint4 *>(a.raw + (valid ? b : 0) * wpb);
+            // stage ks covers bits j in [n - 128(ks+1), n - 128 ks): uint4 index (n/128 - 1 - ks)
+            const uint32_t last = (a.n >> 7) - 1;
+            uint4 pf[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                pf[j] = (valid && (uint32_t)j < a.kst) ? __ldg(blk + (last - j)) : make_uint4(0, 0, 0, 0);
+            for (uint32_t ks0 = 0; ks0 < a.kst; ks0 += 4) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t ks = ks0 + j;
+                    if (ks < a.kst) {
+                        const uint4 cur = pf[j];
+                        if (valid && ks + 4 < a.kst) pf[j] = __ldg(blk + (last - ks - 4));
+                        mbar_wait(&a_empty[as], aph ^ 1);
+                        tc_fence_after();
+                        xform_stage(lane_addr + A_COL0 + as * 32, cur);
+                        tmem_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&a_full[as]);
+                        if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    }
+                }
+            }
+        }
+    } else {
+        // Epilogue: parity of the S32 accumulators, 32 outputs per MSB-first word.
+        const uint32_t row = (warp - W_EPI0) * 32 + lane;
+        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16);
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const uint32_t acc = it & 1, accph = (it >> 1) & 1;
+            mbar_wait(&acc_full[acc], accph);
+            tc_fence_after();
+            uint32_t words[BN / 32];
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(lane_addr + ACC_COL0 + acc * BN + 32 * c, v);
+                tmem_wait_ld();
+                uint32_t w = 0;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) w = (w << 1) | (v[k] & 1u);
+                words[c] = w;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            const uint64_t b = (uint64_t)(t % a.n_mtiles) * BM + row;
+            if (b >= a.n_blocks) continue;
+            const uint32_t n0 = (t / a.n_mtiles) * BN;
+            const uint32_t nvalid = min((uint32_t)BN, a.m - n0);
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) {
+                const int vb = (int)nvalid - 32 * c;  // valid bits in word c
+                if (vb <= 0) words[c] = 0;
+                else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
+            }
+            const uint64_t G_lo = b * a.m + n0, G_hi = G_lo + nvalid;
+            const uint32_t off = (uint32_t)(G_lo & 31);
+            const uint64_t W0 = G_lo >> 5;
+            uint32_t prev = 0;
+#pragma unroll
+            for (int c = 0; c <= BN / 32; ++c) {
+                const uint32_t cur = (c < BN / 32) ? words[c] : 0u;
+                const uint32_t ow = off ? ((prev << (32 - off)) | (cur >> off)) : cur;
+                prev = cur;
+                const uint64_t W = W0 + c;
+                if (W * 32 >= G_hi) break;
+                const bool excl = (W * 32 >= G_lo) && (W * 32 + 32 <= G_hi);
+                emit_word(a.out, W, ow, excl);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == W_MMA) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+// ---- layout probe (test only): D = A * B^T with B[i][k] = h[i + k] ----------------
+// One CTA, 128 threads.  A: 128 x K int8 row-major (global); h: bytes; D: 128 x N s32.
+__global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, const uint8_t *h, int32_t *D, int N,
+                                                           int K) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(smem + 8);
+    uint8_t *cm = smem + 1024;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int ncm = K / 8 + N / 8 - 1;
+    for (int r = tid; r < ncm * 8; r += 128) {
+        int tau = r >> 3, rr = r & 7;
+        for (int c = 0; c < 16; ++c) cm[tau * 128 + rr * 16 + c] = h[8 * tau + rr + c];
+    }
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    // A row tid -> TMEM lane tid, columns [0, K/4)
+    for (int c0 = 0; c0 < K / 4; c0 += 32) {
+        uint32_t v[32];
+        for (int c = 0; c < 32; ++c) {
+            uint32_t w = 0;
+            for (int e = 0; e < 4; ++e) w |= (uint32_t)A[tid * K + 4 * (c0 + c) + e] << (8 * e);
+            v[c] = w;
+        }
+        tmem_st32(lane_addr + c0, v);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+        const uint32_t idesc = idesc_i8(128, N);
+        for (int k = 0; k < K; k += 32) {
+            const uint64_t bdesc = desc_kmajor(smem_u32(cm) + (k / 8) * 128, 256, 128);
+            mma_i8_ts(tmem + 256, tmem + k / 4, bdesc, idesc, k != 0);
+        }
+        mma_commit(bar);
+    }
+    __syncwarp();
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(lane_addr + 256 + c0, v);
+        tmem_wait_ld();
+        for (int c = 0; c < 32 && c0 + c < N; ++c) D[tid * N + c0 + c] = (int32_t)v[c];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ---- host ------------------------------------------------------------------------
+bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n; }
+
+static uint32_t seed_words_needed(uint64_t n, uint64_t m) {
+    const uint64_t n_ntiles = (m + BN - 1) / BN, kst = n / KS, nchunks = (kst + SPC - 1) / SPC;
+    const uint64_t pmax = (n_ntiles - 1) * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
+    return (uint32_t)(pmax / 32 + 2);
+}
+
+static size_t smem_bytes(uint32_t seed_words_n) {
+    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + 18 * 8 + 16;
+}
+
+// seed bytes (MSB-first) -> logical big-endian words, zero past L
+__global__ void seed_words_kernel(const uint8_t *seed, uint64_t L, uint32_t *words, uint64_t nwords) {
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t byte = w * 4 + k;
+            const uint32_t bv = (byte * 8 < L) ? seed[byte] : 0u;
+            v |= bv << (24 - 8 * k);
+        }
+        const uint64_t lo = w * 32;
+        if (lo + 32 > L) v &= (L > lo) ? (0xFFFFFFFFu << (32 - (L - lo))) : 0u;
+        words[w] = v;
+    }
+}
+
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s) {
+    if (!supported(n, m)) {
+        set_error("GEMM path: unsupported n=%llu m=%llu", (unsigned long long)n, (unsigned long long)m);
+        return QRNG_E_UNSUPPORTED;
+    }
+    pl.seed_words_n = seed_words_needed(n, m);
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.seed_words, pl.seed_words_n * 4, s));
+    count_launch();
+    seed_words_kernel<<<(unsigned)((pl.seed_words_n + 255) / 256), 256, 0, s>>>(d_seed, n + m - 1, pl.seed_words,
+                                                                              pl.seed_words_n);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
 }
 
 void plan_free(Plan &pl) {
@@ -17,10 +452,54 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
-qrng_status extract(const Plan &, const uint8_t *, uint64_t, uint64_t, uint64_t, const OutStream &,
-                    cudaStream_t) {
-    set_error("GEMM path not built yet");
-    return QRNG_E_UNSUPPORTED;
+qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                    const OutStream &out, cudaStream_t s) {
+    Args a;
+    a.raw = reinterpret_cast<const uint32_t *>(d_raw);
+    a.n_blocks = n_blocks;
+    a.n = (uint32_t)n;
+    a.m = (uint32_t)m;
+    a.kst = (uint32_t)(n / KS);
+    a.nchunks = (a.kst + SPC - 1) / SPC;
+    a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
+    a.n_ntiles = (uint32_t)((m + BN - 1) / BN);
+    a.seed_words = pl.seed_words;
+    a.seed_words_n = (uint32_t)pl.seed_words_n;
+    a.out = out;
+    if ((uint64_t)a.n_mtiles * a.n_ntiles > 0xFFFFFFFFull) {
+        set_error("GEMM path: too many tiles");
+        return QRNG_E_UNSUPPORTED;
+    }
+    int dev = 0, sms = 148;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = smem_bytes(a.seed_words_n);
+    static bool attr = false;
+    if (!attr) {
+        QRNG_CUDA_TRY(cudaFuncSetAttribute(toeplitz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           227 * 1024));
+        attr = true;
+    }
+    const uint32_t ntiles = a.n_mtiles * a.n_ntiles;
+    const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
+    KernelTimer tm(s);
+    toeplitz_gemm_kernel<<<grid, NTHREADS, smem, s>>>(a);
+    tm.stop();
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s) {
+    if (N < 16 || N > 256 || N % 16 || K < 32 || K % 128) {
+        set_error("probe: N in [16,256] step 16, K multiple of 128");
+        return QRNG_E_INVALID;
+    }
+    const size_t smem = 1024 + (size_t)(K / 8 + N / 8 - 1) * 128;
+    QRNG_CUDA_TRY(cudaFuncSetAttribute(umma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    count_launch();
+    umma_probe_kernel<<<1, 128, smem, s>>>(A, h, D, N, K);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
 }
 
 }  // namespace gemm

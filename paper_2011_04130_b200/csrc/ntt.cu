@@ -30,8 +30,7 @@ namespace ntt {
 
 constexpr uint32_t P = kP;
 constexpr uint32_t P2 = 2u * kP;
-constexpr uint32_t PINV = 3296722945u;  // p^-1 mod 2^32
-constexpr uint32_t R1 = 301989884u;     // 2^32 mod p
+constexpr uint32_t NPINV = 998244351u;  // -p^-1 mod 2^32
 
 constexpr uint64_t powmod_c(uint64_t b, uint64_t e) {
     uint64_t r = 1;
@@ -69,10 +68,19 @@ __device__ __forceinline__ uint32_t shoup(uint32_t a, uint32_t w, uint32_t wp) {
     uint32_t q = __umulhi(a, wp);
     return a * w - q * P;  // a*w mod p in [0, 2p), any 32-bit a
 }
-__device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b) {  // a*b/2^32 mod p, a,b < 2p
-    uint32_t lo = a * b, hi = __umulhi(a, b);
-    uint32_t q = lo * PINV;
-    return hi - __umulhi(q, P) + P;  // in (0, 2p)
+// Montgomery product a*b/2^32 mod p for a, b < 2p, result in [0, 2p):
+// u = a*b + q*p with q = -(a*b)*p^-1 mod 2^32 is divisible by 2^32 and
+// u < 4p^2 + 2^32 p, so u >> 32 < 2p (4p < 2^32).  Three IMADs in SASS.
+__device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("{\n\t.reg .u64 t, u;\n\t.reg .u32 lo, q, d;\n\t"
+        "mul.wide.u32 t, %1, %2;\n\t"
+        "cvt.u32.u64 lo, t;\n\t"
+        "mul.lo.u32 q, lo, %3;\n\t"
+        "mad.wide.u32 u, q, %4, t;\n\t"
+        "mov.b64 {d, %0}, u;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "n"(NPINV), "n"(P));
+    return r;
 }
 
 __host__ __device__ constexpr int brev(int x, int bits) {
@@ -82,22 +90,23 @@ __host__ __device__ constexpr int brev(int x, int bits) {
 }
 
 // Radix-2^R DIF on registers: natural order in, bit-reversed order out.
+// Every loop has a compile-time trip count so the array stays in registers.
 template <int R>
 __device__ __forceinline__ void dft_fwd(uint32_t (&x)[1 << R]) {
     constexpr int N = 1 << R;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-        const int half = N >> (t + 1);
-        const int step = 64 / (2 * half);
 #pragma unroll
-        for (int i0 = 0; i0 < N; i0 += 2 * half)
-#pragma unroll
-            for (int e = 0; e < half; ++e) {
-                uint32_t a = x[i0 + e], b = x[i0 + e + half];
-                uint32_t v = a - b + P2;
-                x[i0 + e] = red2(a + b);
-                x[i0 + e + half] = (e == 0) ? red2(v) : shoup(v, c_roots.w[e * step], c_roots.wp[e * step]);
-            }
+        for (int k = 0; k < N / 2; ++k) {
+            const int half = N >> (t + 1);
+            const int e = k & (half - 1);
+            const int i = ((k / half) * 2 * half) + e;
+            const int step = 64 / (2 * half);
+            uint32_t a = x[i], b = x[i + half];
+            uint32_t v = a - b + P2;
+            x[i] = red2(a + b);
+            x[i + half] = (e == 0) ? red2(v) : shoup(v, c_roots.w[e * step], c_roots.wp[e * step]);
+        }
     }
 }
 
@@ -108,17 +117,17 @@ __device__ __forceinline__ void dft_inv(uint32_t (&x)[1 << R]) {
     constexpr int N = 1 << R;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-        const int half = 1 << t;
-        const int step = 64 / (2 * half);
 #pragma unroll
-        for (int i0 = 0; i0 < N; i0 += 2 * half)
-#pragma unroll
-            for (int e = 0; e < half; ++e) {
-                uint32_t a = x[i0 + e], b = x[i0 + e + half];
-                uint32_t tb = (e == 0) ? b : shoup(b, c_roots.iw[e * step], c_roots.iwp[e * step]);
-                x[i0 + e] = red2(a + tb);
-                x[i0 + e + half] = red2(a - tb + P2);
-            }
+        for (int k = 0; k < N / 2; ++k) {
+            const int half = 1 << t;
+            const int e = k & (half - 1);
+            const int i = ((k / half) * 2 * half) + e;
+            const int step = 64 / (2 * half);
+            uint32_t a = x[i], b = x[i + half];
+            uint32_t tb = (e == 0) ? b : shoup(b, c_roots.iw[e * step], c_roots.iwp[e * step]);
+            x[i] = red2(a + tb);
+            x[i + half] = red2(a - tb + P2);
+        }
     }
 }
 
@@ -184,7 +193,25 @@ struct Level {
 
     __device__ static __forceinline__ void load(uint32_t (&x)[N1], int u, uint32_t *data,
                                                 const FusedArgs &a, uint64_t b0, int nb) {
-        if (LV == 0) {  // level 0 has one segment: idx = q*STRIDE + u
+        if (LV == 0 && STRIDE >= 32) {
+            // the warp holds u = u0..u0+31 (u0 % 32 == 0): for each q it needs one
+            // 32-bit raw word (idx = q*STRIDE + u0 .. +31).  Lane q fetches word q.
+            const int lane = threadIdx.x & 31, u0 = u & ~31;
+            const uint32_t *blk = a.raw + b0 * (a.n >> 5);
+            uint32_t w1 = 0, w2 = 0;
+            const uint32_t myidx = (uint32_t)((lane % N1) * STRIDE + u0);
+            if (lane < N1 && myidx < a.n) {
+                w1 = bswap32(__ldg(blk + (myidx >> 5)));
+                if (PACK && nb > 1) w2 = bswap32(__ldg(blk + (a.n >> 5) + (myidx >> 5)));
+            }
+            const int sh = 31 - lane;
+#pragma unroll
+            for (int q = 0; q < N1; ++q) {
+                uint32_t v = (__shfl_sync(0xffffffffu, w1, q) >> sh) & 1u;
+                if (PACK) v |= ((__shfl_sync(0xffffffffu, w2, q) >> sh) & 1u) << a.shift;
+                x[q] = v;
+            }
+        } else if (LV == 0) {  // small P: idx = q*STRIDE + u
 #pragma unroll
             for (int q = 0; q < N1; ++q) {
                 uint32_t idx = (uint32_t)(q * STRIDE + u), v = 0;
@@ -201,9 +228,46 @@ struct Level {
     }
 
     // Final inverse output at level 0: element q is z_t, t = q*STRIDE + u.
+    __device__ static __forceinline__ void stage_or(uint32_t *stage, uint64_t wfirst, int64_t G, uint32_t bal) {
+        if (!bal) return;
+        const uint32_t V = __brev(bal);  // ballot bit L (output G+L) -> logical bit 31-L
+        const int64_t W0 = G >= 0 ? (G >> 5) : -((31 - G) >> 5);
+        const int o = (int)(G - W0 * 32);
+        const uint32_t hi = V >> o, lo = o ? (V << (32 - o)) : 0u;
+        if (hi) atomicOr(&stage[W0 - (int64_t)wfirst], hi);
+        if (lo) atomicOr(&stage[W0 + 1 - (int64_t)wfirst], lo);
+    }
+
     __device__ static __forceinline__ void emit(uint32_t (&x)[N1], int u, uint32_t *stage,
                                                 const FusedArgs &a, uint64_t b0, int nb,
                                                 uint64_t wfirst) {
+        if (STRIDE >= 32) {
+            // lanes hold 32 consecutive t for every q: one ballot per q gives a
+            // 32-bit output word; lane q keeps word q and ORs it into the stage.
+            const int lane = threadIdx.x & 31, u0 = u & ~31;
+            uint32_t mine1 = 0, mine2 = 0;
+#pragma unroll
+            for (int q = 0; q < N1; ++q) {
+                int64_t i = (int64_t)(q * STRIDE + u) - (int64_t)(a.n - 1);
+                bool valid = i >= 0 && i < (int64_t)a.m;
+                uint32_t z = x[q] >= P ? x[q] - P : x[q];  // canonical residue
+                uint32_t b1 = __ballot_sync(0xffffffffu, valid && (z & 1u));
+                if (lane == (q & 31)) mine1 = b1;
+                if (PACK) {
+                    uint32_t b2 = __ballot_sync(0xffffffffu, valid && ((z >> a.shift) & 1u));
+                    if (lane == (q & 31)) mine2 = b2;
+                }
+                if ((q & 31) == 31 || q == N1 - 1) {
+                    const int qb = q & ~31;
+                    if (lane <= (q & 31)) {
+                        int64_t i0 = (int64_t)((qb + lane) * STRIDE + u0) - (int64_t)(a.n - 1);
+                        stage_or(stage, wfirst, (int64_t)(b0 * a.m) + i0, mine1);
+                        if (PACK && nb > 1) stage_or(stage, wfirst, (int64_t)((b0 + 1) * a.m) + i0, mine2);
+                    }
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int q = 0; q < N1; ++q) {
             int64_t i = (int64_t)(q * STRIDE + u) - (int64_t)(a.n - 1);
@@ -285,7 +349,7 @@ __device__ __forceinline__ void run_levels(uint32_t *data, uint32_t *stage, cons
 }
 
 template <int LOGP, bool PACK>
-__global__ void __launch_bounds__(threads_of(LOGP)) ntt_fused_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(threads_of(LOGP), 1024 / threads_of(LOGP)) ntt_fused_kernel(FusedArgs a) {
     extern __shared__ uint32_t smem[];
     constexpr int PP = 1 << LOGP;
     uint32_t *data = smem;

@@ -80,13 +80,14 @@ int choose_pack_shift(uint64_t n, int logP);
 namespace gemm {
 struct Plan {
     uint32_t *seed_words = nullptr;  // seed as logical big-endian words, zero padded
-    size_t seed_words_n = 0;
+    uint32_t seed_words_n = 0;
 };
 bool supported(uint64_t n, uint64_t m);
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
 void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
+qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
 }  // namespace gemm
 
 // Histogram (hist.cu).

@@ -48,7 +48,7 @@ def assert_same(got, ref, m):
                              f"(block {bad[0] // m}, i {bad[0] % m})")
 
 
-PATHS = ["ntt"]
+PATHS = ["ntt", "gemm"]
 
 
 def path_id(q, name):
@@ -65,6 +65,8 @@ SMALL_CASES = [
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("n,m,B", SMALL_CASES)
 def test_random_small(q, oracle_mod, path, n, m, B):
+    if path == "gemm" and n % 128:
+        pytest.skip("GEMM path needs n % 128 == 0")
     key = n * 7919 + m
     raw = S.random_bytes(key, B * n // 8)
     seed = S.random_bytes(key, (n + m - 1 + 7) // 8, tag=2)
@@ -75,6 +77,8 @@ def test_random_small(q, oracle_mod, path, n, m, B):
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("n,m,B", [(1024, 716, 3), (8192, 5734, 3), (16384, 11468, 2), (96, 95, 5)])
 def test_all_ones_max_window(q, oracle_mod, path, n, m, B):
+    if path == "gemm" and n % 128:
+        pytest.skip("GEMM path needs n % 128 == 0")
     """Every window sum equals n (the maximum): exercises p > n and the
     two-blocks-per-transform separation at its worst case."""
     raw = np.full(B * n // 8, 0xFF, np.uint8)
@@ -88,11 +92,26 @@ def test_all_ones_max_window(q, oracle_mod, path, n, m, B):
 
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_config_full(q, oracle_mod, cfg):
-    """BASELINE configs 1 and 2, every block, in the launch configuration bench.py times."""
+    """BASELINE configs 1 and 2, every block, through the AUTO path (the launch
+    configuration bench.py times) and through each forced path."""
     w = S.CONFIGS[cfg]
     raw, seed = S.workload_inputs(w)
     ref = oracle_mod.extract(raw, w.n_blocks, w.n, w.m, seed)
     assert_same(gpu_extract(q, raw, w.n_blocks, w.n, w.m, seed), ref, w.m)
+    for p in PATHS:
+        assert_same(gpu_extract(q, raw, w.n_blocks, w.n, w.m, seed, path_id(q, p)), ref, w.m)
+
+
+@pytest.mark.parametrize("N,K", [(192, 128), (64, 256), (256, 1024), (16, 128)])
+def test_umma_probe_layouts(q, N, K):
+    """tcgen05 kind::i8 with A in TMEM and the overlapping core-matrix B
+    descriptor (SBO 128 B, LBO 256 B) against an int64 numpy matmul."""
+    rng = np.random.default_rng(N * 1000 + K)
+    for A in (rng.integers(0, 2, (128, K)), rng.integers(0, 256, (128, K))):
+        h = rng.integers(0, 256, N + K).astype(np.uint8)
+        B = np.array([[h[i + k] for k in range(K)] for i in range(N)], np.int64)
+        D = q.umma_probe(dev(A.astype(np.uint8)), dev(h), N, K).cpu().numpy()
+        assert np.array_equal(D.astype(np.int64), A.astype(np.int64) @ B.T)
 
 
 def test_plan_reuse_and_block_slices(q, oracle_mod):
@@ -100,7 +119,7 @@ def test_plan_reuse_and_block_slices(q, oracle_mod):
     raw, seed = S.workload_inputs(w)
     ref = oracle_mod.extract(raw, w.n_blocks, w.n, w.m, seed)
     with q.Plan(w.n, w.m, dev(seed)) as plan:
-        assert plan.path in (q.PATH_NTT, q.PATH_GEMM)
+        assert plan.path == q.PATH_GEMM  # AUTO below the measured crossover
         draw = dev(raw)
         for _ in range(2):
             out = plan.extract(draw, w.n_blocks).cpu().numpy()
