@@ -21,7 +21,9 @@
 //    bytes per block and K-stage, expand bits to int8 0/1 in registers and
 //    tcgen05.st them (32 columns = 128 K per stage, 4-stage ring).
 //  * tcgen05.mma.cta_group::1.kind::i8 M128 N192 K32, S32 accumulators in
-//    TMEM, two accumulators so the epilogue overlaps the next tile.
+//    TMEM.  Each expanded A stage feeds TWO N tiles (two accumulators, 8 MMAs
+//    per stage), halving the bit-expansion work per tensor-core op; the B
+//    chunk for the second tile is the first one shifted by 24 core matrices.
 //  * Epilogue warps tcgen05.ld the accumulators, take parity, pack 32 outputs
 //    per word MSB-first and store them at bit b*m + i (C4).
 //  * Persistent grid (one CTA per SM), warp-specialised, mbarrier pipelines.
@@ -37,13 +39,15 @@ constexpr int A_STAGES = 4;
 constexpr int KC = 1024;       // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
 constexpr int B_SLOTS = 3;
-constexpr int CM_PER_CHUNK = KC / 8 + BN / 8 - 1;  // core matrices per chunk
+constexpr int NT = 2;          // N tiles per A stage (A reuse factor)
+constexpr int CM_PER_CHUNK = KC / 8 + NT * BN / 8 - 1;  // core matrices per chunk
 constexpr int CHUNK_BYTES = CM_PER_CHUNK * 128;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 128)
-constexpr uint32_t ACC_COL0 = 128;  // accumulators: [128, 320) and [320, 512)
-constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, W_EPI0 = 8;
-constexpr int NTHREADS = 12 * 32;
+constexpr uint32_t ACC_COL0 = 128;  // accumulators of the NT N tiles: [128, 320), [320, 512)
+constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4, W_EPI0 = 8, N_EPI = 8;
+constexpr int NTHREADS = 16 * 32;
+constexpr int PF = 4;          // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -107,6 +111,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
         QRNG_R8(0), QRNG_R8(8), QRNG_R8(16), QRNG_R8(24)
         : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16};" ::"r"(taddr),
+        QRNG_R8(0), QRNG_R8(8)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -143,20 +154,21 @@ struct Args {
     uint32_t n, m;
     uint32_t kst;              // K stages per tile = n / 128
     uint32_t nchunks;          // B chunks per tile = ceil(kst / SPC)
-    uint32_t n_mtiles, n_ntiles;
+    uint32_t n_mtiles, n_npairs;  // M tiles; pairs of N tiles (NT = 2 per work tile)
     const uint32_t *seed_words;  // logical big-endian seed words, zero padded
     uint32_t seed_words_n;
     OutStream out;
 };
 
+// One stage: 128 K elements of one block from its 16 raw bytes.  Element
+// c = 32*g4 + c' comes from logical word q = 3 - g4, bit c' (K reversed).
 __device__ __forceinline__ void xform_stage(uint32_t taddr, uint4 w) {
-    // elements c = 32*g4 + c' of this stage come from logical word q = 3 - g4, bit c'
-    uint32_t L[4] = {bswap32(w.x), bswap32(w.y), bswap32(w.z), bswap32(w.w)};
+    const uint32_t L[4] = {bswap32(w.w), bswap32(w.z), bswap32(w.y), bswap32(w.x)};
     uint32_t v[32];
 #pragma unroll
     for (int g4 = 0; g4 < 4; ++g4)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[8 * g4 + e] = expand4((L[3 - g4] >> (4 * e)) & 0xFu);
+        for (int e = 0; e < 8; ++e) v[8 * g4 + e] = expand4((L[g4] >> (4 * e)) & 0xFu);
     tmem_st32(taddr, v);
 }
 
@@ -166,15 +178,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     uint32_t *seed_s = reinterpret_cast<uint32_t *>(smem + B_SLOTS * CHUNK_BYTES);
     uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((a.seed_words_n + 3) & ~3u));
     uint64_t *a_full = bars, *a_empty = bars + 4, *b_full = bars + 8, *b_empty = bars + 11;
-    uint64_t *acc_full = bars + 14, *acc_empty = bars + 16;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 18);
+    uint64_t *acc_full = bars + 14, *acc_empty = bars + 15;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t i = threadIdx.x; i < a.seed_words_n; i += NTHREADS) seed_s[i] = a.seed_words[i];
     if (threadIdx.x == 0) {
-        for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], 4); mbar_init(&a_empty[s], 1); }
+        for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM); mbar_init(&a_empty[s], 1); }
         for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], N_BGEN); mbar_init(&b_empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 4); }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, N_EPI);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_MMA) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -182,17 +195,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t ntiles = a.n_mtiles * a.n_ntiles;
+    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
 
     if (warp == W_MMA) {
         if (lane == 0) {
             const uint32_t idesc = idesc_i8(BM, BN);
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-                const uint32_t acc = it & 1, accph = (it >> 1) & 1;
-                mbar_wait(&acc_empty[acc], accph ^ 1);
+                mbar_wait(acc_empty, (it & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem + ACC_COL0 + acc * BN;
                 for (uint32_t ks = 0; ks < a.kst; ++ks) {
                     const uint32_t kin = ks % SPC;
                     if (kin == 0) {
@@ -206,8 +217,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #pragma unroll
                     for (uint32_t kk = 0; kk < 4; ++kk) {
                         const uint32_t koff = kin * KS + kk * 32;  // K offset inside the chunk
-                        const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
-                        mma_i8_ts(d_tmem, a_tmem + kk * 8, bdesc, idesc, (ks | kk) != 0);
+#pragma unroll
+                        for (uint32_t nt = 0; nt < NT; ++nt) {  // N tile nt starts 24*nt core matrices later
+                            const uint64_t bdesc = desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 256, 128);
+                            mma_i8_ts(tmem + ACC_COL0 + nt * BN, a_tmem + kk * 8, bdesc, idesc, (ks | kk) != 0);
+                        }
                     }
                     mma_commit(&a_empty[as]);
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                         if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
                     }
                 }
-                mma_commit(&acc_full[acc]);
+                mma_commit(acc_full);
             }
         }
         __syncwarp();
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         const int tb = (warp - W_BGEN0) * 32 + lane;
         uint32_t bs = 0, bph = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const uint32_t n0 = (t / a.n_mtiles) * BN;
+            const uint32_t n0 = (t / a.n_mtiles) * (NT * BN);
             for (uint32_t c = 0; c < a.nchunks; ++c) {
                 const uint32_t base = n0 + c * KC;
                 mbar_wait(&b_empty[bs], bph ^ 1);
@@ -248,55 +262,62 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
             }
         }
-    } else if (warp >= W_XFORM0 && warp < W_XFORM0 + 4) {
-        // A transform: lane row = block, 128 K per stage, 4-stage register prefetch.
-        const uint32_t row = (warp - W_XFORM0) * 32 + lane;
+    } else if (warp >= W_XFORM0 && warp < W_XFORM0 + N_XFORM) {
+        // A transform: TMEM lane = block, 128 K per stage; the prefetch ring of
+        // raw chunks runs continuously across this CTA's tiles.
+        const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
         const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16);
-        const uint32_t wpb = a.n >> 5;  // words per block
-        uint32_t as = 0, aph = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t wpb = a.n >> 5;          // words per block
+        const uint32_t last = (a.n >> 7) - 1;   // uint4 index of stage 0
+        uint32_t lt = blockIdx.x, lks = 0;      // load cursor
+        auto load = [&](uint32_t t, uint32_t ks) -> uint4 {
+            if (t >= ntiles) return make_uint4(0, 0, 0, 0);
             const uint64_t b = (uint64_t)(t % a.n_mtiles) * BM + row;
-            const bool valid = b < a.n_blocks;
-            const uint4 *blk = reinterpret_cast<const uint4 *>(a.raw + (valid ? b : 0) * wpb);
-            // stage ks covers bits j in [n - 128(ks+1), n - 128 ks): uint4 index (n/128 - 1 - ks)
-            const uint32_t last = (a.n >> 7) - 1;
-            uint4 pf[4];
+            if (b >= a.n_blocks) return make_uint4(0, 0, 0, 0);
+            return __ldg(reinterpret_cast<const uint4 *>(a.raw + b * wpb) + (last - ks));
+        };
+        uint4 pf[PF];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                pf[j] = (valid && (uint32_t)j < a.kst) ? __ldg(blk + (last - j)) : make_uint4(0, 0, 0, 0);
-            for (uint32_t ks0 = 0; ks0 < a.kst; ks0 += 4) {
+        for (int j = 0; j < PF; ++j) {
+            pf[j] = load(lt, lks);
+            if (++lks == a.kst) { lks = 0; lt += gridDim.x; }
+        }
+        uint32_t as = 0, aph = 0;
+        uint32_t ct = blockIdx.x, cks = 0;
+        while (ct < ntiles) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t ks = ks0 + j;
-                    if (ks < a.kst) {
-                        const uint4 cur = pf[j];
-                        if (valid && ks + 4 < a.kst) pf[j] = __ldg(blk + (last - ks - 4));
-                        mbar_wait(&a_empty[as], aph ^ 1);
-                        tc_fence_after();
-                        xform_stage(lane_addr + A_COL0 + as * 32, cur);
-                        tmem_wait_st();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&a_full[as]);
-                        if (++as == A_STAGES) { as = 0; aph ^= 1; }
-                    }
+            for (int j = 0; j < PF; ++j) {
+                if (ct < ntiles) {
+                    const uint4 cur = pf[j];
+                    pf[j] = load(lt, lks);
+                    if (++lks == a.kst) { lks = 0; lt += gridDim.x; }
+                    mbar_wait(&a_empty[as], aph ^ 1);
+                    tc_fence_after();
+                    xform_stage(lane_addr + A_COL0 + as * 32, cur);
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&a_full[as]);
+                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    if (++cks == a.kst) { cks = 0; ct += gridDim.x; }
                 }
             }
         }
     } else {
-        // Epilogue: parity of the S32 accumulators, 32 outputs per MSB-first word.
-        const uint32_t row = (warp - W_EPI0) * 32 + lane;
-        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16);
+        // Epilogue: warp w drains N tile (w - W_EPI0) / 4 of the pair for its lane
+        // quadrant; parity of the S32 sums, 32 outputs per MSB-first word.
+        const uint32_t nt = (uint32_t)(warp - W_EPI0) >> 2;
+        const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
+        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + nt * BN;
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const uint32_t acc = it & 1, accph = (it >> 1) & 1;
-            mbar_wait(&acc_full[acc], accph);
+            mbar_wait(acc_full, it & 1);
             tc_fence_after();
             uint32_t words[BN / 32];
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
-                tmem_ld32(lane_addr + ACC_COL0 + acc * BN + 32 * c, v);
+                tmem_ld32(lane_addr + 32 * c, v);
                 tmem_wait_ld();
                 uint32_t w = 0;
 #pragma unroll
@@ -305,10 +326,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            if (lane == 0) mbar_arrive(acc_empty);
             const uint64_t b = (uint64_t)(t % a.n_mtiles) * BM + row;
-            if (b >= a.n_blocks) continue;
-            const uint32_t n0 = (t / a.n_mtiles) * BN;
+            const uint32_t n0 = (t / a.n_mtiles) * (NT * BN) + nt * BN;
+            if (b >= a.n_blocks || n0 >= a.m) continue;
             const uint32_t nvalid = min((uint32_t)BN, a.m - n0);
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
@@ -409,13 +430,13 @@ __global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, co
 bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n; }
 
 static uint32_t seed_words_needed(uint64_t n, uint64_t m) {
-    const uint64_t n_ntiles = (m + BN - 1) / BN, kst = n / KS, nchunks = (kst + SPC - 1) / SPC;
-    const uint64_t pmax = (n_ntiles - 1) * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
+    const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = n / KS, nchunks = (kst + SPC - 1) / SPC;
+    const uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
     return (uint32_t)(pmax / 32 + 2);
 }
 
 static size_t smem_bytes(uint32_t seed_words_n) {
-    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + 18 * 8 + 16;
+    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + 16 * 8 + 16;
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L
@@ -462,11 +483,11 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.kst = (uint32_t)(n / KS);
     a.nchunks = (a.kst + SPC - 1) / SPC;
     a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
-    a.n_ntiles = (uint32_t)((m + BN - 1) / BN);
+    a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));
     a.seed_words = pl.seed_words;
     a.seed_words_n = (uint32_t)pl.seed_words_n;
     a.out = out;
-    if ((uint64_t)a.n_mtiles * a.n_ntiles > 0xFFFFFFFFull) {
+    if ((uint64_t)a.n_mtiles * a.n_npairs > 0xFFFFFFFFull) {
         set_error("GEMM path: too many tiles");
         return QRNG_E_UNSUPPORTED;
     }
@@ -480,7 +501,7 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
                                            227 * 1024));
         attr = true;
     }
-    const uint32_t ntiles = a.n_mtiles * a.n_ntiles;
+    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
     KernelTimer tm(s);
     toeplitz_gemm_kernel<<<grid, NTHREADS, smem, s>>>(a);
