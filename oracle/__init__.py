@@ -47,6 +47,9 @@ def _load():
         lib.oracle_extract_blocks.argtypes = [u8p, ctypes.POINTER(u64), u64, u64, u64, u8p, u8p,
                                               ctypes.c_int, ctypes.c_int]
         lib.oracle_extract_blocks.restype = ctypes.c_int
+        lib.oracle_extract_rows.argtypes = [u8p, ctypes.POINTER(u64), ctypes.POINTER(u64), u64, u64, u64,
+                                            u8p, u8p, ctypes.c_int]
+        lib.oracle_extract_rows.restype = ctypes.c_int
         lib.oracle_hist256.argtypes = [u8p, u64, ctypes.POINTER(u64)]
         lib.oracle_hist256.restype = None
         lib.oracle_max_threads.restype = ctypes.c_int
@@ -90,6 +93,24 @@ def extract_blocks(raw: np.ndarray, ids, n: int, m: int, seed: np.ndarray,
     out = np.zeros((ids.size, (m + 7) // 8), dtype=np.uint8)
     rc = _load().oracle_extract_blocks(_p(raw), _p(ids, ctypes.c_uint64), ids.size, n, m,
                                        _p(seed), _p(out), 0 if mode == "scalar" else 1, threads)
+    if rc != 0:
+        raise ValueError("oracle rejected arguments")
+    return out
+
+
+def extract_rows(raw: np.ndarray, blocks, rows, n: int, m: int, seed: np.ndarray,
+                 threads: int = 0) -> np.ndarray:
+    """y_i of block b for each (b, i) pair (0/1 uint8), word-parallel formula."""
+    raw = np.ascontiguousarray(raw, dtype=np.uint8)
+    seed = np.ascontiguousarray(seed, dtype=np.uint8)
+    blocks = np.ascontiguousarray(np.asarray(blocks, dtype=np.uint64))
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.uint64))
+    assert blocks.shape == rows.shape
+    if blocks.size and raw.size * 8 < (int(blocks.max()) + 1) * n:
+        raise ValueError("raw buffer too short")
+    out = np.zeros(blocks.size, dtype=np.uint8)
+    rc = _load().oracle_extract_rows(_p(raw), _p(blocks, ctypes.c_uint64), _p(rows, ctypes.c_uint64),
+                                     blocks.size, n, m, _p(seed), _p(out), threads)
     if rc != 0:
         raise ValueError("oracle rejected arguments")
     return out

@@ -236,3 +236,41 @@ void oracle_hist256(const uint8_t *samples, uint64_t count, uint64_t *counts) {
     memset(counts, 0, 256 * sizeof(uint64_t));
     for (uint64_t q = 0; q < count; ++q) counts[samples[q]]++;
 }
+
+/* Sampled outputs (for full-size checks where a whole block is too slow):
+ * y_i of block b for the `count` pairs (blocks[q], rows[q]); out[q] = 0/1.
+ * Same formula (C1), 64 values of j per AND/XOR. */
+int oracle_extract_rows(const uint8_t *raw, const uint64_t *blocks, const uint64_t *rows,
+                        uint64_t count, uint64_t n, uint64_t m, const uint8_t *seed,
+                        uint8_t *out, int n_threads) {
+    if (check_args(1, n, m)) return -1;
+    for (uint64_t q = 0; q < count; ++q)
+        if (rows[q] >= m) return -1;
+    set_threads(n_threads);
+    seed_ctx c;
+    if (seed_ctx_init(&c, seed, n, m)) return -1;
+    int err = 0;
+#pragma omp parallel
+    {
+        uint64_t *xw = (uint64_t *)malloc(c.nw * sizeof(uint64_t));
+        uint64_t cur = UINT64_MAX;
+        if (!xw) {
+#pragma omp atomic write
+            err = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t q = 0; q < (int64_t)count; ++q) {
+                if (blocks[q] != cur) {
+                    pack_lsb64(raw, blocks[q] * n, n, xw, c.nw);
+                    cur = blocks[q];
+                }
+                uint64_t o = m - 1 - rows[q], acc = 0;
+                for (uint64_t w = 0; w < c.nw; ++w) acc ^= window64(c.rs, o + 64 * w) & xw[w];
+                out[q] = (uint8_t)(__builtin_popcountll(acc) & 1);
+            }
+            free(xw);
+        }
+    }
+    free(c.rs);
+    return err ? -1 : 0;
+}

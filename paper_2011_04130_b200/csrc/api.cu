@@ -29,9 +29,9 @@ static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-KernelTimer::KernelTimer(cudaStream_t st) : s(st) {
+KernelTimer::KernelTimer(cudaStream_t st, bool timed) : s(st) {
     count_launch();
-    if (!g_timing.load()) return;
+    if (!timed || !g_timing.load()) return;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
     cudaEventRecord(a, s);
 }

@@ -503,7 +503,7 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
-    KernelTimer tm(s);
+    KernelTimer tm(s, true);
     toeplitz_gemm_kernel<<<grid, NTHREADS, smem, s>>>(a);
     tm.stop();
     QRNG_CUDA_TRY(cudaGetLastError());

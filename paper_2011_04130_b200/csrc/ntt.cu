@@ -167,7 +167,15 @@ struct FusedArgs {
     const uint32_t *shat, *tw, *itw;
     OutStream out;
     uint32_t stage_words;     // per-CTA staging words
+    uint32_t tw_shift;        // segment mode: log2(P / segment length) (tables are for w_P)
+    uint32_t scaleM;          // forward-only mode: P^-1 * 2^64 mod p
 };
+
+// Level modes: FUSED = one CTA owns a whole transform (bits in, parity bits
+// out); SEG = the CTA owns one segment of a multi-pass transform (shared
+// memory in and out; the global passes live in ntt_pass_kernel); SEGFWD =
+// forward levels only, the last one writes the scaled spectrum (seed prep).
+enum { FUSED = 0, SEG = 1, SEGFWD = 2 };
 
 // bit idx of block b (idx < n), stream MSB-first; n % 32 == 0
 __device__ __forceinline__ uint32_t raw_bit(const uint32_t *raw, uint64_t b, uint32_t n, uint32_t idx) {
@@ -175,7 +183,7 @@ __device__ __forceinline__ uint32_t raw_bit(const uint32_t *raw, uint64_t b, uin
     return (bswap32(w) >> (31 - (idx & 31))) & 1u;
 }
 
-template <int LOGP, int LV, bool PACK>
+template <int LOGP, int LV, bool PACK, int MODE = FUSED>
 struct Level {
     static constexpr int R = radix_of(LOGP, LV);
     static constexpr int S = prefix_of(LOGP, LV);
@@ -193,7 +201,10 @@ struct Level {
 
     __device__ static __forceinline__ void load(uint32_t (&x)[N1], int u, uint32_t *data,
                                                 const FusedArgs &a, uint64_t b0, int nb) {
-        if (LV == 0 && STRIDE >= 32) {
+        if (LV == 0 && MODE != FUSED) {  // segment already in shared memory
+#pragma unroll
+            for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
+        } else if (LV == 0 && STRIDE >= 32) {
             // the warp holds u = u0..u0+31 (u0 % 32 == 0): for each q it needs one
             // 32-bit raw word (idx = q*STRIDE + u0 .. +31).  Lane q fetches word q.
             const int lane = threadIdx.x & 31, u0 = u & ~31;
@@ -293,9 +304,13 @@ struct Level {
             dft_fwd<R>(x);
             if (!LAST) {
                 const int n2 = u % STRIDE;
-                if (n2) twiddle<R>(x, __ldg(a.tw + (n2 << S)));
+                if (n2) twiddle<R>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
 #pragma unroll
                 for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+            } else if (MODE == SEGFWD) {
+                uint32_t *dst = const_cast<uint32_t *>(a.shat) + (size_t)u * N1;
+#pragma unroll
+                for (int q = 0; q < N1; ++q) dst[q] = mont(x[q], a.scaleM);  // * P^-1 * 2^32
             } else {
                 // pointwise product with the seed spectrum (DIF order: position u*N1+q)
                 const uint4 *sh = reinterpret_cast<const uint4 *>(a.shat + (size_t)u * N1);
@@ -308,7 +323,7 @@ struct Level {
                     x[4 * q4 + 3] = mont(x[4 * q4 + 3], s4.w);
                 }
                 dft_inv<R>(x);
-                if (LV == 0) emit(x, u, stage, a, b0, nb, wfirst);
+                if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
                 else {
 #pragma unroll
                     for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
@@ -325,9 +340,9 @@ struct Level {
 #pragma unroll
             for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
             const int n2 = u % STRIDE;
-            if (n2) twiddle<R>(x, __ldg(a.itw + (n2 << S)));
+            if (n2) twiddle<R>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
             dft_inv<R>(x);
-            if (LV == 0) emit(x, u, stage, a, b0, nb, wfirst);
+            if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
             else {
 #pragma unroll
                 for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
@@ -337,14 +352,135 @@ struct Level {
     }
 };
 
-template <int LOGP, int LV, bool PACK>
+template <int LOGP, int LV, bool PACK, int MODE = FUSED>
 __device__ __forceinline__ void run_levels(uint32_t *data, uint32_t *stage, const FusedArgs &a,
                                            uint64_t b0, int nb, uint64_t wfirst) {
-    using L = Level<LOGP, LV, PACK>;
+    using L = Level<LOGP, LV, PACK, MODE>;
     L::fwd(data, stage, a, b0, nb, wfirst);
     if constexpr (!L::LAST) {
-        run_levels<LOGP, LV + 1, PACK>(data, stage, a, b0, nb, wfirst);
-        L::inv(data, stage, a, b0, nb, wfirst);
+        run_levels<LOGP, LV + 1, PACK, MODE>(data, stage, a, b0, nb, wfirst);
+        if constexpr (MODE != SEGFWD) L::inv(data, stage, a, b0, nb, wfirst);
+    }
+}
+
+// ---- multi-pass transform (P > 2^15) ----------------------------------------
+// The first levels of the decomposition run as global passes over a
+// workspace (ntt_pass_kernel); each remaining 2^LOGS-word segment is an
+// independent transform of length 2^LOGS with root w_P^(P/2^LOGS), handled
+// entirely in shared memory by ntt_segment_kernel (forward levels, pointwise
+// product, inverse levels); the global inverse passes follow, the last one
+// emitting parity bits.
+constexpr int kSegLog = 15;
+
+template <int LOGS, int MODE>
+__global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
+    ntt_segment_kernel(FusedArgs a, uint32_t *ws, uint32_t logP) {
+    extern __shared__ uint32_t smem[];
+    constexpr int NS = 1 << LOGS;
+    uint32_t *data = smem;
+    const uint64_t seg = blockIdx.x;
+    uint32_t *src = ws + ((uint64_t)blockIdx.y << logP) + seg * NS;
+    for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(src + i);
+        data[pidx(i)] = v.x;
+        data[pidx(i + 1)] = v.y;
+        data[pidx(i + 2)] = v.z;
+        data[pidx(i + 3)] = v.w;
+    }
+    __syncthreads();
+    FusedArgs b = a;
+    b.shat = a.shat + seg * NS;
+    run_levels<LOGS, 0, false, MODE>(data, nullptr, b, 0, 1, 0);
+    if (MODE == SEGFWD) return;
+    for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4)
+        *reinterpret_cast<uint4 *>(src + i) =
+            make_uint4(data[pidx(i)], data[pidx(i + 1)], data[pidx(i + 2)], data[pidx(i + 3)]);
+}
+
+struct PassArgs {
+    const uint32_t *bits;     // MODE_BITS / MODE_SEED: packed input (raw stream or seed words)
+    uint64_t b0;              // first block of the batch (raw stream / output)
+    uint32_t n, m, len;       // len: input bits per transform (n for data, L for the seed)
+    uint32_t *ws;
+    const uint32_t *tw, *itw;
+    uint32_t logP, S;         // this pass works on segments of 2^(logP - S) words
+    OutStream out;
+};
+enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4 };
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
+    constexpr int N1 = 1 << R;
+    const uint32_t logseg = a.logP - a.S, logstride = logseg - R;
+    const uint32_t u = blockIdx.x * 256 + threadIdx.x;  // sub-transform within the block
+    const uint64_t bb = blockIdx.y;
+    const uint32_t seg = u >> logstride, n2 = u & ((1u << logstride) - 1);
+    const uint32_t STRIDE = 1u << logstride;
+    uint32_t *base = a.ws + (bb << a.logP) + ((uint64_t)seg << logseg) + n2;
+    uint32_t x[N1];
+    if (MODE == PASS_FWD_BITS || MODE == PASS_FWD_SEED) {
+        // level 0, STRIDE >= 32: lanes hold 32 consecutive idx = q*STRIDE + u
+        const int lane = threadIdx.x & 31;
+        const uint32_t u0 = u & ~31u;
+        const uint32_t *src = (MODE == PASS_FWD_BITS) ? a.bits + (a.b0 + bb) * (a.n >> 5) : a.bits;
+        constexpr int NG = (N1 + 31) / 32;  // lane l fetches the words of q = l + 32 g
+        uint32_t w[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            w[g] = 0;
+            const uint32_t myidx = (uint32_t)(lane + 32 * g) * STRIDE + u0;
+            if (lane + 32 * g < N1 && myidx < a.len) {
+                uint32_t v = __ldg(src + (myidx >> 5));
+                if (MODE == PASS_FWD_BITS) v = bswap32(v);  // seed words are already logical
+                const uint32_t rem = a.len - myidx;         // mask bits past the input length
+                if (rem < 32) v &= 0xFFFFFFFFu << (32 - rem);
+                w[g] = v;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < N1; ++q) x[q] = (__shfl_sync(0xffffffffu, w[q >> 5], q & 31) >> (31 - lane)) & 1u;
+    } else {
+#pragma unroll
+        for (int q = 0; q < N1; ++q) x[q] = base[(size_t)q * STRIDE];
+    }
+    if (MODE <= PASS_FWD) {
+        dft_fwd<R>(x);
+        if (n2) twiddle<R>(x, __ldg(a.tw + ((uint64_t)n2 << a.S)));
+#pragma unroll
+        for (int q = 0; q < N1; ++q) base[(size_t)q * STRIDE] = x[q];
+        return;
+    }
+    if (n2) twiddle<R>(x, __ldg(a.itw + ((uint64_t)n2 << a.S)));
+    dft_inv<R>(x);
+    if (MODE == PASS_INV) {
+#pragma unroll
+        for (int q = 0; q < N1; ++q) base[(size_t)q * STRIDE] = x[q];
+        return;
+    }
+    // PASS_INV_EMIT (level 0): element q is z_t with t = q*STRIDE + u
+    const int lane = threadIdx.x & 31;
+    const uint32_t u0 = u & ~31u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) {
+        const int64_t i = (int64_t)q * STRIDE + u - (int64_t)(a.n - 1);
+        const bool valid = i >= 0 && i < (int64_t)a.m;
+        const uint32_t z = x[q] >= P ? x[q] - P : x[q];
+        const uint32_t bal = __ballot_sync(0xffffffffu, valid && (z & 1u));
+        if (lane == (q & 31)) mine = bal;
+        if ((q & 31) == 31 || q == N1 - 1) {
+            const int qb = q & ~31;
+            if (lane <= (q & 31) && mine) {
+                const int64_t i0 = (int64_t)(qb + lane) * STRIDE + u0 - (int64_t)(a.n - 1);
+                const int64_t G = (int64_t)((a.b0 + bb) * a.m) + i0;
+                const uint32_t V = __brev(mine);
+                const int64_t W0 = G >= 0 ? (G >> 5) : -((31 - G) >> 5);
+                const int o = (int)(G - W0 * 32);
+                const uint32_t hi = V >> o, lo = o ? (V << (32 - o)) : 0u;
+                if (hi) emit_word(a.out, (uint64_t)W0, hi, false);
+                if (lo) emit_word(a.out, (uint64_t)(W0 + 1), lo, false);
+            }
+        }
     }
 }
 
@@ -467,7 +603,7 @@ static qrng_status launch_fused(const FusedArgs &a, cudaStream_t s) {
         attr = true;
     }
     uint64_t grid = (a.n_blocks + per - 1) / per;
-    KernelTimer t(s);
+    KernelTimer t(s, true);
     ntt_fused_kernel<LOGP, PACK><<<(unsigned)grid, threads_of(LOGP), smem, s>>>(a);
     t.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
@@ -494,6 +630,59 @@ static qrng_status launch_seed(const uint32_t *seed_words, uint32_t L, const uin
 
 static uint64_t powmod_h(uint64_t b, uint64_t e) { return powmod_c(b, e); }
 
+// ---- multi-pass launch helpers ---------------------------------------------
+// Global radices for P = 2^logP > 2^15: g = logP - 15 levels before the segments.
+static int global_radices(int logP, int r[2]) {
+    const int g = logP - kSegLog;
+    if (g <= 6) { r[0] = g; return 1; }
+    r[0] = g - g / 2;
+    r[1] = g / 2;
+    return 2;
+}
+
+template <int MODE>
+static qrng_status launch_pass(int R, const PassArgs &a, uint64_t nb, cudaStream_t s, bool timed) {
+    const uint64_t nsub = 1ull << (a.logP - R);
+    dim3 grid((unsigned)(nsub / 256), (unsigned)nb);
+    KernelTimer t(s, timed);
+    switch (R) {
+#define X(RR) case RR: ntt_pass_kernel<RR, MODE><<<grid, 256, 0, s>>>(a); break;
+        X(1) X(2) X(3) X(4) X(5) X(6)
+#undef X
+        default:
+            set_error("NTT pass radix 2^%d unsupported", R);
+            return QRNG_E_UNSUPPORTED;
+    }
+    t.stop();
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+template <int MODE>
+static qrng_status launch_segments(const FusedArgs &a, uint32_t *ws, int logP, uint64_t nb, cudaStream_t s,
+                                   bool timed) {
+    const size_t smem = ((size_t)(1 << kSegLog) + (1 << kSegLog) / 32) * 4;
+    static bool attr = false;
+    if (!attr) {
+        QRNG_CUDA_TRY(cudaFuncSetAttribute(ntt_segment_kernel<kSegLog, MODE>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    dim3 grid((unsigned)(1u << (logP - kSegLog)), (unsigned)nb);
+    KernelTimer t(s, timed);
+    ntt_segment_kernel<kSegLog, MODE><<<grid, threads_of(kSegLog), smem, s>>>(a, ws, (uint32_t)logP);
+    t.stop();
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+// Workspace words per multi-pass batch (L2-sized batches keep the passes on chip).
+static uint64_t batch_blocks(int logP, uint64_t n_blocks) {
+    uint64_t cap = (1ull << 24) >> logP;
+    if (cap < 1) cap = 1;
+    return cap < n_blocks ? cap : n_blocks;
+}
+
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s) {
     const uint64_t L = n + m - 1;
     int logP = 0;
@@ -503,12 +692,8 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, c
         set_error("NTT path: L = %llu exceeds 2^23", (unsigned long long)L);
         return QRNG_E_UNSUPPORTED;
     }
-    if (logP > kMaxFusedLogP) {
-        set_error("NTT path: P = 2^%d not implemented yet (fused kernel limit 2^15)", logP);
-        return QRNG_E_UNSUPPORTED;
-    }
     pl.logP = logP;
-    pl.pack_shift = choose_pack_shift(n, logP);
+    pl.pack_shift = logP <= kMaxFusedLogP ? choose_pack_shift(n, logP) : 0;
     const uint64_t Pn = 1ull << logP;
     const uint64_t nwords = (L + 31) / 32 + 1;
     uint32_t *seed_words = nullptr;
@@ -529,11 +714,45 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, c
     const uint64_t r2 = (uint64_t)(((unsigned __int128)1 << 64) % P);
     const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * r2 % P);
     qrng_status st = QRNG_E_UNSUPPORTED;
-    switch (logP) {
+    if (logP <= kMaxFusedLogP) {
+        switch (logP) {
 #define X(LP) case LP: st = launch_seed<LP>(seed_words, (uint32_t)L, pl.tw, pl.shat, scaleM, s); break;
-        QRNG_LOGP_CASES(X)
+            QRNG_LOGP_CASES(X)
 #undef X
-        default: break;
+            default: break;
+        }
+    } else {
+        // seed spectrum through the same multi-pass decomposition, forward only
+        uint32_t *ws = nullptr;
+        QRNG_CUDA_TRY(cudaMallocAsync(&ws, Pn * 4, s));
+        int r[2];
+        const int np = global_radices(logP, r);
+        PassArgs pa{};
+        pa.bits = seed_words;
+        pa.b0 = 0;
+        pa.n = (uint32_t)n;
+        pa.m = (uint32_t)m;
+        pa.len = (uint32_t)L;
+        pa.ws = ws;
+        pa.tw = pl.tw;
+        pa.itw = pl.itw;
+        pa.logP = (uint32_t)logP;
+        pa.S = 0;
+        st = launch_pass<PASS_FWD_SEED>(r[0], pa, 1, s, false);
+        if (st == QRNG_OK && np == 2) {
+            pa.S = (uint32_t)r[0];
+            st = launch_pass<PASS_FWD>(r[1], pa, 1, s, false);
+        }
+        if (st == QRNG_OK) {
+            FusedArgs fa{};
+            fa.shat = pl.shat;
+            fa.tw = pl.tw;
+            fa.itw = pl.itw;
+            fa.tw_shift = (uint32_t)(logP - kSegLog);
+            fa.scaleM = scaleM;
+            st = launch_segments<SEGFWD>(fa, ws, logP, 1, s, false);
+        }
+        cudaFreeAsync(ws, s);
     }
     cudaFreeAsync(seed_words, s);
     return st;
@@ -547,9 +766,57 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
+static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
+                                     uint64_t m, const OutStream &out, cudaStream_t s) {
+    const int logP = pl.logP;
+    const uint64_t bb = batch_blocks(logP, n_blocks);
+    uint32_t *ws = nullptr;
+    QRNG_CUDA_TRY(cudaMallocAsync(&ws, (bb << logP) * 4, s));
+    int r[2];
+    const int np = global_radices(logP, r);
+    PassArgs pa{};
+    pa.bits = reinterpret_cast<const uint32_t *>(d_raw);
+    pa.n = (uint32_t)n;
+    pa.m = (uint32_t)m;
+    pa.len = (uint32_t)n;
+    pa.ws = ws;
+    pa.tw = pl.tw;
+    pa.itw = pl.itw;
+    pa.logP = (uint32_t)logP;
+    pa.out = out;
+    FusedArgs fa{};
+    fa.shat = pl.shat;
+    fa.tw = pl.tw;
+    fa.itw = pl.itw;
+    fa.tw_shift = (uint32_t)(logP - kSegLog);
+    qrng_status st = QRNG_OK;
+    for (uint64_t b0 = 0; b0 < n_blocks && st == QRNG_OK; b0 += bb) {
+        const uint64_t nb = (n_blocks - b0) < bb ? (n_blocks - b0) : bb;
+        pa.b0 = b0;
+        pa.S = 0;
+        st = launch_pass<PASS_FWD_BITS>(r[0], pa, nb, s, true);
+        if (st == QRNG_OK && np == 2) {
+            pa.S = (uint32_t)r[0];
+            st = launch_pass<PASS_FWD>(r[1], pa, nb, s, true);
+        }
+        if (st == QRNG_OK) st = launch_segments<SEG>(fa, ws, logP, nb, s, true);
+        if (st == QRNG_OK && np == 2) {
+            pa.S = (uint32_t)r[0];
+            st = launch_pass<PASS_INV>(r[1], pa, nb, s, true);
+        }
+        if (st == QRNG_OK) {
+            pa.S = 0;
+            st = launch_pass<PASS_INV_EMIT>(r[0], pa, nb, s, true);
+        }
+    }
+    cudaFreeAsync(ws, s);
+    return st;
+}
+
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s) {
-    FusedArgs a;
+    if (pl.logP > kMaxFusedLogP) return extract_multipass(pl, d_raw, n_blocks, n, m, out, s);
+    FusedArgs a{};
     a.raw = reinterpret_cast<const uint32_t *>(d_raw);
     a.n_blocks = n_blocks;
     a.n = (uint32_t)n;
@@ -559,6 +826,7 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.tw = pl.tw;
     a.itw = pl.itw;
     a.out = out;
+    a.tw_shift = 0;
     const int per = pl.pack_shift ? 2 : 1;
     a.stage_words = (uint32_t)((per * m + 31) / 32 + 2);
     switch (pl.logP) {

@@ -22,10 +22,10 @@ void set_error(const char *fmt, ...);
 
 // Launch accounting / optional per-kernel event timing (qrng_debug_*).
 void count_launch();
-struct KernelTimer {  // brackets the main extraction kernel on its stream
+struct KernelTimer {  // brackets one extraction kernel on its stream (counts every launch)
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s;
-    explicit KernelTimer(cudaStream_t st);
+    KernelTimer(cudaStream_t st, bool timed);
     void stop();
 };
 

@@ -182,3 +182,77 @@ def test_hist_sharded_accumulate(q):
     q.hist256_async(dev(x[:half]), counts)
     q.hist256_async(dev(x[half:]), counts)
     assert np.array_equal(counts.cpu().numpy().astype(np.uint64), oracle.hist256(x))
+
+
+# ---- multi-pass NTT (P > 2^15) and full-size configurations -----------------------
+
+@pytest.mark.parametrize("n,m,B", [(32768, 22937, 3), (49152, 30000, 2), (65536, 45875, 3),
+                                   (131072, 91750, 2), (65536, 1, 2), (65536, 65535, 1)])
+def test_multipass_random(q, oracle_mod, n, m, B):
+    key = n * 31 + m
+    raw = S.random_bytes(key, B * n // 8)
+    seed = S.random_bytes(key, (n + m - 1 + 7) // 8, tag=2)
+    ref = oracle_mod.extract(raw, B, n, m, seed)
+    assert_same(gpu_extract(q, raw, B, n, m, seed, q.PATH_NTT), ref, m)
+
+
+def test_multipass_all_ones(q, oracle_mod):
+    n, m, B = 131072, 91750, 2  # window sums reach n: p > n at P = 2^18
+    raw = np.full(B * n // 8, 0xFF, np.uint8)
+    seed = np.full((n + m - 1 + 7) // 8, 0xFF, np.uint8)
+    assert_same(gpu_extract(q, raw, B, n, m, seed, q.PATH_NTT), oracle_mod.extract(raw, B, n, m, seed), m)
+
+
+def sampled_check(oracle_mod, got, raw, seed, n, m, B, n_rows=256, key=0):
+    """Sampled outputs at full size: first/last/middle/random blocks, random rows
+    plus the first and last rows of each block, against the oracle one by one."""
+    rng = np.random.default_rng(key)
+    blocks = sorted({0, B - 1, B // 2, *rng.integers(0, B, 5).tolist()})
+    bl, rw = [], []
+    for b in blocks:
+        rows = np.unique(np.concatenate([[0, 1, m - 2, m - 1], rng.integers(0, m, n_rows)]))
+        bl += [b] * rows.size
+        rw += rows.tolist()
+    bl, rw = np.array(bl, np.uint64), np.array(rw, np.uint64)
+    ref = oracle_mod.extract_rows(raw, bl, rw, n, m, seed)
+    bits = np.unpackbits(got)
+    gb = bits[(bl * m + rw).astype(np.int64)]
+    bad = np.nonzero(gb != ref)[0]
+    assert bad.size == 0, f"{bad.size} sampled bits differ, first (block {bl[bad[0]]}, row {rw[bad[0]]})"
+    # pad bits of the last byte
+    tail = B * m % 8
+    if tail:
+        assert got[-1] & ((1 << (8 - tail)) - 1) == 0
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config_full_size_sampled(q, oracle_mod, cfg):
+    """Configs 3 and 4 at full size through AUTO (what bench.py times), sampled
+    outputs vs the oracle, plus two complete blocks."""
+    w = S.CONFIGS[cfg]
+    raw, seed = S.workload_inputs(w)
+    got = gpu_extract(q, raw, w.n_blocks, w.n, w.m, seed)
+    sampled_check(oracle_mod, got, raw, seed, w.n, w.m, w.n_blocks, key=cfg)
+    for b in (0, w.n_blocks - 1):
+        ref = oracle_mod.extract_blocks(raw, [b], w.n, w.m, seed)[0]
+        gbits = np.unpackbits(got)[b * w.m:(b + 1) * w.m]
+        assert np.array_equal(gbits, np.unpackbits(ref)[:w.m]), b
+
+
+def test_sweep_max_n_sampled(q, oracle_mod):
+    """Config 5's largest point n = 2^22 (P = 2^23, two global passes), 32 blocks."""
+    w = S.sweep_workload(22)
+    B = 32
+    raw, seed = S.workload_inputs(w, 0, B)
+    got = gpu_extract(q, raw, B, w.n, w.m, seed)
+    sampled_check(oracle_mod, got, raw, seed, w.n, w.m, B, n_rows=128, key=22)
+
+
+@pytest.mark.parametrize("log2n,B", [(10, 1024), (12, 512), (14, 256), (16, 64)])
+def test_gemm_equals_ntt_all_blocks(q, log2n, B):
+    """P10: the two independent GPU paths agree bit for bit on every block."""
+    w = S.sweep_workload(log2n)
+    raw, seed = S.workload_inputs(w, 0, B)
+    a = gpu_extract(q, raw, B, w.n, w.m, seed, q.PATH_GEMM)
+    b = gpu_extract(q, raw, B, w.n, w.m, seed, q.PATH_NTT)
+    assert_same(a, b, w.m)
