@@ -30,7 +30,7 @@ namespace ntt {
 
 constexpr uint32_t P = kP;
 constexpr uint32_t P2 = 2u * kP;
-constexpr uint32_t NPINV = 998244351u;  // -p^-1 mod 2^32
+constexpr uint32_t PINV = 3296722945u;  // p^-1 mod 2^32
 
 constexpr uint64_t powmod_c(uint64_t b, uint64_t e) {
     uint64_t r = 1;
@@ -68,18 +68,21 @@ __device__ __forceinline__ uint32_t shoup(uint32_t a, uint32_t w, uint32_t wp) {
     uint32_t q = __umulhi(a, wp);
     return a * w - q * P;  // a*w mod p in [0, 2p), any 32-bit a
 }
-// Montgomery product a*b/2^32 mod p for a, b < 2p, result in [0, 2p):
-// u = a*b + q*p with q = -(a*b)*p^-1 mod 2^32 is divisible by 2^32 and
-// u < 4p^2 + 2^32 p, so u >> 32 < 2p (4p < 2^32).  Three IMADs in SASS.
+// Montgomery product a*b/2^32 mod p for a, b < 2p, result in (0, 2p):
+// t = a*b < 4p^2 < p 2^32; q = t_lo p^-1 mod 2^32 makes t - q p divisible by
+// 2^32, so (t - q p)/2^32 = t_hi - hi(q p) lies in (-p, p); add p.  Written as
+// mul.wide / mul.lo / mul.hi / sub so ptxas emits 4 instructions (IMAD.WIDE,
+// IMAD, IMAD.HI, IADD3) instead of fusing a 64-bit addend chain.
 __device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b) {
     uint32_t r;
-    asm("{\n\t.reg .u64 t, u;\n\t.reg .u32 lo, q, d;\n\t"
+    asm("{\n\t.reg .u64 t;\n\t.reg .u32 lo, hi, q, h;\n\t"
         "mul.wide.u32 t, %1, %2;\n\t"
-        "cvt.u32.u64 lo, t;\n\t"
+        "mov.b64 {lo, hi}, t;\n\t"
         "mul.lo.u32 q, lo, %3;\n\t"
-        "mad.wide.u32 u, q, %4, t;\n\t"
-        "mov.b64 {d, %0}, u;\n\t}"
-        : "=r"(r) : "r"(a), "r"(b), "n"(NPINV), "n"(P));
+        "mul.hi.u32 h, q, %4;\n\t"
+        "sub.u32 %0, hi, h;\n\t"
+        "add.u32 %0, %0, %4;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "n"(PINV), "n"(P));
     return r;
 }
 
@@ -157,7 +160,7 @@ __host__ __device__ constexpr int prefix_of(int logP, int lv) {
 __host__ __device__ constexpr int threads_of(int logP) {
     return (1 << logP) / 32 < 32 ? 32 : ((1 << logP) / 32 > 1024 ? 1024 : (1 << logP) / 32);
 }
-__device__ __forceinline__ int pidx(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int pidx(int i) { return i + (i >> 5); }
 
 struct FusedArgs {
     const uint32_t *raw;      // raw stream as 32-bit words (MSB-first bytes)
@@ -198,12 +201,20 @@ struct Level {
     __device__ static __forceinline__ int addr(int u, int q) {
         return (u / STRIDE) * NSEG + q * STRIDE + (u % STRIDE);
     }
+    // padded smem index of element q of sub-transform u = pbase(u) + poff(q):
+    // exact when NSEG % 32 == 0 or STRIDE == 1 (q*STRIDE never carries into
+    // the padding of the segment base), so the per-q offsets are immediates.
+    static_assert(NSEG % 32 == 0 || STRIDE == 1, "padded addressing needs aligned segments");
+    __device__ static __forceinline__ int pbase(int u) { return pidx((u / STRIDE) * NSEG + (u % STRIDE)); }
+    static constexpr int poff(int q) { return pidx(q * STRIDE); }
 
     __device__ static __forceinline__ void load(uint32_t (&x)[N1], int u, uint32_t *data,
                                                 const FusedArgs &a, uint64_t b0, int nb) {
         if (LV == 0 && MODE != FUSED) {  // segment already in shared memory
 #pragma unroll
-            for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
+            { const int pb = pbase(u);
+#pragma unroll
+            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
         } else if (LV == 0 && STRIDE >= 32) {
             // the warp holds u = u0..u0+31 (u0 % 32 == 0): for each q it needs one
             // 32-bit raw word (idx = q*STRIDE + u0 .. +31).  Lane q fetches word q.
@@ -234,7 +245,9 @@ struct Level {
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
+            { const int pb = pbase(u);
+#pragma unroll
+            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
         }
     }
 
@@ -306,7 +319,9 @@ struct Level {
                 const int n2 = u % STRIDE;
                 if (n2) twiddle<R>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
 #pragma unroll
-                for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+                { const int pb = pbase(u);
+#pragma unroll
+                for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q]; }
             } else if (MODE == SEGFWD) {
                 uint32_t *dst = const_cast<uint32_t *>(a.shat) + (size_t)u * N1;
 #pragma unroll
@@ -326,7 +341,9 @@ struct Level {
                 if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
                 else {
 #pragma unroll
-                    for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+                    { const int pb = pbase(u);
+#pragma unroll
+                for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q]; }
                 }
             }
         }
@@ -338,14 +355,18 @@ struct Level {
         for (int u = threadIdx.x; u < NSUB; u += T) {
             uint32_t x[N1];
 #pragma unroll
-            for (int q = 0; q < N1; ++q) x[q] = data[pidx(addr(u, q))];
+            { const int pb = pbase(u);
+#pragma unroll
+            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
             const int n2 = u % STRIDE;
             if (n2) twiddle<R>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
             dft_inv<R>(x);
             if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
             else {
 #pragma unroll
-                for (int q = 0; q < N1; ++q) data[pidx(addr(u, q))] = x[q];
+                { const int pb = pbase(u);
+#pragma unroll
+                for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q]; }
             }
         }
         __syncthreads();
