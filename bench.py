@@ -232,8 +232,8 @@ def run_ours(args):
             peak = pk["bf16_tflops"] * 2.0  # int8 dense = 2x bf16 (guide's nominal ratio)
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
                     "peak_kind": f"{pk_kind} bf16 x 2 (int8 nominal ratio)"}
-            clk = pk.get("sm_max_mhz", 1965.0)
-            roof["peak_at_sm_max_clock"] = 148 * 8192 * 2 * clk * 1e6 / 1e12
+            clk_mhz = pk.get("sm_max_mhz", 1965.0)
+            roof["peak_at_sm_max_clock"] = 148 * 8192 * 2 * clk_mhz * 1e6 / 1e12
             roof["frac_of_clock_peak"] = achieved / roof["peak_at_sm_max_clock"]
         else:
             achieved = work / per_step_s / 1e9

@@ -106,8 +106,10 @@ QRNG_API qrng_status qrng_entropy_from_counts(const uint64_t *h_counts, uint32_t
  * d_raw_bits : n_blocks*n bits (C2, C3), ceil(n_blocks*n/8) bytes, 16-byte aligned.
  * d_seed     : L = n+m-1 seed bits a_1..a_L (C2), ceil(L/8) bytes, 16-byte aligned;
  *              bits past L are ignored.  One seed serves every block.
- * d_out      : ceil(n_blocks*m/8) bytes, 16-byte aligned, written completely (C4).
- * Errors: E_INVALID if a pointer is NULL or not 16-byte aligned, n == 0, m == 0,
+ * d_out      : ceil(n_blocks*m/8) bytes, 4-byte aligned, written completely (C4); no
+ *              byte past ceil(n_blocks*m/8) is touched.
+ * Errors: E_INVALID if a pointer is NULL or misaligned (d_raw_bits / d_seed 16 bytes,
+ *         d_out 4 bytes), n == 0, m == 0,
  *         m >= n, n_blocks == 0, or d_out overlaps d_raw_bits or d_seed;
  *         E_UNSUPPORTED if n % 32 != 0 or L > 2^23 (2-adic limit of the NTT prime
  *         p = 119*2^23 + 1);  E_CUDA / E_NOMEM on device failures.

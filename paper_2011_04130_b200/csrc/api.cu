@@ -7,6 +7,7 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <algorithm>
 #include <vector>
 #include "qrng_internal.cuh"
 
@@ -190,7 +191,8 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
     const uint64_t n = plan->n, m = plan->m;
     if (n_blocks == 0) { set_error("n_blocks must be > 0"); return QRNG_E_INVALID; }
     if (!d_raw_bits || !d_out) { set_error("NULL buffer"); return QRNG_E_INVALID; }
-    if (!aligned16(d_raw_bits) || !aligned16(d_out)) { set_error("buffers must be 16-byte aligned"); return QRNG_E_INVALID; }
+    if (!aligned16(d_raw_bits)) { set_error("d_raw_bits must be 16-byte aligned"); return QRNG_E_INVALID; }
+    if (((uintptr_t)d_out & 3u) != 0) { set_error("d_out must be 4-byte aligned"); return QRNG_E_INVALID; }
     if (n_blocks > (UINT64_MAX / n)) { set_error("n_blocks * n overflows"); return QRNG_E_INVALID; }
     const uint64_t raw_bytes = n_blocks * n / 8, out_bits = n_blocks * m, out_bytes = (out_bits + 7) / 8;
     if (overlap(d_raw_bits, raw_bytes, d_out, out_bytes)) { set_error("d_out overlaps d_raw_bits"); return QRNG_E_INVALID; }
@@ -236,6 +238,27 @@ qrng_status qrng_toeplitz_extract(const uint8_t *d_raw_bits, uint64_t n_blocks, 
     return QRNG_OK;
 }
 
+// Copy streams of the calling thread (host-buffer path): H2D and D2H run on
+// their own streams so both PCIe directions overlap the kernels.
+struct CopyStreams {
+    int dev = -1;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+static thread_local CopyStreams g_cs;
+
+static qrng_status copy_streams(int dev, cudaStream_t *h2d, cudaStream_t *d2h) {
+    if (g_cs.dev != dev) {
+        if (g_cs.h2d) { cudaStreamDestroy(g_cs.h2d); cudaStreamDestroy(g_cs.d2h); }
+        g_cs = CopyStreams{};
+        QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_cs.h2d, cudaStreamNonBlocking));
+        QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_cs.d2h, cudaStreamNonBlocking));
+        g_cs.dev = dev;
+    }
+    *h2d = g_cs.h2d;
+    *d2h = g_cs.d2h;
+    return QRNG_OK;
+}
+
 qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blocks, uint64_t n, uint64_t m,
                                        const uint8_t *h_seed, uint8_t *h_out, cudaStream_t stream) {
     qrng_status st = check_nm(n, m);
@@ -243,21 +266,73 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     if (!h_raw_bits || !h_seed || !h_out) { set_error("NULL buffer"); return QRNG_E_INVALID; }
     if (n_blocks == 0 || n_blocks > UINT64_MAX / n) { set_error("bad n_blocks"); return QRNG_E_INVALID; }
     if ((st = device_ready()) != QRNG_OK) return st;
+    int dev = 0;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    cudaStream_t s_in, s_out;
+    if ((st = copy_streams(dev, &s_in, &s_out)) != QRNG_OK) return st;
     const uint64_t raw_bytes = n_blocks * n / 8, seed_bytes = (n + m - 1 + 7) / 8,
                    out_bytes = (n_blocks * m + 7) / 8;
     uint8_t *d_raw = nullptr, *d_seed = nullptr, *d_out = nullptr;
     QRNG_CUDA_TRY(cudaMallocAsync(&d_raw, raw_bytes, stream));
     QRNG_CUDA_TRY(cudaMallocAsync(&d_seed, seed_bytes, stream));
     QRNG_CUDA_TRY(cudaMallocAsync(&d_out, out_bytes, stream));
-    QRNG_CUDA_TRY(cudaMemcpyAsync(d_raw, h_raw_bits, raw_bytes, cudaMemcpyHostToDevice, stream));
     QRNG_CUDA_TRY(cudaMemcpyAsync(d_seed, h_seed, seed_bytes, cudaMemcpyHostToDevice, stream));
-    st = qrng_toeplitz_extract_async(d_raw, n_blocks, n, m, d_seed, d_out, stream);
-    if (st == QRNG_OK)
-        QRNG_CUDA_TRY(cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, stream));
+    qrng_plan *plan = nullptr;
+    st = qrng_plan_create(n, m, d_seed, stream, &plan);
+    // Pipeline over chunks of whole 32-block granules: every chunk's key starts
+    // on a 32-bit word boundary (32 m % 32 == 0) and its raw bytes on a 16-byte
+    // boundary, so chunks are independent self-contained extractions.
+    const uint64_t G = (n_blocks + 31) / 32, K = G < 8 ? G : 8;
+    std::vector<cudaEvent_t> ev(3 * K + 1, nullptr);
+    for (auto &e : ev)
+        if (st == QRNG_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            set_error("cudaEventCreate failed");
+            st = QRNG_E_CUDA;
+        }
+    if (st == QRNG_OK) {
+        cudaEventRecord(ev[3 * K], stream);  // buffers allocated, plan enqueued
+        cudaStreamWaitEvent(s_in, ev[3 * K], 0);
+        cudaStreamWaitEvent(s_out, ev[3 * K], 0);
+    }
+    for (uint64_t c = 0; c < K && st == QRNG_OK; ++c) {
+        const uint64_t b0 = 32 * (c * G / K), b1 = std::min(n_blocks, 32 * ((c + 1) * G / K));
+        const uint64_t r0 = b0 * n / 8, r1 = b1 * n / 8;
+        const uint64_t o0 = b0 * m / 8, o1 = (c + 1 == K) ? out_bytes : b1 * m / 8;
+        if (cudaMemcpyAsync(d_raw + r0, h_raw_bits + r0, r1 - r0, cudaMemcpyHostToDevice, s_in) != cudaSuccess) {
+            set_error("H2D copy failed");
+            st = QRNG_E_CUDA;
+            break;
+        }
+        cudaEventRecord(ev[3 * c], s_in);
+        cudaStreamWaitEvent(stream, ev[3 * c], 0);
+        st = qrng_plan_extract(plan, d_raw + r0, b1 - b0, d_out + o0, stream);
+        if (st != QRNG_OK) break;
+        cudaEventRecord(ev[3 * c + 1], stream);
+        cudaStreamWaitEvent(s_out, ev[3 * c + 1], 0);
+        if (cudaMemcpyAsync(h_out + o0, d_out + o0, o1 - o0, cudaMemcpyDeviceToHost, s_out) != cudaSuccess) {
+            set_error("D2H copy failed");
+            st = QRNG_E_CUDA;
+            break;
+        }
+        cudaEventRecord(ev[3 * c + 2], s_out);
+    }
+    if (ev[3 * K]) {  // join the copy streams back into `stream`
+        cudaEventRecord(ev[3 * K], s_in);
+        cudaStreamWaitEvent(stream, ev[3 * K], 0);
+        cudaEventRecord(ev[3 * K], s_out);
+        cudaStreamWaitEvent(stream, ev[3 * K], 0);
+    }
+    if (plan) plan_release(plan, stream, true);
     cudaFreeAsync(d_raw, stream);
     cudaFreeAsync(d_seed, stream);
     cudaFreeAsync(d_out, stream);
-    QRNG_CUDA_TRY(cudaStreamSynchronize(stream));
+    cudaError_t e = cudaStreamSynchronize(stream);
+    for (auto &x : ev)
+        if (x) cudaEventDestroy(x);
+    if (e != cudaSuccess && st == QRNG_OK) {
+        set_error("cudaStreamSynchronize: %s", cudaGetErrorString(e));
+        st = QRNG_E_CUDA;
+    }
     return st;
 }
 

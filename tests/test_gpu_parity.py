@@ -256,3 +256,15 @@ def test_gemm_equals_ntt_all_blocks(q, log2n, B):
     a = gpu_extract(q, raw, B, w.n, w.m, seed, q.PATH_GEMM)
     b = gpu_extract(q, raw, B, w.n, w.m, seed, q.PATH_NTT)
     assert_same(a, b, w.m)
+
+
+@pytest.mark.parametrize("n,m,B", [(1024, 179, 100), (8192, 5734, 333), (2048, 1, 65), (96, 50, 70)])
+def test_host_buffers_pipelined_chunks(q, oracle_mod, n, m, B):
+    """qrng_toeplitz_extract_host splits the batch into 32-block-granule chunks
+    (H2D / kernel / D2H overlapped on three streams); odd m and ragged tails."""
+    raw = S.random_bytes(n + B, B * n // 8)
+    seed = S.random_bytes(n + B, (n + m - 1 + 7) // 8, tag=4)
+    out = np.full(q.out_bytes(B, m) + 8, 0xA5, np.uint8)
+    q.toeplitz_extract_host(raw, B, n, m, seed, out)
+    assert_same(out[:q.out_bytes(B, m)], oracle_mod.extract(raw, B, n, m, seed), m)
+    assert (out[q.out_bytes(B, m):] == 0xA5).all()
