@@ -18,8 +18,9 @@
 //    with SBO = 128 B (row-group stride) and LBO = 256 B (K-chunk stride)
 //    describes every B tile; the MMA simply reads overlapping windows of it.
 //  * A operand (M = 128 blocks) in TMEM: "transform" warps load 16 packed
-//    bytes per block and K-stage, expand bits to int8 0/1 in registers and
-//    tcgen05.st them (32 columns = 128 K per stage, 4-stage ring).
+//    bytes per block and K-stage, expand bits to int8 0/-1 with SHF + PRMT
+//    (sign-replicate) in registers and tcgen05.st them (32 columns = 128 K per
+//    stage, 4-stage ring).
 //  * tcgen05.mma.cta_group::1.kind::i8 M128 N192 K32, S32 accumulators in
 //    TMEM.  Each expanded A stage feeds TWO N tiles (two accumulators, 8 MMAs
 //    per stage), halving the bit-expansion work per tensor-core op; the B
@@ -139,13 +140,30 @@ __device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr, uint32_t lbo, ui
     return d;         // base offset 0, lbo mode 0, layout SWIZZLE_NONE
 }
 
-// kind::i8 instruction descriptor: S32 accumulate, U8 x U8, both K-major.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
-    return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::i8 instruction descriptor: S32 accumulate, S8 x S8, both K-major.
+// Operand bytes are 0x00 / 0xFF = 0 / -1, so every product is 0 or +1 and the
+// S32 sum is exactly the count sum_j T[i][j] x_j (at most n <= 2^16).
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool is_signed = true) {
+    return (2u << 4) | ((is_signed ? 1u : 0u) << 7) | ((is_signed ? 1u : 0u) << 10) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// 4 bits (LSB = first element) -> 4 int8 0/1 bytes (little endian).
-__device__ __forceinline__ uint32_t expand4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+// prmt.b32 with sign-replicate selectors: each output byte is 0x00 or 0xFF,
+// the MSB of the selected byte of {b, a} replicated.
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "n"(SEL));
+    return d;
+}
+
+// K order inside every 16-slot core-matrix chunk (any fixed permutation is
+// allowed because A and B use the same one and a chunk's core matrix still
+// depends only on g + 2q):  slot s = 4*cc + f holds chunk element
+//     r(s) = 15 - 8*(f & 1) - 2*cc - (f >> 1)
+// (elements counted along the reversed K index j'').  This is the order in
+// which 8 shifted copies of a raw word expose their bits at byte MSBs, so both
+// operands are built with SHF + PRMT only.
 
 // ---- the extraction kernel -----------------------------------------------------
 struct Args {
@@ -160,15 +178,26 @@ struct Args {
     OutStream out;
 };
 
-// One stage: 128 K elements of one block from its 16 raw bytes.  Element
-// c = 32*g4 + c' comes from logical word q = 3 - g4, bit c' (K reversed).
+// One stage: 128 K elements of one block from its 16 raw bytes (memory words
+// M_0..M_3, stream order, MSB-first bytes).  S_a = M_q << a puts stream bit
+// 32q + 8k + a (bit a of byte k) at the MSB of byte k.  Chunk G of the stage
+// (16 reversed-K elements) is bytes k0, k0+1 of word q = 3 - G/2, k0 = 2 - 2(G&1);
+// its column cc takes bytes {k0, k0+1} of S_2cc and S_2cc+1 (order of r(s)).
 __device__ __forceinline__ void xform_stage(uint32_t taddr, uint4 w) {
-    const uint32_t L[4] = {bswap32(w.w), bswap32(w.z), bswap32(w.y), bswap32(w.x)};
+    const uint32_t M[4] = {w.x, w.y, w.z, w.w};
     uint32_t v[32];
 #pragma unroll
-    for (int g4 = 0; g4 < 4; ++g4)
+    for (int q = 0; q < 4; ++q) {
+        uint32_t S[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[8 * g4 + e] = expand4((L[g4] >> (4 * e)) & 0xFu);
+        for (int a = 0; a < 8; ++a) S[a] = M[q] << a;
+        const int G0 = 2 * (3 - q);  // chunk of bytes {2,3}; G0 + 1 is bytes {0,1}
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+            v[4 * G0 + cc] = prmt_sign<0xFEBA>(S[2 * cc], S[2 * cc + 1]);
+            v[4 * (G0 + 1) + cc] = prmt_sign<0xDC98>(S[2 * cc], S[2 * cc + 1]);
+        }
+    }
     tmem_st32(taddr, v);
 }
 
@@ -246,14 +275,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 mbar_wait(&b_empty[bs], bph ^ 1);
                 uint8_t *cb = chunks + bs * CHUNK_BYTES;
                 for (int r = tb; r < CM_PER_CHUNK * 8; r += N_BGEN * 32) {
+                    // row holds seed bits p + r(s); in v (seed bit p + d at bit 31 - d) the
+                    // bit of slot s = 4cc + f sits at byte 2 + (f&1), bit 2cc + (f>>1)
                     const uint32_t p = base + 8 * (r >> 3) + (r & 7);
                     const uint32_t v = __funnelshift_l(seed_s[(p >> 5) + 1], seed_s[p >> 5], p & 31);
-                    const uint32_t rv = __brev(v);  // element c at bit c
                     uint4 o;
-                    o.x = expand4(rv & 0xFu);
-                    o.y = expand4((rv >> 4) & 0xFu);
-                    o.z = expand4((rv >> 8) & 0xFu);
-                    o.w = expand4((rv >> 12) & 0xFu);
+                    o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
+                    o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
+                    o.z = prmt_sign<0xFEBA>(v << 3, v << 2);
+                    o.w = prmt_sign<0xFEBA>(v << 1, v);
                     *reinterpret_cast<uint4 *>(cb + (r >> 3) * 128 + (r & 7) * 16) = o;
                 }
                 fence_proxy_async();
@@ -402,7 +432,7 @@ __global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, co
     __syncthreads();
     tc_fence_after();
     if (tid == 0) {
-        const uint32_t idesc = idesc_i8(128, N);
+        const uint32_t idesc = idesc_i8(128, N, false);  // probe: U8 x U8
         for (int k = 0; k < K; k += 32) {
             const uint64_t bdesc = desc_kmajor(smem_u32(cm) + (k / 8) * 128, 256, 128);
             mma_i8_ts(tmem + 256, tmem + k / 4, bdesc, idesc, k != 0);
