@@ -537,11 +537,22 @@ __device__ uint32_t powmod_d(uint64_t b, uint64_t e) {
     return (uint32_t)r;
 }
 
-// tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P.
+// tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P (Montgomery
+// form).  Each thread owns 64 consecutive exponents: one modular power for the
+// first, then a Montgomery chain (mont(x * R, w * R) = x w R), canonicalised.
 __global__ void twiddle_table_kernel(uint32_t *tw, uint32_t *itw, uint32_t Pn, uint32_t w, uint32_t iw) {
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < Pn; e += gridDim.x * blockDim.x) {
-        tw[e] = (uint32_t)(((uint64_t)powmod_d(w, e) << 32) % P);
-        itw[e] = (uint32_t)(((uint64_t)powmod_d(iw, e) << 32) % P);
+    const uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) * 64u;
+    if (e0 >= Pn) return;
+    const uint32_t wM = (uint32_t)(((uint64_t)w << 32) % P), iwM = (uint32_t)(((uint64_t)iw << 32) % P);
+    uint32_t a = (uint32_t)(((uint64_t)powmod_d(w, e0) << 32) % P);
+    uint32_t b = (uint32_t)(((uint64_t)powmod_d(iw, e0) << 32) % P);
+    for (uint32_t k = 0; k < 64 && e0 + k < Pn; ++k) {
+        tw[e0 + k] = a;
+        itw[e0 + k] = b;
+        a = mont(a, wM);
+        a = a >= P ? a - P : a;
+        b = mont(b, iwM);
+        b = b >= P ? b - P : b;
     }
 }
 
@@ -724,8 +735,8 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, c
     QRNG_CUDA_TRY(cudaMallocAsync(&seed_words, nwords * 4, s));
     const uint64_t w = powmod_h(3, (P - 1) >> logP), iw = powmod_h(w, P - 2);
     count_launch();
-    twiddle_table_kernel<<<(unsigned)((Pn + 255) / 256 < 1024 ? (Pn + 255) / 256 : 1024), 256, 0, s>>>(
-        pl.tw, pl.itw, (uint32_t)Pn, (uint32_t)w, (uint32_t)iw);
+    twiddle_table_kernel<<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
+                                                                     (uint32_t)w, (uint32_t)iw);
     QRNG_CUDA_TRY(cudaGetLastError());
     count_launch();
     seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_words, nwords);

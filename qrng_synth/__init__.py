@@ -58,6 +58,14 @@ CONFIGS = {
 }
 
 
+def config4b(m: int) -> Workload:
+    """Config 4b: config 4's samples with m from the corrected min-entropy
+    (qrng_minentropy with s = 0; SURVEY reading A8).  Its seed (L = n + m - 1
+    bits) is drawn with tag 1."""
+    c4 = CONFIGS[4]
+    return Workload("cfg4b_n1048576", 4, c4.n, int(m), c4.n_blocks, c4.sigma)
+
+
 def sweep_workload(log2n: int) -> Workload:
     """Config 5: fixed 2**30-bit raw sequence, n = 2**log2n, m = floor(0.7 n)."""
     n = 1 << log2n
@@ -101,7 +109,7 @@ def workload_inputs(w: Workload, first_block: int = 0, n_blocks: int | None = No
     assert w.n % 8 == 0
     bpb = w.n // 8
     raw = adc_samples(w.key, n_blocks * bpb, w.mu, w.sigma, start=first_block * bpb)
-    tag = w.n if w.key == 5 else 0
+    tag = w.n if w.key == 5 else (1 if w.name.startswith("cfg4b") else 0)
     return raw, uniform_bits(w.key, w.seed_bits, tag)
 
 

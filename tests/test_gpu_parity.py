@@ -268,3 +268,22 @@ def test_host_buffers_pipelined_chunks(q, oracle_mod, n, m, B):
     q.toeplitz_extract_host(raw, B, n, m, seed, out)
     assert_same(out[:q.out_bytes(B, m)], oracle_mod.extract(raw, B, n, m, seed), m)
     assert (out[q.out_bytes(B, m):] == 0xA5).all()
+
+
+def test_config4b_m_from_minentropy(q, oracle_mod):
+    """Config 4b (reading A8): m from qrng_minentropy on config 4's samples
+    (s = 0) equals the oracle's; the extraction with that m is bit-exact on
+    sampled outputs and on one complete block."""
+    from oracle import entropy as E
+    w4 = S.CONFIGS[4]
+    raw, _ = S.workload_inputs(w4)
+    rep = q.minentropy(dev(raw), 8, w4.n, 0)
+    ref = E.report(raw, 8, w4.n, 0)
+    assert rep.m == ref.m and 0 < rep.m < w4.m
+    w = S.config4b(rep.m)
+    raw, seed = S.workload_inputs(w)
+    assert seed.size == (w4.n + rep.m - 1 + 7) // 8
+    got = gpu_extract(q, raw, w.n_blocks, w.n, w.m, seed)
+    sampled_check(oracle_mod, got, raw, seed, w.n, w.m, w.n_blocks, key=41)
+    blk = oracle_mod.extract_blocks(raw, [7], w.n, w.m, seed)[0]
+    assert np.array_equal(np.unpackbits(got)[7 * w.m:8 * w.m], np.unpackbits(blk)[:w.m])
