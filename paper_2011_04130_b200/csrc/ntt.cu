@@ -135,15 +135,32 @@ __device__ __forceinline__ void dft_inv(uint32_t (&x)[1 << R]) {
 }
 
 // Register q holds spectrum index k1 = brev(q): multiply it by tau^k1
-// (tauM = tau * 2^32 mod p, Montgomery form).
+// (tauM = tau * 2^32 mod p, Montgomery form).  The powers come from four
+// independent chains tau^(j+1) * (tau^4)^i, so the Montgomery products are not
+// one serial dependency chain.
 template <int R>
 __device__ __forceinline__ void twiddle(uint32_t (&x)[1 << R], uint32_t tauM) {
     constexpr int N = 1 << R;
-    uint32_t pw = tauM;
+    if constexpr (N <= 4) {
+        uint32_t pw = tauM;
 #pragma unroll
-    for (int k = 1; k < N; ++k) {
-        if (k > 1) pw = mont(pw, tauM);
-        x[brev(k, R)] = mont(x[brev(k, R)], pw);
+        for (int k = 1; k < N; ++k) {
+            if (k > 1) pw = mont(pw, tauM);
+            x[brev(k, R)] = mont(x[brev(k, R)], pw);
+        }
+    } else {
+        const uint32_t t2 = mont(tauM, tauM), t3 = mont(t2, tauM), t4 = mont(t2, t2);
+        uint32_t c[4] = {tauM, t2, t3, t4};
+#pragma unroll
+        for (int i = 0; i < N / 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = 4 * i + j + 1;
+                if (k < N) {
+                    if (i > 0) c[j] = mont(c[j], t4);
+                    x[brev(k, R)] = mont(x[brev(k, R)], c[j]);
+                }
+            }
     }
 }
 
