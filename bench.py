@@ -119,6 +119,16 @@ def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool):
     return bfly, "alu", "Gbutterfly/s"
 
 
+def ncu_traffic(workload_name: str, path_name: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return t.get(f"{workload_name}/{path_name}", {}).get("bytes_per_launch")
+    except Exception:
+        return None
+
+
 def alu_peak_gbfly(pk):
     # 148 SMs x 4 SMSP x 32 lanes issue per clock at the max SM clock, over the
     # 7 integer instructions of one lazy Shoup butterfly (DESIGN.md "Roofline").
@@ -133,9 +143,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; QRNG_BENCH_BACKEND=gloo lets the multi-rank plumbing be
+    # smoke-tested with fewer GPUs than ranks (ranks never wait on each other)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("QRNG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     q.load_library()
     w = workload(args.config)
     B = w.n_blocks
@@ -264,7 +281,7 @@ def run_ours(args):
             roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
                     "peak_kind": "derived: 148 SM x 128 int32 lanes/clk x sm_max_mhz / 7 instr per butterfly"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
+        roof["traffic"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
         roof["kernel_ms_per_step"] = kern_ms / args.steps
         roof["kernel_launches_per_step"] = kern_n / args.steps
         roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total / args.steps)
