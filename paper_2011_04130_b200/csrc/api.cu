@@ -242,20 +242,22 @@ qrng_status qrng_toeplitz_extract(const uint8_t *d_raw_bits, uint64_t n_blocks, 
 // their own streams so both PCIe directions overlap the kernels.
 struct CopyStreams {
     int dev = -1;
-    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr, comp2 = nullptr;
 };
 static thread_local CopyStreams g_cs;
 
-static qrng_status copy_streams(int dev, cudaStream_t *h2d, cudaStream_t *d2h) {
+static qrng_status copy_streams(int dev, cudaStream_t *h2d, cudaStream_t *d2h, cudaStream_t *comp2) {
     if (g_cs.dev != dev) {
-        if (g_cs.h2d) { cudaStreamDestroy(g_cs.h2d); cudaStreamDestroy(g_cs.d2h); }
+        if (g_cs.h2d) { cudaStreamDestroy(g_cs.h2d); cudaStreamDestroy(g_cs.d2h); cudaStreamDestroy(g_cs.comp2); }
         g_cs = CopyStreams{};
         QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_cs.h2d, cudaStreamNonBlocking));
         QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_cs.d2h, cudaStreamNonBlocking));
+        QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_cs.comp2, cudaStreamNonBlocking));
         g_cs.dev = dev;
     }
     *h2d = g_cs.h2d;
     *d2h = g_cs.d2h;
+    *comp2 = g_cs.comp2;
     return QRNG_OK;
 }
 
@@ -268,8 +270,8 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     if ((st = device_ready()) != QRNG_OK) return st;
     int dev = 0;
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
-    cudaStream_t s_in, s_out;
-    if ((st = copy_streams(dev, &s_in, &s_out)) != QRNG_OK) return st;
+    cudaStream_t s_in, s_out, s_c2;
+    if ((st = copy_streams(dev, &s_in, &s_out, &s_c2)) != QRNG_OK) return st;
     const uint64_t raw_bytes = n_blocks * n / 8, seed_bytes = (n + m - 1 + 7) / 8,
                    out_bytes = (n_blocks * m + 7) / 8;
     uint8_t *d_raw = nullptr, *d_seed = nullptr, *d_out = nullptr;
@@ -281,7 +283,10 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     st = qrng_plan_create(n, m, d_seed, stream, &plan);
     // Pipeline over chunks of whole 32-block granules: every chunk's key starts
     // on a 32-bit word boundary (32 m % 32 == 0) and its raw bytes on a 16-byte
-    // boundary, so chunks are independent self-contained extractions.
+    // boundary, so chunks are independent self-contained extractions (only the
+    // last chunk can use the plan's partial-word scratch).  Chunk kernels
+    // alternate between two compute streams so a chunk's CTAs fill the SMs the
+    // previous chunk's tail leaves idle.
     const uint64_t G = (n_blocks + 31) / 32, K = G < 8 ? G : 8;
     std::vector<cudaEvent_t> ev(3 * K + 1, nullptr);
     for (auto &e : ev)
@@ -293,6 +298,7 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
         cudaEventRecord(ev[3 * K], stream);  // buffers allocated, plan enqueued
         cudaStreamWaitEvent(s_in, ev[3 * K], 0);
         cudaStreamWaitEvent(s_out, ev[3 * K], 0);
+        cudaStreamWaitEvent(s_c2, ev[3 * K], 0);
     }
     for (uint64_t c = 0; c < K && st == QRNG_OK; ++c) {
         const uint64_t b0 = 32 * (c * G / K), b1 = std::min(n_blocks, 32 * ((c + 1) * G / K));
@@ -304,10 +310,11 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
             break;
         }
         cudaEventRecord(ev[3 * c], s_in);
-        cudaStreamWaitEvent(stream, ev[3 * c], 0);
-        st = qrng_plan_extract(plan, d_raw + r0, b1 - b0, d_out + o0, stream);
+        cudaStream_t sc = (c & 1) ? s_c2 : stream;
+        cudaStreamWaitEvent(sc, ev[3 * c], 0);
+        st = qrng_plan_extract(plan, d_raw + r0, b1 - b0, d_out + o0, sc);
         if (st != QRNG_OK) break;
-        cudaEventRecord(ev[3 * c + 1], stream);
+        cudaEventRecord(ev[3 * c + 1], sc);
         cudaStreamWaitEvent(s_out, ev[3 * c + 1], 0);
         if (cudaMemcpyAsync(h_out + o0, d_out + o0, o1 - o0, cudaMemcpyDeviceToHost, s_out) != cudaSuccess) {
             set_error("D2H copy failed");
@@ -316,8 +323,10 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
         }
         cudaEventRecord(ev[3 * c + 2], s_out);
     }
-    if (ev[3 * K]) {  // join the copy streams back into `stream`
+    if (ev[3 * K]) {  // join the side streams back into `stream`
         cudaEventRecord(ev[3 * K], s_in);
+        cudaStreamWaitEvent(stream, ev[3 * K], 0);
+        cudaEventRecord(ev[3 * K], s_c2);
         cudaStreamWaitEvent(stream, ev[3 * K], 0);
         cudaEventRecord(ev[3 * K], s_out);
         cudaStreamWaitEvent(stream, ev[3 * K], 0);
