@@ -277,9 +277,11 @@ def run_ours(args):
             roof["frac_of_clock_peak"] = achieved / roof["peak_at_sm_max_clock"]
         else:
             achieved = work / per_step_s / 1e9
-            peak = alu_peak_gbfly(pk)
+            peak = q.butterfly_rate() / 1e9
             roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
-                    "peak_kind": "derived: 148 SM x 128 int32 lanes/clk x sm_max_mhz / 7 instr per butterfly"}
+                    "peak_kind": "measured live: register-resident radix-32 fwd+inv modular butterflies on all SMs "
+                                 "(qrng_debug_butterfly_rate, the kernels' own butterfly code)",
+                    "peak_derived_issue_bound": alu_peak_gbfly(pk)}
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
         roof["kernel_ms_per_step"] = kern_ms / args.steps

@@ -165,6 +165,12 @@ QRNG_API uint64_t    qrng_debug_launch_count(void);
  * path: D (128 x N int32, row-major, device) = A (128 x K uint8 0/1 or any
  * u8, row-major, device) times B^T with the Hankel B[i][k] = h[i + k]
  * (h: N+K bytes, device).  N in [16, 256] multiple of 16, K multiple of 128. */
+/* BENCH ONLY: launch the register-resident radix-32 modular-butterfly
+ * microbenchmark (the NTT path's butterfly code, no memory traffic) on every
+ * SM; *butterflies receives the number of radix-2 butterflies it performs.
+ * Time it with CUDA events on `stream` to get the achievable butterfly rate
+ * (SURVEY.md 8(d) "R_bfly"). */
+QRNG_API qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t stream);
 QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D,
                                            int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);

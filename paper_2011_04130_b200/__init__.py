@@ -31,7 +31,8 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_toeplitz_extract", "qrng_toeplitz_extract_async", "qrng_toeplitz_extract_host",
            "qrng_plan_create", "qrng_plan_extract", "qrng_plan_destroy", "qrng_plan_path",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
-           "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe"]
+           "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
+           "qrng_debug_butterfly_rate"]
 
 
 class QrngError(RuntimeError):
@@ -98,6 +99,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_set_path": ([i32], None),
         "qrng_debug_launch_count": ([], u64),
         "qrng_debug_umma_probe": ([vp, vp, vp, i32, i32, vp], i32),
+        "qrng_debug_butterfly_rate": ([i32, ctypes.POINTER(u64), vp], i32),
         "qrng_debug_kernel_timing": ([i32], None),
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
     }
@@ -163,6 +165,20 @@ def kernel_time_ms() -> tuple[float, int]:
     n = ctypes.c_uint64()
     ms = load_library().qrng_debug_kernel_time_ms(ctypes.byref(n))
     return float(ms), int(n.value)
+
+
+def butterfly_rate(iters: int = 2000, stream=None) -> float:
+    """Achievable modular-butterfly rate (butterflies/s) of the NTT butterfly code."""
+    import torch
+    n = ctypes.c_uint64()
+    s = torch.cuda.current_stream() if stream is None else stream
+    _check(load_library().qrng_debug_butterfly_rate(8, ctypes.byref(n), s.cuda_stream))  # warm-up
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    _check(load_library().qrng_debug_butterfly_rate(iters, ctypes.byref(n), s.cuda_stream))
+    b.record(s)
+    b.synchronize()
+    return n.value / (a.elapsed_time(b) * 1e-3)
 
 
 def umma_probe(A, h, N: int, K: int, stream=None):

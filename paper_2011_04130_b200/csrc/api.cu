@@ -129,6 +129,12 @@ const char *qrng_last_error(void) { return g_err; }
 const char *qrng_version(void) { return "qrng-b200 0.1 sm_100a"; }
 void qrng_debug_set_path(int path) { g_debug_path = path; }
 uint64_t qrng_debug_launch_count(void) { return g_launches.load(); }
+qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t stream) {
+    if (!butterflies || iters <= 0) { set_error("bad arguments"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    return ntt::butterfly_rate(iters, butterflies, stream);
+}
 qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D, int N, int K,
                                   cudaStream_t stream) {
     if (!d_A || !d_h || !d_D) { set_error("NULL buffer"); return QRNG_E_INVALID; }

@@ -679,6 +679,41 @@ static qrng_status launch_seed(const uint32_t *seed_words, uint32_t L, const uin
 
 static uint64_t powmod_h(uint64_t b, uint64_t e) { return powmod_c(b, e); }
 
+// ---- butterfly-rate microbenchmark (the NTT roofline denominator) ----------
+// Register-resident radix-32 forward DIF + inverse DIT with the exact butterfly
+// code of the kernels above (Shoup with constant-bank roots, lazy [0, 2p)
+// reductions, 49 of 80 butterflies per DFT non-trivial), repeated `iters` times
+// per thread on every SM; no memory traffic inside the loop.  Counted work:
+// 160 radix-2 butterflies per iteration per thread.
+__global__ void __launch_bounds__(512, 2) butterfly_rate_kernel(uint32_t *sink, int iters) {
+    uint32_t x[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) x[q] = (threadIdx.x * 32u + q) % P;
+    for (int it = 0; it < iters; ++it) {
+        dft_fwd<5>(x);
+        dft_inv<5>(x);
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc ^= x[q];
+    if (acc == 0xFFFFFFFFu) sink[0] = acc;  // keep the work alive
+}
+
+qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    uint32_t *sink = nullptr;
+    QRNG_CUDA_TRY(cudaMallocAsync(&sink, 4, s));
+    const unsigned grid = (unsigned)sms * 2, block = 512;
+    count_launch();
+    butterfly_rate_kernel<<<grid, block, 0, s>>>(sink, iters);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    cudaFreeAsync(sink, s);
+    *butterflies = (uint64_t)grid * block * (uint64_t)iters * 160u;
+    return QRNG_OK;
+}
+
 // ---- multi-pass launch helpers ---------------------------------------------
 // Global radices for P = 2^logP > 2^15: g = logP - 15 levels before the segments.
 static int global_radices(int logP, int r[2]) {

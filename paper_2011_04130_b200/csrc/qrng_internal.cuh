@@ -74,6 +74,7 @@ void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
 int choose_pack_shift(uint64_t n, int logP);
+qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s);
 }  // namespace ntt
 
 // GEMM path (gemm_tc.cu): tcgen05 kind::i8 batched Toeplitz product.
