@@ -7,6 +7,7 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <set>
 #include <algorithm>
 #include <vector>
 #include "qrng_internal.cuh"
@@ -30,6 +31,18 @@ static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+qrng_status allow_max_smem(const void *func) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({func, dev})) return QRNG_OK;
+    QRNG_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    done.insert({func, dev});
+    return QRNG_OK;
+}
+
 KernelTimer::KernelTimer(cudaStream_t st, bool timed) : s(st) {
     count_launch();
     if (!timed || !g_timing.load()) return;
@@ -45,7 +58,7 @@ void KernelTimer::stop() {
 
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
 static uint64_t g_gemm_max_n = 1ull << 16;
-static int g_debug_path = QRNG_PATH_AUTO;
+static std::atomic<int> g_debug_path{QRNG_PATH_AUTO};
 
 // One-time device check: sm_100 required (no CPU fallback), stream-ordered
 // pool kept warm so per-call workspace allocation is cheap.
@@ -107,7 +120,6 @@ struct qrng_plan {
     int path = QRNG_PATH_NTT;
     ntt::Plan ntt;
     gemm::Plan gemm;
-    uint32_t *tail = nullptr;  // scratch word for a final partial output word
 };
 
 static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
@@ -119,7 +131,6 @@ static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
     };
     fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.work);
     fr(p->gemm.seed_words);
-    fr(p->tail);
     delete p;
 }
 
@@ -127,7 +138,7 @@ extern "C" {
 
 const char *qrng_last_error(void) { return g_err; }
 const char *qrng_version(void) { return "qrng-b200 0.1 sm_100a"; }
-void qrng_debug_set_path(int path) { g_debug_path = path; }
+void qrng_debug_set_path(int path) { g_debug_path.store(path); }
 uint64_t qrng_debug_launch_count(void) { return g_launches.load(); }
 qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t stream) {
     if (!butterflies || iters <= 0) { set_error("bad arguments"); return QRNG_E_INVALID; }
@@ -172,7 +183,7 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     if (!p) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
     p->n = n;
     p->m = m;
-    int want = g_debug_path;
+    int want = g_debug_path.load();
     if (want == QRNG_PATH_AUTO) want = (gemm::supported(n, m) && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
     if (want == QRNG_PATH_GEMM && !gemm::supported(n, m)) {
         set_error("GEMM path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
@@ -180,8 +191,6 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
         return QRNG_E_UNSUPPORTED;
     }
     p->path = want;
-    cudaError_t e = cudaMallocAsync(&p->tail, 4, stream);
-    if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); delete p; return QRNG_E_NOMEM; }
     st = (want == QRNG_PATH_GEMM) ? gemm::plan_init(p->gemm, n, m, d_seed, stream)
                                   : ntt::plan_init(p->ntt, n, m, d_seed, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
@@ -206,16 +215,25 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
     o.words = reinterpret_cast<uint32_t *>(d_out);
     o.total_bits = out_bits;
     o.full_words = out_bytes / 4;
-    o.tail = plan->tail;
+    o.tail = nullptr;
+    // A final partial 32-bit word (out_bytes % 4 != 0) is assembled in a 4-byte
+    // scratch owned by this call (so concurrent calls on one plan never share
+    // it) and its valid bytes copied back: nothing past out_bytes is touched.
+    if (out_bytes % 4) {
+        cudaError_t e = cudaMallocAsync(&o.tail, 4, stream);
+        if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); return QRNG_E_NOMEM; }
+        QRNG_CUDA_TRY(cudaMemsetAsync(o.tail, 0, 4, stream));
+    }
     QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
-    if (out_bytes % 4) QRNG_CUDA_TRY(cudaMemsetAsync(plan->tail, 0, 4, stream));
     qrng_status st = (plan->path == QRNG_PATH_GEMM) ? gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
                                                     : ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream);
-    if (st != QRNG_OK) return st;
-    if (out_bytes % 4)
-        QRNG_CUDA_TRY(cudaMemcpyAsync(d_out + (out_bytes / 4) * 4, plan->tail, out_bytes % 4,
-                                      cudaMemcpyDeviceToDevice, stream));
-    return QRNG_OK;
+    if (st == QRNG_OK && o.tail) {
+        cudaError_t e = cudaMemcpyAsync(d_out + (out_bytes / 4) * 4, o.tail, out_bytes % 4,
+                                        cudaMemcpyDeviceToDevice, stream);
+        if (e != cudaSuccess) { set_error("tail copy: %s", cudaGetErrorString(e)); st = QRNG_E_CUDA; }
+    }
+    if (o.tail) cudaFreeAsync(o.tail, stream);
+    return st;
 }
 
 qrng_status qrng_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks, uint64_t n, uint64_t m,
@@ -289,8 +307,7 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     st = qrng_plan_create(n, m, d_seed, stream, &plan);
     // Pipeline over chunks of whole 32-block granules: every chunk's key starts
     // on a 32-bit word boundary (32 m % 32 == 0) and its raw bytes on a 16-byte
-    // boundary, so chunks are independent self-contained extractions (only the
-    // last chunk can use the plan's partial-word scratch).  Chunk kernels
+    // boundary, so chunks are independent self-contained extractions.  Chunk kernels
     // alternate between two compute streams so a chunk's CTAs fill the SMs the
     // previous chunk's tail leaves idle.
     const uint64_t G = (n_blocks + 31) / 32, K = G < 8 ? G : 8;

@@ -525,11 +525,9 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const size_t smem = smem_bytes(a.seed_words_n);
-    static bool attr = false;
-    if (!attr) {
-        QRNG_CUDA_TRY(cudaFuncSetAttribute(toeplitz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           227 * 1024));
-        attr = true;
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel));
+        if (st != QRNG_OK) return st;
     }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
@@ -546,7 +544,10 @@ qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, 
         return QRNG_E_INVALID;
     }
     const size_t smem = 1024 + (size_t)(K / 8 + N / 8 - 1) * 128;
-    QRNG_CUDA_TRY(cudaFuncSetAttribute(umma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(umma_probe_kernel));
+        if (st != QRNG_OK) return st;
+    }
     count_launch();
     umma_probe_kernel<<<1, 128, smem, s>>>(A, h, D, N, K);
     QRNG_CUDA_TRY(cudaGetLastError());

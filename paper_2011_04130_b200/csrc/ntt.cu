@@ -645,11 +645,9 @@ template <int LOGP, bool PACK>
 static qrng_status launch_fused(const FusedArgs &a, cudaStream_t s) {
     const int per = PACK ? 2 : 1;
     const size_t smem = ((size_t)(1 << LOGP) + (1 << LOGP) / 32 + a.stage_words) * 4;
-    static bool attr = false;
-    if (!attr) {
-        QRNG_CUDA_TRY(cudaFuncSetAttribute(ntt_fused_kernel<LOGP, PACK>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(ntt_fused_kernel<LOGP, PACK>));
+        if (st != QRNG_OK) return st;
     }
     uint64_t grid = (a.n_blocks + per - 1) / per;
     KernelTimer t(s, true);
@@ -663,11 +661,9 @@ template <int LOGP>
 static qrng_status launch_seed(const uint32_t *seed_words, uint32_t L, const uint32_t *tw,
                                uint32_t *shat, uint32_t scaleM, cudaStream_t s) {
     const size_t smem = ((size_t)(1 << LOGP) + (1 << LOGP) / 32) * 4;
-    static bool attr = false;
-    if (!attr) {
-        QRNG_CUDA_TRY(cudaFuncSetAttribute(seed_fused_kernel<LOGP>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(seed_fused_kernel<LOGP>));
+        if (st != QRNG_OK) return st;
     }
     count_launch();
     seed_fused_kernel<LOGP><<<1, threads_of(LOGP), smem, s>>>(seed_words, L, tw, shat, scaleM);
@@ -746,11 +742,9 @@ template <int MODE>
 static qrng_status launch_segments(const FusedArgs &a, uint32_t *ws, int logP, uint64_t nb, cudaStream_t s,
                                    bool timed) {
     const size_t smem = ((size_t)(1 << kSegLog) + (1 << kSegLog) / 32) * 4;
-    static bool attr = false;
-    if (!attr) {
-        QRNG_CUDA_TRY(cudaFuncSetAttribute(ntt_segment_kernel<kSegLog, MODE>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(ntt_segment_kernel<kSegLog, MODE>));
+        if (st != QRNG_OK) return st;
     }
     dim3 grid((unsigned)(1u << (logP - kSegLog)), (unsigned)nb);
     KernelTimer t(s, timed);

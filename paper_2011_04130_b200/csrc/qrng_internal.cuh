@@ -20,6 +20,10 @@ void set_error(const char *fmt, ...);
         }                                                                            \
     } while (0)
 
+// Opt a kernel into the full 227 KB of dynamic shared memory on the current
+// device (once per kernel per device; a process may drive several GPUs).
+qrng_status allow_max_smem(const void *func);
+
 // Launch accounting / optional per-kernel event timing (qrng_debug_*).
 void count_launch();
 struct KernelTimer {  // brackets one extraction kernel on its stream (counts every launch)

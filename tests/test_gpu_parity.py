@@ -287,3 +287,27 @@ def test_config4b_m_from_minentropy(q, oracle_mod):
     sampled_check(oracle_mod, got, raw, seed, w.n, w.m, w.n_blocks, key=41)
     blk = oracle_mod.extract_blocks(raw, [7], w.n, w.m, seed)[0]
     assert np.array_equal(np.unpackbits(got)[7 * w.m:8 * w.m], np.unpackbits(blk)[:w.m])
+
+
+def test_one_plan_two_streams_concurrently(q, oracle_mod):
+    """The header allows one plan on several streams at once: two batches with a
+    partial final word each, launched back to back on two streams."""
+    n, m = 1024, 179
+    seed = S.random_bytes(77, (n + m - 1 + 7) // 8, tag=2)
+    raws = [S.random_bytes(78 + k, B * n // 8) for k, B in enumerate((33, 45))]
+    refs = [oracle_mod.extract(r, len(r) * 8 // n, n, m, seed) for r in raws]
+    for path in (q.PATH_GEMM, q.PATH_NTT):
+        q.set_debug_path(path)
+        try:
+            with q.Plan(n, m, dev(seed)) as plan:
+                streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+                outs = []
+                for r, st in zip(raws, streams):
+                    with torch.cuda.stream(st):
+                        d = dev(r)
+                        outs.append(plan.extract(d, len(r) * 8 // n, stream=st))
+                torch.cuda.synchronize()
+                for o, ref in zip(outs, refs):
+                    assert_same(o.cpu().numpy(), ref, m)
+        finally:
+            q.set_debug_path(q.PATH_AUTO)
