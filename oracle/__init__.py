@@ -7,6 +7,7 @@ with it.
 
 * :mod:`oracle.toeplitz_oracle.c` -- the extraction y = T x mod 2 written out
   from the definition, scalar and 64-bit word modes.
+  Also the modified Toeplitz [T | I_m] of PAPER.md:253-267 (modified_extract).
 * :mod:`oracle.entropy` -- H_min, statistical distance, Delta H_m, corrected
   H_min and the output length m.
 """
@@ -50,6 +51,8 @@ def _load():
         lib.oracle_extract_rows.argtypes = [u8p, ctypes.POINTER(u64), ctypes.POINTER(u64), u64, u64, u64,
                                             u8p, u8p, ctypes.c_int]
         lib.oracle_extract_rows.restype = ctypes.c_int
+        lib.oracle_modified_extract.argtypes = [u8p, u64, u64, u64, u8p, u8p, ctypes.c_int]
+        lib.oracle_modified_extract.restype = ctypes.c_int
         lib.oracle_hist256.argtypes = [u8p, u64, ctypes.POINTER(u64)]
         lib.oracle_hist256.restype = None
         lib.oracle_max_threads.restype = ctypes.c_int
@@ -112,6 +115,19 @@ def extract_rows(raw: np.ndarray, blocks, rows, n: int, m: int, seed: np.ndarray
     rc = _load().oracle_extract_rows(_p(raw), _p(blocks, ctypes.c_uint64), _p(rows, ctypes.c_uint64),
                                      blocks.size, n, m, _p(seed), _p(out), threads)
     if rc != 0:
+        raise ValueError("oracle rejected arguments")
+    return out
+
+
+def modified_extract(raw: np.ndarray, n_blocks: int, n: int, m: int, seed: np.ndarray,
+                     threads: int = 0) -> np.ndarray:
+    """Modified Toeplitz [T | I_m] with an n-bit seed, literal loop."""
+    raw = np.ascontiguousarray(raw, dtype=np.uint8)
+    seed = np.ascontiguousarray(seed, dtype=np.uint8)
+    if raw.size * 8 < n_blocks * n or seed.size * 8 < n:
+        raise ValueError("buffer too short")
+    out = np.zeros((n_blocks * m + 7) // 8, dtype=np.uint8)
+    if _load().oracle_modified_extract(_p(raw), n_blocks, n, m, _p(seed), _p(out), threads) != 0:
         raise ValueError("oracle rejected arguments")
     return out
 

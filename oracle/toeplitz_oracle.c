@@ -274,3 +274,39 @@ int oracle_extract_rows(const uint8_t *raw, const uint64_t *blocks, const uint64
     free(c.rs);
     return err ? -1 : 0;
 }
+
+/* ---- modified Toeplitz (Sec. III.D; Listing 3 at 415-429) ----
+ * k = [T_{m x (n-m)} || I_m] r with an n-bit seed a' = (a_1..a_n).  Reading
+ * A24: T is "the last m rows and the first (n-m) columns" of the
+ * n x n circulant A_c with first column a', A_c[i][j] =
+ * a'[(i - j) mod n] (0-based), and "k_i = k'_i + r_{i+1} (n-m <= i <= n-1)"
+ * adds the last m raw bits.  With t = i - (n-m) in [0, m):
+ *
+ *     y_t = XOR_{j < n-m} ( a'[(n-m+t-j) mod n] AND r_j )  XOR  r_{n-m+t}.
+ *
+ * Literal bit loop; seed buffer holds n bits MSB-first (C2), block b is raw
+ * bits [b n, (b+1) n) (C3), output as C4. */
+int oracle_modified_extract(const uint8_t *raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                            const uint8_t *seed, uint8_t *out, int n_threads) {
+    if (check_args(n_blocks, n, m)) return -1;
+    set_threads(n_threads);
+    memset(out, 0, (n_blocks * m + 7) / 8);
+    uint64_t blk_bytes = (m + 7) / 8;
+    uint8_t *scratch = (uint8_t *)calloc(n_blocks, blk_bytes);
+    if (!scratch) return -1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < (int64_t)n_blocks; ++b) {
+        for (uint64_t t = 0; t < m; ++t) {
+            uint64_t i = n - m + t;  /* row of A_c */
+            int acc = get_bit(raw, (uint64_t)b * n + i);  /* I_m part: r_{i+1} (1-based) */
+            for (uint64_t j = 0; j < n - m; ++j)
+                acc ^= get_bit(seed, (i + n - j) % n) & get_bit(raw, (uint64_t)b * n + j);
+            or_bit(scratch + (uint64_t)b * blk_bytes, t, acc);
+        }
+    }
+    for (uint64_t b = 0; b < n_blocks; ++b)
+        for (uint64_t t = 0; t < m; ++t)
+            or_bit(out, b * m + t, get_bit(scratch + b * blk_bytes, t));
+    free(scratch);
+    return 0;
+}
