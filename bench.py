@@ -107,12 +107,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool):
-    """Roofline numerators, per launch of the main kernel."""
+def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False):
+    """Roofline numerators, per step of the main kernel(s)."""
     import paper_2011_04130_b200 as q
     if path == q.PATH_GEMM:
         return 2.0 * w.m * w.n * n_blocks, "tensor", "TOPS"  # int8 ops of D = T X
-    L = w.n + w.m - 1
+    L = (w.n - 1) if modified else (w.n + w.m - 1)
     P = 1 << max(5, math.ceil(math.log2(L)))
     transforms = (n_blocks + 1) // 2 if pack else n_blocks
     bfly = transforms * (P * math.log2(P) + P)  # fwd + inv radix-2 butterflies (P/2 log P each) + P products
@@ -127,6 +127,15 @@ def ncu_traffic(workload_name: str, path_name: str):
         return t.get(f"{workload_name}/{path_name}", {}).get("bytes_per_launch")
     except Exception:
         return None
+
+
+def ntt_two_blocks(w: S.Workload, modified: bool) -> bool:
+    """Whether the fused NTT kernel packs two blocks per transform (ntt.cu
+    choose_pack_shift): window sums <= n_len < 2^k and n_len (2^k + 1) < p, P <= 2^15."""
+    n_len = w.n - w.m if modified else w.n
+    L = (w.n - 1) if modified else (w.n + w.m - 1)
+    k = n_len.bit_length()
+    return L <= (1 << 15) and n_len * ((1 << k) + 1) < 998244353
 
 
 def alu_peak_gbfly(pk):
@@ -179,9 +188,11 @@ def run_ours(args):
                         "delta_h_m": rep.delta_h_m, "h_min_mod": rep.h_min_mod,
                         "hist_ms": e0.elapsed_time(e1)}
         del samples
-    seed = torch.empty((w.seed_bits + 7) // 8, dtype=torch.uint8, device="cuda")
+    modified = args.variant == "modified"
+    seed_np = S.uniform_bits(w.key, w.n, tag=9) if modified else S.workload_inputs(w, 0, 1)[1]
+    seed = torch.empty(seed_np.size, dtype=torch.uint8, device="cuda")
     if rank == 0:
-        seed.copy_(torch.from_numpy(S.workload_inputs(w, 0, 1)[1]))
+        seed.copy_(torch.from_numpy(seed_np))
     if world > 1:
         from paper_2011_04130_b200 import dist as qd
         qd.broadcast_seed(seed, 0)  # N1: the one collective, outside the timed loop
@@ -193,14 +204,17 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step():
-        q.toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
+        if modified:  # [T | I_m] with an n-bit seed, NTT path
+            q.modified_toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
+        else:
+            q.toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    with q.Plan(w.n, w.m, seed) as pl:
+    with q.Plan(w.n, w.m, seed, modified=modified) as pl:
         path = pl.path
-    pack = w.n <= (1 << 14)
+    pack = ntt_two_blocks(w, modified)
     # timed region
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -233,7 +247,7 @@ def run_ours(args):
 
     # ---- end to end through the host-buffer C-ABI call (pinned buffers) ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not modified:
         h_raw = torch.from_numpy(raw_np).pin_memory()
         h_seed = seed.cpu().pin_memory()
         h_out = torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8).pin_memory()
@@ -260,7 +274,7 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel ----
     pk, pk_kind = peaks()
-    work, bound, unit = algorithmic_work(path, w, B, pack)
+    work, bound, unit = algorithmic_work(path, w, B, pack, modified)
     roof = None
     if kern_n:
         # the path's extraction kernel(s) of one step (GEMM and fused NTT: one
@@ -299,7 +313,9 @@ def run_ours(args):
                    "raw_bits_per_gpu": w.raw_bits, "path": {1: "gemm", 2: "ntt"}[path],
                    "two_blocks_per_transform": bool(pack and path == 2),
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
-                   "step": "one-shot qrng_toeplitz_extract_async (seed prep + clear + extract)",
+                   "variant": args.variant,
+                   "step": ("one-shot qrng_modified_toeplitz_extract_async" if modified else
+                            "one-shot qrng_toeplitz_extract_async") + " (seed prep + clear + extract)",
                    "parallelism": f"block-sharded x{world}"},
         "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
     }
@@ -390,6 +406,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--path", choices=["auto", "gemm", "ntt"], default="auto")
+    ap.add_argument("--variant", choices=["standard", "modified"], default="standard",
+                    help="modified = [T | I_m] with an n-bit seed (PAPER.md:253-267, NEXT-1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

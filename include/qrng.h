@@ -140,6 +140,22 @@ QRNG_API qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_s
 QRNG_API qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits,
                               uint64_t n_blocks, uint8_t *d_out, cudaStream_t stream);
 QRNG_API void        qrng_plan_destroy(qrng_plan *plan);
+
+/* Modified Toeplitz extraction (Sec. III.D; Listing 3 at
+ * PAPER.md:415-429): k = [T_{m x (n-m)} | I_m] r with an n-bit seed a' =
+ * (a_1..a_n) instead of n+m-1 bits.  Reading A24: T = the last m
+ * rows and first n-m columns of the n x n circulant A_c with first column a'
+ * (PAPER.md:257), plus the last m raw bits (k_i = k'_i + r_{i+1}):
+ *     y_t = XOR_{j<n-m} a'[(n-m+t-j) mod n] AND r_j  XOR  r_{n-m+t},  0 <= t < m.
+ * d_seed holds the n seed bits (C2); raw/out layouts, alignment and errors as
+ * qrng_toeplitz_extract (n % 32 == 0, n - 1 <= 2^23).  Runs on the NTT path
+ * (transform length 2^ceil(log2(n-1)) instead of 2^ceil(log2(n+m-1))).  The
+ * plan works with qrng_plan_extract / qrng_plan_destroy. */
+QRNG_API qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uint8_t *d_seed,
+                                               cudaStream_t stream, qrng_plan **plan);
+QRNG_API qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks,
+                                                          uint64_t n, uint64_t m, const uint8_t *d_seed,
+                                                          uint8_t *d_out, cudaStream_t stream);
 /* Path the plan runs (QRNG_PATH_GEMM or QRNG_PATH_NTT); -1 for NULL. */
 QRNG_API int         qrng_plan_path(const qrng_plan *plan);
 

@@ -53,6 +53,9 @@ def _load():
         lib.oracle_extract_rows.restype = ctypes.c_int
         lib.oracle_modified_extract.argtypes = [u8p, u64, u64, u64, u8p, u8p, ctypes.c_int]
         lib.oracle_modified_extract.restype = ctypes.c_int
+        lib.oracle_modified_rows.argtypes = [u8p, ctypes.POINTER(u64), ctypes.POINTER(u64), u64, u64, u64,
+                                             u8p, u8p, ctypes.c_int]
+        lib.oracle_modified_rows.restype = ctypes.c_int
         lib.oracle_hist256.argtypes = [u8p, u64, ctypes.POINTER(u64)]
         lib.oracle_hist256.restype = None
         lib.oracle_max_threads.restype = ctypes.c_int
@@ -128,6 +131,21 @@ def modified_extract(raw: np.ndarray, n_blocks: int, n: int, m: int, seed: np.nd
         raise ValueError("buffer too short")
     out = np.zeros((n_blocks * m + 7) // 8, dtype=np.uint8)
     if _load().oracle_modified_extract(_p(raw), n_blocks, n, m, _p(seed), _p(out), threads) != 0:
+        raise ValueError("oracle rejected arguments")
+    return out
+
+
+def modified_rows(raw: np.ndarray, blocks, rows, n: int, m: int, seed: np.ndarray,
+                  threads: int = 0) -> np.ndarray:
+    """Sampled outputs of the modified Toeplitz (word-parallel form of the same formula)."""
+    raw = np.ascontiguousarray(raw, dtype=np.uint8)
+    seed = np.ascontiguousarray(seed, dtype=np.uint8)
+    blocks = np.ascontiguousarray(np.asarray(blocks, dtype=np.uint64))
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.uint64))
+    out = np.zeros(blocks.size, dtype=np.uint8)
+    rc = _load().oracle_modified_rows(_p(raw), _p(blocks, ctypes.c_uint64), _p(rows, ctypes.c_uint64),
+                                      blocks.size, n, m, _p(seed), _p(out), threads)
+    if rc != 0:
         raise ValueError("oracle rejected arguments")
     return out
 

@@ -310,3 +310,49 @@ int oracle_modified_extract(const uint8_t *raw, uint64_t n_blocks, uint64_t n, u
     free(scratch);
     return 0;
 }
+
+/* Modified Toeplitz, sampled outputs, 64 values of j per AND/XOR: the same
+ * formula as oracle_modified_extract, y_t = XOR_{j<n-m} a'[n-m+t-j] r_j XOR
+ * r_{n-m+t} (no wrap occurs for t < m, j < n-m).  Row t of T, read along j, is
+ * a window of the reversed sequence of a'[1..n-1]. */
+int oracle_modified_rows(const uint8_t *raw, const uint64_t *blocks, const uint64_t *rows,
+                         uint64_t count, uint64_t n, uint64_t m, const uint8_t *seed,
+                         uint8_t *out, int n_threads) {
+    if (check_args(1, n, m)) return -1;
+    for (uint64_t q = 0; q < count; ++q)
+        if (rows[q] >= m) return -1;
+    set_threads(n_threads);
+    const uint64_t np = n - m;  /* columns of T */
+    /* s[k] = a'[k+1], k < n-1 (packed MSB-first) */
+    uint8_t *s = (uint8_t *)calloc((n + 7) / 8 + 1, 1);
+    if (!s) return -1;
+    for (uint64_t k = 0; k + 1 < n; ++k) or_bit(s, k, get_bit(seed, k + 1));
+    seed_ctx c;
+    if (seed_ctx_init(&c, s, np, m)) { free(s); return -1; }  /* L = np + m - 1 = n - 1 */
+    int err = 0;
+#pragma omp parallel
+    {
+        uint64_t *xw = (uint64_t *)malloc(c.nw * sizeof(uint64_t));
+        uint64_t cur = UINT64_MAX;
+        if (!xw) {
+#pragma omp atomic write
+            err = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t q = 0; q < (int64_t)count; ++q) {
+                if (blocks[q] != cur) {
+                    pack_lsb64(raw, blocks[q] * n, np, xw, c.nw);
+                    cur = blocks[q];
+                }
+                /* T[t][j] = s[t - j + np - 1] = rs[m-1-t+j] */
+                uint64_t o = m - 1 - rows[q], acc = 0;
+                for (uint64_t w = 0; w < c.nw; ++w) acc ^= window64(c.rs, o + 64 * w) & xw[w];
+                out[q] = (uint8_t)((__builtin_popcountll(acc) & 1) ^ get_bit(raw, blocks[q] * n + np + rows[q]));
+            }
+            free(xw);
+        }
+    }
+    free(c.rs);
+    free(s);
+    return err ? -1 : 0;
+}

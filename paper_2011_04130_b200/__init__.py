@@ -30,6 +30,7 @@ STATUS_NAMES = {0: "QRNG_OK", 1: "QRNG_E_INVALID", 2: "QRNG_E_UNSUPPORTED", 3: "
 EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_toeplitz_extract", "qrng_toeplitz_extract_async", "qrng_toeplitz_extract_host",
            "qrng_plan_create", "qrng_plan_extract", "qrng_plan_destroy", "qrng_plan_path",
+           "qrng_plan_create_modified", "qrng_modified_toeplitz_extract_async",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
            "qrng_debug_butterfly_rate"]
@@ -92,6 +93,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_toeplitz_extract_host": ([vp, u64, u64, u64, vp, vp, vp], i32),
         "qrng_plan_create": ([u64, u64, vp, vp, ctypes.POINTER(vp)], i32),
         "qrng_plan_extract": ([vp, vp, u64, vp, vp], i32),
+        "qrng_plan_create_modified": ([u64, u64, vp, vp, ctypes.POINTER(vp)], i32),
+        "qrng_modified_toeplitz_extract_async": ([vp, u64, u64, u64, vp, vp, vp], i32),
         "qrng_plan_destroy": ([vp], None),
         "qrng_plan_path": ([vp], i32),
         "qrng_last_error": ([], ctypes.c_char_p),
@@ -204,6 +207,19 @@ def toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=
     return out
 
 
+def modified_toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=None):
+    """Modified Toeplitz [T | I_m] with an n-bit seed (NTT path)."""
+    import torch
+    _need_cuda_u8(raw, "raw")
+    _need_cuda_u8(seed, "seed")
+    if out is None:
+        out = torch.empty(out_bytes(n_blocks, m), dtype=torch.uint8, device=raw.device)
+    _need_cuda_u8(out, "out")
+    _check(load_library().qrng_modified_toeplitz_extract_async(_ptr(raw), n_blocks, n, m, _ptr(seed), _ptr(out),
+                                                               _stream_handle(stream)))
+    return out
+
+
 def toeplitz_extract_host(raw: np.ndarray, n_blocks: int, n: int, m: int, seed: np.ndarray,
                           out: np.ndarray, stream=None) -> np.ndarray:
     """End-to-end call with HOST buffers (numpy views; pinned memory recommended)."""
@@ -220,11 +236,12 @@ def toeplitz_extract_host(raw: np.ndarray, n_blocks: int, n: int, m: int, seed: 
 class Plan:
     """Seed preparation once per (seed, n, m); extract many batches."""
 
-    def __init__(self, n: int, m: int, seed, stream=None):
+    def __init__(self, n: int, m: int, seed, stream=None, modified: bool = False):
         _need_cuda_u8(seed, "seed")
         self.n, self.m = n, m
         h = ctypes.c_void_p()
-        _check(load_library().qrng_plan_create(n, m, _ptr(seed), _stream_handle(stream), ctypes.byref(h)))
+        create = load_library().qrng_plan_create_modified if modified else load_library().qrng_plan_create
+        _check(create(n, m, _ptr(seed), _stream_handle(stream), ctypes.byref(h)))
         self._h = h
 
     @property

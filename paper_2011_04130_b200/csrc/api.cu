@@ -192,10 +192,59 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     }
     p->path = want;
     st = (want == QRNG_PATH_GEMM) ? gemm::plan_init(p->gemm, n, m, d_seed, stream)
-                                  : ntt::plan_init(p->ntt, n, m, d_seed, stream);
+                                  : ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
     *plan = p;
     return QRNG_OK;
+}
+
+// Modified Toeplitz [T_{m x (n-m)} | I_m]: the product of the
+// first n-m raw bits of each block with T (seed bits a_2..a_n, C1 form with
+// n' = n-m) XOR the block's last m raw bits; always the NTT path.
+qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
+                                      qrng_plan **plan) {
+    if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
+    *plan = nullptr;
+    if (n == 0 || m == 0 || m >= n) {
+        set_error("need 0 < m < n (got n=%llu, m=%llu)", (unsigned long long)n, (unsigned long long)m);
+        return QRNG_E_INVALID;
+    }
+    if (n % 32 != 0) { set_error("n must be a multiple of 32"); return QRNG_E_UNSUPPORTED; }
+    if (n - 1 > (1ull << ntt::kMaxLogP)) { set_error("n - 1 exceeds 2^23"); return QRNG_E_UNSUPPORTED; }
+    if (!d_seed || !aligned16(d_seed)) { set_error("d_seed is NULL or not 16-byte aligned"); return QRNG_E_INVALID; }
+    if (g_debug_path.load() == QRNG_PATH_GEMM) {
+        set_error("the modified Toeplitz runs on the NTT path only");
+        return QRNG_E_UNSUPPORTED;
+    }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    qrng_plan *p = new (std::nothrow) qrng_plan;
+    if (!p) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
+    p->n = n;
+    p->m = m;
+    p->path = QRNG_PATH_NTT;
+    st = ntt::plan_init(p->ntt, n - m, m, d_seed, 1, true, stream);
+    if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
+    *plan = p;
+    return QRNG_OK;
+}
+
+qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks, uint64_t n,
+                                                 uint64_t m, const uint8_t *d_seed, uint8_t *d_out,
+                                                 cudaStream_t stream) {
+    if (!d_raw_bits || !d_seed || !d_out) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    if (n_blocks == 0) { set_error("n_blocks must be > 0"); return QRNG_E_INVALID; }
+    if (n != 0 && m != 0 && n_blocks <= UINT64_MAX / m &&
+        overlap(d_seed, (n + 7) / 8, d_out, (n_blocks * m + 7) / 8)) {
+        set_error("d_out overlaps d_seed");
+        return QRNG_E_INVALID;
+    }
+    qrng_plan *p = nullptr;
+    qrng_status st = qrng_plan_create_modified(n, m, d_seed, stream, &p);
+    if (st != QRNG_OK) return st;
+    st = qrng_plan_extract(p, d_raw_bits, n_blocks, d_out, stream);
+    plan_release(p, stream, true);
+    return st;
 }
 
 void qrng_plan_destroy(qrng_plan *plan) { plan_release(plan, 0, false); }

@@ -189,6 +189,8 @@ struct FusedArgs {
     uint32_t stage_words;     // per-CTA staging words
     uint32_t tw_shift;        // segment mode: log2(P / segment length) (tables are for w_P)
     uint32_t scaleM;          // forward-only mode: P^-1 * 2^64 mod p
+    uint32_t len;             // raw bits used per block (n, or n - m for the modified Toeplitz)
+    uint32_t xor_tail;        // modified Toeplitz: output t also XORs raw bit t + 1 of its block
 };
 
 // Level modes: FUSED = one CTA owns a whole transform (bits in, parity bits
@@ -239,9 +241,14 @@ struct Level {
             const uint32_t *blk = a.raw + b0 * (a.n >> 5);
             uint32_t w1 = 0, w2 = 0;
             const uint32_t myidx = (uint32_t)((lane % N1) * STRIDE + u0);
-            if (lane < N1 && myidx < a.n) {
+            if (lane < N1 && myidx < a.len) {
                 w1 = bswap32(__ldg(blk + (myidx >> 5)));
                 if (PACK && nb > 1) w2 = bswap32(__ldg(blk + (a.n >> 5) + (myidx >> 5)));
+                const uint32_t rem = a.len - myidx;  // bits past len are not part of the product
+                if (rem < 32) {
+                    w1 &= 0xFFFFFFFFu << (32 - rem);
+                    w2 &= 0xFFFFFFFFu << (32 - rem);
+                }
             }
             const int sh = 31 - lane;
 #pragma unroll
@@ -254,7 +261,7 @@ struct Level {
 #pragma unroll
             for (int q = 0; q < N1; ++q) {
                 uint32_t idx = (uint32_t)(q * STRIDE + u), v = 0;
-                if (idx < a.n) {
+                if (idx < a.len) {
                     v = raw_bit(a.raw, b0, a.n, idx);
                     if (PACK && nb > 1) v |= raw_bit(a.raw, b0 + 1, a.n, idx) << a.shift;
                 }
@@ -289,19 +296,25 @@ struct Level {
             uint32_t mine1 = 0, mine2 = 0;
 #pragma unroll
             for (int q = 0; q < N1; ++q) {
-                int64_t i = (int64_t)(q * STRIDE + u) - (int64_t)(a.n - 1);
+                const uint32_t t = (uint32_t)(q * STRIDE + u);
+                int64_t i = (int64_t)t - (int64_t)(a.len - 1);
                 bool valid = i >= 0 && i < (int64_t)a.m;
                 uint32_t z = x[q] >= P ? x[q] - P : x[q];  // canonical residue
-                uint32_t b1 = __ballot_sync(0xffffffffu, valid && (z & 1u));
+                uint32_t x1 = 0, x2 = 0;                   // identity block of [T | I_m]
+                if (a.xor_tail && valid) {
+                    x1 = raw_bit(a.raw, b0, a.n, t + 1);
+                    if (PACK && nb > 1) x2 = raw_bit(a.raw, b0 + 1, a.n, t + 1) << a.shift;
+                }
+                uint32_t b1 = __ballot_sync(0xffffffffu, valid && ((z ^ x1) & 1u));
                 if (lane == (q & 31)) mine1 = b1;
                 if (PACK) {
-                    uint32_t b2 = __ballot_sync(0xffffffffu, valid && ((z >> a.shift) & 1u));
+                    uint32_t b2 = __ballot_sync(0xffffffffu, valid && (((z ^ x2) >> a.shift) & 1u));
                     if (lane == (q & 31)) mine2 = b2;
                 }
                 if ((q & 31) == 31 || q == N1 - 1) {
                     const int qb = q & ~31;
                     if (lane <= (q & 31)) {
-                        int64_t i0 = (int64_t)((qb + lane) * STRIDE + u0) - (int64_t)(a.n - 1);
+                        int64_t i0 = (int64_t)((qb + lane) * STRIDE + u0) - (int64_t)(a.len - 1);
                         stage_or(stage, wfirst, (int64_t)(b0 * a.m) + i0, mine1);
                         if (PACK && nb > 1) stage_or(stage, wfirst, (int64_t)((b0 + 1) * a.m) + i0, mine2);
                     }
@@ -311,9 +324,14 @@ struct Level {
         }
 #pragma unroll
         for (int q = 0; q < N1; ++q) {
-            int64_t i = (int64_t)(q * STRIDE + u) - (int64_t)(a.n - 1);
+            const uint32_t t = (uint32_t)(q * STRIDE + u);
+            int64_t i = (int64_t)t - (int64_t)(a.len - 1);
             if (i >= 0 && i < (int64_t)a.m) {
                 uint32_t z = x[q] >= P ? x[q] - P : x[q];  // canonical residue
+                if (a.xor_tail) {
+                    z ^= raw_bit(a.raw, b0, a.n, t + 1);
+                    if (PACK && nb > 1) z ^= raw_bit(a.raw, b0 + 1, a.n, t + 1) << a.shift;
+                }
                 if (z & 1u) {
                     uint64_t g = b0 * a.m + (uint64_t)i;
                     atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
@@ -443,6 +461,7 @@ struct PassArgs {
     const uint32_t *tw, *itw;
     uint32_t logP, S;         // this pass works on segments of 2^(logP - S) words
     OutStream out;
+    uint32_t xor_tail;        // modified Toeplitz: output t also XORs raw bit t + 1 of its block
 };
 enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4 };
 
@@ -501,15 +520,17 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
     uint32_t mine = 0;
 #pragma unroll
     for (int q = 0; q < N1; ++q) {
-        const int64_t i = (int64_t)q * STRIDE + u - (int64_t)(a.n - 1);
+        const uint32_t t = (uint32_t)q * STRIDE + u;
+        const int64_t i = (int64_t)t - (int64_t)(a.len - 1);
         const bool valid = i >= 0 && i < (int64_t)a.m;
-        const uint32_t z = x[q] >= P ? x[q] - P : x[q];
+        uint32_t z = x[q] >= P ? x[q] - P : x[q];
+        if (a.xor_tail && valid) z ^= raw_bit(a.bits, a.b0 + bb, a.n, t + 1);  // identity block
         const uint32_t bal = __ballot_sync(0xffffffffu, valid && (z & 1u));
         if (lane == (q & 31)) mine = bal;
         if ((q & 31) == 31 || q == N1 - 1) {
             const int qb = q & ~31;
             if (lane <= (q & 31) && mine) {
-                const int64_t i0 = (int64_t)(qb + lane) * STRIDE + u0 - (int64_t)(a.n - 1);
+                const int64_t i0 = (int64_t)(qb + lane) * STRIDE + u0 - (int64_t)(a.len - 1);
                 const int64_t G = (int64_t)((a.b0 + bb) * a.m) + i0;
                 const uint32_t V = __brev(mine);
                 const int64_t W0 = G >= 0 ? (G >> 5) : -((31 - G) >> 5);
@@ -616,19 +637,21 @@ __global__ void __launch_bounds__(threads_of(LOGP)) seed_fused_kernel(const uint
     seed_levels<LOGP, 0>(smem, seed_words, L, tw, shat, scaleM);
 }
 
-// Seed bytes (MSB-first) -> logical big-endian words (bit k at 31-(k&31)), zero padded.
-__global__ void seed_words_kernel(const uint8_t *seed, uint64_t L, uint32_t *words, uint64_t nwords) {
+// Seed bits [off, off + L) of an MSB-first byte buffer -> logical big-endian
+// words (bit k at 31-(k&31) of word k>>5), zero past L.  off = 1 drops a_1 for
+// the modified Toeplitz (its T uses a_2..a_n).
+__global__ void seed_words_kernel(const uint8_t *seed, uint64_t L, uint32_t off, uint32_t *words,
+                                  uint64_t nwords) {
+    const uint64_t nbytes = (off + L + 7) / 8;
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
          w += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t v = 0;
-        for (int k = 0; k < 4; ++k) {
-            uint64_t byte = w * 4 + k;
-            uint32_t bv = (byte * 8 < L) ? seed[byte] : 0u;
-            v |= bv << (24 - 8 * k);
-        }
-        uint64_t lo = w * 32;  // mask bits >= L
-        if (lo + 32 > L) v &= (L > lo) ? (0xFFFFFFFFu << (32 - (L - lo))) : 0u;
-        words[w] = v;
+        const uint64_t pos = off + w * 32, b0 = pos / 8;
+        uint64_t v = 0;  // 40 bits starting at byte b0
+        for (int k = 0; k < 5; ++k) v = (v << 8) | (b0 + k < nbytes ? seed[b0 + k] : 0u);
+        uint32_t r = (uint32_t)(v >> (8 - (pos & 7)));
+        const uint64_t lo = w * 32;  // mask bits >= L
+        if (lo + 32 > L) r &= (L > lo) ? (0xFFFFFFFFu << (32 - (L - lo))) : 0u;
+        words[w] = r;
     }
 }
 
@@ -761,8 +784,13 @@ static uint64_t batch_blocks(int logP, uint64_t n_blocks) {
     return cap < n_blocks ? cap : n_blocks;
 }
 
-qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s) {
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t seed_bit_offset,
+                      bool xor_tail, cudaStream_t s) {
+    // n here is the number of raw bits per block that enter the product
+    // (n, or n - m for the modified Toeplitz, whose seed starts at bit 1)
     const uint64_t L = n + m - 1;
+    pl.len = (uint32_t)n;
+    pl.xor_tail = xor_tail;
     int logP = 0;
     while ((1ull << logP) < L) ++logP;
     if (logP < 5) logP = 5;
@@ -771,7 +799,7 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, c
         return QRNG_E_UNSUPPORTED;
     }
     pl.logP = logP;
-    pl.pack_shift = logP <= kMaxFusedLogP ? choose_pack_shift(n, logP) : 0;
+    pl.pack_shift = logP <= kMaxFusedLogP ? choose_pack_shift(n, logP) : 0;  // window sums <= n
     const uint64_t Pn = 1ull << logP;
     const uint64_t nwords = (L + 31) / 32 + 1;
     uint32_t *seed_words = nullptr;
@@ -785,7 +813,8 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, c
                                                                      (uint32_t)w, (uint32_t)iw);
     QRNG_CUDA_TRY(cudaGetLastError());
     count_launch();
-    seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_words, nwords);
+    seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_bit_offset, seed_words,
+                                                                      nwords);
     QRNG_CUDA_TRY(cudaGetLastError());
     // scale = P^-1 * 2^64 mod p, so mont(v, scale) = v * P^-1 * 2^32 (Montgomery form for the pointwise product)
     const uint64_t pinvP = powmod_h(Pn % P, P - 2);
@@ -854,9 +883,10 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
     const int np = global_radices(logP, r);
     PassArgs pa{};
     pa.bits = reinterpret_cast<const uint32_t *>(d_raw);
-    pa.n = (uint32_t)n;
+    pa.n = (uint32_t)n;  // block stride
     pa.m = (uint32_t)m;
-    pa.len = (uint32_t)n;
+    pa.len = pl.len;     // bits per block that enter the product
+    pa.xor_tail = pl.xor_tail ? 1u : 0u;
     pa.ws = ws;
     pa.tw = pl.tw;
     pa.itw = pl.itw;
@@ -905,6 +935,8 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.itw = pl.itw;
     a.out = out;
     a.tw_shift = 0;
+    a.len = pl.len;
+    a.xor_tail = pl.xor_tail ? 1u : 0u;
     const int per = pl.pack_shift ? 2 : 1;
     a.stage_words = (uint32_t)((per * m + 31) / 32 + 2);
     switch (pl.logP) {

@@ -66,6 +66,8 @@ constexpr int kMaxFusedLogP = 15;  // one CTA holds the whole transform in smem
 
 struct Plan {
     int logP = 0;
+    uint32_t len = 0;            // raw bits per block entering the product
+    bool xor_tail = false;       // modified Toeplitz identity block
     int pack_shift = 0;          // >0: two blocks share one transform (x1 + 2^shift x2)
     uint32_t *shat = nullptr;    // P words: NTT(seed) * P^-1 * 2^32 mod p, DIF order
     uint32_t *tw = nullptr;      // P words: w_P^e * 2^32 mod p
@@ -73,8 +75,10 @@ struct Plan {
     uint32_t *work = nullptr;    // multipass scratch (not used by the fused kernel)
     size_t work_words = 0;
 };
-qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t seed_bit_offset,
+                      bool xor_tail, cudaStream_t s);
 void plan_free(Plan &pl);
+// n = block stride in bits (the product uses the plan's len bits of each block)
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
 int choose_pack_shift(uint64_t n, int logP);

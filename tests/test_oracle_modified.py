@@ -99,3 +99,16 @@ def test_linearity(oracle_mod):
     a = rng.integers(0, 2, n).astype(np.uint8)
     h = lambda x: run(oracle_mod, x[None], a, n, m)[0]
     assert np.array_equal(h(x1 ^ x2), h(x1) ^ h(x2))
+
+
+def test_rows_mode_equals_literal(oracle_mod):
+    """The word-parallel sampled-row form equals the literal bit loop."""
+    rng = np.random.default_rng(13)
+    for n, m, B in [(64, 20, 3), (96, 95, 2), (1024, 716, 3), (800, 1, 2), (256, 200, 4)]:
+        X = rng.integers(0, 2, (B, n)).astype(np.uint8)
+        a = rng.integers(0, 2, n).astype(np.uint8)
+        full = run(oracle_mod, X, a, n, m)
+        bl = np.repeat(np.arange(B), m)
+        rw = np.tile(np.arange(m), B)
+        got = oracle_mod.modified_rows(pack(X.reshape(-1)), bl, rw, n, m, pack(a))
+        assert np.array_equal(got.reshape(B, m), full)
