@@ -463,7 +463,7 @@ struct PassArgs {
     OutStream out;
     uint32_t xor_tail;        // modified Toeplitz: output t also XORs raw bit t + 1 of its block
 };
-enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4 };
+enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4, PASS_INV_EMIT_XOR = 5 };
 
 template <int R, int MODE>
 __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
         for (int q = 0; q < N1; ++q) base[(size_t)q * STRIDE] = x[q];
         return;
     }
-    // PASS_INV_EMIT (level 0): element q is z_t with t = q*STRIDE + u
+    // PASS_INV_EMIT[_XOR] (level 0): element q is z_t with t = q*STRIDE + u
     const int lane = threadIdx.x & 31;
     const uint32_t u0 = u & ~31u;
     uint32_t mine = 0;
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
         const int64_t i = (int64_t)t - (int64_t)(a.len - 1);
         const bool valid = i >= 0 && i < (int64_t)a.m;
         uint32_t z = x[q] >= P ? x[q] - P : x[q];
-        if (a.xor_tail && valid) z ^= raw_bit(a.bits, a.b0 + bb, a.n, t + 1);  // identity block
+        if (MODE == PASS_INV_EMIT_XOR && valid) z ^= raw_bit(a.bits, a.b0 + bb, a.n, t + 1);  // identity block
         const uint32_t bal = __ballot_sync(0xffffffffu, valid && (z & 1u));
         if (lane == (q & 31)) mine = bal;
         if ((q & 31) == 31 || q == N1 - 1) {
@@ -914,7 +914,8 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
         }
         if (st == QRNG_OK) {
             pa.S = 0;
-            st = launch_pass<PASS_INV_EMIT>(r[0], pa, nb, s, true);
+            st = pl.xor_tail ? launch_pass<PASS_INV_EMIT_XOR>(r[0], pa, nb, s, true)
+                             : launch_pass<PASS_INV_EMIT>(r[0], pa, nb, s, true);
         }
     }
     cudaFreeAsync(ws, s);
