@@ -311,3 +311,37 @@ def test_one_plan_two_streams_concurrently(q, oracle_mod):
                     assert_same(o.cpu().numpy(), ref, m)
         finally:
             q.set_debug_path(q.PATH_AUTO)
+
+
+def test_max_seed_length_2_23(q, oracle_mod):
+    """L = n + m - 1 = 2^23 exactly: the largest transform (P = 2^23, the 2-adic
+    limit of p = 119*2^23 + 1); one bit more is rejected."""
+    n = 5033152  # multiple of 32
+    m = (1 << 23) + 1 - n
+    B = 2
+    raw = S.random_bytes(123, B * n // 8)
+    seed = S.random_bytes(123, (n + m - 1 + 7) // 8, tag=3)
+    got = gpu_extract(q, raw, B, n, m, seed)
+    sampled_check(oracle_mod, got, raw, seed, n, m, B, n_rows=200, key=23)
+    with pytest.raises(q.QrngError) as ei:
+        q.toeplitz_extract(dev(raw), 1, n, m + 1, dev(S.random_bytes(1, (n + m + 7) // 8)))
+    assert ei.value.status == q.QRNG_E_UNSUPPORTED
+
+
+@pytest.mark.parametrize("log2n", [18, 20, 22])
+def test_sweep_points_full_size_sampled(q, oracle_mod, log2n):
+    """Config 5 points over the whole 2^30-bit sequence (what tools/sweep.py times)."""
+    w = S.sweep_workload(log2n)
+    raw, seed = S.workload_inputs(w)
+    got = gpu_extract(q, raw, w.n_blocks, w.n, w.m, seed)
+    sampled_check(oracle_mod, got, raw, seed, w.n, w.m, w.n_blocks, n_rows=64, key=log2n)
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_zero_seed_and_zero_raw(q, oracle_mod, path):
+    n, m, B = 1024, 716, 40
+    raw = S.random_bytes(9, B * n // 8)
+    zero_seed = np.zeros((n + m - 1 + 7) // 8, np.uint8)
+    assert not gpu_extract(q, raw, B, n, m, zero_seed, path_id(q, path)).any()
+    seed = S.random_bytes(9, (n + m - 1 + 7) // 8, tag=2)
+    assert not gpu_extract(q, np.zeros_like(raw), B, n, m, seed, path_id(q, path)).any()
