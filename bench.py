@@ -107,11 +107,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False):
+def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False,
+                     macs_per_block: int = 0):
     """Roofline numerators, per step of the main kernel(s)."""
     import paper_2011_04130_b200 as q
     if path == q.PATH_GEMM:
-        return 2.0 * w.m * w.n * n_blocks, "tensor", "TOPS"  # int8 ops of D = T X
+        # int8 ops the tensor cores run: 2 x the leaf MACs of the Karatsuba
+        # decomposition (= 2 m n per block for the dense product, depth 0)
+        return 2.0 * (macs_per_block or w.m * w.n) * n_blocks, "tensor", "TOPS"
     L = (w.n - 1) if modified else (w.n + w.m - 1)
     P = 1 << max(5, math.ceil(math.log2(L)))
     transforms = (n_blocks + 1) // 2 if pack else n_blocks
@@ -200,6 +203,7 @@ def run_ours(args):
     out = torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8, device="cuda")
     if args.path != "auto":
         q.set_debug_path({"gemm": q.PATH_GEMM, "ntt": q.PATH_NTT}[args.path])
+    q.set_karatsuba(args.karatsuba)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -214,6 +218,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     with q.Plan(w.n, w.m, seed, modified=modified) as pl:
         path = pl.path
+        pinfo = pl.info()
     pack = ntt_two_blocks(w, modified)
     # timed region
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -274,7 +279,7 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel ----
     pk, pk_kind = peaks()
-    work, bound, unit = algorithmic_work(path, w, B, pack, modified)
+    work, bound, unit = algorithmic_work(path, w, B, pack, modified, pinfo["macs_per_block"])
     roof = None
     if kern_n:
         # the path's extraction kernel(s) of one step (GEMM and fused NTT: one
@@ -289,6 +294,8 @@ def run_ours(args):
             clk_mhz = pk.get("sm_max_mhz", 1965.0)
             roof["peak_at_sm_max_clock"] = 148 * 8192 * 2 * clk_mhz * 1e6 / 1e12
             roof["frac_of_clock_peak"] = achieved / roof["peak_at_sm_max_clock"]
+            roof["ops_per_step"] = work
+            roof["dense_ops_per_step"] = 2.0 * w.m * w.n * B  # the O(mn) product without Karatsuba
         else:
             achieved = work / per_step_s / 1e9
             peak = q.butterfly_rate() / 1e9
@@ -312,6 +319,8 @@ def run_ours(args):
         "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_per_gpu": B, "seed_bits": w.seed_bits,
                    "raw_bits_per_gpu": w.raw_bits, "path": {1: "gemm", 2: "ntt"}[path],
                    "two_blocks_per_transform": bool(pack and path == 2),
+                   "karatsuba_depth": pinfo["karatsuba_depth"] if path == 1 else None,
+                   "karatsuba_leaves": pinfo["leaves"] if path == 1 else None,
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
                    "variant": args.variant,
                    "step": ("one-shot qrng_modified_toeplitz_extract_async" if modified else
@@ -408,6 +417,8 @@ def main():
     ap.add_argument("--path", choices=["auto", "gemm", "ntt"], default="auto")
     ap.add_argument("--variant", choices=["standard", "modified"], default="standard",
                     help="modified = [T | I_m] with an n-bit seed (PAPER.md:253-267, NEXT-1)")
+    ap.add_argument("--karatsuba", type=int, default=-1,
+                    help="GEMM path: GF(2) Karatsuba depth (-1 = the library's cost model, 0 = dense)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

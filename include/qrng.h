@@ -159,6 +159,23 @@ QRNG_API qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_b
 /* Path the plan runs (QRNG_PATH_GEMM or QRNG_PATH_NTT); -1 for NULL. */
 QRNG_API int         qrng_plan_path(const qrng_plan *plan);
 
+/* How a plan computes its product (for benchmarks and tests).
+ *   path                 QRNG_PATH_GEMM or QRNG_PATH_NTT
+ *   karatsuba_depth      GEMM path: depth of the GF(2) Karatsuba decomposition
+ *                        (0 = one dense product); see qrng_debug_set_karatsuba
+ *   leaves               GEMM path: Toeplitz products the tensor cores run
+ *   macs_per_block       GEMM path: int8 multiply-accumulates per block over all
+ *                        leaves (n*m for the dense product)
+ *   log2_transform       NTT path: log2 of the cyclic length P
+ *   blocks_per_transform NTT path: 2 when two blocks share one transform
+ * Errors: E_INVALID for NULL arguments. */
+typedef struct {
+    int32_t path, karatsuba_depth, leaves, log2_transform;
+    int32_t blocks_per_transform, reserved;
+    uint64_t macs_per_block;
+} qrng_plan_info_t;
+QRNG_API qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info);
+
 /* Thread-local message for the last non-OK status returned on this thread. */
 QRNG_API const char *qrng_last_error(void);
 /* Library version string, e.g. "qrng-b200 0.1 sm_100a". */
@@ -168,6 +185,31 @@ QRNG_API const char *qrng_version(void);
  * (QRNG_PATH_AUTO restores the measured crossover).  Used to cross-check the
  * two independent GPU paths and to measure the crossover; not a backend switch. */
 QRNG_API void        qrng_debug_set_path(int path);
+
+/* TEST / BENCH ONLY: depth of the GF(2) Karatsuba decomposition used by GEMM-path
+ * plans created afterwards on this process (DESIGN.md "Karatsuba over the GEMM
+ * path"; the identity y = T x is unchanged, only the schedule of tensor-core
+ * products).  -1 (default): the planner's cost model chooses; 0: one dense
+ * product; d > 0: split whenever allowed down to depth d. */
+QRNG_API void        qrng_debug_set_karatsuba(int max_depth);
+
+/* TEST ONLY, host-only (no GPU): the planner's decomposition of an m x n
+ * extraction with max_depth as in qrng_debug_set_karatsuba.  counts[0..3] =
+ * leaves, terms, combine entries, depth.  If the buffers are large enough
+ * (leaf_cap >= leaves, term_cap >= terms, comb_cap >= words + 1 + entries,
+ * words = ceil(m/32)) they receive, per leaf l, leaf_rw[6l..6l+5] = {r, w,
+ * out_off, first term, seed terms, input terms}; terms = the seed-term bit
+ * offsets into s followed by the input-term bit offsets into the block; comb
+ * = CSR row pointers (words + 1) then Y-row word offsets: output word j of a
+ * block is the XOR of Y[comb[...]] where leaf l's parities occupy words
+ * [out_off, out_off + ceil(r/32)) of Y, row i at bit 31 - (i % 32).
+ * Leaf l computes y_l[i] = XOR_j d_l[i - j + w - 1] x_l[j] (i < r, j < w) with
+ * d_l[k] = XOR over seed terms t of s[t + k] (0 past n+m-1) and
+ * x_l[j] = XOR over input terms u of x[u + j].  Errors: E_UNSUPPORTED when no
+ * decomposition exists (n % 128 != 0, m >= n). */
+QRNG_API qrng_status qrng_debug_karatsuba_plan(uint64_t n, uint64_t m, int max_depth, uint32_t *leaf_rw,
+                                               uint32_t leaf_cap, uint32_t *terms, uint32_t term_cap,
+                                               uint32_t *comb, uint32_t comb_cap, uint32_t *counts);
 
 /* BENCH / TEST ONLY instrumentation.
  * qrng_debug_launch_count: number of kernels this library has launched in the
@@ -190,6 +232,10 @@ QRNG_API qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies,
 QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D,
                                            int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);
+/* PROFILING ONLY: 16 clock64 counters summed over all CTAs of the tcgen05 kernel
+ * (waits per warp role, see gemm_tc.cu "cycle tracing"); E_UNSUPPORTED unless
+ * the library was built with -DQRNG_GEMM_TRACE.  reset != 0 clears them. */
+QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);
 
 #ifdef __cplusplus

@@ -19,7 +19,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqrng.so")
+# QRNG_LIB_PATH selects an experiment build (build.py --variant); default: the in-tree library
+LIB_PATH = os.environ.get("QRNG_LIB_PATH") or os.path.join(_HERE, "libqrng.so")
 
 QRNG_OK, QRNG_E_INVALID, QRNG_E_UNSUPPORTED, QRNG_E_NO_OUTPUT, QRNG_E_CUDA, QRNG_E_NOMEM = range(6)
 PATH_AUTO, PATH_GEMM, PATH_NTT = 0, 1, 2
@@ -33,7 +34,8 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_plan_create_modified", "qrng_modified_toeplitz_extract_async",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
-           "qrng_debug_butterfly_rate"]
+           "qrng_debug_butterfly_rate", "qrng_debug_set_karatsuba", "qrng_plan_info",
+           "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace"]
 
 
 class QrngError(RuntimeError):
@@ -44,6 +46,12 @@ class QrngError(RuntimeError):
 
 class _Gauss(ctypes.Structure):
     _fields_ = [("mu", ctypes.c_double), ("sigma", ctypes.c_double)]
+
+
+class _PlanInfo(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("karatsuba_depth", ctypes.c_int32), ("leaves", ctypes.c_int32),
+                ("log2_transform", ctypes.c_int32), ("blocks_per_transform", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("macs_per_block", ctypes.c_uint64)]
 
 
 class _Report(ctypes.Structure):
@@ -105,6 +113,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_butterfly_rate": ([i32, ctypes.POINTER(u64), vp], i32),
         "qrng_debug_kernel_timing": ([i32], None),
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
+        "qrng_debug_set_karatsuba": ([i32], None),
+        "qrng_debug_gemm_trace": ([vp, i32], i32),
+        "qrng_plan_info": ([vp, vp], i32),
+        "qrng_debug_karatsuba_plan": ([u64, u64, i32, vp, u32, vp, u32, vp, u32, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -152,6 +164,47 @@ def last_error() -> str:
 def set_debug_path(path: int) -> None:
     """TEST ONLY: force QRNG_PATH_GEMM / QRNG_PATH_NTT for plans created afterwards."""
     load_library().qrng_debug_set_path(int(path))
+
+
+def set_karatsuba(max_depth: int) -> None:
+    """TEST/BENCH ONLY: Karatsuba depth of GEMM-path plans created afterwards
+    (-1 = cost model, 0 = one dense product, d > 0 = split down to depth d)."""
+    load_library().qrng_debug_set_karatsuba(int(max_depth))
+
+
+@dataclasses.dataclass
+class KaratsubaPlan:
+    """Host planner output (qrng_debug_karatsuba_plan): see include/qrng.h."""
+    depth: int
+    leaves: list   # (r, w, out_off, seed_terms, input_terms)
+    comb_ptr: np.ndarray
+    comb_idx: np.ndarray
+
+
+def karatsuba_plan(n: int, m: int, max_depth: int) -> KaratsubaPlan:
+    """TEST ONLY (no GPU): the decomposition the library would run for (n, m)."""
+    lib = load_library()
+    counts = (ctypes.c_uint32 * 4)()
+    _check(lib.qrng_debug_karatsuba_plan(n, m, max_depth, None, 0, None, 0, None, 0, counts))
+    nl, nt, nc, depth = counts[0], counts[1], counts[2], counts[3]
+    words = (m + 31) // 32
+    leaf = np.zeros(6 * nl, np.uint32)
+    terms = np.zeros(max(nt, 1), np.uint32)
+    comb = np.zeros(words + 1 + nc, np.uint32)
+    _check(lib.qrng_debug_karatsuba_plan(n, m, max_depth, leaf.ctypes.data, nl, terms.ctypes.data, nt,
+                                         comb.ctypes.data, comb.size, counts))
+    leaves = []
+    for l in range(nl):
+        r, w, off, t0, ns, ni = (int(v) for v in leaf[6 * l:6 * l + 6])
+        leaves.append((r, w, off, [int(v) for v in terms[t0:t0 + ns]], [int(v) for v in terms[t0 + ns:t0 + ns + ni]]))
+    return KaratsubaPlan(depth, leaves, comb[:words + 1].copy(), comb[words + 1:].copy())
+
+
+def gemm_trace(reset: bool = True) -> np.ndarray:
+    """PROFILING ONLY (-DQRNG_GEMM_TRACE builds): the 16 cycle counters."""
+    c = np.zeros(16, np.uint64)
+    _check(load_library().qrng_debug_gemm_trace(c.ctypes.data, 1 if reset else 0))
+    return c
 
 
 def launch_count() -> int:
@@ -247,6 +300,12 @@ class Plan:
     @property
     def path(self) -> int:
         return load_library().qrng_plan_path(self._h)
+
+    def info(self) -> dict:
+        """qrng_plan_info: path, Karatsuba depth / leaves / MACs per block, NTT length."""
+        i = _PlanInfo()
+        _check(load_library().qrng_plan_info(self._h, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in _PlanInfo._fields_ if k != "reserved"}
 
     def extract(self, raw, n_blocks: int, out=None, stream=None):
         import torch

@@ -59,6 +59,9 @@ void KernelTimer::stop() {
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
 static uint64_t g_gemm_max_n = 1ull << 16;
 static std::atomic<int> g_debug_path{QRNG_PATH_AUTO};
+// Karatsuba depth over the GEMM path: -1 = the planner's cost model, 0 = plain
+// GEMM kernel, d > 0 = split whenever allowed down to depth d (tests).
+static std::atomic<int> g_kara_depth{-1};
 
 // One-time device check: sm_100 required (no CPU fallback), stream-ordered
 // pool kept warm so per-call workspace allocation is cheap.
@@ -118,8 +121,10 @@ using namespace qrng;
 struct qrng_plan {
     uint64_t n = 0, m = 0;
     int path = QRNG_PATH_NTT;
+    bool kara_on = false;  // GEMM path through the Karatsuba decomposition
     ntt::Plan ntt;
     gemm::Plan gemm;
+    kara::Plan kara;
 };
 
 static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
@@ -131,6 +136,7 @@ static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
     };
     fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.work);
     fr(p->gemm.seed_words);
+    fr(p->kara.seeds);
     delete p;
 }
 
@@ -153,6 +159,10 @@ qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_
     if (st != QRNG_OK) return st;
     return gemm::probe(d_A, d_h, d_D, N, K, stream);
 }
+qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset) {
+    if (!h_counters16) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    return gemm::trace(h_counters16, reset);
+}
 void qrng_debug_kernel_timing(int enable) { g_timing.store(enable ? 1 : 0); }
 double qrng_debug_kernel_time_ms(uint64_t *launches) {
     std::lock_guard<std::mutex> lk(g_tmu);
@@ -171,6 +181,29 @@ double qrng_debug_kernel_time_ms(uint64_t *launches) {
 
 int qrng_plan_path(const qrng_plan *plan) { return plan ? plan->path : -1; }
 
+void qrng_debug_set_karatsuba(int max_depth) { g_kara_depth.store(max_depth < -1 ? -1 : max_depth); }
+
+qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info) {
+    if (!plan || !info) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    memset(info, 0, sizeof *info);
+    info->path = plan->path;
+    if (plan->path == QRNG_PATH_NTT) {
+        info->log2_transform = plan->ntt.logP;
+        info->blocks_per_transform = plan->ntt.pack_shift ? 2 : 1;
+    } else if (plan->kara_on) {
+        int d = 0, l = 0;
+        uint64_t macs = 0;
+        kara::describe(plan->kara, &d, &l, &macs);
+        info->karatsuba_depth = d;
+        info->leaves = l;
+        info->macs_per_block = macs;
+    } else {
+        info->leaves = 1;
+        info->macs_per_block = plan->n * plan->m;
+    }
+    return QRNG_OK;
+}
+
 qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
                              qrng_plan **plan) {
     if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
@@ -184,15 +217,18 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     p->n = n;
     p->m = m;
     int want = g_debug_path.load();
-    if (want == QRNG_PATH_AUTO) want = (gemm::supported(n, m) && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
-    if (want == QRNG_PATH_GEMM && !gemm::supported(n, m)) {
+    const int kd = g_kara_depth.load();
+    if (want == QRNG_PATH_AUTO) want = (n % 128 == 0 && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
+    if (want == QRNG_PATH_GEMM) p->kara_on = kara::choose(n, m, kd);
+    if (want == QRNG_PATH_GEMM && !p->kara_on && !gemm::supported(n, m)) {
         set_error("GEMM path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
         delete p;
         return QRNG_E_UNSUPPORTED;
     }
     p->path = want;
-    st = (want == QRNG_PATH_GEMM) ? gemm::plan_init(p->gemm, n, m, d_seed, stream)
-                                  : ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream);
+    st = (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
+         : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream)
+                                 : gemm::plan_init(p->gemm, n, m, d_seed, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
     *plan = p;
     return QRNG_OK;
@@ -273,9 +309,12 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
         if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); return QRNG_E_NOMEM; }
         QRNG_CUDA_TRY(cudaMemsetAsync(o.tail, 0, 4, stream));
     }
-    QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
-    qrng_status st = (plan->path == QRNG_PATH_GEMM) ? gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
-                                                    : ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream);
+    // the Karatsuba pack kernel writes every output word once; the other
+    // epilogues OR the words they share with a neighbouring tile / CTA
+    if (!(plan->path == QRNG_PATH_GEMM && plan->kara_on)) QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
+    qrng_status st = (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
+                     : plan->kara_on ? kara::extract(plan->kara, d_raw_bits, n_blocks, n, m, o, stream)
+                                     : gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream);
     if (st == QRNG_OK && o.tail) {
         cudaError_t e = cudaMemcpyAsync(d_out + (out_bytes / 4) * 4, o.tail, out_bytes % 4,
                                         cudaMemcpyDeviceToDevice, stream);

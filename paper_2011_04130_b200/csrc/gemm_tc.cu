@@ -40,16 +40,27 @@ constexpr int A_STAGES = 4;
 constexpr int KC = 1024;       // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
 constexpr int B_SLOTS = 3;
-constexpr int NT = 2;          // N tiles per A stage (A reuse factor)
+constexpr int NT = QRNG_GEMM_NT;  // N tiles per A stage (A reuse factor)
+// accumulator sets in TMEM (2 lets the MMAs of tile k+1 overlap the drain of tile k; needs NT = 1)
+constexpr int ACC_BUFS = QRNG_GEMM_NT == 1 ? 2 : 1;
 constexpr int CM_PER_CHUNK = KC / 8 + NT * BN / 8 - 1;  // core matrices per chunk
 constexpr int CHUNK_BYTES = CM_PER_CHUNK * 128;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 128)
-constexpr uint32_t ACC_COL0 = 128;  // accumulators of the NT N tiles: [128, 320), [320, 512)
-constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4, W_EPI0 = 8, N_EPI = 8;
-constexpr int NTHREADS = 16 * 32;
+constexpr uint32_t ACC_COL0 = 128;  // accumulator sets (buffer x N tile): [128, 320), [320, 512)
+static_assert(A_STAGES * 32 + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
+static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (NT = 1) or one per N tile");
+// Warp roles.  The A transform uses XF_PAR warps per TMEM lane quadrant, each
+// taking every XF_PAR-th stage, so the per-stage latency chain (wait slot ->
+// expand -> tcgen05.st -> wait::st -> arrive) of one warp is overlapped.
+constexpr int XF_PAR = 2;
+constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4 * XF_PAR, W_EPI0 = W_XFORM0 + N_XFORM,
+              N_EPI = 8;
+constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
+static_assert(A_STAGES % XF_PAR == 0, "each transform warp owns fixed ring slots");
 constexpr int PF = 4;          // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
+static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile");
 
 // ---- PTX helpers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -165,6 +176,21 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
 // which 8 shifted copies of a raw word expose their bits at byte MSBs, so both
 // operands are built with SHF + PRMT only.
 
+// ---- optional cycle tracing (build with -DQRNG_GEMM_TRACE; qrng_debug_gemm_trace) ----
+// Slots: 0 MMA wait a_full, 1 MMA wait b_full, 2 MMA wait acc_empty, 3 MMA total,
+// 4 xform wait a_empty, 5 xform expand+st+wait::st, 6 xform total, 7 B-gen wait b_empty,
+// 8 B-gen total, 9 epilogue wait acc_full, 10 epilogue total, 11 stages (MMA side)
+#ifdef QRNG_GEMM_TRACE
+__device__ unsigned long long g_trace[16];
+#define TRACE_T0(v) const long long v = clock64()
+#define TRACE_ADD(slot, t0) atomicAdd(&g_trace[slot], (unsigned long long)(clock64() - (t0)))
+#define TRACE_ADDV(slot, v) atomicAdd(&g_trace[slot], (unsigned long long)(v))
+#else
+#define TRACE_T0(v)
+#define TRACE_ADD(slot, t0)
+#define TRACE_ADDV(slot, v)
+#endif
+
 // ---- the extraction kernel -----------------------------------------------------
 struct Args {
     const uint32_t *raw;       // packed raw stream (MSB-first bytes) as words
@@ -176,7 +202,69 @@ struct Args {
     const uint32_t *seed_words;  // logical big-endian seed words, zero padded
     uint32_t seed_words_n;
     OutStream out;
+    // grouped (Karatsuba leaf) mode only: tiles walk the leaf table, operands
+    // come from per-leaf inputs and parities go to a word-aligned workspace
+    const Leaf *leaves;
+    uint32_t n_leaves;
+    const uint32_t *xws;       // workspace of XOR-combined leaf inputs
+    uint32_t x_stride;         // words per block in xws
+    uint32_t *yws;             // leaf parity workspace
+    uint32_t y_stride;         // words per block in yws
 };
+
+// Geometry of one work tile (M tile of BM blocks x up to NT*BN output rows).
+struct Tile {
+    uint32_t mt, n0;           // M tile; first output row of the N pair
+    uint32_t kst, nchunks;     // K stages of 128, B chunks of KC
+    uint32_t r;                // valid output rows of the product this tile belongs to
+    uint32_t ntc, nlast;       // N tiles used (1..NT); N of the last one (multiple of 16)
+    const uint32_t *seed;      // seed words of the product (smem in plain mode)
+    const uint32_t *xb;        // block-0 input words of the product
+    uint32_t xs;               // words per block of the input
+    uint32_t out_off;          // grouped: word offset of the leaf in a block's yws row
+};
+
+__device__ __forceinline__ void tile_rows(Tile &ti) {
+    const uint32_t left = ti.r > ti.n0 ? min((uint32_t)(NT * BN), ti.r - ti.n0) : 16u;
+    ti.ntc = (left + BN - 1) / BN;
+    const uint32_t lastrows = left - (ti.ntc - 1) * BN;
+    ti.nlast = (lastrows + 15) & ~15u;
+}
+
+// Plain mode: one product (the whole extraction), tiles (N pair, M tile).
+// Grouped mode: tiles of leaf l are [npair_base*n_mtiles, (npair_base+npairs)*n_mtiles);
+// `cur` is a per-role cursor into the leaf table (tiles only increase).
+template <bool GROUPED>
+__device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s, uint32_t t, uint32_t &cur) {
+    Tile ti;
+    if (!GROUPED) {
+        ti.mt = t % a.n_mtiles;
+        ti.n0 = (t / a.n_mtiles) * (NT * BN);
+        ti.kst = a.kst;
+        ti.nchunks = a.nchunks;
+        ti.r = a.m;
+        ti.seed = seed_s;
+        ti.xb = a.raw;
+        ti.xs = a.n >> 5;
+        ti.out_off = 0;
+    } else {
+        while (cur + 1 < a.n_leaves && t >= (__ldg(&a.leaves[cur].npair_base) + __ldg(&a.leaves[cur].npairs)) * a.n_mtiles)
+            ++cur;
+        const Leaf &L = a.leaves[cur];
+        const uint32_t tl = t - __ldg(&L.npair_base) * a.n_mtiles;
+        ti.mt = tl % a.n_mtiles;
+        ti.n0 = (tl / a.n_mtiles) * (NT * BN);
+        ti.kst = __ldg(&L.w) / KS;
+        ti.nchunks = (ti.kst + SPC - 1) / SPC;
+        ti.r = __ldg(&L.r);
+        ti.seed = a.seed_words + __ldg(&L.seed_off);
+        if (__ldg(&L.x_src) == 0) { ti.xb = a.raw + __ldg(&L.x_off); ti.xs = a.n >> 5; }
+        else { ti.xb = a.xws + __ldg(&L.x_off); ti.xs = a.x_stride; }
+        ti.out_off = __ldg(&L.out_off);
+    }
+    tile_rows(ti);
+    return ti;
+}
 
 // One stage: 128 K elements of one block from its 16 raw bytes (memory words
 // M_0..M_3, stream order, MSB-first bytes).  S_a = M_q << a puts stream bit
@@ -201,22 +289,23 @@ __device__ __forceinline__ void xform_stage(uint32_t taddr, uint4 w) {
     tmem_st32(taddr, v);
 }
 
+template <bool GROUPED>
 __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *chunks = smem;
     uint32_t *seed_s = reinterpret_cast<uint32_t *>(smem + B_SLOTS * CHUNK_BYTES);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((a.seed_words_n + 3) & ~3u));
+    const uint32_t seed_stage = GROUPED ? 0u : a.seed_words_n;  // grouped: leaf seeds stay in global (L1)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
     uint64_t *a_full = bars, *a_empty = bars + 4, *b_full = bars + 8, *b_empty = bars + 11;
-    uint64_t *acc_full = bars + 14, *acc_empty = bars + 15;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 16);
+    uint64_t *acc_full = bars + 14, *acc_empty = bars + 14 + ACC_BUFS;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 14 + 2 * ACC_BUFS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint32_t i = threadIdx.x; i < a.seed_words_n; i += NTHREADS) seed_s[i] = a.seed_words[i];
+    for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
     if (threadIdx.x == 0) {
-        for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM); mbar_init(&a_empty[s], 1); }
+        for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM / XF_PAR); mbar_init(&a_empty[s], 1); }
         for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], N_BGEN); mbar_init(&b_empty[s], 1); }
-        mbar_init(acc_full, 1);
-        mbar_init(acc_empty, N_EPI);
+        for (int s = 0; s < ACC_BUFS; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], N_EPI / ACC_BUFS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_MMA) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -224,22 +313,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
+    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: total over leaves in grouped mode
+    uint32_t cur = 0;                                 // leaf cursor of this role
+    TRACE_T0(t_role);
 
     if (warp == W_MMA) {
         if (lane == 0) {
-            const uint32_t idesc = idesc_i8(BM, BN);
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-                mbar_wait(acc_empty, (it & 1) ^ 1);
+                const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+                // N tiles before the last use N = BN; the last one only the rows it needs
+                const uint32_t idesc_full = idesc_i8(BM, BN), idesc_last = idesc_i8(BM, (int)ti.nlast);
+                const uint32_t ab = it % ACC_BUFS, acc0 = ACC_COL0 + ab * NT * BN;
+                { TRACE_T0(tw); mbar_wait(&acc_empty[ab], ((it / ACC_BUFS) & 1) ^ 1); TRACE_ADD(2, tw); }
                 tc_fence_after();
-                for (uint32_t ks = 0; ks < a.kst; ++ks) {
+                for (uint32_t ks = 0; ks < ti.kst; ++ks) {
                     const uint32_t kin = ks % SPC;
                     if (kin == 0) {
-                        mbar_wait(&b_full[bs], bph);
+                        { TRACE_T0(tw); mbar_wait(&b_full[bs], bph); TRACE_ADD(1, tw); }
                         tc_fence_after();
                     }
-                    mbar_wait(&a_full[as], aph);
+                    { TRACE_T0(tw); mbar_wait(&a_full[as], aph); TRACE_ADD(0, tw); }
+                    TRACE_ADDV(11, 1);
                     tc_fence_after();
                     const uint32_t a_tmem = tmem + A_COL0 + as * 32;
                     const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
@@ -248,18 +343,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                         const uint32_t koff = kin * KS + kk * 32;  // K offset inside the chunk
 #pragma unroll
                         for (uint32_t nt = 0; nt < NT; ++nt) {  // N tile nt starts 24*nt core matrices later
-                            const uint64_t bdesc = desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 256, 128);
-                            mma_i8_ts(tmem + ACC_COL0 + nt * BN, a_tmem + kk * 8, bdesc, idesc, (ks | kk) != 0);
+                            if (nt < ti.ntc) {
+                                const uint64_t bdesc = desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 256, 128);
+                                mma_i8_ts(tmem + acc0 + nt * BN, a_tmem + kk * 8, bdesc,
+                                          nt + 1 == ti.ntc ? idesc_last : idesc_full, (ks | kk) != 0);
+                            }
                         }
                     }
                     mma_commit(&a_empty[as]);
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
-                    if (kin == SPC - 1 || ks == a.kst - 1) {
+                    if (kin == SPC - 1 || ks == ti.kst - 1) {
                         mma_commit(&b_empty[bs]);
                         if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
                     }
                 }
-                mma_commit(acc_full);
+                mma_commit(&acc_full[ab]);
             }
         }
         __syncwarp();
@@ -269,16 +367,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         const int tb = (warp - W_BGEN0) * 32 + lane;
         uint32_t bs = 0, bph = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const uint32_t n0 = (t / a.n_mtiles) * (NT * BN);
-            for (uint32_t c = 0; c < a.nchunks; ++c) {
-                const uint32_t base = n0 + c * KC;
-                mbar_wait(&b_empty[bs], bph ^ 1);
+            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+            // core-matrix rows the MMAs of this tile read (K chunk + the N rows in use)
+            const int ncm = KC / 8 + (int)(((ti.ntc - 1) * BN + ti.nlast) / 8) - 1;
+            for (uint32_t c = 0; c < ti.nchunks; ++c) {
+                const uint32_t base = ti.n0 + c * KC;
+                { TRACE_T0(tw); mbar_wait(&b_empty[bs], bph ^ 1); if (lane == 0) TRACE_ADD(7, tw); }
                 uint8_t *cb = chunks + bs * CHUNK_BYTES;
-                for (int r = tb; r < CM_PER_CHUNK * 8; r += N_BGEN * 32) {
+                for (int r = tb; r < ncm * 8; r += N_BGEN * 32) {
                     // row holds seed bits p + r(s); in v (seed bit p + d at bit 31 - d) the
                     // bit of slot s = 4cc + f sits at byte 2 + (f&1), bit 2cc + (f>>1)
                     const uint32_t p = base + 8 * (r >> 3) + (r & 7);
-                    const uint32_t v = __funnelshift_l(seed_s[(p >> 5) + 1], seed_s[p >> 5], p & 31);
+                    uint32_t w0, w1;
+                    if (GROUPED) { w0 = __ldg(ti.seed + (p >> 5)); w1 = __ldg(ti.seed + (p >> 5) + 1); }
+                    else { w0 = ti.seed[p >> 5]; w1 = ti.seed[(p >> 5) + 1]; }
+                    const uint32_t v = __funnelshift_l(w1, w0, p & 31);
                     uint4 o;
                     o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
                     o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
@@ -293,79 +396,115 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             }
         }
     } else if (warp >= W_XFORM0 && warp < W_XFORM0 + N_XFORM) {
-        // A transform: TMEM lane = block, 128 K per stage; the prefetch ring of
-        // raw chunks runs continuously across this CTA's tiles.
-        const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
+        // A transform: TMEM lane = block, 128 K per stage.  Stages are numbered
+        // g = 0, 1, 2, ... over this CTA's (tile, K stage) pairs; this warp takes
+        // g = par (mod XF_PAR) for its lane quadrant.  The prefetch ring of input
+        // chunks runs continuously across tiles.
+        const uint32_t xw = (uint32_t)(warp - W_XFORM0), par = xw / 4;
+        const uint32_t row = (xw & 3) * 32 + lane;  // warp % 4 == xw % 4: TMEM lane quadrant
         const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16);
-        const uint32_t wpb = a.n >> 5;          // words per block
-        const uint32_t last = (a.n >> 7) - 1;   // uint4 index of stage 0
-        uint32_t lt = blockIdx.x, lks = 0;      // load cursor
-        auto load = [&](uint32_t t, uint32_t ks) -> uint4 {
-            if (t >= ntiles) return make_uint4(0, 0, 0, 0);
-            const uint64_t b = (uint64_t)(t % a.n_mtiles) * BM + row;
-            if (b >= a.n_blocks) return make_uint4(0, 0, 0, 0);
-            return __ldg(reinterpret_cast<const uint4 *>(a.raw + b * wpb) + (last - ks));
+        uint32_t lcur = 0;                      // leaf cursor of the load side
+        uint32_t lt = blockIdx.x, lks = 0;      // load cursor (tile, K stage)
+        Tile lti{};
+        if (lt < ntiles) lti = tile_info<GROUPED>(a, seed_s, lt, lcur);
+        auto step1 = [&]() {
+            if (lt >= ntiles) return;
+            if (++lks == lti.kst) {
+                lks = 0;
+                lt += gridDim.x;
+                if (lt < ntiles) lti = tile_info<GROUPED>(a, seed_s, lt, lcur);
+            }
         };
+        auto load = [&]() -> uint4 {
+            if (lt >= ntiles) return make_uint4(0, 0, 0, 0);
+            const uint64_t b = (uint64_t)lti.mt * BM + row;
+            if (b >= a.n_blocks) return make_uint4(0, 0, 0, 0);
+            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + b * lti.xs) + (lti.kst - 1 - lks));
+        };
+        for (uint32_t i = 0; i < par; ++i) step1();
         uint4 pf[PF];
+        bool ok[PF];
 #pragma unroll
         for (int j = 0; j < PF; ++j) {
-            pf[j] = load(lt, lks);
-            if (++lks == a.kst) { lks = 0; lt += gridDim.x; }
+            ok[j] = lt < ntiles;
+            pf[j] = load();
+#pragma unroll
+            for (int i = 0; i < XF_PAR; ++i) step1();
         }
-        uint32_t as = 0, aph = 0;
-        uint32_t ct = blockIdx.x, cks = 0;
-        while (ct < ntiles) {
+        uint32_t g = par;
+        bool more = true;
+        while (more) {
 #pragma unroll
             for (int j = 0; j < PF; ++j) {
-                if (ct < ntiles) {
-                    const uint4 cur = pf[j];
-                    pf[j] = load(lt, lks);
-                    if (++lks == a.kst) { lks = 0; lt += gridDim.x; }
-                    mbar_wait(&a_empty[as], aph ^ 1);
+                if (more && !ok[j]) more = false;
+                if (more) {
+                    const uint4 cur4 = pf[j];
+                    ok[j] = lt < ntiles;
+                    pf[j] = load();
+#pragma unroll
+                    for (int i = 0; i < XF_PAR; ++i) step1();
+                    const uint32_t as = g % A_STAGES, aph = (g / A_STAGES) & 1;
+                    { TRACE_T0(tw); mbar_wait(&a_empty[as], aph ^ 1); if (lane == 0) TRACE_ADD(4, tw); }
                     tc_fence_after();
-                    xform_stage(lane_addr + A_COL0 + as * 32, cur);
+                    TRACE_T0(tx);
+                    xform_stage(lane_addr + A_COL0 + as * 32, cur4);
                     tmem_wait_st();
+                    if (lane == 0) TRACE_ADD(5, tx);
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&a_full[as]);
-                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
-                    if (++cks == a.kst) { cks = 0; ct += gridDim.x; }
+                    g += XF_PAR;
                 }
             }
         }
     } else {
-        // Epilogue: warp w drains N tile (w - W_EPI0) / 4 of the pair for its lane
-        // quadrant; parity of the S32 sums, 32 outputs per MSB-first word.
-        const uint32_t nt = (uint32_t)(warp - W_EPI0) >> 2;
+        // Epilogue: with ACC_BUFS = 2 warp group g = (w - W_EPI0) / 4 drains the
+        // tiles k = g mod 2 of this CTA (accumulator set g) while the MMAs of the
+        // next tile fill the other set; with one set, group g drains N tile g.
+        // Parity of the S32 sums, 32 outputs per MSB-first word.
+        const uint32_t grp = (uint32_t)(warp - W_EPI0) >> 2;
+        const uint32_t nt = ACC_BUFS == 1 ? grp : 0u, ab = ACC_BUFS == 1 ? 0u : grp;
         const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
-        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + nt * BN;
+        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + ab * NT * BN + nt * BN;
         uint32_t it = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            mbar_wait(acc_full, it & 1);
+        for (uint32_t t = blockIdx.x + ab * gridDim.x; t < ntiles; t += ACC_BUFS * gridDim.x, ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+            { TRACE_T0(tw); mbar_wait(&acc_full[ab], it & 1); if (lane == 0) TRACE_ADD(9, tw); }
             tc_fence_after();
+            const uint32_t ncols = nt < ti.ntc ? (nt + 1 == ti.ntc ? ti.nlast : (uint32_t)BN) : 0u;
             uint32_t words[BN / 32];
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld32(lane_addr + 32 * c, v);
-                tmem_wait_ld();
                 uint32_t w = 0;
+                if ((uint32_t)(32 * c) < ncols) {
+                    uint32_t v[32];
+                    tmem_ld32(lane_addr + 32 * c, v);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 32; ++k) w = (w << 1) | (v[k] & 1u);
+                    for (int k = 0; k < 32; ++k) w = (w << 1) | (v[k] & 1u);
+                }
                 words[c] = w;
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty);
-            const uint64_t b = (uint64_t)(t % a.n_mtiles) * BM + row;
-            const uint32_t n0 = (t / a.n_mtiles) * (NT * BN) + nt * BN;
-            if (b >= a.n_blocks || n0 >= a.m) continue;
-            const uint32_t nvalid = min((uint32_t)BN, a.m - n0);
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            const uint64_t b = (uint64_t)ti.mt * BM + row;
+            const uint32_t n0 = ti.n0 + nt * BN;
+            if (b >= a.n_blocks || n0 >= ti.r) continue;
+            const uint32_t nvalid = min((uint32_t)BN, ti.r - n0);
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
                 const int vb = (int)nvalid - 32 * c;  // valid bits in word c
                 if (vb <= 0) words[c] = 0;
                 else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
+            }
+            if (GROUPED) {
+                // word-aligned leaf parities (n0 % 32 == 0), logical words
+                uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c)
+                    if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
+                continue;
             }
             const uint64_t G_lo = b * a.m + n0, G_hi = G_lo + nvalid;
             const uint32_t off = (uint32_t)(G_lo & 31);
@@ -373,9 +512,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             uint32_t prev = 0;
 #pragma unroll
             for (int c = 0; c <= BN / 32; ++c) {
-                const uint32_t cur = (c < BN / 32) ? words[c] : 0u;
-                const uint32_t ow = off ? ((prev << (32 - off)) | (cur >> off)) : cur;
-                prev = cur;
+                const uint32_t cw = (c < BN / 32) ? words[c] : 0u;
+                const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
+                prev = cw;
                 const uint64_t W = W0 + c;
                 if (W * 32 >= G_hi) break;
                 const bool excl = (W * 32 >= G_lo) && (W * 32 + 32 <= G_hi);
@@ -384,6 +523,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         }
     }
 
+#ifdef QRNG_GEMM_TRACE
+    if (lane == 0) {
+        const int slot = warp == W_MMA ? 3 : (warp < W_XFORM0 ? 8 : (warp < W_EPI0 ? 6 : 10));
+        TRACE_ADD(slot, t_role);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == W_MMA) {
@@ -391,6 +536,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         tmem_dealloc(tmem, TMEM_COLS);
     }
 }
+
 
 // ---- layout probe (test only): D = A * B^T with B[i][k] = h[i + k] ----------------
 // One CTA, 128 threads.  A: 128 x K int8 row-major (global); h: bytes; D: 128 x N s32.
@@ -459,14 +605,14 @@ __global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, co
 // ---- host ------------------------------------------------------------------------
 bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n; }
 
-static uint32_t seed_words_needed(uint64_t n, uint64_t m) {
+uint32_t seed_words_needed(uint64_t n, uint64_t m) {
     const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = n / KS, nchunks = (kst + SPC - 1) / SPC;
     const uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
     return (uint32_t)(pmax / 32 + 2);
 }
 
 static size_t smem_bytes(uint32_t seed_words_n) {
-    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + 16 * 8 + 16;
+    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + 20 * 8 + 16;
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L
@@ -503,20 +649,8 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
-qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
-                    const OutStream &out, cudaStream_t s) {
-    Args a;
-    a.raw = reinterpret_cast<const uint32_t *>(d_raw);
-    a.n_blocks = n_blocks;
-    a.n = (uint32_t)n;
-    a.m = (uint32_t)m;
-    a.kst = (uint32_t)(n / KS);
-    a.nchunks = (a.kst + SPC - 1) / SPC;
-    a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
-    a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));
-    a.seed_words = pl.seed_words;
-    a.seed_words_n = (uint32_t)pl.seed_words_n;
-    a.out = out;
+template <bool GROUPED>
+static qrng_status launch(const Args &a, cudaStream_t s) {
     if ((uint64_t)a.n_mtiles * a.n_npairs > 0xFFFFFFFFull) {
         set_error("GEMM path: too many tiles");
         return QRNG_E_UNSUPPORTED;
@@ -524,18 +658,72 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     int dev = 0, sms = 148;
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = smem_bytes(a.seed_words_n);
+    const size_t smem = smem_bytes(GROUPED ? 0u : a.seed_words_n);
     {
-        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel));
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel<GROUPED>));
         if (st != QRNG_OK) return st;
     }
-    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
+    const uint32_t ntiles = a.n_mtiles * a.n_npairs;
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
     KernelTimer tm(s, true);
-    toeplitz_gemm_kernel<<<grid, NTHREADS, smem, s>>>(a);
+    toeplitz_gemm_kernel<GROUPED><<<grid, NTHREADS, smem, s>>>(a);
     tm.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
+}
+
+qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                    const OutStream &out, cudaStream_t s) {
+    Args a{};
+    a.raw = reinterpret_cast<const uint32_t *>(d_raw);
+    a.n_blocks = n_blocks;
+    a.n = (uint32_t)n;
+    a.m = (uint32_t)m;
+    a.kst = (uint32_t)(n / KS);
+    a.nchunks = (a.kst + SPC - 1) / SPC;
+    a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
+    a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
+    a.seed_words = pl.seed_words;
+    a.seed_words_n = (uint32_t)pl.seed_words_n;
+    a.out = out;
+    return launch<false>(a, s);
+}
+
+qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t total_npairs,
+                            const uint32_t *d_seeds, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
+                            const uint32_t *xws, uint32_t x_stride, uint32_t *yws, uint32_t y_stride,
+                            cudaStream_t s) {
+    Args a{};
+    a.raw = reinterpret_cast<const uint32_t *>(d_raw);
+    a.n_blocks = n_blocks;
+    a.n = (uint32_t)n;
+    a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
+    a.n_npairs = total_npairs;
+    a.seed_words = d_seeds;
+    a.leaves = d_leaves;
+    a.n_leaves = n_leaves;
+    a.xws = xws;
+    a.x_stride = x_stride;
+    a.yws = yws;
+    a.y_stride = y_stride;
+    return launch<true>(a, s);
+}
+
+qrng_status trace(uint64_t *h_out, int reset) {
+#ifdef QRNG_GEMM_TRACE
+    QRNG_CUDA_TRY(cudaDeviceSynchronize());
+    QRNG_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_trace, sizeof(g_trace)));
+    if (reset) {
+        unsigned long long z[16] = {};
+        QRNG_CUDA_TRY(cudaMemcpyToSymbol(g_trace, z, sizeof z));
+    }
+    return QRNG_OK;
+#else
+    (void)h_out;
+    (void)reset;
+    set_error("built without -DQRNG_GEMM_TRACE");
+    return QRNG_E_UNSUPPORTED;
+#endif
 }
 
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s) {

@@ -91,13 +91,57 @@ struct Plan {
     uint32_t *seed_words = nullptr;  // seed as logical big-endian words, zero padded
     uint32_t seed_words_n = 0;
 };
+// One leaf product of the Karatsuba decomposition (karatsuba.cu): an r x w
+// Toeplitz product applied to every block, run as a group of tiles of the
+// same tcgen05 kernel.  Device-resident table entry.
+struct Leaf {
+    uint32_t w, r;              // K (input bits) and output rows; w % 128 == 0
+    uint32_t npairs, npair_base;  // N pairs (NT*BN rows) of this leaf; prefix over leaves
+    uint32_t seed_off;          // word offset of the leaf seed in the plan's seed buffer
+    uint32_t seed_n;            // words of that leaf seed the kernel reads (seed_words_needed)
+    uint32_t x_src;             // 0: input is a window of the raw block; 1: XOR combination in the workspace
+    uint32_t x_off;             // x_src 0: word offset inside the raw block; 1: word offset in a block's X row
+    uint32_t out_off;           // word offset of the leaf parities in a block's Y row
+    uint32_t sterm_base, sterm_n;  // seed terms (bit offsets into the root seed) in the term table
+    uint32_t iterm_base, iterm_n;  // input terms (bit offsets into the raw block)
+};
+#ifndef QRNG_GEMM_NT
+#define QRNG_GEMM_NT 2  // N tiles of 192 rows per A stage in the tcgen05 kernel (build-time choice)
+#endif
+constexpr int kTileRows = 192 * QRNG_GEMM_NT;  // output rows per work tile (NT * BN)
+uint32_t seed_words_needed(uint64_t n, uint64_t m);
+// Grouped launch over the leaf table (Karatsuba): parities of leaf l, block b,
+// row i go to bit 31 - (i & 31) of yws[b * y_stride + out_off + i / 32] (logical words).
+qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t total_npairs,
+                            const uint32_t *d_seeds, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
+                            const uint32_t *xws, uint32_t x_stride, uint32_t *yws, uint32_t y_stride,
+                            cudaStream_t s);
 bool supported(uint64_t n, uint64_t m);
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
 void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
+qrng_status trace(uint64_t *h_out, int reset);  // 16 cycle counters (-DQRNG_GEMM_TRACE builds)
 }  // namespace gemm
+
+// Karatsuba decomposition over the GEMM path (karatsuba.cu).
+namespace kara {
+struct Tables;  // device-resident leaf / term / combine tables, cached per (n, m, depth)
+struct Plan {
+    const Tables *tab = nullptr;
+    uint32_t *seeds = nullptr;  // leaf seeds (logical big-endian words)
+};
+// Chooses the decomposition for (n, m); returns false if no leaf split pays off
+// (the plain GEMM kernel is then used).  max_depth < 0: cost model decides.
+bool choose(uint64_t n, uint64_t m, int max_depth);
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s);
+void plan_free(Plan &pl);
+qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                    const OutStream &out, cudaStream_t s);
+// host-side description for bench/tests: depth, number of leaves, leaf MACs per block
+void describe(const Plan &pl, int *depth, int *n_leaves, uint64_t *macs_per_block);
+}  // namespace kara
 
 // Histogram (hist.cu).
 qrng_status hist256_launch(const uint8_t *d_samples, uint64_t n, unsigned long long *d_counts,
