@@ -34,26 +34,29 @@ namespace qrng {
 namespace gemm {
 
 constexpr int BM = 128;        // blocks per tile (TMEM lanes)
-constexpr int BN = 192;        // output rows per tile
+constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
 constexpr int KS = 128;        // K per A stage
-constexpr int A_STAGES = 4;
+constexpr int A_STAGES = QRNG_GEMM_ASTAGES;  // A ring slots in TMEM (32 columns each)
 constexpr int KC = 1024;       // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
 constexpr int B_SLOTS = 3;
 constexpr int NT = QRNG_GEMM_NT;  // N tiles per A stage (A reuse factor)
 // accumulator sets in TMEM (2 lets the MMAs of tile k+1 overlap the drain of tile k; needs NT = 1)
-constexpr int ACC_BUFS = QRNG_GEMM_NT == 1 ? 2 : 1;
+constexpr int ACC_BUFS = QRNG_GEMM_ACCBUFS;
 constexpr int CM_PER_CHUNK = KC / 8 + NT * BN / 8 - 1;  // core matrices per chunk
 constexpr int CHUNK_BYTES = CM_PER_CHUNK * 128;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 128)
-constexpr uint32_t ACC_COL0 = 128;  // accumulator sets (buffer x N tile): [128, 320), [320, 512)
+constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 32 A_STAGES)
+constexpr uint32_t ACC_COL0 = 32 * A_STAGES;  // accumulator sets (buffer x N tile) follow
 static_assert(A_STAGES * 32 + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
 static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (NT = 1) or one per N tile");
 // Warp roles.  The A transform uses XF_PAR warps per TMEM lane quadrant, each
 // taking every XF_PAR-th stage, so the per-stage latency chain (wait slot ->
 // expand -> tcgen05.st -> wait::st -> arrive) of one warp is overlapped.
-constexpr int XF_PAR = 2;
+#ifndef QRNG_GEMM_XFPAR
+#define QRNG_GEMM_XFPAR 2
+#endif
+constexpr int XF_PAR = QRNG_GEMM_XFPAR;
 constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4 * XF_PAR, W_EPI0 = W_XFORM0 + N_XFORM,
               N_EPI = 8;
 constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
@@ -69,15 +72,26 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
 }
+#ifndef QRNG_GEMM_POLL
+#define QRNG_GEMM_POLL 0  // 1: spin on mbarrier.test_wait instead of the suspending try_wait
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
     const uint32_t a = smem_u32(b);
     uint32_t done;
     do {
+#if QRNG_GEMM_POLL
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+#else
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done) : "r"(a), "r"(parity) : "memory");
+#endif
     } while (!done);
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
@@ -175,6 +189,10 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
 // (elements counted along the reversed K index j'').  This is the order in
 // which 8 shifted copies of a raw word expose their bits at byte MSBs, so both
 // operands are built with SHF + PRMT only.
+
+#ifndef QRNG_GEMM_EXP
+#define QRNG_GEMM_EXP 0  // timing experiments only (results wrong when != 0)
+#endif
 
 // ---- optional cycle tracing (build with -DQRNG_GEMM_TRACE; qrng_debug_gemm_trace) ----
 // Slots: 0 MMA wait a_full, 1 MMA wait b_full, 2 MMA wait acc_empty, 3 MMA total,
@@ -296,9 +314,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     uint32_t *seed_s = reinterpret_cast<uint32_t *>(smem + B_SLOTS * CHUNK_BYTES);
     const uint32_t seed_stage = GROUPED ? 0u : a.seed_words_n;  // grouped: leaf seeds stay in global (L1)
     uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
-    uint64_t *a_full = bars, *a_empty = bars + 4, *b_full = bars + 8, *b_empty = bars + 11;
-    uint64_t *acc_full = bars + 14, *acc_empty = bars + 14 + ACC_BUFS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 14 + 2 * ACC_BUFS);
+    uint64_t *a_full = bars, *a_empty = bars + A_STAGES, *b_full = bars + 2 * A_STAGES;
+    uint64_t *b_empty = b_full + B_SLOTS, *acc_full = b_empty + B_SLOTS, *acc_empty = acc_full + ACC_BUFS;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + ACC_BUFS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
@@ -345,8 +363,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                         for (uint32_t nt = 0; nt < NT; ++nt) {  // N tile nt starts 24*nt core matrices later
                             if (nt < ti.ntc) {
                                 const uint64_t bdesc = desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 256, 128);
+#if QRNG_GEMM_EXP != 1  // experiment 1: no MMAs (transform / B-gen / epilogue throughput alone)
                                 mma_i8_ts(tmem + acc0 + nt * BN, a_tmem + kk * 8, bdesc,
                                           nt + 1 == ti.ntc ? idesc_last : idesc_full, (ks | kk) != 0);
+#endif
                             }
                         }
                     }
@@ -415,19 +435,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 if (lt < ntiles) lti = tile_info<GROUPED>(a, seed_s, lt, lcur);
             }
         };
-        auto load = [&]() -> uint4 {
-            if (lt >= ntiles) return make_uint4(0, 0, 0, 0);
+        // Branch-free prefetch: always load from a valid address (clamped block,
+        // stale tile past the end) and keep a validity flag, so every ring slot
+        // stays in its own registers and the load latency is really hidden.
+        auto load = [&](bool &v) -> uint4 {
             const uint64_t b = (uint64_t)lti.mt * BM + row;
-            if (b >= a.n_blocks) return make_uint4(0, 0, 0, 0);
-            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + b * lti.xs) + (lti.kst - 1 - lks));
+            v = lt < ntiles && b < a.n_blocks;
+#if QRNG_GEMM_EXP == 3  // experiment 3: every lane reads block 0 (coalesced broadcast loads)
+            const uint64_t bc = 0;
+#else
+            const uint64_t bc = b < a.n_blocks ? b : a.n_blocks - 1;
+#endif
+            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (lti.kst - 1 - lks));
         };
         for (uint32_t i = 0; i < par; ++i) step1();
         uint4 pf[PF];
-        bool ok[PF];
+        bool ok[PF], vd[PF];
 #pragma unroll
         for (int j = 0; j < PF; ++j) {
             ok[j] = lt < ntiles;
-            pf[j] = load();
+            pf[j] = load(vd[j]);
 #pragma unroll
             for (int i = 0; i < XF_PAR; ++i) step1();
         }
@@ -438,17 +465,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             for (int j = 0; j < PF; ++j) {
                 if (more && !ok[j]) more = false;
                 if (more) {
-                    const uint4 cur4 = pf[j];
+                    const uint4 cur4 = vd[j] ? pf[j] : make_uint4(0, 0, 0, 0);
                     ok[j] = lt < ntiles;
-                    pf[j] = load();
+                    pf[j] = load(vd[j]);
 #pragma unroll
                     for (int i = 0; i < XF_PAR; ++i) step1();
                     const uint32_t as = g % A_STAGES, aph = (g / A_STAGES) & 1;
                     { TRACE_T0(tw); mbar_wait(&a_empty[as], aph ^ 1); if (lane == 0) TRACE_ADD(4, tw); }
                     tc_fence_after();
                     TRACE_T0(tx);
+#if QRNG_GEMM_EXP != 2  // experiment 2: no A expansion/TMEM store (MMA throughput alone)
                     xform_stage(lane_addr + A_COL0 + as * 32, cur4);
                     tmem_wait_st();
+#else
+                    if (cur4.x == 0x12345678u) __nanosleep(1);
+#endif
                     if (lane == 0) TRACE_ADD(5, tx);
                     tc_fence_before();
                     __syncwarp();
@@ -612,7 +643,7 @@ uint32_t seed_words_needed(uint64_t n, uint64_t m) {
 }
 
 static size_t smem_bytes(uint32_t seed_words_n) {
-    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + 20 * 8 + 16;
+    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + 2 * ACC_BUFS) * 8 + 16;
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L

@@ -39,18 +39,20 @@ namespace kara {
 constexpr uint32_t kMinLeafW = 128;   // narrowest leaf the planner creates (one K stage)
 constexpr int kMaxLeaves = 1024;
 constexpr int kMaxDepth = 10;
+constexpr int kAutoMaxDepth = 5;  // auto mode: deeper trees spill the leaf parities out of L2
 
 // ---- planner (host only; no CUDA calls) ------------------------------------
 // Cost model in units of (output row x K) for one M tile of 128 blocks on the
 // tensor cores; per-tile pipeline overhead and the workspace traffic of the
 // input / parity combinations are expressed in the same unit (calibrated on
 // B200).
-constexpr double kTileOverhead = 150e3;  // per work tile (pipeline fill, accumulator drain)
-constexpr double kPrepPerBit = 100.0;    // forming x0 ^ x1 in the workspace, per input bit
-constexpr double kCombPerRow = 50.0;     // leaf parities written + combined, per output row
+constexpr double kTileOverhead = 186e3;  // per work tile (pipeline fill, accumulator drain; ~3.6k SM clocks)
+constexpr double kPrepPerBit = 180.0;    // forming x0 ^ x1 in the workspace, per input bit
+constexpr double kLeafRow = 450.0;       // leaf parities written by the GEMM and read by the combine, per row
+constexpr double kCombPerRow = 0.0;      // internal node row written and read back, per row
 
 static double leaf_cost(uint32_t r, uint32_t w) {
-    double c = 0;
+    double c = kLeafRow * r;
     for (uint32_t n0 = 0; n0 < r; n0 += gemm::kTileRows) {
         const uint32_t left = std::min<uint32_t>(gemm::kTileRows, r - n0);
         const uint32_t rows = std::max<uint32_t>((left + 15) & ~15u, 128);  // A expansion floor
@@ -137,6 +139,7 @@ struct HostTables {
     // h/32, dst word in a block's Z row, child locations (word offset | 1<<31 if in Z)}
     std::vector<std::array<uint32_t, 8>> inner;
     std::vector<uint32_t> height_end;      // inner[height_end[h-1] .. height_end[h]) have height h
+    std::vector<std::array<uint32_t, 4>> levels;  // {first node, end node, units per block, 0}; root last
     uint32_t z_stride = 0, root_z = 0;
     std::vector<uint32_t> comb_ptr, comb_idx;  // CSR per root output word -> Y-row word offsets
     uint32_t y_stride = 0, x_stride = 0, total_npairs = 0, root_words = 0, seed_total = 0;
@@ -205,7 +208,7 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
 static bool plan_host(uint64_t n, uint64_t m, int max_depth, HostTables &T) {
     if (n % 128 || m == 0 || m >= n || n > (1u << 22)) return false;
     // auto: the cost model's best tree with at most kMaxLeaves leaves
-    for (int depth = max_depth >= 0 ? std::min(max_depth, kMaxDepth) : kMaxDepth; depth >= 0; --depth)
+    for (int depth = max_depth >= 0 ? std::min(max_depth, kMaxDepth) : kAutoMaxDepth; depth >= 0; --depth)
         if (plan_host_depth(n, m, depth, max_depth >= 0, T)) return true;
     return false;
 }
@@ -232,7 +235,7 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
     uint32_t yo = 0;
     for (auto &L : leaves) {
         L.out_off = yo;
-        yo += (L.r + 31) / 32;
+        yo += ((L.r + 31) / 32 + 3) & ~3u;  // 16-byte aligned rows: the combine moves uint4
         T.macs += (uint64_t)L.r * L.w;
     }
     T.y_stride = (yo + 3) & ~3u;
@@ -253,7 +256,8 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
     std::stable_sort(inner_ids.begin(), inner_ids.end(), [&](int a, int b) { return height[a] < height[b]; });
     std::vector<uint32_t> zoff(nodes.size(), 0);
     uint32_t zo = 0;
-    for (int i : inner_ids) { zoff[i] = zo; zo += (nodes[i].r + 31) / 32; }
+    for (int i : inner_ids)
+        if (i != 0) { zoff[i] = zo; zo += ((nodes[i].r + 31) / 32 + 3) & ~3u; }  // the root is packed directly
     T.z_stride = (zo + 3) & ~3u;
     T.root_z = zoff[0];
     auto loc = [&](int c) -> uint32_t {
@@ -261,11 +265,27 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
         return nodes[c].kind == LEAF ? leaves[leaf_of_node[c]].out_off : (zoff[c] | 0x80000000u);
     };
     T.height_end.assign(maxd + 1, 0);
+    uint32_t pre = 0;
+    int cur_h = 0;
     for (int i : inner_ids) {
         const Node &nd = nodes[i];
-        T.inner.push_back({(uint32_t)nd.kind, (nd.r + 31) / 32, nd.h / 32, zoff[i], loc(nd.child[0]),
-                           loc(nd.child[1]), loc(nd.child[2]), 0u});
+        if (height[i] != cur_h) { cur_h = height[i]; pre = 0; }
+        const uint32_t words = (nd.r + 31) / 32;
+        // nd[7]: first 16-byte unit of this node within its level (item numbering)
+        T.inner.push_back({(uint32_t)nd.kind, words, nd.h / 32, zoff[i], loc(nd.child[0]), loc(nd.child[1]),
+                           loc(nd.child[2]), pre});
+        pre += (words + 3) / 4;
         for (int h = height[i]; h <= maxd; ++h) T.height_end[h] = (uint32_t)T.inner.size();
+    }
+    // levels {first node, end node, 16-byte units per block}; the root level (last)
+    // counts the root row plus one zero unit (the pack reads one word past a row)
+    for (int h = 1; h <= maxd; ++h) {
+        const uint32_t i0 = T.height_end[h - 1], i1 = T.height_end[h];
+        if (i1 == i0) continue;
+        const auto &last = T.inner[i1 - 1];
+        uint32_t u = last[7] + (last[1] + 3) / 4;
+        if (h == maxd) u += 1;
+        T.levels.push_back({i0, i1, u, 0u});
     }
     std::stable_sort(leaves.begin(), leaves.end(), [](const HostLeaf &a, const HostLeaf &b) { return a.w > b.w; });
     T.leaves = leaves;
@@ -307,6 +327,7 @@ struct Tables {
     uint32_t *terms = nullptr;     // device: seed and input terms
     uint4 *qbufs = nullptr;        // device: {src word offset (raw: in block; X: in row), words, dst, src is X}
     uint32_t *inner = nullptr;     // device: internal-node table (8 words per node)
+    uint4 *levels = nullptr;       // device: level table
     std::vector<gemm::Leaf> hleaves;
 };
 
@@ -332,7 +353,7 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
     std::vector<uint4> hq;
     for (const auto &Q : H.qbufs) {
         const uint32_t off = Q.src < 0 ? Q.src_off / 32 : H.qbufs[Q.src].dst + Q.src_off / 32;
-        hq.push_back(make_uint4(off, Q.h / 32, Q.dst, Q.src < 0 ? 0u : 1u));
+        hq.push_back(make_uint4(off, Q.h / 32, Q.dst, (Q.src < 0 ? 0u : 1u) | (Q.gen << 1)));
     }
     for (const auto &L : H.leaves) {
         gemm::Leaf g{};
@@ -363,9 +384,12 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
     if (e == cudaSuccess) e = cudaMemcpy(t->terms, terms.data(), terms.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !H.inner.empty())
         e = cudaMemcpy(t->inner, H.inner.data(), H.inner.size() * 32, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&t->levels, H.levels.size() * 16 + 16);
+    if (e == cudaSuccess && !H.levels.empty())
+        e = cudaMemcpy(t->levels, H.levels.data(), H.levels.size() * 16, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         set_error("Karatsuba tables: %s", cudaGetErrorString(e));
-        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs);
+        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs); cudaFree(t->levels);
         delete t;
         return QRNG_E_CUDA;
     }
@@ -417,81 +441,188 @@ __global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms
     }
 }
 
-// Q buffers of one generation: X[b][dst + g] = S[b][off + g] ^ S[b][off + h/32 + g]
-// (x0 ^ x1 of a Karatsuba node; S = raw block or an earlier Q buffer; 16-byte
-// granules).  blockIdx.y = buffer; each CTA covers `per` blocks per pass.
-__global__ void __launch_bounds__(256) qbuf_kernel(const uint4 *qb, uint32_t q0, const uint4 *raw, uint64_t n_blocks,
-                                                   uint32_t n, uint4 *xws, uint32_t x_stride) {
-    const uint4 Q = qb[q0 + blockIdx.y];  // {src word offset, words, dst word offset, src is X}
-    const uint32_t gper = Q.y / 4;
-    const uint32_t per = gper >= blockDim.x ? 1u : blockDim.x / gper;
-    const uint32_t bl = gper >= blockDim.x ? 0u : threadIdx.x / gper;
-    const uint32_t g0 = gper >= blockDim.x ? threadIdx.x : threadIdx.x - bl * gper;
-    const uint32_t gstep = gper >= blockDim.x ? blockDim.x : gper;
-    if (bl >= per) return;
-    for (uint64_t b = (uint64_t)blockIdx.x * per + bl; b < n_blocks; b += (uint64_t)gridDim.x * per) {
-        const uint4 *src = Q.w ? xws + b * (x_stride / 4) : raw + b * (n / 128);
-        uint4 *dst = xws + b * (x_stride / 4) + Q.z / 4;
-        for (uint32_t g = g0; g < gper; g += gstep) {
+// All Q buffers of a few blocks, generation by generation (one launch):
+// X[b][dst + g] = S[b][off + g] ^ S[b][off + h/32 + g]  (x0 ^ x1 of a Karatsuba
+// node; S = the raw block or an earlier Q buffer of the same block, written
+// by this CTA before the __syncthreads that separates generations).
+// qb[i] = {src word offset, words, dst word offset, src is X | gen << 1}.
+__global__ void __launch_bounds__(256) qbuf_kernel(const uint4 *qb, uint32_t n_q, const uint4 *raw, uint64_t n_blocks,
+                                                   uint32_t n, uint4 *xws, uint32_t x_stride, uint32_t bpc) {
+    const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
+    const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
+    uint32_t gen = 1;
+    for (uint32_t i = 0; i < n_q; ++i) {
+        const uint4 Q = qb[i];
+        if ((Q.w >> 1) != gen) {  // next generation reads this one
+            __syncthreads();
+            gen = Q.w >> 1;
+        }
+        const uint32_t gper = Q.y / 4;
+        for (uint32_t idx = threadIdx.x; idx < nb * gper; idx += blockDim.x) {
+            const uint32_t bl = idx / gper, g = idx - bl * gper;
+            const uint64_t b = b0 + bl;
+            const uint4 *src = (Q.w & 1) ? xws + b * (x_stride / 4) : raw + b * (n / 128);
             const uint4 u = src[Q.x / 4 + g], v = src[(Q.x + Q.y) / 4 + g];
-            dst[g] = make_uint4(u.x ^ v.x, u.y ^ v.y, u.z ^ v.z, u.w ^ v.w);
+            xws[b * (x_stride / 4) + Q.z / 4 + g] = make_uint4(u.x ^ v.x, u.y ^ v.y, u.z ^ v.z, u.w ^ v.w);
         }
     }
 }
 
-// Combine, one launch per height: node output word j of block b (Z row) =
-//   KARA: j < h/32 ? Q[j] ^ P2[j] : Q[j - h/32] ^ P3[j - h/32]      (y0 = Q^P2, y1 = Q^P3)
-//   COLS: L[j] ^ R[j]
-// children read from the leaf parities (Y) or lower nodes (Z); coalesced words.
-__global__ void __launch_bounds__(256) combine_kernel(const uint32_t *inner, uint32_t i0, const uint32_t *yws,
-                                                      uint32_t y_stride, uint32_t *zws, uint32_t z_stride,
-                                                      uint64_t n_blocks) {
-    const uint32_t *nd = inner + 8 * (i0 + blockIdx.y);
-    const uint32_t kind = nd[0], words = nd[1], hw = nd[2], dst = nd[3];
-    const uint32_t c0 = nd[4], c1 = nd[5], c2 = nd[6];
-    const uint32_t per = words >= blockDim.x ? 1u : blockDim.x / words;
-    const uint32_t bl = words >= blockDim.x ? 0u : threadIdx.x / words;
-    const uint32_t j0 = words >= blockDim.x ? threadIdx.x : threadIdx.x - bl * words;
-    const uint32_t jstep = words >= blockDim.x ? blockDim.x : words;
-    if (bl >= per) return;
-    for (uint64_t b = (uint64_t)blockIdx.x * per + bl; b < n_blocks; b += (uint64_t)gridDim.x * per) {
-        const uint32_t *Y = yws + b * y_stride;
-        uint32_t *Z = zws + b * z_stride;
-        auto at = [&](uint32_t c, uint32_t w) { return (c >> 31) ? Z[(c & 0x7FFFFFFFu) + w] : Y[c + w]; };
-        for (uint32_t j = j0; j < words; j += jstep) {
-            uint32_t v;
-            if (kind == 1) v = j < hw ? (at(c0, j) ^ at(c1, j)) : (at(c0, j - hw) ^ at(c2, j - hw));
-            else v = at(c0, j) ^ at(c1, j);
-            Z[dst + j] = v;
+// Combine, one launch per height: node output words [4q, 4q+4) of block b (Z row) =
+//   KARA: 4q < h/32 ? Q ^ P2 : Q[. - h/32] ^ P3[. - h/32]          (y0 = Q^P2, y1 = Q^P3)
+//   COLS: L ^ R
+// children read from the leaf parities (Y) or lower nodes (Z).  Every row and
+// h/32 are multiples of 4 words, so each thread moves 16-byte vectors; words
+// past a child's rows are don't-care (they only reach rows >= the node's r).
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) { return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w); }
+__device__ __forceinline__ uint4 node_word4(const uint32_t *nd, const uint4 *Y, const uint4 *Z, uint32_t q) {
+    const uint32_t kind = nd[0], hq = nd[2] / 4;
+    auto at = [&](uint32_t c, uint32_t i) { return (c >> 31) ? Z[(c & 0x7FFFFFFFu) / 4 + i] : Y[c / 4 + i]; };
+    if (kind == 1) return q < hq ? xor4(at(nd[4], q), at(nd[5], q)) : xor4(at(nd[4], q - hq), at(nd[6], q - hq));
+    return xor4(at(nd[4], q), at(nd[5], q));
+}
+
+// One combine level for the nb blocks of a CTA: every (block, node, 16-byte
+// unit) of the level is an independent item; each thread takes U items at a
+// time with all their loads in flight before the stores.  Y: leaf parities of
+// block b0 (row stride ys4 units); Z: node rows (stride zs4); the root level
+// writes R (stride rs4; units past the root row are zero).
+template <int U>
+__device__ __forceinline__ void combine_level(const uint32_t *inner, uint4 lv, uint32_t nb, const uint4 *Y, uint32_t ys4,
+                                              uint4 *Z, uint32_t zs4, uint4 *R, uint32_t rs4) {
+    const uint32_t total = nb * lv.z;
+    for (uint32_t base = threadIdx.x; base < total; base += U * blockDim.x) {
+        uint4 va[U], vb[U];
+        uint4 *dst[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t idx = base + u * blockDim.x;
+            dst[u] = nullptr;
+            va[u] = vb[u] = make_uint4(0, 0, 0, 0);
+            if (idx < total) {
+                const uint32_t bl = idx / lv.z, r = idx - bl * lv.z;
+                uint32_t i = lv.x;
+                while (i + 1 < lv.y && r >= inner[8 * (i + 1) + 7]) ++i;
+                const uint32_t *nd = inner + 8 * i;
+                const uint32_t q = r - nd[7], hq = nd[2] / 4;
+                const uint4 *Yb = Y + bl * ys4;
+                uint4 *Zb = Z + bl * zs4;
+                dst[u] = R ? R + bl * rs4 + q : Zb + nd[3] / 4 + q;
+                if (q < (nd[1] + 3) / 4) {
+                    uint32_t c0 = nd[4], c1 = nd[5], qq = q;
+                    if (nd[0] == 1 && q >= hq) { c1 = nd[6]; qq = q - hq; }  // y1 = Q ^ P3
+                    const uint4 *p0 = (c0 >> 31) ? Zb + (c0 & 0x7FFFFFFFu) / 4 : Yb + c0 / 4;
+                    const uint4 *p1 = (c1 >> 31) ? Zb + (c1 & 0x7FFFFFFFu) / 4 : Yb + c1 / 4;
+                    va[u] = p0[qq];
+                    vb[u] = p1[qq];
+                }
+            }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (dst[u]) *dst[u] = xor4(va[u], vb[u]);
+    }
+}
+
+// Every level below the root for bpc blocks per CTA (node rows in global Z).
+__global__ void __launch_bounds__(256) combine_kernel(const uint32_t *inner, const uint4 *levels, uint32_t n_levels,
+                                                      const uint32_t *yws, uint32_t y_stride, uint32_t *zws,
+                                                      uint32_t z_stride, uint64_t n_blocks, uint32_t bpc) {
+    const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
+    const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
+    for (uint32_t l = 0; l < n_levels; ++l) {
+        if (l) __syncthreads();  // the next level reads this one
+        combine_level<4>(inner, levels[l], nb, reinterpret_cast<const uint4 *>(yws + b0 * y_stride), y_stride / 4,
+                         reinterpret_cast<uint4 *>(zws + b0 * z_stride), z_stride / 4, nullptr, 0);
     }
 }
 
 // Key stream (C4): CTA c owns blocks [32c, 32c+32), whose keys fill exactly
-// the output words [c*m, (c+1)*m) (32 m bits).  Word w of the group holds bits
-// [32w, 32w+32) of the group; block b's key is the first m bits of its root
-// row.  Every word has one writer (no pre-zeroing); a final partial word goes
-// to the tail scratch.
-__global__ void __launch_bounds__(256) pack_kernel(const uint32_t *rows, uint32_t stride, uint32_t off,
-                                                   uint64_t n_blocks, uint32_t m, OutStream out) {
+// the output words [c*m, (c+1)*m) (32 m bits).  The root node (the last
+// combine level) is evaluated here: STAGED = into shared memory first (rows of
+// up to ~1600 words), else word by word from the children.  Word w of the group
+// = bits [32w, 32w+32) of the concatenated keys (block b's key = the first m
+// bits of its root row).  Every output word has one writer (no pre-zeroing); a
+// final partial word goes to the tail scratch.
+template <bool STAGED>
+__global__ void __launch_bounds__(256) pack_kernel(const uint32_t *root, const uint32_t *yws, uint32_t y_stride,
+                                                   const uint32_t *zws, uint32_t z_stride, uint64_t n_blocks,
+                                                   uint32_t m, OutStream out) {
+    extern __shared__ uint4 rs4[];  // STAGED: 32 rows of rw4 uint4 (last one zero)
+    const uint32_t *rs = reinterpret_cast<const uint32_t *>(rs4);
     const uint64_t b0 = (uint64_t)blockIdx.x * 32;
     const uint32_t nb = (uint32_t)min((uint64_t)32, n_blocks - b0);
-    const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32, rw = (m + 31) / 32;
+    const uint32_t rw4 = ((m + 31) / 32 + 3) / 4 + 1, rwords = 4 * rw4;
+    if (STAGED) {
+        for (uint32_t i = threadIdx.x; i < nb * rw4; i += blockDim.x) {
+            const uint32_t bl = i / rw4, q = i - bl * rw4;
+            const uint64_t b = b0 + bl;
+            rs4[i] = q + 1 < rw4 ? node_word4(root, reinterpret_cast<const uint4 *>(yws + b * y_stride),
+                                              reinterpret_cast<const uint4 *>(zws + b * z_stride), q)
+                                 : make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+    }
+    auto rword = [&](uint32_t bl, uint32_t q) -> uint32_t {  // word q of block b0+bl's root row
+        if (STAGED) return rs[bl * rwords + q];
+        const uint64_t b = b0 + bl;
+        const uint4 v = node_word4(root, reinterpret_cast<const uint4 *>(yws + b * y_stride),
+                                   reinterpret_cast<const uint4 *>(zws + b * z_stride), q / 4);
+        const uint32_t r = q & 3;
+        return r == 0 ? v.x : r == 1 ? v.y : r == 2 ? v.z : v.w;
+    };
+    const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
     for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
         const uint32_t G = w * 32, end = min(G + 32, gbits);
         uint32_t b = G / m, i = G - b * m, pos = G, word = 0;
         while (pos < end) {
             const uint32_t len = min(m - i, end - pos);  // 1..32 bits of block b
-            const uint32_t *row = rows + (b0 + b) * stride + off;
             const uint32_t q = i >> 5, s = i & 31;
-            const uint32_t w0 = row[q], w1 = (s && q + 1 < rw) ? row[q + 1] : 0u;
-            const uint32_t bits = s ? ((w0 << s) | (w1 >> (32 - s))) : w0;  // rows i.. at the MSB
+            const uint32_t w0 = rword(b, q);
+            const uint32_t bits = s ? ((w0 << s) | (rword(b, q + 1) >> (32 - s))) : w0;  // rows i.. at the MSB
             word |= (bits >> (32 - len)) << (32 - len - (pos - G));
             pos += len;
             ++b;
             i = 0;
         }
-        emit_word(out, (uint64_t)blockIdx.x * m + w, word, true);
+        emit_word(out, b0 * m / 32 + w, word, true);
+    }
+}
+
+// Fused tree combine + pack for 32 blocks whose internal node rows and root
+// rows fit in shared memory: leaf parities are read from Y (L2), every combine
+// level stays in shared memory, then the key words [c*m, (c+1)*m) of the
+// group are written (one writer each, no pre-zeroing).
+__global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, const uint4 *levels, uint32_t n_levels,
+                                                        const uint32_t *yws, uint32_t y_stride, uint32_t z_stride,
+                                                        uint64_t n_blocks, uint32_t m, OutStream out) {
+    extern __shared__ uint4 sm4[];
+    const uint64_t b0 = (uint64_t)blockIdx.x * 32;
+    const uint32_t nb = (uint32_t)min((uint64_t)32, n_blocks - b0);
+    const uint32_t zs4 = z_stride / 4, rw4 = levels[n_levels - 1].z, rwords = 4 * rw4;
+    uint4 *Zs = sm4, *Rs = Zs + 32 * zs4;
+    const uint4 *Ys = reinterpret_cast<const uint4 *>(yws + b0 * y_stride);
+    for (uint32_t l = 0; l < n_levels; ++l) {
+        if (l) __syncthreads();
+        combine_level<4>(inner, levels[l], nb, Ys, y_stride / 4, Zs, zs4, l + 1 == n_levels ? Rs : nullptr, rw4);
+    }
+    __syncthreads();
+    const uint32_t *rs = reinterpret_cast<const uint32_t *>(Rs);
+    const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
+    for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
+        const uint32_t G = w * 32, end = min(G + 32, gbits);
+        uint32_t b = G / m, i = G - b * m, pos = G, word = 0;
+        while (pos < end) {
+            const uint32_t len = min(m - i, end - pos);  // 1..32 bits of block b
+            const uint32_t *row = rs + b * rwords;
+            const uint32_t q = i >> 5, s = i & 31;
+            const uint32_t bits = s ? ((row[q] << s) | (row[q + 1] >> (32 - s))) : row[q];
+            word |= (bits >> (32 - len)) << (32 - len - (pos - G));
+            pos += len;
+            ++b;
+            i = 0;
+        }
+        emit_word(out, b0 * m / 32 + w, word, true);
     }
 }
 
@@ -538,42 +669,57 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     if (H.x_stride) QRNG_CUDA_TRY(cudaMallocAsync(&xws, (size_t)n_blocks * H.x_stride * 4, s));
     QRNG_CUDA_TRY(cudaMallocAsync(&yws, (size_t)n_blocks * H.y_stride * 4, s));
     qrng_status st = QRNG_OK;
-    // Q buffers generation by generation (each reads its parent generation)
-    for (uint32_t gen = 1, q0 = 0; gen <= H.max_gen && st == QRNG_OK; ++gen) {
-        uint32_t q1 = q0, maxw = 0;
-        while (q1 < H.qbufs.size() && H.qbufs[q1].gen == gen) maxw = std::max(maxw, H.qbufs[q1++].h / 32);
-        const uint32_t per = std::max<uint32_t>(1, 256 / std::max<uint32_t>(1, maxw / 4));
-        const unsigned gx = (unsigned)std::min<uint64_t>((n_blocks + per - 1) / per, 4096);
+    if (!H.qbufs.empty()) {  // Q buffers, generation by generation, 4 blocks per CTA
         count_launch();
-        qbuf_kernel<<<dim3(gx, q1 - q0), 256, 0, s>>>(t->qbufs, q0, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
-                                                      (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride);
+        qbuf_kernel<<<(unsigned)((n_blocks + 3) / 4), 256, 0, s>>>(t->qbufs, (uint32_t)H.qbufs.size(),
+                                                                  reinterpret_cast<const uint4 *>(d_raw), n_blocks,
+                                                                  (uint32_t)n, reinterpret_cast<uint4 *>(xws),
+                                                                  H.x_stride, 4u);
         if (cudaGetLastError() != cudaSuccess) { set_error("qbuf_kernel launch failed"); st = QRNG_E_CUDA; }
-        q0 = q1;
     }
     if (st == QRNG_OK)
         st = gemm::extract_grouped(t->leaves, (uint32_t)t->hleaves.size(), H.total_npairs, pl.seeds, d_raw, n_blocks,
                                    n, xws, H.x_stride, yws, H.y_stride, s);
+    const uint32_t rw4 = (uint32_t)(((m + 31) / 32 + 3) / 4 + 1);
+    const size_t fused_smem = (size_t)32 * (H.z_stride + 4 * rw4) * 4;
     uint32_t *zws = nullptr;
-    if (st == QRNG_OK && cudaMallocAsync(&zws, (size_t)n_blocks * H.z_stride * 4, s) != cudaSuccess) {
-        set_error("cudaMallocAsync failed");
-        st = QRNG_E_NOMEM;
-    }
-    for (size_t h = 1; h < H.height_end.size() && st == QRNG_OK; ++h) {
-        const uint32_t i0 = H.height_end[h - 1], i1 = H.height_end[h];
-        if (i1 == i0) continue;
-        uint32_t maxw = 0;
-        for (uint32_t i = i0; i < i1; ++i) maxw = std::max(maxw, H.inner[i][1]);
-        const uint32_t per = std::max<uint32_t>(1, 256 / std::max<uint32_t>(1, maxw));
-        const unsigned gx = (unsigned)std::min<uint64_t>((n_blocks + per - 1) / per, 8192);
+    if (st == QRNG_OK && fused_smem <= 200 * 1024) {
+        // whole tree of 32 blocks in shared memory
+        if (fused_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(tree_pack_kernel));
         count_launch();
-        combine_kernel<<<dim3(gx, i1 - i0), 256, 0, s>>>(t->inner, i0, yws, H.y_stride, zws, H.z_stride, n_blocks);
-        if (cudaGetLastError() != cudaSuccess) { set_error("combine_kernel launch failed"); st = QRNG_E_CUDA; }
-    }
-    if (st == QRNG_OK) {
-        count_launch();
-        pack_kernel<<<(unsigned)((n_blocks + 31) / 32), 256, 0, s>>>(
-            zws, H.z_stride, H.root_z, n_blocks, (uint32_t)m, out);
-        if (cudaGetLastError() != cudaSuccess) { set_error("pack_kernel launch failed"); st = QRNG_E_CUDA; }
+        tree_pack_kernel<<<(unsigned)((n_blocks + 31) / 32), 512, fused_smem, s>>>(
+            t->inner, t->levels, (uint32_t)H.levels.size(), yws, H.y_stride, H.z_stride, n_blocks, (uint32_t)m, out);
+        if (cudaGetLastError() != cudaSuccess) { set_error("tree_pack_kernel launch failed"); st = QRNG_E_CUDA; }
+    } else if (st == QRNG_OK) {
+        if (cudaMallocAsync(&zws, (size_t)n_blocks * H.z_stride * 4, s) != cudaSuccess) {
+            set_error("cudaMallocAsync failed");
+            st = QRNG_E_NOMEM;
+        }
+        // every node below the root; CTAs of bpc blocks, at least ~2 CTAs per SM
+        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / 296));
+        if (st == QRNG_OK && H.levels.size() > 1) {
+            count_launch();
+            combine_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), 256, 0, s>>>(
+                t->inner, t->levels, (uint32_t)H.levels.size() - 1, yws, H.y_stride, zws, H.z_stride, n_blocks, bpc);
+            if (cudaGetLastError() != cudaSuccess) { set_error("combine_kernel launch failed"); st = QRNG_E_CUDA; }
+        }
+        if (st == QRNG_OK) {
+            // 32 blocks per CTA (their keys are exactly m output words); stage the
+            // root rows in shared memory when they fit
+            const size_t smem = (size_t)32 * rw4 * 16;
+            const unsigned grid = (unsigned)((n_blocks + 31) / 32);
+            const uint32_t *root = t->inner + 8 * (H.inner.size() - 1);
+            count_launch();
+            if (smem <= 200 * 1024) {
+                if (smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(pack_kernel<true>));
+                pack_kernel<true><<<grid, 256, smem, s>>>(root, yws, H.y_stride, zws, H.z_stride, n_blocks,
+                                                          (uint32_t)m, out);
+            } else {
+                pack_kernel<false><<<grid, 256, 0, s>>>(root, yws, H.y_stride, zws, H.z_stride, n_blocks,
+                                                        (uint32_t)m, out);
+            }
+            if (cudaGetLastError() != cudaSuccess) { set_error("pack_kernel launch failed"); st = QRNG_E_CUDA; }
+        }
     }
     if (zws) cudaFreeAsync(zws, s);
     if (xws) cudaFreeAsync(xws, s);

@@ -105,10 +105,21 @@ struct Leaf {
     uint32_t sterm_base, sterm_n;  // seed terms (bit offsets into the root seed) in the term table
     uint32_t iterm_base, iterm_n;  // input terms (bit offsets into the raw block)
 };
-#ifndef QRNG_GEMM_NT
-#define QRNG_GEMM_NT 2  // N tiles of 192 rows per A stage in the tcgen05 kernel (build-time choice)
+// tcgen05 kernel geometry (build-time; gemm_tc.cu): rows per N tile, N tiles per
+// A stage, A ring slots, accumulator sets.
+#ifndef QRNG_GEMM_BN
+#define QRNG_GEMM_BN 192
 #endif
-constexpr int kTileRows = 192 * QRNG_GEMM_NT;  // output rows per work tile (NT * BN)
+#ifndef QRNG_GEMM_NT
+#define QRNG_GEMM_NT 2
+#endif
+#ifndef QRNG_GEMM_ASTAGES
+#define QRNG_GEMM_ASTAGES 4
+#endif
+#ifndef QRNG_GEMM_ACCBUFS
+#define QRNG_GEMM_ACCBUFS 1
+#endif
+constexpr int kTileRows = QRNG_GEMM_BN * QRNG_GEMM_NT;  // output rows per work tile (NT * BN)
 uint32_t seed_words_needed(uint64_t n, uint64_t m);
 // Grouped launch over the leaf table (Karatsuba): parities of leaf l, block b,
 // row i go to bit 31 - (i & 31) of yws[b * y_stride + out_off + i / 32] (logical words).
