@@ -48,7 +48,7 @@ constexpr int kAutoMaxDepth = 5;  // auto mode: deeper trees spill the leaf pari
 // B200).
 constexpr double kTileOverhead = 186e3;  // per work tile (pipeline fill, accumulator drain; ~3.6k SM clocks)
 constexpr double kPrepPerBit = 180.0;    // forming x0 ^ x1 in the workspace, per input bit
-constexpr double kLeafRow = 450.0;       // leaf parities written by the GEMM and read by the combine, per row
+constexpr double kLeafRow = 250.0;       // leaf parities written by the GEMM and read by the combine, per row
 constexpr double kCombPerRow = 0.0;      // internal node row written and read back, per row
 
 static double leaf_cost(uint32_t r, uint32_t w) {
@@ -139,7 +139,8 @@ struct HostTables {
     // h/32, dst word in a block's Z row, child locations (word offset | 1<<31 if in Z)}
     std::vector<std::array<uint32_t, 8>> inner;
     std::vector<uint32_t> height_end;      // inner[height_end[h-1] .. height_end[h]) have height h
-    std::vector<std::array<uint32_t, 4>> levels;  // {first node, end node, units per block, 0}; root last
+    std::vector<std::array<uint32_t, 4>> levels;  // {first node, end node, units per block, unit_node offset}; root last
+    std::vector<uint32_t> unit_node;       // per level: 16-byte unit -> node index
     uint32_t z_stride = 0, root_z = 0;
     std::vector<uint32_t> comb_ptr, comb_idx;  // CSR per root output word -> Y-row word offsets
     uint32_t y_stride = 0, x_stride = 0, total_npairs = 0, root_words = 0, seed_total = 0;
@@ -285,7 +286,10 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
         const auto &last = T.inner[i1 - 1];
         uint32_t u = last[7] + (last[1] + 3) / 4;
         if (h == maxd) u += 1;
-        T.levels.push_back({i0, i1, u, 0u});
+        T.levels.push_back({i0, i1, u, (uint32_t)T.unit_node.size()});
+        for (uint32_t i = i0; i < i1; ++i)  // unit -> node of this level
+            for (uint32_t v = 0; v < (T.inner[i][1] + 3) / 4; ++v) T.unit_node.push_back(i);
+        if (h == maxd) T.unit_node.push_back(i1 - 1);  // the root's zero unit
     }
     std::stable_sort(leaves.begin(), leaves.end(), [](const HostLeaf &a, const HostLeaf &b) { return a.w > b.w; });
     T.leaves = leaves;
@@ -328,6 +332,7 @@ struct Tables {
     uint4 *qbufs = nullptr;        // device: {src word offset (raw: in block; X: in row), words, dst, src is X}
     uint32_t *inner = nullptr;     // device: internal-node table (8 words per node)
     uint4 *levels = nullptr;       // device: level table
+    uint32_t *unit_node = nullptr; // device: unit -> node per level
     std::vector<gemm::Leaf> hleaves;
 };
 
@@ -385,11 +390,14 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
     if (e == cudaSuccess && !H.inner.empty())
         e = cudaMemcpy(t->inner, H.inner.data(), H.inner.size() * 32, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&t->levels, H.levels.size() * 16 + 16);
+    if (e == cudaSuccess) e = cudaMalloc(&t->unit_node, H.unit_node.size() * 4 + 4);
+    if (e == cudaSuccess && !H.unit_node.empty())
+        e = cudaMemcpy(t->unit_node, H.unit_node.data(), H.unit_node.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !H.levels.empty())
         e = cudaMemcpy(t->levels, H.levels.data(), H.levels.size() * 16, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         set_error("Karatsuba tables: %s", cudaGetErrorString(e));
-        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs); cudaFree(t->levels);
+        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs); cudaFree(t->levels); cudaFree(t->unit_node);
         delete t;
         return QRNG_E_CUDA;
     }
@@ -488,8 +496,9 @@ __device__ __forceinline__ uint4 node_word4(const uint32_t *nd, const uint4 *Y, 
 // block b0 (row stride ys4 units); Z: node rows (stride zs4); the root level
 // writes R (stride rs4; units past the root row are zero).
 template <int U>
-__device__ __forceinline__ void combine_level(const uint32_t *inner, uint4 lv, uint32_t nb, const uint4 *Y, uint32_t ys4,
-                                              uint4 *Z, uint32_t zs4, uint4 *R, uint32_t rs4) {
+__device__ __forceinline__ void combine_level(const uint32_t *inner, const uint32_t *unit_node, uint4 lv, uint32_t nb,
+                                              const uint4 *Y, uint32_t ys4, uint4 *Z, uint32_t zs4, uint4 *R,
+                                              uint32_t rs4) {
     const uint32_t total = nb * lv.z;
     for (uint32_t base = threadIdx.x; base < total; base += U * blockDim.x) {
         uint4 va[U], vb[U];
@@ -501,9 +510,7 @@ __device__ __forceinline__ void combine_level(const uint32_t *inner, uint4 lv, u
             va[u] = vb[u] = make_uint4(0, 0, 0, 0);
             if (idx < total) {
                 const uint32_t bl = idx / lv.z, r = idx - bl * lv.z;
-                uint32_t i = lv.x;
-                while (i + 1 < lv.y && r >= inner[8 * (i + 1) + 7]) ++i;
-                const uint32_t *nd = inner + 8 * i;
+                const uint32_t *nd = inner + 8 * __ldg(unit_node + lv.w + r);
                 const uint32_t q = r - nd[7], hq = nd[2] / 4;
                 const uint4 *Yb = Y + bl * ys4;
                 uint4 *Zb = Z + bl * zs4;
@@ -525,15 +532,16 @@ __device__ __forceinline__ void combine_level(const uint32_t *inner, uint4 lv, u
 }
 
 // Every level below the root for bpc blocks per CTA (node rows in global Z).
-__global__ void __launch_bounds__(256) combine_kernel(const uint32_t *inner, const uint4 *levels, uint32_t n_levels,
+__global__ void __launch_bounds__(512) combine_kernel(const uint32_t *inner, const uint32_t *unit_node,
+                                                      const uint4 *levels, uint32_t n_levels,
                                                       const uint32_t *yws, uint32_t y_stride, uint32_t *zws,
                                                       uint32_t z_stride, uint64_t n_blocks, uint32_t bpc) {
     const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
     const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
     for (uint32_t l = 0; l < n_levels; ++l) {
         if (l) __syncthreads();  // the next level reads this one
-        combine_level<4>(inner, levels[l], nb, reinterpret_cast<const uint4 *>(yws + b0 * y_stride), y_stride / 4,
-                         reinterpret_cast<uint4 *>(zws + b0 * z_stride), z_stride / 4, nullptr, 0);
+        combine_level<8>(inner, unit_node, levels[l], nb, reinterpret_cast<const uint4 *>(yws + b0 * y_stride),
+                         y_stride / 4, reinterpret_cast<uint4 *>(zws + b0 * z_stride), z_stride / 4, nullptr, 0);
     }
 }
 
@@ -593,7 +601,8 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t *root, const u
 // rows fit in shared memory: leaf parities are read from Y (L2), every combine
 // level stays in shared memory, then the key words [c*m, (c+1)*m) of the
 // group are written (one writer each, no pre-zeroing).
-__global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, const uint4 *levels, uint32_t n_levels,
+__global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, const uint32_t *unit_node,
+                                                        const uint4 *levels, uint32_t n_levels,
                                                         const uint32_t *yws, uint32_t y_stride, uint32_t z_stride,
                                                         uint64_t n_blocks, uint32_t m, OutStream out) {
     extern __shared__ uint4 sm4[];
@@ -604,7 +613,8 @@ __global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, c
     const uint4 *Ys = reinterpret_cast<const uint4 *>(yws + b0 * y_stride);
     for (uint32_t l = 0; l < n_levels; ++l) {
         if (l) __syncthreads();
-        combine_level<4>(inner, levels[l], nb, Ys, y_stride / 4, Zs, zs4, l + 1 == n_levels ? Rs : nullptr, rw4);
+        combine_level<8>(inner, unit_node, levels[l], nb, Ys, y_stride / 4, Zs, zs4, l + 1 == n_levels ? Rs : nullptr,
+                         rw4);
     }
     __syncthreads();
     const uint32_t *rs = reinterpret_cast<const uint32_t *>(Rs);
@@ -688,19 +698,21 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
         if (fused_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(tree_pack_kernel));
         count_launch();
         tree_pack_kernel<<<(unsigned)((n_blocks + 31) / 32), 512, fused_smem, s>>>(
-            t->inner, t->levels, (uint32_t)H.levels.size(), yws, H.y_stride, H.z_stride, n_blocks, (uint32_t)m, out);
+            t->inner, t->unit_node, t->levels, (uint32_t)H.levels.size(), yws, H.y_stride, H.z_stride, n_blocks,
+            (uint32_t)m, out);
         if (cudaGetLastError() != cudaSuccess) { set_error("tree_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK) {
         if (cudaMallocAsync(&zws, (size_t)n_blocks * H.z_stride * 4, s) != cudaSuccess) {
             set_error("cudaMallocAsync failed");
             st = QRNG_E_NOMEM;
         }
-        // every node below the root; CTAs of bpc blocks, at least ~2 CTAs per SM
-        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / 296));
+        // every node below the root; CTAs of bpc blocks, at least ~4 CTAs per SM
+        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / 592));
         if (st == QRNG_OK && H.levels.size() > 1) {
             count_launch();
-            combine_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), 256, 0, s>>>(
-                t->inner, t->levels, (uint32_t)H.levels.size() - 1, yws, H.y_stride, zws, H.z_stride, n_blocks, bpc);
+            combine_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, 0, s>>>(
+                t->inner, t->unit_node, t->levels, (uint32_t)H.levels.size() - 1, yws, H.y_stride, zws, H.z_stride,
+                n_blocks, bpc);
             if (cudaGetLastError() != cudaSuccess) { set_error("combine_kernel launch failed"); st = QRNG_E_CUDA; }
         }
         if (st == QRNG_OK) {

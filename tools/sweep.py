@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--min", type=int, default=10)
     ap.add_argument("--max", type=int, default=22)
     ap.add_argument("--step", type=int, default=1)
+    ap.add_argument("--gemm-max", type=int, default=20, help="largest log2 n timed on the GEMM path")
     args = ap.parse_args()
     q.load_library()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -55,13 +56,18 @@ def main():
         res = {}
         outs = {}
         for name, path in (("gemm", q.PATH_GEMM), ("ntt", q.PATH_NTT)):
-            if name == "gemm" and w.n > (1 << 16):
+            if name == "gemm" and w.n > (1 << args.gemm_max):
                 continue
             ms, out = time_path(path, raw, seed, w, args.steps, args.warmup, flush)
             res[name] = ms
             outs[name] = out
-            print(json.dumps({"n": w.n, "m": w.m, "blocks": w.n_blocks, "path": name, "ms": ms,
-                              "gbit_s": w.raw_bits / ms / 1e6}), flush=True)
+            rec = {"n": w.n, "m": w.m, "blocks": w.n_blocks, "path": name, "ms": ms, "gbit_s": w.raw_bits / ms / 1e6}
+            if name == "gemm":
+                q.set_debug_path(path)
+                with q.Plan(w.n, w.m, seed) as pl:
+                    rec["karatsuba_depth"] = pl.info()["karatsuba_depth"]
+                q.set_debug_path(q.PATH_AUTO)
+            print(json.dumps(rec), flush=True)
         if len(outs) == 2:
             assert torch.equal(outs["gemm"], outs["ntt"]), f"paths disagree at n={w.n}"
         best[w.n] = min(res, key=res.get)
