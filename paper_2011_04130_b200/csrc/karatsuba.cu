@@ -329,10 +329,13 @@ struct Tables {
     HostTables host;
     gemm::Leaf *leaves = nullptr;  // device
     uint32_t *terms = nullptr;     // device: seed and input terms
-    uint4 *qbufs = nullptr;        // device: {src word offset (raw: in block; X: in row), words, dst, src is X}
+    uint4 *qbufs = nullptr;        // device: per 16-byte unit of the Q buffers (see get_tables)
+    std::vector<uint32_t> qgen;    // first unit of each generation (+ end)
+    uint32_t *qgen_dev = nullptr;
     uint32_t *inner = nullptr;     // device: internal-node table (8 words per node)
     uint4 *levels = nullptr;       // device: level table
     uint32_t *unit_node = nullptr; // device: unit -> node per level
+    uint32_t *csr = nullptr;       // device: root word -> Y-row words (row pointers, then offsets)
     std::vector<gemm::Leaf> hleaves;
 };
 
@@ -356,10 +359,18 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
     std::vector<uint32_t> terms;
     uint32_t npb = 0, so = 0;
     std::vector<uint4> hq;
-    for (const auto &Q : H.qbufs) {
-        const uint32_t off = Q.src < 0 ? Q.src_off / 32 : H.qbufs[Q.src].dst + Q.src_off / 32;
-        hq.push_back(make_uint4(off, Q.h / 32, Q.dst, (Q.src < 0 ? 0u : 1u) | (Q.gen << 1)));
+    // one entry per 16-byte unit of every Q buffer, generation by generation:
+    // {x0 word offset in the source row, h/32, destination word in the X row, source is X}
+    for (uint32_t gen = 1; gen <= H.max_gen; ++gen) {
+        t->qgen.push_back((uint32_t)hq.size());
+        for (const auto &Q : H.qbufs) {
+            if (Q.gen != gen) continue;
+            const uint32_t off = Q.src < 0 ? Q.src_off / 32 : H.qbufs[Q.src].dst + Q.src_off / 32;
+            for (uint32_t g = 0; g < Q.h / 128; ++g)
+                hq.push_back(make_uint4(off + 4 * g, Q.h / 32, Q.dst + 4 * g, Q.src < 0 ? 0u : 1u));
+        }
     }
+    t->qgen.push_back((uint32_t)hq.size());
     for (const auto &L : H.leaves) {
         gemm::Leaf g{};
         g.w = L.w;
@@ -385,19 +396,26 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
     if (e == cudaSuccess) e = cudaMalloc(&t->inner, H.inner.size() * 32 + 32);
     if (e == cudaSuccess && !hq.empty()) e = cudaMalloc(&t->qbufs, hq.size() * sizeof(uint4));
     if (e == cudaSuccess && !hq.empty()) e = cudaMemcpy(t->qbufs, hq.data(), hq.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&t->qgen_dev, t->qgen.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(t->qgen_dev, t->qgen.data(), t->qgen.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(t->leaves, t->hleaves.data(), t->hleaves.size() * sizeof(gemm::Leaf), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(t->terms, terms.data(), terms.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !H.inner.empty())
         e = cudaMemcpy(t->inner, H.inner.data(), H.inner.size() * 32, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&t->levels, H.levels.size() * 16 + 16);
     if (e == cudaSuccess) e = cudaMalloc(&t->unit_node, H.unit_node.size() * 4 + 4);
+    if (e == cudaSuccess) e = cudaMalloc(&t->csr, (H.comb_ptr.size() + H.comb_idx.size()) * 4);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(t->csr, H.comb_ptr.data(), H.comb_ptr.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(t->csr + H.comb_ptr.size(), H.comb_idx.data(), H.comb_idx.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !H.unit_node.empty())
         e = cudaMemcpy(t->unit_node, H.unit_node.data(), H.unit_node.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !H.levels.empty())
         e = cudaMemcpy(t->levels, H.levels.data(), H.levels.size() * 16, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         set_error("Karatsuba tables: %s", cudaGetErrorString(e));
-        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs); cudaFree(t->levels); cudaFree(t->unit_node);
+        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs); cudaFree(t->levels); cudaFree(t->unit_node); cudaFree(t->csr); cudaFree(t->qgen_dev);
         delete t;
         return QRNG_E_CUDA;
     }
@@ -416,62 +434,69 @@ bool choose(uint64_t n, uint64_t m, int max_depth) {
 // ---- kernels ---------------------------------------------------------------
 __device__ __forceinline__ uint32_t bswap(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// seed bytes (MSB-first) -> logical big-endian words, zero past L
-__global__ void root_words_kernel(const uint8_t *seed, uint64_t L, uint32_t *words, uint32_t nwords) {
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += gridDim.x * blockDim.x) {
-        uint32_t v = 0;
-        for (int k = 0; k < 4; ++k) {
-            const uint64_t byte = (uint64_t)w * 4 + k;
-            v |= (byte * 8 < L ? (uint32_t)seed[byte] : 0u) << (24 - 8 * k);
-        }
-        const uint64_t lo = (uint64_t)w * 32;
-        if (lo + 32 > L) v &= (L > lo) ? (0xFFFFFFFFu << (32 - (L - lo))) : 0u;
-        words[w] = v;
-    }
+// 32 seed bits [pos, pos+32) of an MSB-first byte buffer as a logical
+// big-endian word, zero at and past bit L.
+__device__ __forceinline__ uint32_t seed_window32(const uint8_t *seed, uint64_t L, uint64_t pos) {
+    if (pos >= L) return 0u;
+    const uint64_t b = pos >> 3, nbytes = (L + 7) / 8;
+    uint64_t v = 0;
+    for (int i = 0; i < 5; ++i) v = (v << 8) | (b + i < nbytes ? seed[b + i] : 0u);
+    uint32_t r = (uint32_t)(v >> (8 - (pos & 7)));
+    if (pos + 32 > L) r &= 0xFFFFFFFFu << (32 - (uint32_t)(L - pos));
+    return r;
 }
 
-// Leaf seeds: word q of leaf l = XOR over its terms t of root bits [t + 32q, t + 32q + 32),
-// zero at and past the leaf seed length r + w - 1.
-__global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms, const uint32_t *root,
+// Leaf seeds: word q of leaf l = XOR over its terms t of seed bits [t + 32q, t + 32q + 32)
+// (zero past n+m-1), zero at and past the leaf seed length r + w - 1.
+__global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms, const uint8_t *seed, uint64_t L,
                                  uint32_t *seeds) {
-    const gemm::Leaf L = leaves[blockIdx.y];
-    const uint32_t nw = L.seed_n;
-    const uint32_t len = L.r + L.w - 1;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nw; q += gridDim.x * blockDim.x) {
+    const gemm::Leaf Lf = leaves[blockIdx.y];
+    const uint32_t len = Lf.r + Lf.w - 1;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < Lf.seed_n; q += gridDim.x * blockDim.x) {
         uint32_t v = 0;
-        for (uint32_t k = 0; k < L.sterm_n; ++k) {
-            const uint32_t pos = terms[L.sterm_base + k] + 32 * q;
-            v ^= __funnelshift_l(root[(pos >> 5) + 1], root[pos >> 5], pos & 31);
-        }
+        for (uint32_t k = 0; k < Lf.sterm_n; ++k) v ^= seed_window32(seed, L, terms[Lf.sterm_base + k] + 32ull * q);
         const uint32_t lo = 32 * q;
         if (lo + 32 > len) v &= (len > lo) ? (0xFFFFFFFFu << (32 - (len - lo))) : 0u;
-        seeds[L.seed_off + q] = v;
+        seeds[Lf.seed_off + q] = v;
     }
 }
 
 // All Q buffers of a few blocks, generation by generation (one launch):
-// X[b][dst + g] = S[b][off + g] ^ S[b][off + h/32 + g]  (x0 ^ x1 of a Karatsuba
-// node; S = the raw block or an earlier Q buffer of the same block, written
-// by this CTA before the __syncthreads that separates generations).
-// qb[i] = {src word offset, words, dst word offset, src is X | gen << 1}.
-__global__ void __launch_bounds__(256) qbuf_kernel(const uint4 *qb, uint32_t n_q, const uint4 *raw, uint64_t n_blocks,
-                                                   uint32_t n, uint4 *xws, uint32_t x_stride, uint32_t bpc) {
+// X[b][dst] = S[b][x0] ^ S[b][x0 + h/32] per 16-byte unit (x0 ^ x1 of a
+// Karatsuba node; S = the raw block or an earlier Q buffer of the same block,
+// written by this CTA before the __syncthreads that separates generations).
+// Every (block, unit) of a generation is an independent item; U per thread
+// with their loads in flight together.
+template <int U>
+__global__ void __launch_bounds__(512) qbuf_kernel(const uint4 *units, const uint32_t *gen_start, uint32_t n_gen,
+                                                   const uint4 *raw, uint64_t n_blocks, uint32_t n, uint4 *xws,
+                                                   uint32_t x_stride, uint32_t bpc) {
     const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
     const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
-    uint32_t gen = 1;
-    for (uint32_t i = 0; i < n_q; ++i) {
-        const uint4 Q = qb[i];
-        if ((Q.w >> 1) != gen) {  // next generation reads this one
-            __syncthreads();
-            gen = Q.w >> 1;
-        }
-        const uint32_t gper = Q.y / 4;
-        for (uint32_t idx = threadIdx.x; idx < nb * gper; idx += blockDim.x) {
-            const uint32_t bl = idx / gper, g = idx - bl * gper;
-            const uint64_t b = b0 + bl;
-            const uint4 *src = (Q.w & 1) ? xws + b * (x_stride / 4) : raw + b * (n / 128);
-            const uint4 u = src[Q.x / 4 + g], v = src[(Q.x + Q.y) / 4 + g];
-            xws[b * (x_stride / 4) + Q.z / 4 + g] = make_uint4(u.x ^ v.x, u.y ^ v.y, u.z ^ v.z, u.w ^ v.w);
+    const uint32_t xs4 = x_stride / 4, rs4 = n / 128;
+    for (uint32_t gi = 0; gi < n_gen; ++gi) {
+        if (gi) __syncthreads();  // this generation reads the previous one
+        const uint32_t u0 = gen_start[gi], per = gen_start[gi + 1] - u0, total = nb * per;
+        for (uint32_t base = threadIdx.x; base < total; base += U * blockDim.x) {
+            uint4 a[U], c[U];
+            uint4 *dst[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t idx = base + u * blockDim.x;
+                dst[u] = nullptr;
+                if (idx < total) {
+                    const uint32_t bl = idx / per, r = idx - bl * per;
+                    const uint4 e = __ldg(units + u0 + r);
+                    const uint64_t b = b0 + bl;
+                    const uint4 *src = e.w ? xws + b * xs4 : raw + b * rs4;
+                    a[u] = src[e.x / 4];
+                    c[u] = src[(e.x + e.y) / 4];
+                    dst[u] = xws + b * xs4 + e.z / 4;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (dst[u]) *dst[u] = make_uint4(a[u].x ^ c[u].x, a[u].y ^ c[u].y, a[u].z ^ c[u].z, a[u].w ^ c[u].w);
         }
     }
 }
@@ -636,6 +661,63 @@ __global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, c
     }
 }
 
+// Combine + pack for 32 blocks whose leaf parities fit in shared memory: the
+// 32 Y rows (contiguous in the workspace) are copied in with coalesced 16-byte
+// loads, each root word is the XOR of its leaf words (the flattened tree: the
+// CSR of qrng_debug_karatsuba_plan, also staged in shared memory), then the key
+// words [c*m, (c+1)*m) of the group are written (one writer each).
+__global__ void __launch_bounds__(512) csr_pack_kernel(const uint32_t *csr, uint32_t csr_words, const uint32_t *yws,
+                                                       uint32_t y_stride, uint64_t n_blocks, uint32_t m, OutStream out) {
+    extern __shared__ uint4 sm4[];
+    const uint64_t b0 = (uint64_t)blockIdx.x * 32;
+    const uint32_t nb = (uint32_t)min((uint64_t)32, n_blocks - b0);
+    const uint32_t ywords = (m + 31) / 32, rwords = ywords + 1;
+    uint32_t *Ys = reinterpret_cast<uint32_t *>(sm4);
+    uint32_t *Rs = Ys + 32 * y_stride;
+    uint32_t *Cs = Rs + 32 * rwords;
+    const uint4 *src = reinterpret_cast<const uint4 *>(yws + b0 * y_stride);
+    {  // coalesced copy with 8 independent 16-byte loads in flight per thread
+        const uint32_t n4 = nb * (y_stride / 4);
+        for (uint32_t base = threadIdx.x; base < n4; base += 8 * blockDim.x) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (base + u * blockDim.x < n4) v[u] = __ldg(src + base + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (base + u * blockDim.x < n4) sm4[base + u * blockDim.x] = v[u];
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < csr_words; i += blockDim.x) Cs[i] = __ldg(csr + i);
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < nb * rwords; idx += blockDim.x) {
+        const uint32_t bl = idx / rwords, j = idx - bl * rwords;
+        uint32_t v = 0;
+        if (j < ywords) {
+            const uint32_t *yr = Ys + bl * y_stride;
+            for (uint32_t e = Cs[j], e1 = Cs[j + 1]; e < e1; ++e) v ^= yr[Cs[ywords + 1 + e]];
+        }
+        Rs[idx] = v;
+    }
+    __syncthreads();
+    const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
+    for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
+        const uint32_t G = w * 32, end = min(G + 32, gbits);
+        uint32_t b = G / m, i = G - b * m, pos = G, word = 0;
+        while (pos < end) {
+            const uint32_t len = min(m - i, end - pos);  // 1..32 bits of block b
+            const uint32_t *row = Rs + b * rwords;
+            const uint32_t q = i >> 5, s = i & 31;
+            const uint32_t bits = s ? ((row[q] << s) | (row[q + 1] >> (32 - s))) : row[q];
+            word |= (bits >> (32 - len)) << (32 - len - (pos - G));
+            pos += len;
+            ++b;
+            i = 0;
+        }
+        emit_word(out, b0 * m / 32 + w, word, true);
+    }
+}
+
 // ---- host entry points -----------------------------------------------------
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s) {
     const Tables *t = nullptr;
@@ -643,19 +725,13 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uin
     if (st != QRNG_OK) return st;
     pl.tab = t;
     const HostTables &H = t->host;
-    uint32_t *root = nullptr;
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.seeds, (size_t)H.seed_total * 4, s));
-    QRNG_CUDA_TRY(cudaMallocAsync(&root, (size_t)H.root_words * 4, s));
-    count_launch();
-    root_words_kernel<<<(H.root_words + 255) / 256, 256, 0, s>>>(d_seed, n + m - 1, root, H.root_words);
-    QRNG_CUDA_TRY(cudaGetLastError());
     uint32_t maxw = 0;
     for (const auto &g : t->hleaves) maxw = std::max(maxw, g.seed_n);
     count_launch();
-    leaf_seed_kernel<<<dim3((maxw + 127) / 128, (unsigned)t->hleaves.size()), 128, 0, s>>>(t->leaves, t->terms, root,
-                                                                                           pl.seeds);
+    leaf_seed_kernel<<<dim3((maxw + 127) / 128, (unsigned)t->hleaves.size()), 128, 0, s>>>(t->leaves, t->terms, d_seed,
+                                                                                           n + m - 1, pl.seeds);
     QRNG_CUDA_TRY(cudaGetLastError());
-    cudaFreeAsync(root, s);
     return QRNG_OK;
 }
 
@@ -679,12 +755,12 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     if (H.x_stride) QRNG_CUDA_TRY(cudaMallocAsync(&xws, (size_t)n_blocks * H.x_stride * 4, s));
     QRNG_CUDA_TRY(cudaMallocAsync(&yws, (size_t)n_blocks * H.y_stride * 4, s));
     qrng_status st = QRNG_OK;
-    if (!H.qbufs.empty()) {  // Q buffers, generation by generation, 4 blocks per CTA
+    if (!H.qbufs.empty()) {  // Q buffers, generation by generation, bpc blocks per CTA
+        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / 296));
         count_launch();
-        qbuf_kernel<<<(unsigned)((n_blocks + 3) / 4), 256, 0, s>>>(t->qbufs, (uint32_t)H.qbufs.size(),
-                                                                  reinterpret_cast<const uint4 *>(d_raw), n_blocks,
-                                                                  (uint32_t)n, reinterpret_cast<uint4 *>(xws),
-                                                                  H.x_stride, 4u);
+        qbuf_kernel<4><<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, 0, s>>>(
+            t->qbufs, t->qgen_dev, (uint32_t)t->qgen.size() - 1, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
+            (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc);
         if (cudaGetLastError() != cudaSuccess) { set_error("qbuf_kernel launch failed"); st = QRNG_E_CUDA; }
     }
     if (st == QRNG_OK)
@@ -692,8 +768,17 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
                                    n, xws, H.x_stride, yws, H.y_stride, s);
     const uint32_t rw4 = (uint32_t)(((m + 31) / 32 + 3) / 4 + 1);
     const size_t fused_smem = (size_t)32 * (H.z_stride + 4 * rw4) * 4;
+    const uint32_t ywords = (uint32_t)((m + 31) / 32), csr_words = (uint32_t)(H.comb_ptr.size() + H.comb_idx.size());
+    const size_t csr_smem = ((size_t)32 * (H.y_stride + ywords + 1) + csr_words) * 4;
     uint32_t *zws = nullptr;
-    if (st == QRNG_OK && fused_smem <= 200 * 1024) {
+    if (st == QRNG_OK && csr_smem <= 200 * 1024) {
+        // flattened tree over 32 blocks of leaf parities in shared memory
+        if (csr_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_pack_kernel));
+        count_launch();
+        csr_pack_kernel<<<(unsigned)((n_blocks + 31) / 32), 512, csr_smem, s>>>(t->csr, csr_words, yws, H.y_stride,
+                                                                                 n_blocks, (uint32_t)m, out);
+        if (cudaGetLastError() != cudaSuccess) { set_error("csr_pack_kernel launch failed"); st = QRNG_E_CUDA; }
+    } else if (st == QRNG_OK && fused_smem <= 200 * 1024) {
         // whole tree of 32 blocks in shared memory
         if (fused_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(tree_pack_kernel));
         count_launch();
