@@ -873,12 +873,60 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
+// Second stream of the calling thread (per device): consecutive multi-pass
+// batches alternate between the caller's stream and this one, so one batch's
+// passes fill the SMs the other batch's barrier tails leave idle.
+struct SideStream {
+    int dev = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static thread_local SideStream g_side;
+
+static qrng_status side_stream(cudaStream_t *s2, cudaEvent_t *fork, cudaEvent_t *join) {
+    int dev = 0;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    if (g_side.dev != dev) {
+        if (g_side.s) {
+            cudaStreamDestroy(g_side.s);
+            cudaEventDestroy(g_side.fork);
+            cudaEventDestroy(g_side.join);
+        }
+        g_side = SideStream{};
+        QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
+        QRNG_CUDA_TRY(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
+        QRNG_CUDA_TRY(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
+        g_side.dev = dev;
+    }
+    *s2 = g_side.s;
+    *fork = g_side.fork;
+    *join = g_side.join;
+    return QRNG_OK;
+}
+
 static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                                      uint64_t m, const OutStream &out, cudaStream_t s) {
     const int logP = pl.logP;
-    const uint64_t bb = batch_blocks(logP, n_blocks);
-    uint32_t *ws = nullptr;
-    QRNG_CUDA_TRY(cudaMallocAsync(&ws, (bb << logP) * 4, s));
+    // two batches in flight (one per stream), each half the L2-sized budget
+    uint64_t bb = (1ull << 23) >> logP;  // 2^23-word (32 MiB) workspace per batch
+    if (bb < 1) bb = 1;
+    if (bb > n_blocks) bb = n_blocks;
+    const bool two = n_blocks > bb;
+    cudaStream_t s2 = s;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (two) {
+        qrng_status st2 = side_stream(&s2, &fork, &join);
+        if (st2 != QRNG_OK) return st2;
+    }
+    uint32_t *wsb[2] = {nullptr, nullptr};
+    QRNG_CUDA_TRY(cudaMallocAsync(&wsb[0], (bb << logP) * 4, s));
+    if (two) {
+        QRNG_CUDA_TRY(cudaMallocAsync(&wsb[1], (bb << logP) * 4, s));
+        QRNG_CUDA_TRY(cudaEventRecord(fork, s));
+        QRNG_CUDA_TRY(cudaStreamWaitEvent(s2, fork, 0));
+    }
+    uint32_t *ws = wsb[0];
+    const cudaStream_t s_main = s;
     int r[2];
     const int np = global_radices(logP, r);
     PassArgs pa{};
@@ -898,8 +946,11 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
     fa.itw = pl.itw;
     fa.tw_shift = (uint32_t)(logP - kSegLog);
     qrng_status st = QRNG_OK;
-    for (uint64_t b0 = 0; b0 < n_blocks && st == QRNG_OK; b0 += bb) {
+    for (uint64_t b0 = 0, it = 0; b0 < n_blocks && st == QRNG_OK; b0 += bb, ++it) {
         const uint64_t nb = (n_blocks - b0) < bb ? (n_blocks - b0) : bb;
+        const cudaStream_t s = (it & 1) ? s2 : s_main;
+        ws = wsb[it & 1];
+        pa.ws = ws;
         pa.b0 = b0;
         pa.S = 0;
         st = launch_pass<PASS_FWD_BITS>(r[0], pa, nb, s, true);
@@ -918,7 +969,12 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
                              : launch_pass<PASS_INV_EMIT>(r[0], pa, nb, s, true);
         }
     }
-    cudaFreeAsync(ws, s);
+    if (two) {  // join the side stream back before the workspaces are released
+        cudaEventRecord(join, s2);
+        cudaStreamWaitEvent(s_main, join, 0);
+        cudaFreeAsync(wsb[1], s_main);
+    }
+    cudaFreeAsync(wsb[0], s_main);
     return st;
 }
 
