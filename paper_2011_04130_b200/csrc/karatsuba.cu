@@ -36,6 +36,9 @@
 namespace qrng {
 namespace kara {
 
+#ifndef QRNG_KARA_EXP
+#define QRNG_KARA_EXP 0  // timing experiments only (results wrong when != 0)
+#endif
 constexpr uint32_t kMinLeafW = 128;   // narrowest leaf the planner creates (one K stage)
 constexpr int kMaxLeaves = 1024;
 constexpr int kMaxDepth = 10;
@@ -335,7 +338,8 @@ struct Tables {
     uint32_t *inner = nullptr;     // device: internal-node table (8 words per node)
     uint4 *levels = nullptr;       // device: level table
     uint32_t *unit_node = nullptr; // device: unit -> node per level
-    uint32_t *csr = nullptr;       // device: root word -> Y-row words (row pointers, then offsets)
+    uint32_t *csr = nullptr;       // device: root word -> Y-row words (counts, then column-major entries)
+    uint32_t csr_words = 0;
     std::vector<gemm::Leaf> hleaves;
 };
 
@@ -404,11 +408,22 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
         e = cudaMemcpy(t->inner, H.inner.data(), H.inner.size() * 32, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&t->levels, H.levels.size() * 16 + 16);
     if (e == cudaSuccess) e = cudaMalloc(&t->unit_node, H.unit_node.size() * 4 + 4);
-    if (e == cudaSuccess) e = cudaMalloc(&t->csr, (H.comb_ptr.size() + H.comb_idx.size()) * 4);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(t->csr, H.comb_ptr.data(), H.comb_ptr.size() * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(t->csr + H.comb_ptr.size(), H.comb_idx.data(), H.comb_idx.size() * 4, cudaMemcpyHostToDevice);
+    // the flattened tree for the combine kernel, column-major so that threads
+    // taking consecutive key words read consecutive shared-memory words:
+    // [count per word (ywords)] [entry k of word j at ywords + k*ywords + j]
+    {
+        const uint32_t yw = (uint32_t)H.comb_ptr.size() - 1;
+        uint32_t kmax = 0;
+        for (uint32_t j = 0; j < yw; ++j) kmax = std::max(kmax, H.comb_ptr[j + 1] - H.comb_ptr[j]);
+        std::vector<uint32_t> cm(yw + (size_t)kmax * yw, 0);
+        for (uint32_t j = 0; j < yw; ++j) {
+            cm[j] = H.comb_ptr[j + 1] - H.comb_ptr[j];
+            for (uint32_t q = 0; q < cm[j]; ++q) cm[yw + (size_t)q * yw + j] = H.comb_idx[H.comb_ptr[j] + q];
+        }
+        t->csr_words = (uint32_t)cm.size();
+        if (e == cudaSuccess) e = cudaMalloc(&t->csr, cm.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(t->csr, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess && !H.unit_node.empty())
         e = cudaMemcpy(t->unit_node, H.unit_node.data(), H.unit_node.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !H.levels.empty())
@@ -424,11 +439,23 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
     return QRNG_OK;
 }
 
+// Planner decision, cached on the host per (n, m, depth) (plan creation sits
+// inside the one-shot call; re-planning would stall the launch sequence).
 bool choose(uint64_t n, uint64_t m, int max_depth) {
     if (max_depth == 0) return false;
+    static std::mutex mu;
+    static std::map<std::tuple<uint64_t, uint64_t, int>, bool> cache;
+    const auto key = std::make_tuple(n, m, max_depth);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     HostTables T;
-    if (!plan_host(n, m, max_depth, T)) return false;
-    return T.depth > 0;
+    const bool use = plan_host(n, m, max_depth, T) && T.depth > 0;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = use;
+    return use;
 }
 
 // ---- kernels ---------------------------------------------------------------
@@ -661,20 +688,22 @@ __global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, c
     }
 }
 
-// Combine + pack for 32 blocks whose leaf parities fit in shared memory: the
-// 32 Y rows (contiguous in the workspace) are copied in with coalesced 16-byte
-// loads, each root word is the XOR of its leaf words (the flattened tree: the
-// CSR of qrng_debug_karatsuba_plan, also staged in shared memory), then the key
-// words [c*m, (c+1)*m) of the group are written (one writer each).
+// Combine + pack for bpc blocks whose leaf parities fit in shared memory
+// (bpc m % 32 == 0, so the group's key is whole output words): the bpc Y rows
+// (contiguous in the workspace) are copied in with coalesced 16-byte loads,
+// each root word is the XOR of its leaf words (the flattened tree: the CSR of
+// qrng_debug_karatsuba_plan, also staged in shared memory), then the key words
+// [c bpc m/32, (c+1) bpc m/32) of the group are written (one writer each).
 __global__ void __launch_bounds__(512) csr_pack_kernel(const uint32_t *csr, uint32_t csr_words, const uint32_t *yws,
-                                                       uint32_t y_stride, uint64_t n_blocks, uint32_t m, OutStream out) {
+                                                       uint32_t y_stride, uint64_t n_blocks, uint32_t m, uint32_t bpc,
+                                                       OutStream out) {
     extern __shared__ uint4 sm4[];
-    const uint64_t b0 = (uint64_t)blockIdx.x * 32;
-    const uint32_t nb = (uint32_t)min((uint64_t)32, n_blocks - b0);
+    const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
+    const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
     const uint32_t ywords = (m + 31) / 32, rwords = ywords + 1;
     uint32_t *Ys = reinterpret_cast<uint32_t *>(sm4);
-    uint32_t *Rs = Ys + 32 * y_stride;
-    uint32_t *Cs = Rs + 32 * rwords;
+    uint32_t *Rs = Ys + bpc * y_stride;
+    uint32_t *Cs = Rs + bpc * rwords;
     const uint4 *src = reinterpret_cast<const uint4 *>(yws + b0 * y_stride);
     {  // coalesced copy with 8 independent 16-byte loads in flight per thread
         const uint32_t n4 = nb * (y_stride / 4);
@@ -695,12 +724,20 @@ __global__ void __launch_bounds__(512) csr_pack_kernel(const uint32_t *csr, uint
         uint32_t v = 0;
         if (j < ywords) {
             const uint32_t *yr = Ys + bl * y_stride;
-            for (uint32_t e = Cs[j], e1 = Cs[j + 1]; e < e1; ++e) v ^= yr[Cs[ywords + 1 + e]];
+#if QRNG_KARA_EXP == 1  // timing experiment: no combine
+            v = yr[j];
+#else
+            for (uint32_t e = 0, c = Cs[j]; e < c; ++e) v ^= yr[Cs[ywords + e * ywords + j]];
+#endif
         }
         Rs[idx] = v;
     }
     __syncthreads();
     const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
+#if QRNG_KARA_EXP == 2  // timing experiment: no packing
+    for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) emit_word(out, b0 * m / 32 + w, Rs[w], true);
+    return;
+#endif
     for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
         const uint32_t G = w * 32, end = min(G + 32, gbits);
         uint32_t b = G / m, i = G - b * m, pos = G, word = 0;
@@ -768,15 +805,21 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
                                    n, xws, H.x_stride, yws, H.y_stride, s);
     const uint32_t rw4 = (uint32_t)(((m + 31) / 32 + 3) / 4 + 1);
     const size_t fused_smem = (size_t)32 * (H.z_stride + 4 * rw4) * 4;
-    const uint32_t ywords = (uint32_t)((m + 31) / 32), csr_words = (uint32_t)(H.comb_ptr.size() + H.comb_idx.size());
-    const size_t csr_smem = ((size_t)32 * (H.y_stride + ywords + 1) + csr_words) * 4;
+    const uint32_t ywords = (uint32_t)((m + 31) / 32), csr_words = t->csr_words;
+    // blocks per CTA: the smallest count whose keys are whole 32-bit words
+    // (32 / gcd(m, 32)), doubled while the staged rows stay small
+    uint32_t bpc = 32;
+    while (bpc > 1 && (bpc / 2) * m % 32 == 0) bpc /= 2;
+    auto csr_bytes = [&](uint32_t b) { return ((size_t)b * (H.y_stride + ywords + 1) + csr_words) * 4; };
+    while (bpc < 8 && csr_bytes(2 * bpc) <= 72 * 1024) bpc *= 2;
+    const size_t csr_smem = csr_bytes(bpc);
     uint32_t *zws = nullptr;
     if (st == QRNG_OK && csr_smem <= 200 * 1024) {
-        // flattened tree over 32 blocks of leaf parities in shared memory
+        // flattened tree over bpc blocks of leaf parities in shared memory
         if (csr_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_pack_kernel));
         count_launch();
-        csr_pack_kernel<<<(unsigned)((n_blocks + 31) / 32), 512, csr_smem, s>>>(t->csr, csr_words, yws, H.y_stride,
-                                                                                 n_blocks, (uint32_t)m, out);
+        csr_pack_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, csr_smem, s>>>(t->csr, csr_words, yws, H.y_stride,
+                                                                                       n_blocks, (uint32_t)m, bpc, out);
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && fused_smem <= 200 * 1024) {
         // whole tree of 32 blocks in shared memory
