@@ -250,32 +250,56 @@ def run_ours(args):
     bits_all = float(w.raw_bits) * world * args.steps
     value = bits_all / (ms_max * 1e-3) / 1e9
 
-    # ---- end to end through the host-buffer C-ABI call (pinned buffers) ----
+    # ---- end to end from pinned HOST buffers through the public API ----
+    # Streaming ingest (qrng_stream_*, the continuous-stream use of the paper):
+    # every step copies its batch host->device, extracts it with the plan and
+    # copies the key back; three steps in flight on their own streams.  Timed
+    # on the host clock with full synchronisation on both sides (the work runs
+    # on the library's internal streams), max over ranks.  Also reported: the
+    # one-shot synchronous call (plan creation + chunked pipeline per step).
     e2e = None
     if not args.no_e2e and not modified:
         h_raw = torch.from_numpy(raw_np).pin_memory()
         h_seed = seed.cpu().pin_memory()
-        h_out = torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8).pin_memory()
-        hr, hs, ho = h_raw.numpy(), h_seed.numpy(), h_out.numpy()
+        depth = 3
+        h_outs = [torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8).pin_memory() for _ in range(depth)]
+        hr, hs = h_raw.numpy(), h_seed.numpy()
+        hos = [h.numpy() for h in h_outs]
+        with q.Plan(w.n, w.m, seed) as splan, q.Stream(splan, B, depth=depth) as qs:
+            for i in range(depth + 1):
+                qs.submit(hr, B, hos[i % depth])
+            qs.synchronize()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                qs.submit(hr, B, hos[i % depth])
+            qs.synchronize()
+            t_stream = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        # one-shot synchronous host-buffer call (plan + chunked H2D/extract/D2H per step)
         for _ in range(2):
-            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, ho, stream=stream)
-        if world > 1:
-            dist.barrier()
+            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, hos[0], stream=stream)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
         for a, b in ev:
             flush.zero_()
             a.record(stream)
-            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, ho, stream=stream)
+            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, hos[0], stream=stream)
             b.record(stream)
         torch.cuda.synchronize()
-        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device="cuda")
+        e_t = torch.tensor([t_stream * 1e3, sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device="cuda")
         if world > 1:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": bits_all / (float(e_ms.item()) * 1e-3) / 1e9, "unit": "Gbit/s",
-               "h2d_bytes_per_step": int(h_raw.numel() + h_seed.numel()),
-               "d2h_bytes_per_step": int(h_out.numel()),
-               "api": "qrng_toeplitz_extract_host (pinned host buffers)"}
+            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": bits_all / (float(e_t[0].item()) * 1e-3) / 1e9, "unit": "Gbit/s",
+               "h2d_bytes_per_step": int(h_raw.numel()), "d2h_bytes_per_step": int(h_outs[0].numel()),
+               "api": f"qrng_stream_submit (pinned host buffers, plan reused, {depth} batches in flight; "
+                      "host clock, synchronised)",
+               "oneshot_value": bits_all / (float(e_t[1].item()) * 1e-3) / 1e9,
+               "oneshot_api": "qrng_toeplitz_extract_host per step (plan incl. seed prep, chunked pipeline; "
+                              "CUDA events)",
+               "oneshot_h2d_bytes_per_step": int(h_raw.numel() + h_seed.numel())}
 
     # ---- roofline of the dominant kernel ----
     pk, pk_kind = peaks()

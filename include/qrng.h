@@ -130,6 +130,37 @@ QRNG_API qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint6
                                        uint64_t m, const uint8_t *h_seed, uint8_t *h_out,
                                        cudaStream_t stream);
 
+/* Streaming ingest (the paper's continuous 10 Gbit
+ * stream): batches of raw bits arriving in HOST memory are
+ * extracted with a reused plan in a three-stage pipeline (host->device copy,
+ * extraction, device->host copy, each on its own CUDA stream) with `depth`
+ * device buffer pairs, so the copy of one batch, the extraction of the
+ * previous one and the key copy of the one before overlap.
+ *   qrng_stream_create: plan (not owned; must outlive the stream), max_blocks
+ *     per batch (device buffers are sized for it), depth >= 2 (<= 8), flags:
+ *     QRNG_STREAM_HIST also accumulates the 256-bin histogram of every
+ *     submitted batch's bytes (the ADC samples, C2) for on-line min-entropy
+ *     monitoring (qrng_stream_counts -> qrng_entropy_from_counts).
+ *   qrng_stream_submit: enqueue one batch (h_raw_bits: n_blocks * n bits,
+ *     h_out: ceil(n_blocks * m / 8) bytes; pinned host memory for overlap);
+ *     returns once enqueued; blocks only while all `depth` slots are busy.
+ *     Both host buffers must stay valid until the batch completes
+ *     (qrng_stream_synchronize, or `depth` further submits).
+ *   qrng_stream_synchronize: wait for every submitted batch; returns the first
+ *     error of any batch since the last call.
+ *   qrng_stream_counts: synchronise and copy the accumulated counts (256 x u64).
+ * Errors: E_INVALID for NULL arguments, n_blocks == 0 or > max_blocks, depth
+ * outside [2, 8]; E_NOMEM / E_CUDA on device failures. */
+typedef struct qrng_stream qrng_stream;
+#define QRNG_STREAM_HIST 1u
+QRNG_API qrng_status qrng_stream_create(const qrng_plan *plan, uint64_t max_blocks, uint32_t depth, uint32_t flags,
+                                        qrng_stream **out);
+QRNG_API qrng_status qrng_stream_submit(qrng_stream *stream, const uint8_t *h_raw_bits, uint64_t n_blocks,
+                                        uint8_t *h_out);
+QRNG_API qrng_status qrng_stream_synchronize(qrng_stream *stream);
+QRNG_API qrng_status qrng_stream_counts(qrng_stream *stream, uint64_t *h_counts256);
+QRNG_API void        qrng_stream_destroy(qrng_stream *stream);
+
 /* Plans: seed preparation (a3) once per (seed, n, m), reused over many batches.
  * qrng_plan_create reads d_seed on `stream` (the seed may be freed once that
  * stream has passed the call).  qrng_plan_extract has the layouts of

@@ -35,7 +35,8 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
            "qrng_debug_butterfly_rate", "qrng_debug_set_karatsuba", "qrng_plan_info",
-           "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace"]
+           "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
+           "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy"]
 
 
 class QrngError(RuntimeError):
@@ -115,6 +116,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
         "qrng_debug_set_karatsuba": ([i32], None),
         "qrng_debug_gemm_trace": ([vp, i32], i32),
+        "qrng_stream_create": ([vp, u64, u32, u32, ctypes.POINTER(vp)], i32),
+        "qrng_stream_submit": ([vp, vp, u64, vp], i32),
+        "qrng_stream_synchronize": ([vp], i32),
+        "qrng_stream_counts": ([vp, vp], i32),
+        "qrng_stream_destroy": ([vp], None),
         "qrng_plan_info": ([vp, vp], i32),
         "qrng_debug_karatsuba_plan": ([u64, u64, i32, vp, u32, vp, u32, vp, u32, vp], i32),
     }
@@ -320,6 +326,55 @@ class Plan:
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             load_library().qrng_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+STREAM_HIST = 1
+
+
+class Stream:
+    """Streaming ingest (qrng_stream_*): host batches extracted with a reused
+    plan, `depth` batches in flight (H2D / extraction / D2H overlap).  Host
+    buffers (numpy uint8, pinned for overlap) must stay alive until the batch
+    completes (synchronize(), or `depth` further submits)."""
+
+    def __init__(self, plan: "Plan", max_blocks: int, depth: int = 3, hist: bool = False):
+        h = ctypes.c_void_p()
+        _check(load_library().qrng_stream_create(plan._h, max_blocks, depth, STREAM_HIST if hist else 0,
+                                                 ctypes.byref(h)))
+        self._h, self.plan = h, plan
+
+    def submit(self, raw: np.ndarray, n_blocks: int, out: np.ndarray):
+        for a in (raw, out):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.uint8 and a.flags.c_contiguous):
+                raise TypeError("host buffers must be contiguous uint8 numpy arrays")
+        if raw.size * 8 < n_blocks * self.plan.n or out.size < out_bytes(n_blocks, self.plan.m):
+            raise ValueError("buffer too small")
+        _check(load_library().qrng_stream_submit(self._h, raw.ctypes.data, n_blocks, out.ctypes.data))
+
+    def synchronize(self):
+        _check(load_library().qrng_stream_synchronize(self._h))
+
+    def counts(self) -> np.ndarray:
+        c = np.zeros(256, np.uint64)
+        _check(load_library().qrng_stream_counts(self._h, c.ctypes.data))
+        return c
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().qrng_stream_destroy(self._h)
             self._h = ctypes.c_void_p()
 
     def __del__(self):

@@ -2,6 +2,7 @@
 // plans and the block scheduler that picks the extraction path, and the
 // host-side finalisation of the min-entropy chain.
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -398,7 +399,12 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     // boundary, so chunks are independent self-contained extractions.  Chunk kernels
     // alternate between two compute streams so a chunk's CTAs fill the SMs the
     // previous chunk's tail leaves idle.
-    const uint64_t G = (n_blocks + 31) / 32, K = G < 8 ? G : 8;
+    static const uint64_t kChunks = [] {  // QRNG_HOST_CHUNKS: pipeline depth override (experiments)
+        const char *e = getenv("QRNG_HOST_CHUNKS");
+        const long v = e ? atol(e) : 0;
+        return (uint64_t)(v > 0 ? v : 8);
+    }();
+    const uint64_t G = (n_blocks + 31) / 32, K = G < kChunks ? G : kChunks;
     std::vector<cudaEvent_t> ev(3 * K + 1, nullptr);
     for (auto &e : ev)
         if (st == QRNG_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
@@ -455,6 +461,141 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     }
     return st;
 }
+
+// ---- streaming ingest (NEXT-3) ------------------------------------------------
+// Three-stage pipeline: host->device copies on s_in, extraction on s_comp (one
+// batch at a time gets the whole GPU), device->host copies on s_out; `depth`
+// device buffer pairs rotate, a slot being reused once its key copy is done.
+struct qrng_stream {
+    const qrng_plan *plan = nullptr;
+    uint64_t max_blocks = 0;
+    uint32_t depth = 0, flags = 0, next = 0;
+    int dev = 0;
+    cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+    struct Slot {
+        cudaEvent_t in_done = nullptr, comp_done = nullptr, out_done = nullptr;
+        uint8_t *d_raw = nullptr, *d_out = nullptr;
+        bool busy = false;
+    } slot[8];
+    uint64_t *d_counts = nullptr;
+    qrng_status err = QRNG_OK;
+    char errmsg[256] = "";
+};
+
+static void stream_release(qrng_stream *st) {
+    if (!st) return;
+    for (cudaStream_t s : {st->s_in, st->s_comp, st->s_out})
+        if (s) cudaStreamSynchronize(s);
+    for (auto &sl : st->slot) {
+        if (sl.d_raw) cudaFree(sl.d_raw);
+        if (sl.d_out) cudaFree(sl.d_out);
+        for (cudaEvent_t e : {sl.in_done, sl.comp_done, sl.out_done})
+            if (e) cudaEventDestroy(e);
+    }
+    for (cudaStream_t s : {st->s_in, st->s_comp, st->s_out})
+        if (s) cudaStreamDestroy(s);
+    if (st->d_counts) cudaFree(st->d_counts);
+    delete st;
+}
+
+qrng_status qrng_stream_create(const qrng_plan *plan, uint64_t max_blocks, uint32_t depth, uint32_t flags,
+                               qrng_stream **out) {
+    if (!plan || !out) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    *out = nullptr;
+    if (max_blocks == 0 || depth < 2 || depth > 8) { set_error("need max_blocks > 0 and depth in [2, 8]"); return QRNG_E_INVALID; }
+    if (max_blocks > UINT64_MAX / plan->n) { set_error("max_blocks * n overflows"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    qrng_stream *q = new (std::nothrow) qrng_stream;
+    if (!q) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
+    q->plan = plan;
+    q->max_blocks = max_blocks;
+    q->depth = depth;
+    q->flags = flags;
+    cudaGetDevice(&q->dev);
+    bool ok = cudaStreamCreateWithFlags(&q->s_in, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&q->s_comp, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&q->s_out, cudaStreamNonBlocking) == cudaSuccess;
+    const size_t raw_bytes = max_blocks * plan->n / 8, out_bytes = (max_blocks * plan->m + 7) / 8;
+    for (uint32_t i = 0; i < depth && ok; ++i) {
+        auto &sl = q->slot[i];
+        ok = cudaEventCreateWithFlags(&sl.in_done, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming) == cudaSuccess &&
+             cudaMalloc(&sl.d_raw, raw_bytes) == cudaSuccess && cudaMalloc(&sl.d_out, out_bytes) == cudaSuccess;
+    }
+    if (ok && (flags & QRNG_STREAM_HIST))
+        ok = cudaMalloc(&q->d_counts, 256 * sizeof(uint64_t)) == cudaSuccess &&
+             cudaMemset(q->d_counts, 0, 256 * sizeof(uint64_t)) == cudaSuccess;
+    if (!ok) {
+        set_error("stream allocation failed");
+        stream_release(q);
+        return QRNG_E_NOMEM;
+    }
+    *out = q;
+    return QRNG_OK;
+}
+
+qrng_status qrng_stream_submit(qrng_stream *q, const uint8_t *h_raw_bits, uint64_t n_blocks, uint8_t *h_out) {
+    if (!q || !h_raw_bits || !h_out) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    if (n_blocks == 0 || n_blocks > q->max_blocks) { set_error("n_blocks must be in [1, max_blocks]"); return QRNG_E_INVALID; }
+    QRNG_CUDA_TRY(cudaSetDevice(q->dev));
+    auto &sl = q->slot[q->next];
+    q->next = (q->next + 1) % q->depth;
+    if (sl.busy) QRNG_CUDA_TRY(cudaEventSynchronize(sl.out_done));  // the slot's previous batch is finished
+    const uint64_t n = q->plan->n, m = q->plan->m;
+    const size_t raw_bytes = n_blocks * n / 8, out_bytes = (n_blocks * m + 7) / 8;
+    QRNG_CUDA_TRY(cudaMemcpyAsync(sl.d_raw, h_raw_bits, raw_bytes, cudaMemcpyHostToDevice, q->s_in));
+    QRNG_CUDA_TRY(cudaEventRecord(sl.in_done, q->s_in));
+    QRNG_CUDA_TRY(cudaStreamWaitEvent(q->s_comp, sl.in_done, 0));
+    qrng_status st = QRNG_OK;
+    if (q->d_counts)
+        st = hist256_launch(sl.d_raw, raw_bytes, reinterpret_cast<unsigned long long *>(q->d_counts), q->s_comp);
+    if (st == QRNG_OK) st = qrng_plan_extract(q->plan, sl.d_raw, n_blocks, sl.d_out, q->s_comp);
+    if (st == QRNG_OK) {
+        cudaError_t e = cudaEventRecord(sl.comp_done, q->s_comp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(q->s_out, sl.comp_done, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out, sl.d_out, out_bytes, cudaMemcpyDeviceToHost, q->s_out);
+        if (e == cudaSuccess) e = cudaEventRecord(sl.out_done, q->s_out);
+        if (e != cudaSuccess) { set_error("stream copy: %s", cudaGetErrorString(e)); st = QRNG_E_CUDA; }
+    }
+    sl.busy = true;
+    if (st != QRNG_OK && q->err == QRNG_OK) {
+        q->err = st;
+        snprintf(q->errmsg, sizeof q->errmsg, "%s", g_err);
+    }
+    return st;
+}
+
+qrng_status qrng_stream_synchronize(qrng_stream *q) {
+    if (!q) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    for (uint32_t i = 0; i < q->depth; ++i) {
+        auto &sl = q->slot[i];
+        if (sl.busy) {
+            cudaError_t e = cudaEventSynchronize(sl.out_done);
+            sl.busy = false;
+            if (e != cudaSuccess && q->err == QRNG_OK) {
+                q->err = QRNG_E_CUDA;
+                snprintf(q->errmsg, sizeof q->errmsg, "stream batch: %s", cudaGetErrorString(e));
+            }
+        }
+    }
+    const qrng_status st = q->err;
+    if (st != QRNG_OK) set_error("%s", q->errmsg);
+    q->err = QRNG_OK;
+    return st;
+}
+
+qrng_status qrng_stream_counts(qrng_stream *q, uint64_t *h_counts256) {
+    if (!q || !h_counts256) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    if (!q->d_counts) { set_error("stream created without QRNG_STREAM_HIST"); return QRNG_E_INVALID; }
+    const qrng_status st = qrng_stream_synchronize(q);
+    if (st != QRNG_OK) return st;
+    QRNG_CUDA_TRY(cudaMemcpy(h_counts256, q->d_counts, 256 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return QRNG_OK;
+}
+
+void qrng_stream_destroy(qrng_stream *q) { stream_release(q); }
 
 // ---- min-entropy ------------------------
 

@@ -345,3 +345,27 @@ def test_zero_seed_and_zero_raw(q, oracle_mod, path):
     assert not gpu_extract(q, raw, B, n, m, zero_seed, path_id(q, path)).any()
     seed = S.random_bytes(9, (n + m - 1 + 7) // 8, tag=2)
     assert not gpu_extract(q, np.zeros_like(raw), B, n, m, seed, path_id(q, path)).any()
+
+
+@pytest.mark.parametrize("n,m,path", [(1024, 179, "gemm"), (8192, 5734, "gemm"), (2048, 1433, "ntt"),
+                                      (131072, 91750, "ntt")])
+def test_stream_batches_and_histogram(q, oracle_mod, n, m, path):
+    """qrng_stream_*: several host batches of different sizes (ragged, partial
+    final words) with three in flight; every key bit-exact, and the streamed
+    histogram equals the oracle's over all submitted bytes."""
+    seed = S.random_bytes(n + 5, (n + m - 1 + 7) // 8, tag=6)
+    sizes = [37, 64, 5, 40, 1] if n < 65536 else [3, 2, 1, 2]
+    q.set_debug_path(path_id(q, path))
+    try:
+        with q.Plan(n, m, dev(seed)) as plan, q.Stream(plan, max(sizes), depth=3, hist=True) as st:
+            raws = [S.random_bytes(n * 31 + k, B * n // 8) for k, B in enumerate(sizes)]
+            outs = [np.full(q.out_bytes(B, m) + 4, 0xC3, np.uint8) for B in sizes]
+            for r, o, B in zip(raws, outs, sizes):
+                st.submit(r, B, o)
+            st.synchronize()
+            for r, o, B in zip(raws, outs, sizes):
+                assert_same(o[:q.out_bytes(B, m)], oracle_mod.extract(r, B, n, m, seed), m)
+                assert (o[q.out_bytes(B, m):] == 0xC3).all()
+            assert np.array_equal(st.counts(), oracle_mod.hist256(np.concatenate(raws)))
+    finally:
+        q.set_debug_path(q.PATH_AUTO)
