@@ -376,7 +376,9 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0):
     sample of the same workload: consecutive blocks until ~budget_s."""
     import oracle
     oracle.build()
-    cores = oracle.max_threads() if threads == 0 else threads
+    if threads == 0:
+        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else oracle.max_threads()
+    cores = threads
     sample_blocks = min(w.n_blocks, 4096)
     raw, seed = S.workload_inputs(w, 0, sample_blocks)
     blocks_done, t_total, nb, pos = 0, 0.0, max(1, min(cores, sample_blocks)), 0
@@ -409,16 +411,17 @@ def run_reference(args):
     if args.config == 41:
         from oracle import entropy as E
         w = S.config4b(E.report(S.workload_inputs(w)[0], 8, w.n, 0).m)
-    cores = oracle.max_threads()
+    # all host cores (torchrun sets OMP_NUM_THREADS=1 for its workers)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else oracle.max_threads()
     per_step_blocks = max(cores, min(w.n_blocks, int(os.environ.get("QRNG_REF_BLOCKS", "0")) or
                                      _ref_blocks(w, cores)))
     raw, seed = S.workload_inputs(w, 0, per_step_blocks)
     for _ in range(args.warmup):
-        oracle.extract(raw[:cores * w.n // 8], cores, w.n, w.m, seed)
+        oracle.extract(raw[:cores * w.n // 8], cores, w.n, w.m, seed, "words", cores)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.extract(raw, per_step_blocks, w.n, w.m, seed)
+        oracle.extract(raw, per_step_blocks, w.n, w.m, seed, "words", cores)
         ts.append(time.perf_counter() - t0)
     total = sum(ts)
     value = per_step_blocks * w.n * args.steps / total / 1e9
