@@ -32,6 +32,34 @@ static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+struct SideStream {
+    int dev = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static thread_local SideStream g_side;
+
+qrng_status side_stream(cudaStream_t *s2, cudaEvent_t *fork, cudaEvent_t *join) {
+    int dev = 0;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    if (g_side.dev != dev) {
+        if (g_side.s) {
+            cudaStreamDestroy(g_side.s);
+            cudaEventDestroy(g_side.fork);
+            cudaEventDestroy(g_side.join);
+        }
+        g_side = SideStream{};
+        QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
+        QRNG_CUDA_TRY(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
+        QRNG_CUDA_TRY(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
+        g_side.dev = dev;
+    }
+    *s2 = g_side.s;
+    *fork = g_side.fork;
+    *join = g_side.join;
+    return QRNG_OK;
+}
+
 qrng_status allow_max_smem(const void *func) {
     static std::mutex mu;
     static std::set<std::pair<const void *, int>> done;

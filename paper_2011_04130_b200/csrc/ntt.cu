@@ -873,37 +873,6 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
-// Second stream of the calling thread (per device): consecutive multi-pass
-// batches alternate between the caller's stream and this one, so one batch's
-// passes fill the SMs the other batch's barrier tails leave idle.
-struct SideStream {
-    int dev = -1;
-    cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-static thread_local SideStream g_side;
-
-static qrng_status side_stream(cudaStream_t *s2, cudaEvent_t *fork, cudaEvent_t *join) {
-    int dev = 0;
-    QRNG_CUDA_TRY(cudaGetDevice(&dev));
-    if (g_side.dev != dev) {
-        if (g_side.s) {
-            cudaStreamDestroy(g_side.s);
-            cudaEventDestroy(g_side.fork);
-            cudaEventDestroy(g_side.join);
-        }
-        g_side = SideStream{};
-        QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
-        QRNG_CUDA_TRY(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
-        QRNG_CUDA_TRY(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
-        g_side.dev = dev;
-    }
-    *s2 = g_side.s;
-    *fork = g_side.fork;
-    *join = g_side.join;
-    return QRNG_OK;
-}
-
 static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                                      uint64_t m, const OutStream &out, cudaStream_t s) {
     const int logP = pl.logP;

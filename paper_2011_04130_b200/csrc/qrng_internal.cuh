@@ -24,6 +24,12 @@ void set_error(const char *fmt, ...);
 // device (once per kernel per device; a process may drive several GPUs).
 qrng_status allow_max_smem(const void *func);
 
+// Second stream of the calling thread (per device) plus a fork and a join
+// event: multi-pass NTT batches and Karatsuba block chunks alternate between
+// the caller's stream and this one so one batch's kernels fill the SMs another
+// batch leaves idle.
+qrng_status side_stream(cudaStream_t *s2, cudaEvent_t *fork, cudaEvent_t *join);
+
 // Launch accounting / optional per-kernel event timing (qrng_debug_*).
 void count_launch();
 struct KernelTimer {  // brackets one extraction kernel on its stream (counts every launch)
