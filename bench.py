@@ -241,7 +241,7 @@ def run_ours(args):
         dist.barrier()
     ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_total = sum(ms_steps)
-    kern_ms, kern_n = q.kernel_time_ms()
+    kern_ms, kern_n, aux_ms, aux_n = q.kernel_time_split()
     q.kernel_timing(False)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -343,6 +343,16 @@ def run_ours(args):
         roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total / args.steps)
         hbm_bytes = B * w.n / 8 + B * w.m / 8
         roof["hbm_gbs_algorithmic"] = hbm_bytes / per_step_s / 1e9
+        if aux_n:
+            # Karatsuba auxiliary stages (HBM/L2-bound): Q buffers (each reads its
+            # two halves and writes itself: 3 x the X workspace) and combine +
+            # pack (leaf parities in, packed key out)
+            aux_s = aux_ms / args.steps * 1e-3
+            aux_bytes = B * (3 * 4.0 * pinfo["x_words"] + 4.0 * pinfo["y_words"] + w.m / 8)
+            roof["aux"] = {"kernels": "qbuf_kernel + csr_pack_kernel", "ms_per_step": aux_ms / args.steps,
+                           "launches_per_step": aux_n / args.steps, "bytes_per_step": aux_bytes,
+                           "achieved_gbs": aux_bytes / aux_s / 1e9,
+                           "frac_of_hbm": aux_bytes / aux_s / 1e9 / pk["hbm_gbs"]}
 
     line = {
         "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,

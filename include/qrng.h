@@ -199,11 +199,14 @@ QRNG_API int         qrng_plan_path(const qrng_plan *plan);
  *                        leaves (n*m for the dense product)
  *   log2_transform       NTT path: log2 of the cyclic length P
  *   blocks_per_transform NTT path: 2 when two blocks share one transform
+ *   x_words, y_words     Karatsuba: 32-bit workspace words per block of the
+ *                        combined inputs (Q buffers) and of the leaf parities
  * Errors: E_INVALID for NULL arguments. */
 typedef struct {
     int32_t path, karatsuba_depth, leaves, log2_transform;
     int32_t blocks_per_transform, reserved;
     uint64_t macs_per_block;
+    uint32_t x_words, y_words;
 } qrng_plan_info_t;
 QRNG_API qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info);
 
@@ -268,6 +271,9 @@ QRNG_API void        qrng_debug_kernel_timing(int enable);
  * the library was built with -DQRNG_GEMM_TRACE.  reset != 0 clears them. */
 QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);
+/* As qrng_debug_kernel_time_ms, also returning the auxiliary launches timed on
+ * channel 1 (Karatsuba Q buffers and combine/pack kernels) in *aux_ms. */
+QRNG_API double      qrng_debug_kernel_time_split(double *aux_ms, uint64_t *launches, uint64_t *aux_launches);
 
 #ifdef __cplusplus
 }

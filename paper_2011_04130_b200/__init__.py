@@ -36,7 +36,7 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
            "qrng_debug_butterfly_rate", "qrng_debug_set_karatsuba", "qrng_plan_info",
            "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
-           "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy"]
+           "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split"]
 
 
 class QrngError(RuntimeError):
@@ -52,7 +52,8 @@ class _Gauss(ctypes.Structure):
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("karatsuba_depth", ctypes.c_int32), ("leaves", ctypes.c_int32),
                 ("log2_transform", ctypes.c_int32), ("blocks_per_transform", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("macs_per_block", ctypes.c_uint64)]
+                ("reserved", ctypes.c_int32), ("macs_per_block", ctypes.c_uint64),
+                ("x_words", ctypes.c_uint32), ("y_words", ctypes.c_uint32)]
 
 
 class _Report(ctypes.Structure):
@@ -117,6 +118,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_set_karatsuba": ([i32], None),
         "qrng_debug_gemm_trace": ([vp, i32], i32),
         "qrng_stream_create": ([vp, u64, u32, u32, ctypes.POINTER(vp)], i32),
+        "qrng_debug_kernel_time_split": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64), ctypes.POINTER(u64)],
+                                         ctypes.c_double),
         "qrng_stream_submit": ([vp, vp, u64, vp], i32),
         "qrng_stream_synchronize": ([vp], i32),
         "qrng_stream_counts": ([vp, vp], i32),
@@ -227,6 +230,13 @@ def kernel_time_ms() -> tuple[float, int]:
     n = ctypes.c_uint64()
     ms = load_library().qrng_debug_kernel_time_ms(ctypes.byref(n))
     return float(ms), int(n.value)
+
+
+def kernel_time_split() -> tuple[float, int, float, int]:
+    """(main ms, main launches, auxiliary ms, auxiliary launches) since the last read."""
+    aux, n, na = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
+    ms = load_library().qrng_debug_kernel_time_split(ctypes.byref(aux), ctypes.byref(n), ctypes.byref(na))
+    return float(ms), int(n.value), float(aux.value), int(na.value)
 
 
 def butterfly_rate(iters: int = 2000, stream=None) -> float:

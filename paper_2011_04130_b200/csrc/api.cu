@@ -28,7 +28,11 @@ void set_error(const char *fmt, ...) {
 static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int> g_timing{0};
 static std::mutex g_tmu;
-static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+struct TimedLaunch {
+    cudaEvent_t a, b;
+    int channel;
+};
+static std::vector<TimedLaunch> g_events;
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -72,7 +76,7 @@ qrng_status allow_max_smem(const void *func) {
     return QRNG_OK;
 }
 
-KernelTimer::KernelTimer(cudaStream_t st, bool timed) : s(st) {
+KernelTimer::KernelTimer(cudaStream_t st, bool timed, int ch) : s(st), channel(ch) {
     count_launch();
     if (!timed || !g_timing.load()) return;
     if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
@@ -82,7 +86,7 @@ void KernelTimer::stop() {
     if (!a) return;
     cudaEventRecord(b, s);
     std::lock_guard<std::mutex> lk(g_tmu);
-    g_events.emplace_back(a, b);
+    g_events.push_back(TimedLaunch{a, b, channel});
 }
 
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
@@ -193,20 +197,25 @@ qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset) {
     return gemm::trace(h_counters16, reset);
 }
 void qrng_debug_kernel_timing(int enable) { g_timing.store(enable ? 1 : 0); }
-double qrng_debug_kernel_time_ms(uint64_t *launches) {
+double qrng_debug_kernel_time_split(double *aux_ms, uint64_t *launches, uint64_t *aux_launches) {
     std::lock_guard<std::mutex> lk(g_tmu);
-    double total = 0;
+    double tot[2] = {0, 0};
+    uint64_t cnt[2] = {0, 0};
     for (auto &e : g_events) {
         float ms = 0;
-        if (cudaEventSynchronize(e.second) == cudaSuccess && cudaEventElapsedTime(&ms, e.first, e.second) == cudaSuccess)
-            total += ms;
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
+        if (cudaEventSynchronize(e.b) == cudaSuccess && cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess)
+            tot[e.channel ? 1 : 0] += ms;
+        ++cnt[e.channel ? 1 : 0];
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
     }
-    if (launches) *launches = g_events.size();
     g_events.clear();
-    return total;
+    if (aux_ms) *aux_ms = tot[1];
+    if (launches) *launches = cnt[0];
+    if (aux_launches) *aux_launches = cnt[1];
+    return tot[0];
 }
+double qrng_debug_kernel_time_ms(uint64_t *launches) { return qrng_debug_kernel_time_split(nullptr, launches, nullptr); }
 
 int qrng_plan_path(const qrng_plan *plan) { return plan ? plan->path : -1; }
 
@@ -222,7 +231,7 @@ qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info) {
     } else if (plan->kara_on) {
         int d = 0, l = 0;
         uint64_t macs = 0;
-        kara::describe(plan->kara, &d, &l, &macs);
+        kara::describe(plan->kara, &d, &l, &macs, &info->x_words, &info->y_words);
         info->karatsuba_depth = d;
         info->leaves = l;
         info->macs_per_block = macs;

@@ -811,11 +811,13 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     return st;
 }
 
-void describe(const Plan &pl, int *depth, int *n_leaves, uint64_t *macs_per_block) {
-    if (!pl.tab) { *depth = 0; *n_leaves = 0; *macs_per_block = 0; return; }
+void describe(const Plan &pl, int *depth, int *n_leaves, uint64_t *macs_per_block, uint32_t *x_words, uint32_t *y_words) {
+    if (!pl.tab) { *depth = 0; *n_leaves = 0; *macs_per_block = 0; *x_words = *y_words = 0; return; }
     *depth = pl.tab->host.depth;
     *n_leaves = (int)pl.tab->host.leaves.size();
     *macs_per_block = pl.tab->host.macs;
+    *x_words = pl.tab->host.x_stride;
+    *y_words = pl.tab->host.y_stride;
 }
 
 static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
@@ -828,10 +830,11 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
     qrng_status st = QRNG_OK;
     if (!H.qbufs.empty()) {  // Q buffers, generation by generation, bpc blocks per CTA
         const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / 296));
-        count_launch();
+        KernelTimer tq(s, true, 1);
         qbuf_kernel<4><<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, 0, s>>>(
             t->qbufs, t->qgen_dev, (uint32_t)t->qgen.size() - 1, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
             (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc);
+        tq.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("qbuf_kernel launch failed"); st = QRNG_E_CUDA; }
     }
     if (st == QRNG_OK)
@@ -851,9 +854,10 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
     if (st == QRNG_OK && csr_smem <= 200 * 1024) {
         // flattened tree over bpc blocks of leaf parities in shared memory
         if (csr_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_pack_kernel));
-        count_launch();
+        KernelTimer tc(s, true, 1);
         csr_pack_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, csr_smem, s>>>(t->csr, csr_words, yws, H.y_stride,
                                                                                        n_blocks, (uint32_t)m, bpc, out);
+        tc.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && fused_smem <= 200 * 1024) {
         // whole tree of 32 blocks in shared memory

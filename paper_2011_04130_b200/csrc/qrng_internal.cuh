@@ -32,10 +32,11 @@ qrng_status side_stream(cudaStream_t *s2, cudaEvent_t *fork, cudaEvent_t *join);
 
 // Launch accounting / optional per-kernel event timing (qrng_debug_*).
 void count_launch();
-struct KernelTimer {  // brackets one extraction kernel on its stream (counts every launch)
+struct KernelTimer {  // brackets one kernel on its stream (counts every launch)
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s;
-    KernelTimer(cudaStream_t st, bool timed);
+    int channel;             // 0: main extraction kernel(s); 1: auxiliary (Karatsuba Q buffers, combine/pack)
+    KernelTimer(cudaStream_t st, bool timed, int channel = 0);
     void stop();
 };
 
@@ -157,7 +158,7 @@ void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s);
 // host-side description for bench/tests: depth, number of leaves, leaf MACs per block
-void describe(const Plan &pl, int *depth, int *n_leaves, uint64_t *macs_per_block);
+void describe(const Plan &pl, int *depth, int *n_leaves, uint64_t *macs_per_block, uint32_t *x_words, uint32_t *y_words);
 }  // namespace kara
 
 // Histogram (hist.cu).
