@@ -270,6 +270,11 @@ QRNG_API void        qrng_debug_kernel_timing(int enable);
  * (waits per warp role, see gemm_tc.cu "cycle tracing"); E_UNSUPPORTED unless
  * the library was built with -DQRNG_GEMM_TRACE.  reset != 0 clears them. */
 QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset);
+/* PROFILING ONLY: back-to-back int8 MMAs on fixed operands, one CTA per SM
+ * (form 0: cta_group::1 A in TMEM; 1: cta_group::1 A in SMEM; 2: cta_group::2
+ * pair, A in SMEM, needs a -DQRNG_GEMM_2CTA build), N = n; *macs = work done.
+ * Time with CUDA events on `stream`. */
+QRNG_API qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);
 /* As qrng_debug_kernel_time_ms, also returning the auxiliary launches timed on
  * channel 1 (Karatsuba Q buffers and combine/pack kernels) in *aux_ms. */

@@ -36,7 +36,8 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
            "qrng_debug_butterfly_rate", "qrng_debug_set_karatsuba", "qrng_plan_info",
            "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
-           "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split"]
+           "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split",
+           "qrng_debug_mma_rate"]
 
 
 class QrngError(RuntimeError):
@@ -117,6 +118,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
         "qrng_debug_set_karatsuba": ([i32], None),
         "qrng_debug_gemm_trace": ([vp, i32], i32),
+        "qrng_debug_mma_rate": ([i32, i32, i32, ctypes.POINTER(u64), vp], i32),
         "qrng_stream_create": ([vp, u64, u32, u32, ctypes.POINTER(vp)], i32),
         "qrng_debug_kernel_time_split": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64), ctypes.POINTER(u64)],
                                          ctypes.c_double),
@@ -237,6 +239,20 @@ def kernel_time_split() -> tuple[float, int, float, int]:
     aux, n, na = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
     ms = load_library().qrng_debug_kernel_time_split(ctypes.byref(aux), ctypes.byref(n), ctypes.byref(na))
     return float(ms), int(n.value), float(aux.value), int(na.value)
+
+
+def mma_rate(form: int, n: int, iters: int = 20000, stream=None) -> float:
+    """PROFILING ONLY: int8 MAC/s of back-to-back MMAs of one form (see qrng.h)."""
+    import torch
+    macs = ctypes.c_uint64()
+    s = torch.cuda.current_stream() if stream is None else stream
+    _check(load_library().qrng_debug_mma_rate(form, 100, n, ctypes.byref(macs), s.cuda_stream))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    _check(load_library().qrng_debug_mma_rate(form, iters, n, ctypes.byref(macs), s.cuda_stream))
+    b.record(s)
+    b.synchronize()
+    return macs.value / (a.elapsed_time(b) * 1e-3)
 
 
 def butterfly_rate(iters: int = 2000, stream=None) -> float:

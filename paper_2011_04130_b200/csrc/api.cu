@@ -192,6 +192,12 @@ qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_
     if (st != QRNG_OK) return st;
     return gemm::probe(d_A, d_h, d_D, N, K, stream);
 }
+qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream) {
+    if (!macs || iters <= 0 || n < 16 || n > 256 || n % 16) { set_error("bad arguments"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    return gemm::mma_rate(form, iters, n, macs, stream);
+}
 qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset) {
     if (!h_counters16) { set_error("NULL buffer"); return QRNG_E_INVALID; }
     return gemm::trace(h_counters16, reset);

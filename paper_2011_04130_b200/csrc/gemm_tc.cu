@@ -28,6 +28,7 @@
 //  * Epilogue warps tcgen05.ld the accumulators, take parity, pack 32 outputs
 //    per word MSB-first and store them at bit b*m + i (C4).
 //  * Persistent grid (one CTA per SM), warp-specialised, mbarrier pipelines.
+#include <algorithm>
 #include "qrng_internal.cuh"
 
 namespace qrng {
@@ -63,7 +64,9 @@ constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
 static_assert(A_STAGES % XF_PAR == 0, "each transform warp owns fixed ring slots");
 constexpr int PF = 4;          // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
+#if !QRNG_GEMM_2CTA
 static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile");
+#endif
 
 // ---- PTX helpers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -97,6 +100,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
                  : "memory");
+}
+// true in exactly one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -336,48 +345,54 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     TRACE_T0(t_role);
 
     if (warp == W_MMA) {
-        if (lane == 0) {
+        // the whole warp runs the issue loop converged (operands stay warp-uniform);
+        // one elected lane issues each tcgen05.mma / commit
+        {
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
                 const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
                 // N tiles before the last use N = BN; the last one only the rows it needs
                 const uint32_t idesc_full = idesc_i8(BM, BN), idesc_last = idesc_i8(BM, (int)ti.nlast);
                 const uint32_t ab = it % ACC_BUFS, acc0 = ACC_COL0 + ab * NT * BN;
-                { TRACE_T0(tw); mbar_wait(&acc_empty[ab], ((it / ACC_BUFS) & 1) ^ 1); TRACE_ADD(2, tw); }
+                { TRACE_T0(tw); mbar_wait(&acc_empty[ab], ((it / ACC_BUFS) & 1) ^ 1); if (lane == 0) TRACE_ADD(2, tw); }
                 tc_fence_after();
                 for (uint32_t ks = 0; ks < ti.kst; ++ks) {
                     const uint32_t kin = ks % SPC;
                     if (kin == 0) {
-                        { TRACE_T0(tw); mbar_wait(&b_full[bs], bph); TRACE_ADD(1, tw); }
+                        { TRACE_T0(tw); mbar_wait(&b_full[bs], bph); if (lane == 0) TRACE_ADD(1, tw); }
                         tc_fence_after();
                     }
-                    { TRACE_T0(tw); mbar_wait(&a_full[as], aph); TRACE_ADD(0, tw); }
-                    TRACE_ADDV(11, 1);
+                    { TRACE_T0(tw); mbar_wait(&a_full[as], aph); if (lane == 0) TRACE_ADD(0, tw); }
+                    if (lane == 0) TRACE_ADDV(11, 1);
                     tc_fence_after();
                     const uint32_t a_tmem = tmem + A_COL0 + as * 32;
                     const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                    if (elect_one()) {
 #pragma unroll
-                    for (uint32_t kk = 0; kk < 4; ++kk) {
-                        const uint32_t koff = kin * KS + kk * 32;  // K offset inside the chunk
+                        for (uint32_t kk = 0; kk < 4; ++kk) {
+                            const uint32_t koff = kin * KS + kk * 32;  // K offset inside the chunk
 #pragma unroll
-                        for (uint32_t nt = 0; nt < NT; ++nt) {  // N tile nt starts 24*nt core matrices later
-                            if (nt < ti.ntc) {
-                                const uint64_t bdesc = desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 256, 128);
+                            for (uint32_t nt = 0; nt < NT; ++nt) {  // N tile nt starts 24*nt core matrices later
+                                if (nt < ti.ntc) {
+                                    const uint64_t bdesc = desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 256, 128);
 #if QRNG_GEMM_EXP != 1  // experiment 1: no MMAs (transform / B-gen / epilogue throughput alone)
-                                mma_i8_ts(tmem + acc0 + nt * BN, a_tmem + kk * 8, bdesc,
-                                          nt + 1 == ti.ntc ? idesc_last : idesc_full, (ks | kk) != 0);
+                                    mma_i8_ts(tmem + acc0 + nt * BN, a_tmem + kk * 8, bdesc,
+                                              nt + 1 == ti.ntc ? idesc_last : idesc_full, (ks | kk) != 0);
 #endif
+                                }
                             }
                         }
+                        mma_commit(&a_empty[as]);
+                        if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
                     }
-                    mma_commit(&a_empty[as]);
+                    __syncwarp();
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
                     if (kin == SPC - 1 || ks == ti.kst - 1) {
-                        mma_commit(&b_empty[bs]);
                         if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
                     }
                 }
-                mma_commit(&acc_full[ab]);
+                if (elect_one()) mma_commit(&acc_full[ab]);
+                __syncwarp();
             }
         }
         __syncwarp();
@@ -569,6 +584,514 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 }
 
 
+
+// ---- 2-SM variant (build with -DQRNG_GEMM_2CTA=1) ---------------------------------
+// A CTA pair (cluster of 2, one per SM of a TPC) runs tcgen05.mma.cta_group::2
+// M256 N256 K32: each CTA holds 128 blocks of the A operand (expanded in its
+// own shared memory, K-major canonical layout) and 128 of the 256 output rows
+// of the Toeplitz B operand (generated on chip as in the 1-SM kernel); each
+// CTA's TMEM receives its 128 blocks x all 256 rows.  With A out of TMEM the
+// 512 TMEM columns hold two 256-column accumulator sets, so the MMAs of tile
+// k+1 run while the epilogue drains tile k.  The leader CTA (rank 0) issues
+// the MMAs; the full barriers live in the leader and count both CTAs'
+// producers (remote arrives), the empty barriers are signalled in both CTAs
+// by a multicast commit.
+#if QRNG_GEMM_2CTA
+namespace two {
+constexpr int BM2 = 256, BH = 128;          // blocks per tile, per CTA
+constexpr int BN2 = 256;                    // output rows per tile (N of one MMA)
+constexpr int A2_STAGES = 4;                // A ring in shared memory (16 KB each)
+constexpr int A2_BYTES = BH * KS;           // 128 rows x 128 K-bytes
+constexpr int CM2 = KC / 8 + (BN2 / 2) / 8 - 1;  // core matrices per B chunk per CTA
+constexpr int CHUNK2_BYTES = CM2 * 128;
+constexpr int W2_MMA = 0, W2_BGEN0 = 1, N2_BGEN = 3, W2_XF0 = 4, N2_XF = 8, W2_EPI0 = 12, N2_EPI = 8;
+constexpr int NTHREADS2 = 20 * 32;
+constexpr int XF2_PAR = 2;                  // transform warps per 32-row quarter, alternating stages
+static_assert(kTileRows == BN2, "leaf tables assume 256 rows per work tile");
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_rank(uint64_t *b, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void mma2_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive once on `bar` (same offset) in both CTAs when the issued MMAs complete
+__device__ __forceinline__ void mma2_commit_both(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+struct Tile2 {
+    uint32_t mt, n0, kst, nchunks, r, ntile;  // ntile: rows of this tile (N, multiple of 16)
+    const uint32_t *seed, *xb;
+    uint32_t xs, out_off;
+};
+
+template <bool GROUPED>
+__device__ __forceinline__ Tile2 tile2_info(const Args &a, const uint32_t *seed_s, uint32_t t, uint32_t &cur) {
+    Tile2 ti;
+    uint32_t tl;
+    if (!GROUPED) {
+        ti.kst = a.kst;
+        ti.r = a.m;
+        ti.seed = seed_s;
+        ti.xb = a.raw;
+        ti.xs = a.n >> 5;
+        ti.out_off = 0;
+        tl = t;
+    } else {
+        while (cur + 1 < a.n_leaves && t >= (__ldg(&a.leaves[cur].npair_base) + __ldg(&a.leaves[cur].npairs)) * a.n_mtiles)
+            ++cur;
+        const Leaf &L = a.leaves[cur];
+        tl = t - __ldg(&L.npair_base) * a.n_mtiles;
+        ti.kst = __ldg(&L.w) / KS;
+        ti.r = __ldg(&L.r);
+        ti.seed = a.seed_words + __ldg(&L.seed_off);
+        if (__ldg(&L.x_src) == 0) { ti.xb = a.raw + __ldg(&L.x_off); ti.xs = a.n >> 5; }
+        else { ti.xb = a.xws + __ldg(&L.x_off); ti.xs = a.x_stride; }
+        ti.out_off = __ldg(&L.out_off);
+    }
+    ti.mt = tl % a.n_mtiles;
+    ti.n0 = (tl / a.n_mtiles) * BN2;
+    ti.nchunks = (ti.kst + SPC - 1) / SPC;
+    const uint32_t left = ti.r > ti.n0 ? min((uint32_t)BN2, ti.r - ti.n0) : 16u;
+    ti.ntile = (left + 15) & ~15u;
+    return ti;
+}
+
+template <bool GROUPED>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toeplitz_gemm2_kernel(Args a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *abuf = smem;                                   // A2_STAGES x 16 KB
+    uint8_t *chunks = smem + A2_STAGES * A2_BYTES;          // B_SLOTS x CHUNK2_BYTES
+    uint32_t *seed_s = reinterpret_cast<uint32_t *>(chunks + B_SLOTS * CHUNK2_BYTES);
+    const uint32_t seed_stage = GROUPED ? 0u : a.seed_words_n;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
+    uint64_t *a_full = bars, *a_empty = bars + A2_STAGES, *b_full = bars + 2 * A2_STAGES;
+    uint64_t *b_empty = b_full + B_SLOTS, *acc_full = b_empty + B_SLOTS, *acc_empty = acc_full + 2;
+    uint64_t *a_local = acc_empty + 2;  // peer CTA: its transform warps' arrivals, relayed to the leader
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_local + A2_STAGES);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank();
+    for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS2) seed_s[i] = a.seed_words[i];
+    if (threadIdx.x == 0) {
+        // leader a_full: its own 4 transform warps of the stage + one relayed arrive from the peer
+        for (int s = 0; s < A2_STAGES; ++s) {
+            mbar_init(&a_full[s], 4 + 1);
+            mbar_init(&a_empty[s], 1);
+            mbar_init(&a_local[s], 4);
+        }
+        for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], 2 * N2_BGEN); mbar_init(&b_empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], 2 * 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == W2_MMA) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t pair = blockIdx.x >> 1, npairs_grid = gridDim.x >> 1;
+    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: N tiles of 256 rows (total over leaves)
+    uint32_t cur = 0;
+
+    if (warp == W2_MMA) {
+        if (rank == 0 && lane == 0) {
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            for (uint32_t t = pair; t < ntiles; t += npairs_grid, ++it) {
+                const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
+                const uint32_t idesc = idesc_i8(BM2, (int)ti.ntile);
+                const uint32_t ab = it & 1, acc = ab * BN2;
+                mbar_wait_cluster(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                    const uint32_t kin = ks % SPC;
+                    if (kin == 0) {
+                        mbar_wait_cluster(&b_full[bs], bph);
+                        tc_fence_after();
+                    }
+                    mbar_wait_cluster(&a_full[as], aph);
+                    tc_fence_after();
+                    const uint32_t abase = smem_u32(abuf + as * A2_BYTES);
+                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK2_BYTES);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < 4; ++kk) {
+                        // A: core matrix (row group g, K chunk q) at g*1024 + q*128: SBO 1024, LBO 128
+                        const uint64_t adesc = desc_kmajor(abase + kk * 2 * 128, 128, 1024);
+                        const uint32_t koff = kin * KS + kk * 32;
+                        const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
+                        mma2_i8_ss(tmem + acc, adesc, bdesc, idesc, (ks | kk) != 0);
+                    }
+                    mma2_commit_both(&a_empty[as]);
+                    if (++as == A2_STAGES) { as = 0; aph ^= 1; }
+                    if (kin == SPC - 1 || ks == ti.kst - 1) {
+                        mma2_commit_both(&b_empty[bs]);
+                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                    }
+                }
+                mma2_commit_both(&acc_full[ab]);
+            }
+        } else if (rank == 1 && lane == 0) {
+            // relay: the peer's transform warps arrive on a_local (CTA scope, no
+            // memory barrier); this thread, which has no loads in flight, forwards
+            // each completed stage to the leader's a_full with one cluster-release arrive
+            uint32_t g = 0;
+            for (uint32_t t = pair; t < ntiles; t += npairs_grid) {
+                const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
+                for (uint32_t ks = 0; ks < ti.kst; ++ks, ++g) {
+                    mbar_wait(&a_local[g % A2_STAGES], (g / A2_STAGES) & 1);
+                    mbar_arrive_rank(&a_full[g % A2_STAGES], 0);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp >= W2_BGEN0 && warp < W2_BGEN0 + N2_BGEN) {
+        // this CTA's half of the B tile: rows n0 + rank*ntile/2 .. + ntile/2
+        const int tb = (warp - W2_BGEN0) * 32 + lane;
+        uint32_t bs = 0, bph = 0;
+        for (uint32_t t = pair; t < ntiles; t += npairs_grid) {
+            const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
+            const uint32_t half = ti.ntile / 2;
+            const int ncm = KC / 8 + (int)(half / 8) - 1;
+            for (uint32_t c = 0; c < ti.nchunks; ++c) {
+                const uint32_t base = ti.n0 + rank * half + c * KC;
+                mbar_wait(&b_empty[bs], bph ^ 1);
+                uint8_t *cb = chunks + bs * CHUNK2_BYTES;
+                for (int r = tb; r < ncm * 8; r += N2_BGEN * 32) {
+                    const uint32_t p = base + 8 * (r >> 3) + (r & 7);
+                    uint32_t w0, w1;
+                    if (GROUPED) { w0 = __ldg(ti.seed + (p >> 5)); w1 = __ldg(ti.seed + (p >> 5) + 1); }
+                    else { w0 = ti.seed[p >> 5]; w1 = ti.seed[(p >> 5) + 1]; }
+                    const uint32_t v = __funnelshift_l(w1, w0, p & 31);
+                    uint4 o;
+                    o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
+                    o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
+                    o.z = prmt_sign<0xFEBA>(v << 3, v << 2);
+                    o.w = prmt_sign<0xFEBA>(v << 1, v);
+                    *reinterpret_cast<uint4 *>(cb + (r >> 3) * 128 + (r & 7) * 16) = o;
+                }
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_rank(&b_full[bs], 0);
+                if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+            }
+        }
+    } else if (warp >= W2_XF0 && warp < W2_XF0 + N2_XF) {
+        // A transform into shared memory: row = block (this CTA's 128 of the
+        // tile's 256), 128 K per stage, chunk G (16 K-bytes) of row r goes to
+        // core matrix (r/8, G): offset (r/8)*1024 + G*128 + (r%8)*16.
+        const uint32_t xw = (uint32_t)(warp - W2_XF0), par = xw / 4;
+        const uint32_t row = (xw & 3) * 32 + lane;
+        uint32_t lcur = 0, lt = pair, lks = 0;
+        Tile2 lti{};
+        if (lt < ntiles) lti = tile2_info<GROUPED>(a, seed_s, lt, lcur);
+        auto step1 = [&]() {
+            if (lt >= ntiles) return;
+            if (++lks == lti.kst) {
+                lks = 0;
+                lt += npairs_grid;
+                if (lt < ntiles) lti = tile2_info<GROUPED>(a, seed_s, lt, lcur);
+            }
+        };
+        auto load = [&](bool &v) -> uint4 {
+            const uint64_t b = (uint64_t)lti.mt * BM2 + rank * BH + row;
+            v = lt < ntiles && b < a.n_blocks;
+            const uint64_t bc = b < a.n_blocks ? b : a.n_blocks - 1;
+            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (lti.kst - 1 - lks));
+        };
+        for (uint32_t i = 0; i < par; ++i) step1();
+        uint4 pf[PF];
+        bool ok[PF], vd[PF];
+#pragma unroll
+        for (int j = 0; j < PF; ++j) {
+            ok[j] = lt < ntiles;
+            pf[j] = load(vd[j]);
+#pragma unroll
+            for (int i = 0; i < XF2_PAR; ++i) step1();
+        }
+        uint32_t g = par;
+        bool more = true;
+        while (more) {
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                if (more && !ok[j]) more = false;
+                if (more) {
+                    const uint4 cur4 = vd[j] ? pf[j] : make_uint4(0, 0, 0, 0);
+                    const uint32_t as = g % A2_STAGES, aph = (g / A2_STAGES) & 1;
+                    mbar_wait(&a_empty[as], aph ^ 1);
+                    // expand the 16 raw bytes (same K order as the 1-SM kernel's TMEM stage)
+                    const uint32_t M[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
+                    uint8_t *dst = abuf + as * A2_BYTES + (row >> 3) * 1024 + (row & 7) * 16;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t S[8];
+#pragma unroll
+                        for (int b2 = 0; b2 < 8; ++b2) S[b2] = M[q] << b2;
+                        const int G0 = 2 * (3 - q);
+                        uint4 lo, hi;
+                        lo.x = prmt_sign<0xFEBA>(S[0], S[1]);
+                        lo.y = prmt_sign<0xFEBA>(S[2], S[3]);
+                        lo.z = prmt_sign<0xFEBA>(S[4], S[5]);
+                        lo.w = prmt_sign<0xFEBA>(S[6], S[7]);
+                        hi.x = prmt_sign<0xDC98>(S[0], S[1]);
+                        hi.y = prmt_sign<0xDC98>(S[2], S[3]);
+                        hi.z = prmt_sign<0xDC98>(S[4], S[5]);
+                        hi.w = prmt_sign<0xDC98>(S[6], S[7]);
+                        *reinterpret_cast<uint4 *>(dst + G0 * 128) = lo;
+                        *reinterpret_cast<uint4 *>(dst + (G0 + 1) * 128) = hi;
+                    }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(rank == 0 ? &a_full[as] : &a_local[as]);
+                    // refill this ring slot after the arrive
+                    ok[j] = lt < ntiles;
+                    pf[j] = load(vd[j]);
+#pragma unroll
+                    for (int i = 0; i < XF2_PAR; ++i) step1();
+                    g += XF2_PAR;
+                }
+            }
+        }
+    } else {
+        // Epilogue: group ab = (w - W2_EPI0) / 4 drains accumulator set ab (tiles
+        // k = ab mod 2 of this pair); warp % 4 = TMEM lane quadrant.
+        const uint32_t ab = (uint32_t)(warp - W2_EPI0) >> 2;
+        const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
+        const uint32_t lane_addr = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ab * BN2;
+        uint32_t it = 0;
+        for (uint32_t t = pair + ab * npairs_grid; t < ntiles; t += 2 * npairs_grid, ++it) {
+            const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
+            mbar_wait(&acc_full[ab], it & 1);
+            tc_fence_after();
+            uint32_t words[BN2 / 32];
+#pragma unroll
+            for (int c = 0; c < BN2 / 32; ++c) {
+                uint32_t w = 0;
+                if ((uint32_t)(32 * c) < ti.ntile) {
+                    uint32_t v[32];
+                    tmem_ld32(lane_addr + 32 * c, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) w = (w << 1) | (v[k] & 1u);
+                }
+                words[c] = w;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_rank(&acc_empty[ab], 0);
+            const uint64_t b = (uint64_t)ti.mt * BM2 + rank * BH + row;
+            const uint32_t n0 = ti.n0;
+            if (b >= a.n_blocks || n0 >= ti.r) continue;
+            const uint32_t nvalid = min((uint32_t)BN2, ti.r - n0);
+#pragma unroll
+            for (int c = 0; c < BN2 / 32; ++c) {
+                const int vb = (int)nvalid - 32 * c;
+                if (vb <= 0) words[c] = 0;
+                else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
+            }
+            if (GROUPED) {
+                uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
+#pragma unroll
+                for (int c = 0; c < BN2 / 32; ++c)
+                    if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
+                continue;
+            }
+            const uint64_t G_lo = b * a.m + n0, G_hi = G_lo + nvalid;
+            const uint32_t off = (uint32_t)(G_lo & 31);
+            const uint64_t W0 = G_lo >> 5;
+            uint32_t prev = 0;
+#pragma unroll
+            for (int c = 0; c <= BN2 / 32; ++c) {
+                const uint32_t cw = (c < BN2 / 32) ? words[c] : 0u;
+                const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
+                prev = cw;
+                const uint64_t W = W0 + c;
+                if (W * 32 >= G_hi) break;
+                const bool excl = (W * 32 >= G_lo) && (W * 32 + 32 <= G_hi);
+                emit_word(a.out, W, ow, excl);
+            }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();  // the leader's last MMAs (which read this CTA's smem) are complete
+    if (warp == W2_MMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
+}
+
+static size_t smem_bytes2(uint32_t seed_words_n) {
+    return (size_t)A2_STAGES * A2_BYTES + (size_t)B_SLOTS * CHUNK2_BYTES + ((seed_words_n + 3) & ~3u) * 4 +
+           (3 * A2_STAGES + 2 * B_SLOTS + 4) * 8 + 16;
+}
+
+template <bool GROUPED>
+static qrng_status launch2(Args a, cudaStream_t s) {
+    // tiles of 256 blocks x 256 rows; a.n_npairs counts 256-row N tiles
+    a.n_mtiles = (uint32_t)((a.n_blocks + BM2 - 1) / BM2);
+    if ((uint64_t)a.n_mtiles * a.n_npairs > 0xFFFFFFFFull) {
+        set_error("GEMM path: too many tiles");
+        return QRNG_E_UNSUPPORTED;
+    }
+    int dev = 0, sms = 148;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = smem_bytes2(GROUPED ? 0u : a.seed_words_n);
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm2_kernel<GROUPED>));
+        if (st != QRNG_OK) return st;
+    }
+    const uint32_t ntiles = a.n_mtiles * a.n_npairs;
+    const uint32_t pairs = std::min<uint32_t>(ntiles, (uint32_t)sms / 2);
+    KernelTimer tm(s, true);
+    toeplitz_gemm2_kernel<GROUPED><<<2 * pairs, NTHREADS2, smem, s>>>(a);
+    tm.stop();
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+}  // namespace two
+#endif
+
+// ---- MMA-rate microbenchmark (profiling only) ---------------------------------------
+// One elected thread per CTA issues `iters` back-to-back int8 MMAs on fixed
+// operands (no data movement): form 0 = cta_group::1, A in TMEM, M128 N=n;
+// form 1 = cta_group::1, A in SMEM, M128 N=n; form 2 = cta_group::2 (cluster
+// pair), A in SMEM, M256 N=n.  Time it with CUDA events; MACs = CTAs x iters x
+// (M/ctas) x N x 32.
+template <int FORM>
+__global__ void __cluster_dims__(FORM == 2 ? 2 : 1, 1, 1) __launch_bounds__(128, 1)
+    mma_rate_kernel(int iters, int n, uint32_t *sink, int commit_every) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t &bar = *reinterpret_cast<uint64_t *>(smem + 64 * 1024);
+    uint32_t &slot = *reinterpret_cast<uint32_t *>(smem + 64 * 1024 + 16);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 64 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init(&bar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        if (FORM == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            tmem_alloc(&slot, 512);
+        }
+    }
+    tc_fence_before();
+#if QRNG_GEMM_2CTA
+    if (FORM == 2) two::cluster_sync(); else __syncthreads();
+#else
+    __syncthreads();
+#endif
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    uint32_t rank = 0;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    if (threadIdx.x == 0 && rank == 0) {
+        const uint32_t idesc = idesc_i8(FORM == 2 ? 256 : 128, n);
+        const uint64_t bdesc = desc_kmajor(smem_u32(smem), 256, 128);
+        const uint64_t adesc = desc_kmajor(smem_u32(smem + 32768), 128, 1024);
+        for (int it = 0; it < iters; ++it) {
+            if (commit_every > 0 && it % commit_every == commit_every - 1) {
+                if (FORM == 2)
+                    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar + 1)), "h"((uint16_t)3) : "memory");
+                else
+                    mma_commit(&bar + 1);
+            }
+            if (FORM == 0) mma_i8_ts(tmem + 256, tmem, bdesc, idesc, 1);
+            else if (FORM == 1)
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + 256),
+                             "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
+            else
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                             "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + 256),
+                             "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
+        }
+        if (FORM == 2)
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+        else
+            mma_commit(&bar);
+    }
+    if (FORM == 2 || rank == 0) {
+        if (threadIdx.x == 0) mbar_wait(&bar, 0);
+    }
+    tc_fence_before();
+#if QRNG_GEMM_2CTA
+    if (FORM == 2) two::cluster_sync(); else __syncthreads();
+#else
+    __syncthreads();
+#endif
+    if (warp == 0) {
+        tc_fence_after();
+        if (FORM == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+        else tmem_dealloc(tmem, 512);
+    }
+    if (threadIdx.x == 0 && iters < 0) sink[0] = tmem;
+}
+
+qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s) {
+    const int commit_every = form / 16;  // form + 16*k: a commit every k MMAs
+    form %= 16;
+    int dev = 0, sms = 148;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = 64 * 1024 + 64;
+    const unsigned grid = (unsigned)sms;
+    count_launch();
+    switch (form) {
+        case 0: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<0>)); mma_rate_kernel<0><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
+        case 1: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<1>)); mma_rate_kernel<1><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
+#if QRNG_GEMM_2CTA
+        case 2: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<2>)); mma_rate_kernel<2><<<grid & ~1u, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
+#endif
+        default: set_error("mma_rate: unsupported form"); return QRNG_E_UNSUPPORTED;
+    }
+    QRNG_CUDA_TRY(cudaGetLastError());
+    *macs = (uint64_t)(form == 2 ? (grid & ~1u) : grid) * (uint64_t)iters * 128ull * (uint64_t)n * 32ull;
+    return QRNG_OK;
+}
+
 // ---- layout probe (test only): D = A * B^T with B[i][k] = h[i + k] ----------------
 // One CTA, 128 threads.  A: 128 x K int8 row-major (global); h: bytes; D: 128 x N s32.
 __global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, const uint8_t *h, int32_t *D, int N,
@@ -638,7 +1161,10 @@ bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m 
 
 uint32_t seed_words_needed(uint64_t n, uint64_t m) {
     const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = n / KS, nchunks = (kst + SPC - 1) / SPC;
-    const uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
+    uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
+    // 2-SM kernel: 256-row tiles, the second CTA's half starts 128 rows later
+    const uint64_t nt2 = (m + 255) / 256, pmax2 = (nt2 - 1) * 256 + 128 + (nchunks - 1) * KC + 8 * (KC / 8 + 16 - 1) + 7;
+    if (pmax2 > pmax) pmax = pmax2;
     return (uint32_t)(pmax / 32 + 2);
 }
 
@@ -717,7 +1243,12 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.seed_words = pl.seed_words;
     a.seed_words_n = (uint32_t)pl.seed_words_n;
     a.out = out;
+#if QRNG_GEMM_2CTA
+    a.n_npairs = (uint32_t)((m + kTileRows - 1) / kTileRows);
+    return two::launch2<false>(a, s);
+#else
     return launch<false>(a, s);
+#endif
 }
 
 qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t total_npairs,
@@ -737,7 +1268,11 @@ qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t to
     a.x_stride = x_stride;
     a.yws = yws;
     a.y_stride = y_stride;
+#if QRNG_GEMM_2CTA
+    return two::launch2<true>(a, s);
+#else
     return launch<true>(a, s);
+#endif
 }
 
 qrng_status trace(uint64_t *h_out, int reset) {

@@ -126,7 +126,14 @@ struct Leaf {
 #ifndef QRNG_GEMM_ACCBUFS
 #define QRNG_GEMM_ACCBUFS 1
 #endif
+#ifndef QRNG_GEMM_2CTA
+#define QRNG_GEMM_2CTA 0  // 1: the cta_group::2 kernel (256 x 256 tiles, A in smem, double-buffered accumulators)
+#endif
+#if QRNG_GEMM_2CTA
+constexpr int kTileRows = 256;  // output rows per work tile of the 2-SM kernel
+#else
 constexpr int kTileRows = QRNG_GEMM_BN * QRNG_GEMM_NT;  // output rows per work tile (NT * BN)
+#endif
 uint32_t seed_words_needed(uint64_t n, uint64_t m);
 // Grouped launch over the leaf table (Karatsuba): parities of leaf l, block b,
 // row i go to bit 31 - (i & 31) of yws[b * y_stride + out_off + i / 32] (logical words).
@@ -140,7 +147,8 @@ void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
-qrng_status trace(uint64_t *h_out, int reset);  // 16 cycle counters (-DQRNG_GEMM_TRACE builds)
+qrng_status trace(uint64_t *h_out, int reset);
+qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s);  // 16 cycle counters (-DQRNG_GEMM_TRACE builds)
 }  // namespace gemm
 
 // Karatsuba decomposition over the GEMM path (karatsuba.cu).
