@@ -55,7 +55,7 @@ static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (N
 // taking every XF_PAR-th stage, so the per-stage latency chain (wait slot ->
 // expand -> tcgen05.st -> wait::st -> arrive) of one warp is overlapped.
 #ifndef QRNG_GEMM_XFPAR
-#define QRNG_GEMM_XFPAR 2
+#define QRNG_GEMM_XFPAR 1
 #endif
 constexpr int XF_PAR = QRNG_GEMM_XFPAR;
 constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4 * XF_PAR, W_EPI0 = W_XFORM0 + N_XFORM,
@@ -732,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
     uint32_t cur = 0;
 
     if (warp == W2_MMA) {
-        if (rank == 0 && lane == 0) {
+        if (rank == 0) {  // converged warp, one elected lane issues
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
             for (uint32_t t = pair; t < ntiles; t += npairs_grid, ++it) {
                 const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
@@ -750,22 +750,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
                     tc_fence_after();
                     const uint32_t abase = smem_u32(abuf + as * A2_BYTES);
                     const uint32_t cbase = smem_u32(chunks + bs * CHUNK2_BYTES);
+                    if (elect_one()) {
 #pragma unroll
-                    for (uint32_t kk = 0; kk < 4; ++kk) {
-                        // A: core matrix (row group g, K chunk q) at g*1024 + q*128: SBO 1024, LBO 128
-                        const uint64_t adesc = desc_kmajor(abase + kk * 2 * 128, 128, 1024);
-                        const uint32_t koff = kin * KS + kk * 32;
-                        const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
-                        mma2_i8_ss(tmem + acc, adesc, bdesc, idesc, (ks | kk) != 0);
+                        for (uint32_t kk = 0; kk < 4; ++kk) {
+                            // A: core matrix (row group g, K chunk q) at g*1024 + q*128: SBO 1024, LBO 128
+                            const uint64_t adesc = desc_kmajor(abase + kk * 2 * 128, 128, 1024);
+                            const uint32_t koff = kin * KS + kk * 32;
+                            const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
+                            mma2_i8_ss(tmem + acc, adesc, bdesc, idesc, (ks | kk) != 0);
+                        }
+                        mma2_commit_both(&a_empty[as]);
+                        if (kin == SPC - 1 || ks == ti.kst - 1) mma2_commit_both(&b_empty[bs]);
                     }
-                    mma2_commit_both(&a_empty[as]);
+                    __syncwarp();
                     if (++as == A2_STAGES) { as = 0; aph ^= 1; }
                     if (kin == SPC - 1 || ks == ti.kst - 1) {
-                        mma2_commit_both(&b_empty[bs]);
                         if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
                     }
                 }
-                mma2_commit_both(&acc_full[ab]);
+                if (elect_one()) mma2_commit_both(&acc_full[ab]);
+                __syncwarp();
             }
         } else if (rank == 1 && lane == 0) {
             // relay: the peer's transform warps arrive on a_local (CTA scope, no
