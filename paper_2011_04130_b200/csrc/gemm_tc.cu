@@ -161,6 +161,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "r"(taddr)
         : "memory");
 }
+// 64 consecutive S32 columns of this thread's lane, the low 16 bits of columns
+// 2k and 2k+1 packed into register k (bit 0 and bit 16 carry their parities)
+__device__ __forceinline__ void tmem_ld32_pack16(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : QRNG_W8(0), QRNG_W8(8), QRNG_W8(16), QRNG_W8(24)
+        : "r"(taddr)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -199,6 +209,9 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
 // which 8 shifted copies of a raw word expose their bits at byte MSBs, so both
 // operands are built with SHF + PRMT only.
 
+#ifndef QRNG_GEMM_PACK16
+#define QRNG_GEMM_PACK16 1  // epilogue: tcgen05.ld .pack::16b (two S32 columns per register, low halves)
+#endif
 #ifndef QRNG_GEMM_EXP
 #define QRNG_GEMM_EXP 0  // timing experiments only (results wrong when != 0)
 #endif
@@ -519,6 +532,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             tc_fence_after();
             const uint32_t ncols = nt < ti.ntc ? (nt + 1 == ti.ntc ? ti.nlast : (uint32_t)BN) : 0u;
             uint32_t words[BN / 32];
+#if QRNG_GEMM_PACK16
+            // 64 columns per load: only the parity (bit 0) of each S32 sum is
+            // needed and it survives truncation to 16 bits
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) {
+                uint32_t w0 = 0, w1 = 0;
+                if ((uint32_t)(64 * c) < ncols) {
+                    uint32_t v[32];
+                    tmem_ld32_pack16(lane_addr + 64 * c, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) w0 = (w0 << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
+#pragma unroll
+                    for (int k = 16; k < 32; ++k) w1 = (w1 << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
+                }
+                words[2 * c] = w0;
+                words[2 * c + 1] = w1;
+            }
+#else
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t w = 0;
@@ -531,6 +563,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 }
                 words[c] = w;
             }
+#endif
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[ab]);

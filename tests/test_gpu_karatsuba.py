@@ -71,11 +71,13 @@ def test_random(q, oracle_mod, n, m, B, depth):
     assert_same(got, oracle_mod.extract(raw, B, n, m, seed), m)
 
 
-@pytest.mark.parametrize("depth", [1, 3, -1])
-@pytest.mark.parametrize("n,m,B", [(1024, 716, 3), (8192, 5734, 3), (16384, 11468, 2)])
+@pytest.mark.parametrize("depth", [0, 1, 3, -1])
+@pytest.mark.parametrize("n,m,B", [(1024, 716, 3), (8192, 5734, 3), (16384, 11468, 2), (65536, 45875, 2)])
 def test_all_ones(q, oracle_mod, n, m, B, depth):
-    """All-ones seed and raw: every leaf window sum is maximal and every XOR
-    combination of seed windows / block windows is exercised with dense data."""
+    """All-ones seed and raw: every leaf window sum is maximal (n = 2^16 at depth
+    0: the S32 sums reach 65536, whose parity survives the epilogue's 16-bit
+    packed accumulator reads) and every XOR combination of seed windows / block
+    windows is exercised with dense data."""
     raw = np.full(B * n // 8, 0xFF, np.uint8)
     seed = np.full((n + m - 1 + 7) // 8, 0xFF, np.uint8)
     got, _ = kara_extract(q, raw, B, n, m, seed, depth)
