@@ -34,6 +34,10 @@
 namespace qrng {
 namespace gemm {
 
+#ifndef QRNG_GEMM_DEFER
+#define QRNG_GEMM_DEFER 2  // MMAs of N tile 1 of the next tile start this many A stages late (0: off)
+#endif
+
 constexpr int BM = 128;        // blocks per tile (TMEM lanes)
 constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
 constexpr int KS = 128;        // K per A stage
@@ -51,6 +55,14 @@ constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 32 A_STAGES)
 constexpr uint32_t ACC_COL0 = 32 * A_STAGES;  // accumulator sets (buffer x N tile) follow
 static_assert(A_STAGES * 32 + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
 static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (NT = 1) or one per N tile");
+// Deferred second N tile (NT = 2, one accumulator set): the epilogue drains
+// N tile 0 and then N tile 1 (all 8 warps, half the columns each); the next
+// tile's MMAs start on N tile 0 as soon as it is drained and catch up N tile 1
+// after QRNG_GEMM_DEFER A stages, so half of the drain overlaps the MMAs.
+constexpr bool DEFER_ON = QRNG_GEMM_DEFER > 0 && NT == 2 && ACC_BUFS == 1 && BN == 192;
+constexpr int DEFER = QRNG_GEMM_DEFER > 0 ? QRNG_GEMM_DEFER : 1;
+static_assert(!DEFER_ON || (DEFER < A_STAGES && DEFER < KC / KS), "deferred stages stay resident in one chunk");
+constexpr int ACC_EMPTY = DEFER_ON ? 2 : ACC_BUFS;
 // Warp roles.  The A transform uses XF_PAR warps per TMEM lane quadrant, each
 // taking every XF_PAR-th stage, so the per-stage latency chain (wait slot ->
 // expand -> tcgen05.st -> wait::st -> arrive) of one warp is overlapped.
@@ -168,6 +180,14 @@ __device__ __forceinline__ void tmem_ld32_pack16(uint32_t taddr, uint32_t (&v)[3
         "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
         "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
         : QRNG_W8(0), QRNG_W8(8), QRNG_W8(16), QRNG_W8(24)
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16_pack16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];"
+        : QRNG_W8(0), QRNG_W8(8)
         : "r"(taddr)
         : "memory");
 }
@@ -338,14 +358,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
     uint64_t *a_full = bars, *a_empty = bars + A_STAGES, *b_full = bars + 2 * A_STAGES;
     uint64_t *b_empty = b_full + B_SLOTS, *acc_full = b_empty + B_SLOTS, *acc_empty = acc_full + ACC_BUFS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + ACC_BUFS);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + ACC_EMPTY);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM / XF_PAR); mbar_init(&a_empty[s], 1); }
         for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], N_BGEN); mbar_init(&b_empty[s], 1); }
-        for (int s = 0; s < ACC_BUFS; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&acc_empty[s], N_EPI / ACC_BUFS); }
+        for (int s = 0; s < ACC_BUFS; ++s) mbar_init(&acc_full[s], 1);
+        for (int s = 0; s < ACC_EMPTY; ++s) mbar_init(&acc_empty[s], DEFER_ON ? N_EPI : N_EPI / ACC_BUFS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == W_MMA) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -357,7 +378,77 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     uint32_t cur = 0;                                 // leaf cursor of this role
     TRACE_T0(t_role);
 
-    if (warp == W_MMA) {
+    if (DEFER_ON && warp == W_MMA) {
+        // converged warp, elected issue; N tile 1 of each tile is deferred DEFER stages
+        uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+            const uint32_t idesc_full = idesc_i8(BM, BN), idesc_last = idesc_i8(BM, (int)ti.nlast);
+            const uint32_t ph = (it & 1) ^ 1;
+            mbar_wait(&acc_empty[0], ph);
+            const bool defer = ti.ntc == 2 && ti.kst > (uint32_t)DEFER;
+            if (!defer) mbar_wait(&acc_empty[1], ph);
+            tc_fence_after();
+            bool nt1_on = !defer;
+            uint32_t dslot[DEFER];
+            uint32_t cb0 = 0;
+            for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                const uint32_t kin = ks % SPC;
+                if (kin == 0) {
+                    mbar_wait(&b_full[bs], bph);
+                    tc_fence_after();
+                }
+                mbar_wait(&a_full[as], aph);
+                tc_fence_after();
+                const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                if (ks == 0) cb0 = cbase;
+                if (!nt1_on && ks == (uint32_t)DEFER) {
+                    // N tile 1 drained: its MMAs for the held stages, then release them
+                    mbar_wait(&acc_empty[1], ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+#pragma unroll
+                        for (int d = 0; d < DEFER; ++d) {
+#pragma unroll
+                            for (uint32_t kk = 0; kk < 4; ++kk) {
+                                const uint32_t koff = d * KS + kk * 32;
+                                const uint64_t bdesc = desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 256, 128);
+                                mma_i8_ts(tmem + ACC_COL0 + BN, tmem + A_COL0 + dslot[d] * 32 + kk * 8, bdesc,
+                                          idesc_last, (d | kk) != 0);
+                            }
+                            mma_commit(&a_empty[dslot[d]]);
+                        }
+                    }
+                    __syncwarp();
+                    nt1_on = true;
+                }
+                const uint32_t a_tmem = tmem + A_COL0 + as * 32;
+                if (elect_one()) {
+#pragma unroll
+                    for (uint32_t kk = 0; kk < 4; ++kk) {
+                        const uint32_t koff = kin * KS + kk * 32;
+                        const uint64_t bdesc0 = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
+                        mma_i8_ts(tmem + ACC_COL0, a_tmem + kk * 8, bdesc0, ti.ntc == 1 ? idesc_last : idesc_full,
+                                  (ks | kk) != 0);
+                        if (nt1_on && ti.ntc == 2) {
+                            const uint64_t bdesc1 = desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 256, 128);
+                            mma_i8_ts(tmem + ACC_COL0 + BN, a_tmem + kk * 8, bdesc1, idesc_last, (ks | kk) != 0);
+                        }
+                    }
+                    if (nt1_on) mma_commit(&a_empty[as]);
+                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                }
+                __syncwarp();
+                if (!nt1_on) dslot[ks] = as;
+                if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                if (kin == SPC - 1 || ks == ti.kst - 1) {
+                    if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                }
+            }
+            if (elect_one()) mma_commit(&acc_full[0]);
+            __syncwarp();
+        }
+    } else if (warp == W_MMA) {
         // the whole warp runs the issue loop converged (operands stay warp-uniform);
         // one elected lane issues each tcgen05.mma / commit
         {
@@ -513,6 +604,73 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&a_full[as]);
                     g += XF_PAR;
+                }
+            }
+        }
+    } else if (DEFER_ON) {
+        // Epilogue (deferred mode): every warp drains columns [96 h, 96 h + 96) of
+        // N tile 0, releases it, then the same columns of N tile 1 (h = warp
+        // group, lanes = TMEM quadrant).  Parity of the S32 sums, 32 outputs per
+        // MSB-first word; the two halves of a tile row meet in one word, which is
+        // OR-ed (the output is pre-zeroed in the plain mode).
+        const uint32_t h = (uint32_t)(warp - W_EPI0) >> 2;
+        const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
+        const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + 96 * h;
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+            mbar_wait(&acc_full[0], it & 1);
+            tc_fence_after();
+            const uint64_t b = (uint64_t)ti.mt * BM + row;
+#pragma unroll
+            for (uint32_t nt = 0; nt < 2; ++nt) {
+                const uint32_t ncols = nt < ti.ntc ? (nt + 1 == ti.ntc ? ti.nlast : (uint32_t)BN) : 0u;
+                uint32_t words[3] = {0u, 0u, 0u};
+                if (96 * h < ncols) {
+                    uint32_t v[32];
+                    tmem_ld32_pack16(quad + nt * BN, v);
+                    uint32_t u[16];
+                    tmem_ld16_pack16(quad + nt * BN + 64, u);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) words[0] = (words[0] << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
+#pragma unroll
+                    for (int k = 16; k < 32; ++k) words[1] = (words[1] << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) words[2] = (words[2] << 2) | ((u[k] & 1u) << 1) | ((u[k] >> 16) & 1u);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[nt]);
+                const uint32_t n0 = ti.n0 + nt * BN + 96 * h;  // first row of these 3 words
+                if (b >= a.n_blocks || n0 >= ti.r || 96 * h >= ncols) continue;
+                const uint32_t nvalid = min(96u, ti.r - n0);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int vb = (int)nvalid - 32 * c;
+                    if (vb <= 0) words[c] = 0;
+                    else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
+                }
+                if (GROUPED) {
+                    uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
+                    continue;
+                }
+                const uint64_t G_lo = b * a.m + n0, G_hi = G_lo + nvalid;
+                const uint32_t off = (uint32_t)(G_lo & 31);
+                const uint64_t W0 = G_lo >> 5;
+                uint32_t prev = 0;
+#pragma unroll
+                for (int c = 0; c <= 3; ++c) {
+                    const uint32_t cw = (c < 3) ? words[c] : 0u;
+                    const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
+                    prev = cw;
+                    const uint64_t W = W0 + c;
+                    if (W * 32 >= G_hi) break;
+                    const bool excl = (W * 32 >= G_lo) && (W * 32 + 32 <= G_hi);
+                    emit_word(a.out, W, ow, excl);
                 }
             }
         }
@@ -1206,7 +1364,7 @@ uint32_t seed_words_needed(uint64_t n, uint64_t m) {
 }
 
 static size_t smem_bytes(uint32_t seed_words_n) {
-    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + 2 * ACC_BUFS) * 8 + 16;
+    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + ACC_BUFS + ACC_EMPTY) * 8 + 16;
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L

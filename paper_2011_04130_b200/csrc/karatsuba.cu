@@ -36,6 +36,9 @@
 namespace qrng {
 namespace kara {
 
+#ifndef QRNG_CSR_THREADS
+#define QRNG_CSR_THREADS 512  // threads of the combine+pack kernel
+#endif
 #ifndef QRNG_KARA_EXP
 #define QRNG_KARA_EXP 0  // timing experiments only (results wrong when != 0)
 #endif
@@ -694,7 +697,7 @@ __global__ void __launch_bounds__(512) tree_pack_kernel(const uint32_t *inner, c
 // each root word is the XOR of its leaf words (the flattened tree: the CSR of
 // qrng_debug_karatsuba_plan, also staged in shared memory), then the key words
 // [c bpc m/32, (c+1) bpc m/32) of the group are written (one writer each).
-__global__ void __launch_bounds__(512) csr_pack_kernel(const uint32_t *csr, uint32_t csr_words, const uint32_t *yws,
+__global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_pack_kernel(const uint32_t *csr, uint32_t csr_words, const uint32_t *yws,
                                                        uint32_t y_stride, uint64_t n_blocks, uint32_t m, uint32_t bpc,
                                                        OutStream out) {
     extern __shared__ uint4 sm4[];
@@ -855,7 +858,7 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         // flattened tree over bpc blocks of leaf parities in shared memory
         if (csr_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_pack_kernel));
         KernelTimer tc(s, true, 1);
-        csr_pack_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, csr_smem, s>>>(t->csr, csr_words, yws, H.y_stride,
+        csr_pack_kernel<<<(unsigned)((n_blocks + bpc - 1) / bpc), QRNG_CSR_THREADS, csr_smem, s>>>(t->csr, csr_words, yws, H.y_stride,
                                                                                        n_blocks, (uint32_t)m, bpc, out);
         tc.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_pack_kernel launch failed"); st = QRNG_E_CUDA; }
