@@ -45,7 +45,9 @@ namespace kara {
 constexpr uint32_t kMinLeafW = 128;   // narrowest leaf the planner creates (one K stage)
 constexpr int kMaxLeaves = 1024;
 constexpr int kMaxDepth = 10;
-constexpr int kAutoMaxDepth = 5;  // auto mode: deeper trees spill the leaf parities out of L2
+// auto mode: deeper trees spill the leaf parities out of L2 (measured: depth 6
+// loses at n = 2^16, wins at 2^17)
+static int auto_max_depth(uint64_t n) { return n >= (1u << 17) ? 6 : 5; }
 
 // ---- planner (host only; no CUDA calls) ------------------------------------
 // Cost model in units of (output row x K) for one M tile of 128 blocks on the
@@ -215,7 +217,7 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
 static bool plan_host(uint64_t n, uint64_t m, int max_depth, HostTables &T) {
     if (n % 128 || m == 0 || m >= n || n > (1u << 22)) return false;
     // auto: the cost model's best tree with at most kMaxLeaves leaves
-    for (int depth = max_depth >= 0 ? std::min(max_depth, kMaxDepth) : kAutoMaxDepth; depth >= 0; --depth)
+    for (int depth = max_depth >= 0 ? std::min(max_depth, kMaxDepth) : auto_max_depth(n); depth >= 0; --depth)
         if (plan_host_depth(n, m, depth, max_depth >= 0, T)) return true;
     return false;
 }
