@@ -23,6 +23,7 @@
 // is bit 0, parity of c2 is bit k).  Values are kept lazily in [0, 2p); the
 // final residue is made canonical before its parity is taken.
 #include <cstdio>
+#include <cstdlib>
 #include "qrng_internal.cuh"
 
 namespace qrng {
@@ -877,7 +878,12 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
                                      uint64_t m, const OutStream &out, cudaStream_t s) {
     const int logP = pl.logP;
     // two batches in flight (one per stream), each half the L2-sized budget
-    uint64_t bb = (1ull << 23) >> logP;  // 2^23-word (32 MiB) workspace per batch
+    static const int kBatchLog = [] {  // QRNG_NTT_BATCH_LOG: workspace words per batch (experiments)
+        const char *e = getenv("QRNG_NTT_BATCH_LOG");
+        const int v = e ? atoi(e) : 0;
+        return v >= 18 && v <= 27 ? v : 26;
+    }();
+    uint64_t bb = (1ull << kBatchLog) >> logP;  // 2^26-word (256 MiB) workspace per batch by default
     if (bb < 1) bb = 1;
     if (bb > n_blocks) bb = n_blocks;
     const bool two = n_blocks > bb;
