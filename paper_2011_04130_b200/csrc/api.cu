@@ -76,10 +76,29 @@ qrng_status allow_max_smem(const void *func) {
     return QRNG_OK;
 }
 
+// Timing events are recycled (bench mode records two per timed launch; creating
+// them on every launch would put host work inside the timed region).
+static std::vector<cudaEvent_t> g_event_pool;
+static cudaEvent_t pooled_event() {
+    {
+        std::lock_guard<std::mutex> lk(g_tmu);
+        if (!g_event_pool.empty()) {
+            cudaEvent_t e = g_event_pool.back();
+            g_event_pool.pop_back();
+            return e;
+        }
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+}
+
 KernelTimer::KernelTimer(cudaStream_t st, bool timed, int ch) : s(st), channel(ch) {
     count_launch();
     if (!timed || !g_timing.load()) return;
-    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { a = b = nullptr; return; }
+    a = pooled_event();
+    b = pooled_event();
+    if (!a || !b) { a = b = nullptr; return; }
     cudaEventRecord(a, s);
 }
 void KernelTimer::stop() {
@@ -212,8 +231,8 @@ double qrng_debug_kernel_time_split(double *aux_ms, uint64_t *launches, uint64_t
         if (cudaEventSynchronize(e.b) == cudaSuccess && cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess)
             tot[e.channel ? 1 : 0] += ms;
         ++cnt[e.channel ? 1 : 0];
-        cudaEventDestroy(e.a);
-        cudaEventDestroy(e.b);
+        g_event_pool.push_back(e.a);
+        g_event_pool.push_back(e.b);
     }
     g_events.clear();
     if (aux_ms) *aux_ms = tot[1];
