@@ -336,6 +336,12 @@ def run_ours(args):
                     "peak_kind": "measured live: register-resident radix-32 fwd+inv modular butterflies on all SMs "
                                  "(qrng_debug_butterfly_rate, the kernels' own butterfly code)",
                     "peak_derived_issue_bound": alu_peak_gbfly(pk)}
+            # the same butterflies with the inter-pass twiddle chains included
+            # (the passes' whole register-resident instruction mix): the part of
+            # the gap to `peak` the twiddles explain; the rest is shared-memory /
+            # global traffic, barriers and occupancy
+            roof["pass_rate_peak"] = q.butterfly_rate(with_twiddles=True) / 1e9
+            roof["frac_of_pass_rate"] = achieved / roof["pass_rate_peak"]
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
         roof["kernel_ms_per_step"] = kern_ms / args.steps  # summed per-launch device times

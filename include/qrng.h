@@ -263,16 +263,25 @@ QRNG_API uint64_t    qrng_debug_launch_count(void);
  * Time it with CUDA events on `stream` to get the achievable butterfly rate
  * (SURVEY.md 8(d) "R_bfly"). */
 QRNG_API qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t stream);
+/* BENCH ONLY: the same microbenchmark with every radix-32 DFT followed by the
+ * inter-pass twiddle multiplication (Montgomery power chains), i.e. the full
+ * register-resident instruction mix of a non-final NTT pass.  *butterflies
+ * counts the same 160 butterflies per iteration, so the rate is directly
+ * comparable with qrng_debug_butterfly_rate. */
+QRNG_API qrng_status qrng_debug_pass_rate(int iters, uint64_t *butterflies, cudaStream_t stream);
 QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D,
                                            int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);
-/* PROFILING ONLY: 16 clock64 counters summed over all CTAs of the tcgen05 kernel
+/* PROFILING ONLY: 32 clock64 counters summed over all CTAs of the tcgen05 kernel
  * (waits per warp role, see gemm_tc.cu "cycle tracing"); E_UNSUPPORTED unless
  * the library was built with -DQRNG_GEMM_TRACE.  reset != 0 clears them. */
-QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset);
+QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters32, int reset);
 /* PROFILING ONLY: back-to-back int8 MMAs on fixed operands, one CTA per SM
  * (form 0: cta_group::1 A in TMEM; 1: cta_group::1 A in SMEM; 2: cta_group::2
- * pair, A in SMEM, needs a -DQRNG_GEMM_2CTA build), N = n; *macs = work done.
+ * pair, A in SMEM, needs a -DQRNG_GEMM_2CTA build; 3: the GEMM kernel's stage
+ * shape, 4 K steps x two N tiles per elected issue + one commit, N0 = n & 511,
+ * N1 = n >> 9 or N0 if 0), N = n; *macs = work done.  form + 16k (forms 0-2):
+ * a commit every k MMAs.
  * Time with CUDA events on `stream`. */
 QRNG_API qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);

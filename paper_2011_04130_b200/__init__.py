@@ -34,7 +34,7 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_plan_create_modified", "qrng_modified_toeplitz_extract_async",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
-           "qrng_debug_butterfly_rate", "qrng_debug_set_karatsuba", "qrng_plan_info",
+           "qrng_debug_butterfly_rate", "qrng_debug_pass_rate", "qrng_debug_set_karatsuba", "qrng_plan_info",
            "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
            "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split",
            "qrng_debug_mma_rate"]
@@ -114,6 +114,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_launch_count": ([], u64),
         "qrng_debug_umma_probe": ([vp, vp, vp, i32, i32, vp], i32),
         "qrng_debug_butterfly_rate": ([i32, ctypes.POINTER(u64), vp], i32),
+        "qrng_debug_pass_rate": ([i32, ctypes.POINTER(u64), vp], i32),
         "qrng_debug_kernel_timing": ([i32], None),
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
         "qrng_debug_set_karatsuba": ([i32], None),
@@ -212,8 +213,8 @@ def karatsuba_plan(n: int, m: int, max_depth: int) -> KaratsubaPlan:
 
 
 def gemm_trace(reset: bool = True) -> np.ndarray:
-    """PROFILING ONLY (-DQRNG_GEMM_TRACE builds): the 16 cycle counters."""
-    c = np.zeros(16, np.uint64)
+    """PROFILING ONLY (-DQRNG_GEMM_TRACE builds): the 32 cycle counters."""
+    c = np.zeros(32, np.uint64)
     _check(load_library().qrng_debug_gemm_trace(c.ctypes.data, 1 if reset else 0))
     return c
 
@@ -255,15 +256,17 @@ def mma_rate(form: int, n: int, iters: int = 20000, stream=None) -> float:
     return macs.value / (a.elapsed_time(b) * 1e-3)
 
 
-def butterfly_rate(iters: int = 2000, stream=None) -> float:
-    """Achievable modular-butterfly rate (butterflies/s) of the NTT butterfly code."""
+def butterfly_rate(iters: int = 2000, stream=None, with_twiddles: bool = False) -> float:
+    """Achievable modular-butterfly rate (butterflies/s) of the NTT butterfly code
+    (with_twiddles: each DFT followed by the inter-pass twiddle, qrng_debug_pass_rate)."""
     import torch
     n = ctypes.c_uint64()
     s = torch.cuda.current_stream() if stream is None else stream
-    _check(load_library().qrng_debug_butterfly_rate(8, ctypes.byref(n), s.cuda_stream))  # warm-up
+    fn = load_library().qrng_debug_pass_rate if with_twiddles else load_library().qrng_debug_butterfly_rate
+    _check(fn(8, ctypes.byref(n), s.cuda_stream))  # warm-up
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s)
-    _check(load_library().qrng_debug_butterfly_rate(iters, ctypes.byref(n), s.cuda_stream))
+    _check(fn(iters, ctypes.byref(n), s.cuda_stream))
     b.record(s)
     b.synchronize()
     return n.value / (a.elapsed_time(b) * 1e-3)

@@ -202,7 +202,13 @@ qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies, cudaStre
     if (!butterflies || iters <= 0) { set_error("bad arguments"); return QRNG_E_INVALID; }
     qrng_status st = device_ready();
     if (st != QRNG_OK) return st;
-    return ntt::butterfly_rate(iters, butterflies, stream);
+    return ntt::butterfly_rate(iters, butterflies, stream, false);
+}
+qrng_status qrng_debug_pass_rate(int iters, uint64_t *butterflies, cudaStream_t stream) {
+    if (!butterflies || iters <= 0) { set_error("bad arguments"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    return ntt::butterfly_rate(iters, butterflies, stream, true);
 }
 qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D, int N, int K,
                                   cudaStream_t stream) {
@@ -212,14 +218,18 @@ qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_
     return gemm::probe(d_A, d_h, d_D, N, K, stream);
 }
 qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream) {
-    if (!macs || iters <= 0 || n < 16 || n > 256 || n % 16) { set_error("bad arguments"); return QRNG_E_INVALID; }
+    const int n0 = n & 511, n1 = n >> 9;  // form 3: two N tiles (n1 = 0: same as n0)
+    if (!macs || iters <= 0 || n0 < 16 || n0 > 256 || n0 % 16 || n1 > 192 || n1 % 16 || ((form % 16) != 3 && n1)) {
+        set_error("bad arguments");
+        return QRNG_E_INVALID;
+    }
     qrng_status st = device_ready();
     if (st != QRNG_OK) return st;
     return gemm::mma_rate(form, iters, n, macs, stream);
 }
-qrng_status qrng_debug_gemm_trace(uint64_t *h_counters16, int reset) {
-    if (!h_counters16) { set_error("NULL buffer"); return QRNG_E_INVALID; }
-    return gemm::trace(h_counters16, reset);
+qrng_status qrng_debug_gemm_trace(uint64_t *h_counters32, int reset) {
+    if (!h_counters32) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    return gemm::trace(h_counters32, reset);
 }
 void qrng_debug_kernel_timing(int enable) { g_timing.store(enable ? 1 : 0); }
 double qrng_debug_kernel_time_split(double *aux_ms, uint64_t *launches, uint64_t *aux_launches) {

@@ -239,13 +239,19 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
 // ---- optional cycle tracing (build with -DQRNG_GEMM_TRACE; qrng_debug_gemm_trace) ----
 // Slots: 0 MMA wait a_full, 1 MMA wait b_full, 2 MMA wait acc_empty, 3 MMA total,
 // 4 xform wait a_empty, 5 xform expand+st+wait::st, 6 xform total, 7 B-gen wait b_empty,
-// 8 B-gen total, 9 epilogue wait acc_full, 10 epilogue total, 11 stages (MMA side)
+// 8 B-gen total, 9 epilogue wait acc_full, 10 epilogue total, 11 stages (MMA side),
+// 12 MMA wait acc_empty[1], 13 prologue, 14/15 CTA span (globaltimer), 16 MMA
+// elected issue blocks, 17 MMA per-tile setup (tile_info + descriptors)
 #ifdef QRNG_GEMM_TRACE
-__device__ unsigned long long g_trace[16];
+__device__ unsigned long long g_trace[32];
+// counters accumulate in registers (constant slots) and are flushed once per
+// warp at exit, so tracing does not put global atomics inside the pipeline
+#define TRACE_DECL unsigned long long trl[32] = {}
 #define TRACE_T0(v) const long long v = clock64()
-#define TRACE_ADD(slot, t0) atomicAdd(&g_trace[slot], (unsigned long long)(clock64() - (t0)))
-#define TRACE_ADDV(slot, v) atomicAdd(&g_trace[slot], (unsigned long long)(v))
+#define TRACE_ADD(slot, t0) (trl[slot] += (unsigned long long)(clock64() - (t0)))
+#define TRACE_ADDV(slot, v) (trl[slot] += (unsigned long long)(v))
 #else
+#define TRACE_DECL
 #define TRACE_T0(v)
 #define TRACE_ADD(slot, t0)
 #define TRACE_ADDV(slot, v)
@@ -270,7 +276,23 @@ struct Args {
     uint32_t x_stride;         // words per block in xws
     uint32_t *yws;             // leaf parity workspace
     uint32_t y_stride;         // words per block in yws
+    uint64_t mt_magic;         // ceil(2^64 / n_mtiles) (0 when n_mtiles == 1): q = umul64hi(x, magic)
 };
+
+// Leaf table row as the kernel reads it (grouped mode, staged in shared memory
+// at kernel start: the per-tile lookup is on the MMA issuer's critical path).
+struct TLeaf {
+    uint32_t tile_base, tile_end;  // work tiles [tile_base, tile_end) of this leaf
+    uint32_t prows, kst, r;        // rows per N pair, K stages, output rows
+    uint32_t seed_off;             // leaf seed (word offset in the plan's seed buffer)
+    uint32_t x_off_src;            // input word offset | (1 << 31) when it is in the X workspace
+    uint32_t out_off;              // word offset of the leaf parities in a block's Y row
+};
+static_assert(sizeof(TLeaf) == 32, "TLeaf is 8 words");
+
+__device__ __forceinline__ uint32_t div_mtiles(const Args &a, uint32_t x) {
+    return a.mt_magic ? (uint32_t)__umul64hi((uint64_t)x, a.mt_magic) : x;
+}
 
 // Geometry of one work tile (M tile of BM blocks x up to NT*BN output rows).
 struct Tile {
@@ -284,8 +306,8 @@ struct Tile {
     uint32_t out_off;          // grouped: word offset of the leaf in a block's yws row
 };
 
-__device__ __forceinline__ void tile_rows(Tile &ti) {
-    const uint32_t left = ti.r > ti.n0 ? min((uint32_t)(NT * BN), ti.r - ti.n0) : 16u;
+__device__ __forceinline__ void tile_rows(Tile &ti, uint32_t cap = NT * BN) {
+    const uint32_t left = ti.r > ti.n0 ? min(cap, ti.r - ti.n0) : 16u;
     ti.ntc = (left + BN - 1) / BN;
     const uint32_t lastrows = left - (ti.ntc - 1) * BN;
     ti.nlast = (lastrows + 15) & ~15u;
@@ -308,19 +330,22 @@ __device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s,
         ti.xs = a.n >> 5;
         ti.out_off = 0;
     } else {
-        while (cur + 1 < a.n_leaves && t >= (__ldg(&a.leaves[cur].npair_base) + __ldg(&a.leaves[cur].npairs)) * a.n_mtiles)
-            ++cur;
-        const Leaf &L = a.leaves[cur];
-        const uint32_t tl = t - __ldg(&L.npair_base) * a.n_mtiles;
-        ti.mt = tl % a.n_mtiles;
-        ti.n0 = (tl / a.n_mtiles) * (NT * BN);
-        ti.kst = __ldg(&L.w) / KS;
+        const TLeaf *lv = reinterpret_cast<const TLeaf *>(seed_s);  // shared-memory leaf table
+        while (cur + 1 < a.n_leaves && t >= lv[cur].tile_end) ++cur;
+        const TLeaf L = lv[cur];
+        const uint32_t tl = t - L.tile_base, q = div_mtiles(a, tl);
+        ti.mt = tl - q * a.n_mtiles;
+        ti.n0 = q * L.prows;
+        ti.kst = L.kst;
         ti.nchunks = (ti.kst + SPC - 1) / SPC;
-        ti.r = __ldg(&L.r);
-        ti.seed = a.seed_words + __ldg(&L.seed_off);
-        if (__ldg(&L.x_src) == 0) { ti.xb = a.raw + __ldg(&L.x_off); ti.xs = a.n >> 5; }
-        else { ti.xb = a.xws + __ldg(&L.x_off); ti.xs = a.x_stride; }
-        ti.out_off = __ldg(&L.out_off);
+        ti.r = L.r;
+        ti.seed = a.seed_words + L.seed_off;
+        const uint32_t xo = L.x_off_src & 0x7FFFFFFFu;
+        if (!(L.x_off_src >> 31)) { ti.xb = a.raw + xo; ti.xs = a.n >> 5; }
+        else { ti.xb = a.xws + xo; ti.xs = a.x_stride; }
+        ti.out_off = L.out_off;
+        tile_rows(ti, L.prows);
+        return ti;
     }
     tile_rows(ti);
     return ti;
@@ -354,14 +379,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *chunks = smem;
     uint32_t *seed_s = reinterpret_cast<uint32_t *>(smem + B_SLOTS * CHUNK_BYTES);
-    const uint32_t seed_stage = GROUPED ? 0u : a.seed_words_n;  // grouped: leaf seeds stay in global (L1)
+    // plain mode: the seed words; grouped mode: the leaf table (leaf seeds stay in global / L1)
+    const uint32_t seed_stage = GROUPED ? a.n_leaves * 8u : a.seed_words_n;
     uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
     uint64_t *a_full = bars, *a_empty = bars + A_STAGES, *b_full = bars + 2 * A_STAGES;
     uint64_t *b_empty = b_full + B_SLOTS, *acc_full = b_empty + B_SLOTS, *acc_empty = acc_full + ACC_BUFS;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + ACC_EMPTY);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
+#ifdef QRNG_GEMM_TRACE
+    const long long t_entry = clock64();
+    if (threadIdx.x == 0) {  // CTA span in global ns: slot 14 max end (set at exit), slot 15 max ~start
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        atomicMax(&g_trace[15], ~g);
+    }
+#endif
+    if (GROUPED) {
+        for (uint32_t i = threadIdx.x; i < a.n_leaves; i += NTHREADS) {
+            const Leaf &L = a.leaves[i];
+            TLeaf o;
+            o.tile_base = L.npair_base * a.n_mtiles;
+            o.tile_end = (L.npair_base + L.npairs) * a.n_mtiles;
+            o.prows = L.pair_rows;
+            o.kst = L.w / KS;
+            o.r = L.r;
+            o.seed_off = L.seed_off;
+            o.x_off_src = L.x_off | (L.x_src ? 0x80000000u : 0u);
+            o.out_off = L.out_off;
+            reinterpret_cast<TLeaf *>(seed_s)[i] = o;
+        }
+    } else {
+        for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM / XF_PAR); mbar_init(&a_empty[s], 1); }
         for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], N_BGEN); mbar_init(&b_empty[s], 1); }
@@ -377,17 +427,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: total over leaves in grouped mode
     uint32_t cur = 0;                                 // leaf cursor of this role
     TRACE_T0(t_role);
+    TRACE_DECL;
 
     if (DEFER_ON && warp == W_MMA) {
         // converged warp, elected issue; N tile 1 of each tile is deferred DEFER stages
         uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            TRACE_T0(tsetup);
             const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
             const uint32_t idesc_full = idesc_i8(BM, BN), idesc_last = idesc_i8(BM, (int)ti.nlast);
             const uint32_t ph = (it & 1) ^ 1;
-            mbar_wait(&acc_empty[0], ph);
+            if (lane == 0) TRACE_ADD(17, tsetup);
+            { TRACE_T0(tw); mbar_wait(&acc_empty[0], ph); if (lane == 0) TRACE_ADD(2, tw); }
             const bool defer = ti.ntc == 2 && ti.kst > (uint32_t)DEFER;
-            if (!defer) mbar_wait(&acc_empty[1], ph);
+            if (!defer) { TRACE_T0(tw); mbar_wait(&acc_empty[1], ph); if (lane == 0) TRACE_ADD(12, tw); }
             tc_fence_after();
             bool nt1_on = !defer;
             uint32_t dslot[DEFER];
@@ -395,16 +448,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             for (uint32_t ks = 0; ks < ti.kst; ++ks) {
                 const uint32_t kin = ks % SPC;
                 if (kin == 0) {
-                    mbar_wait(&b_full[bs], bph);
+                    { TRACE_T0(tw); mbar_wait(&b_full[bs], bph); if (lane == 0) TRACE_ADD(1, tw); }
                     tc_fence_after();
                 }
-                mbar_wait(&a_full[as], aph);
+                { TRACE_T0(tw); mbar_wait(&a_full[as], aph); if (lane == 0) TRACE_ADD(0, tw); }
+                if (lane == 0) TRACE_ADDV(11, 1);
                 tc_fence_after();
                 const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
                 if (ks == 0) cb0 = cbase;
                 if (!nt1_on && ks == (uint32_t)DEFER) {
                     // N tile 1 drained: its MMAs for the held stages, then release them
-                    mbar_wait(&acc_empty[1], ph);
+                    { TRACE_T0(tw); mbar_wait(&acc_empty[1], ph); if (lane == 0) TRACE_ADD(12, tw); }
                     tc_fence_after();
                     if (elect_one()) {
 #pragma unroll
@@ -423,6 +477,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     nt1_on = true;
                 }
                 const uint32_t a_tmem = tmem + A_COL0 + as * 32;
+                TRACE_T0(tiss);
                 if (elect_one()) {
 #pragma unroll
                     for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -439,6 +494,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
                 }
                 __syncwarp();
+                if (lane == 0) TRACE_ADD(16, tiss);
                 if (!nt1_on) dslot[ks] = as;
                 if (++as == A_STAGES) { as = 0; aph ^= 1; }
                 if (kin == SPC - 1 || ks == ti.kst - 1) {
@@ -513,6 +569,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 const uint32_t base = ti.n0 + c * KC;
                 { TRACE_T0(tw); mbar_wait(&b_empty[bs], bph ^ 1); if (lane == 0) TRACE_ADD(7, tw); }
                 uint8_t *cb = chunks + bs * CHUNK_BYTES;
+#if QRNG_GEMM_EXP >= 16 && (QRNG_GEMM_EXP & 8)  // experiment 8 (bitmask >= 16): no B generation
+                if (ncm < 0)
+#endif
                 for (int r = tb; r < ncm * 8; r += N_BGEN * 32) {
                     // row holds seed bits p + r(s); in v (seed bit p + d at bit 31 - d) the
                     // bit of slot s = 4cc + f sits at byte 2 + (f&1), bit 2cc + (f>>1)
@@ -593,7 +652,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     { TRACE_T0(tw); mbar_wait(&a_empty[as], aph ^ 1); if (lane == 0) TRACE_ADD(4, tw); }
                     tc_fence_after();
                     TRACE_T0(tx);
-#if QRNG_GEMM_EXP != 2  // experiment 2: no A expansion/TMEM store (MMA throughput alone)
+#if !(QRNG_GEMM_EXP == 2 || (QRNG_GEMM_EXP >= 16 && (QRNG_GEMM_EXP & 2)))  // experiment 2: no A expansion/TMEM store
                     xform_stage(lane_addr + A_COL0 + as * 32, cur4);
                     tmem_wait_st();
 #else
@@ -619,7 +678,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
-            mbar_wait(&acc_full[0], it & 1);
+            { TRACE_T0(tw); mbar_wait(&acc_full[0], it & 1); if (lane == 0) TRACE_ADD(9, tw); }
             tc_fence_after();
             const uint64_t b = (uint64_t)ti.mt * BM + row;
 #pragma unroll
@@ -628,10 +687,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 uint32_t words[3] = {0u, 0u, 0u};
                 if (96 * h < ncols) {
                     uint32_t v[32];
-                    tmem_ld32_pack16(quad + nt * BN, v);
                     uint32_t u[16];
+#if QRNG_GEMM_EXP == 4 || (QRNG_GEMM_EXP >= 16 && (QRNG_GEMM_EXP & 4))  // experiment 4: no accumulator reads
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = row + k;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) u[k] = row ^ k;
+#else
+                    tmem_ld32_pack16(quad + nt * BN, v);
                     tmem_ld16_pack16(quad + nt * BN + 64, u);
                     tmem_wait_ld();
+#endif
 #pragma unroll
                     for (int k = 0; k < 16; ++k) words[0] = (words[0] << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
 #pragma unroll
@@ -644,7 +710,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 if (lane == 0) mbar_arrive(&acc_empty[nt]);
                 const uint32_t n0 = ti.n0 + nt * BN + 96 * h;  // first row of these 3 words
                 if (b >= a.n_blocks || n0 >= ti.r || 96 * h >= ncols) continue;
-                const uint32_t nvalid = min(96u, ti.r - n0);
+                const uint32_t nvalid = min(min(96u, ncols - 96 * h), ti.r - n0);  // tile end, then leaf end
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     const int vb = (int)nvalid - 32 * c;
@@ -728,7 +794,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             const uint64_t b = (uint64_t)ti.mt * BM + row;
             const uint32_t n0 = ti.n0 + nt * BN;
             if (b >= a.n_blocks || n0 >= ti.r) continue;
-            const uint32_t nvalid = min((uint32_t)BN, ti.r - n0);
+            const uint32_t nvalid = min(ncols, ti.r - n0);
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) {
                 const int vb = (int)nvalid - 32 * c;  // valid bits in word c
@@ -763,7 +829,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #ifdef QRNG_GEMM_TRACE
     if (lane == 0) {
         const int slot = warp == W_MMA ? 3 : (warp < W_XFORM0 ? 8 : (warp < W_EPI0 ? 6 : 10));
-        TRACE_ADD(slot, t_role);
+        atomicAdd(&g_trace[slot], (unsigned long long)(clock64() - t_role));
+        if (warp == W_MMA) atomicAdd(&g_trace[13], (unsigned long long)(t_role - t_entry));  // prologue
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (trl[i]) atomicAdd(&g_trace[i], trl[i]);
     }
 #endif
     tc_fence_before();
@@ -772,6 +842,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
+#ifdef QRNG_GEMM_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        atomicMax(&g_trace[14], g);
+    }
+#endif
 }
 
 
@@ -1222,31 +1299,59 @@ __global__ void __cluster_dims__(FORM == 2 ? 2 : 1, 1, 1) __launch_bounds__(128,
     const uint32_t tmem = slot;
     uint32_t rank = 0;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    if (threadIdx.x == 0 && rank == 0) {
+    if (warp == 0 && rank == 0) {  // converged warp, elected issue (as in the kernels)
         const uint32_t idesc = idesc_i8(FORM == 2 ? 256 : 128, n);
         const uint64_t bdesc = desc_kmajor(smem_u32(smem), 256, 128);
         const uint64_t adesc = desc_kmajor(smem_u32(smem + 32768), 128, 1024);
-        for (int it = 0; it < iters; ++it) {
-            if (commit_every > 0 && it % commit_every == commit_every - 1) {
-                if (FORM == 2)
-                    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar + 1)), "h"((uint16_t)3) : "memory");
-                else
+        if (FORM == 3) {
+            // the kernels' stage shape: 4 K32 steps x 2 N tiles (N0 = n & 511,
+            // N1 = n >> 9) and one commit per stage, runtime descriptors
+            const uint32_t n0 = n & 511, n1 = (n >> 9) ? (n >> 9) : n0;
+            const uint32_t id0 = idesc_i8(128, n0), id1 = idesc_i8(128, n1);
+            const uint32_t cb = smem_u32(smem);
+            for (int it = 0; it < iters; ++it) {
+                if (elect_one()) {
+#pragma unroll
+                    for (uint32_t kk = 0; kk < 4; ++kk) {
+                        const uint32_t koff = (it & 3) * 128 + kk * 32;
+                        mma_i8_ts(tmem + 128, tmem + (it & 3) * 32 + kk * 8,
+                                  desc_kmajor(cb + (koff / 8) * 128, 256, 128), id0, 1);
+                        mma_i8_ts(tmem + 128 + 192, tmem + (it & 3) * 32 + kk * 8,
+                                  desc_kmajor(cb + (koff / 8 + 24) * 128, 256, 128), id1, 1);
+                    }
                     mma_commit(&bar + 1);
+                }
+                __syncwarp();
             }
-            if (FORM == 0) mma_i8_ts(tmem + 256, tmem, bdesc, idesc, 1);
-            else if (FORM == 1)
-                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + 256),
-                             "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
-            else
-                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-                             "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + 256),
-                             "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
+        } else
+        for (int it = 0; it < iters; ++it) {
+            if (elect_one()) {
+                if (commit_every > 0 && it % commit_every == commit_every - 1) {
+                    if (FORM == 2)
+                        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar + 1)), "h"((uint16_t)3) : "memory");
+                    else
+                        mma_commit(&bar + 1);
+                }
+                if (FORM == 0) mma_i8_ts(tmem + 256, tmem, bdesc, idesc, 1);
+                else if (FORM == 1)
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + 256),
+                                 "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
+                else
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                                 "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + 256),
+                                 "l"(adesc), "l"(bdesc), "r"(idesc) : "memory");
+            }
+            __syncwarp();
         }
-        if (FORM == 2)
-            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
-        else
-            mma_commit(&bar);
+        __syncwarp();
+        if (elect_one()) {
+            if (FORM == 2)
+                asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+            else
+                mma_commit(&bar);
+        }
+        __syncwarp();
     }
     if (FORM == 2 || rank == 0) {
         if (threadIdx.x == 0) mbar_wait(&bar, 0);
@@ -1277,13 +1382,17 @@ qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s)
     switch (form) {
         case 0: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<0>)); mma_rate_kernel<0><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
         case 1: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<1>)); mma_rate_kernel<1><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
+        case 3: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<3>)); mma_rate_kernel<3><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
 #if QRNG_GEMM_2CTA
         case 2: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<2>)); mma_rate_kernel<2><<<grid & ~1u, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
 #endif
         default: set_error("mma_rate: unsupported form"); return QRNG_E_UNSUPPORTED;
     }
     QRNG_CUDA_TRY(cudaGetLastError());
-    *macs = (uint64_t)(form == 2 ? (grid & ~1u) : grid) * (uint64_t)iters * 128ull * (uint64_t)n * 32ull;
+    if (form == 3)
+        *macs = (uint64_t)grid * iters * 4ull * 128ull * (uint64_t)((n & 511) + ((n >> 9) ? (n >> 9) : (n & 511))) * 32ull;
+    else
+        *macs = (uint64_t)(form == 2 ? (grid & ~1u) : grid) * (uint64_t)iters * 128ull * (uint64_t)n * 32ull;
     return QRNG_OK;
 }
 
@@ -1410,7 +1519,7 @@ static qrng_status launch(const Args &a, cudaStream_t s) {
     int dev = 0, sms = 148;
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = smem_bytes(GROUPED ? 0u : a.seed_words_n);
+    const size_t smem = smem_bytes(GROUPED ? a.n_leaves * 8u : a.seed_words_n);
     {
         const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel<GROUPED>));
         if (st != QRNG_OK) return st;
@@ -1463,6 +1572,8 @@ qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t to
     a.x_stride = x_stride;
     a.yws = yws;
     a.y_stride = y_stride;
+    // q = floor(x / d) = umul64hi(x, ceil(2^64 / d)) exactly for x, d < 2^32
+    a.mt_magic = a.n_mtiles > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / a.n_mtiles) + 1 : 0;
 #if QRNG_GEMM_2CTA
     return two::launch2<true>(a, s);
 #else
@@ -1475,7 +1586,7 @@ qrng_status trace(uint64_t *h_out, int reset) {
     QRNG_CUDA_TRY(cudaDeviceSynchronize());
     QRNG_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_trace, sizeof(g_trace)));
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[32] = {};
         QRNG_CUDA_TRY(cudaMemcpyToSymbol(g_trace, z, sizeof z));
     }
     return QRNG_OK;

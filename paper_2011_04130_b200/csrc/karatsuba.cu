@@ -385,6 +385,9 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
         g.w = L.w;
         g.r = L.r;
         g.npairs = (L.r + gemm::kTileRows - 1) / gemm::kTileRows;
+        // equal tiles (no narrow N = 64 tail MMA, which runs at ~60% of the pipe rate)
+        g.pair_rows = ((L.r + g.npairs - 1) / g.npairs + 31) & ~31u;
+        if (g.pair_rows > gemm::kTileRows || QRNG_GEMM_2CTA) g.pair_rows = gemm::kTileRows;
         g.npair_base = npb;
         npb += g.npairs;
         g.seed_off = so;

@@ -719,7 +719,27 @@ __global__ void __launch_bounds__(512, 2) butterfly_rate_kernel(uint32_t *sink, 
     if (acc == 0xFFFFFFFFu) sink[0] = acc;  // keep the work alive
 }
 
-qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s) {
+// Same loop with each DFT followed by the inter-pass twiddle (twiddle<5>, the
+// Montgomery power chains every non-final pass of the transforms runs): the
+// rate of the passes' full register-resident instruction mix.  Counted work is
+// still 160 butterflies per iteration, so the two rates compare directly.
+__global__ void __launch_bounds__(512, 2) pass_rate_kernel(uint32_t *sink, int iters) {
+    uint32_t x[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) x[q] = (threadIdx.x * 32u + q) % P;
+    for (int it = 0; it < iters; ++it) {
+        dft_fwd<5>(x);
+        twiddle<5>(x, c_roots.w[(it & 31) + 1]);
+        dft_inv<5>(x);
+        twiddle<5>(x, c_roots.iw[(it & 31) + 1]);
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc ^= x[q];
+    if (acc == 0xFFFFFFFFu) sink[0] = acc;
+}
+
+qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s, bool with_twiddles) {
     int dev = 0, sms = 148;
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -727,7 +747,10 @@ qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s) {
     QRNG_CUDA_TRY(cudaMallocAsync(&sink, 4, s));
     const unsigned grid = (unsigned)sms * 2, block = 512;
     count_launch();
-    butterfly_rate_kernel<<<grid, block, 0, s>>>(sink, iters);
+    if (with_twiddles)
+        pass_rate_kernel<<<grid, block, 0, s>>>(sink, iters);
+    else
+        butterfly_rate_kernel<<<grid, block, 0, s>>>(sink, iters);
     QRNG_CUDA_TRY(cudaGetLastError());
     cudaFreeAsync(sink, s);
     *butterflies = (uint64_t)grid * block * (uint64_t)iters * 160u;

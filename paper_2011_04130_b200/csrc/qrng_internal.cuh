@@ -89,7 +89,7 @@ void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
 int choose_pack_shift(uint64_t n, int logP);
-qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s);
+qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s, bool with_twiddles);
 }  // namespace ntt
 
 // GEMM path (gemm_tc.cu): tcgen05 kind::i8 batched Toeplitz product.
@@ -111,6 +111,7 @@ struct Leaf {
     uint32_t out_off;           // word offset of the leaf parities in a block's Y row
     uint32_t sterm_base, sterm_n;  // seed terms (bit offsets into the root seed) in the term table
     uint32_t iterm_base, iterm_n;  // input terms (bit offsets into the raw block)
+    uint32_t pair_rows;         // rows per N pair (<= NT*BN, multiple of 32): r split evenly over npairs
 };
 // tcgen05 kernel geometry (build-time; gemm_tc.cu): rows per N tile, N tiles per
 // A stage, A ring slots, accumulator sets.

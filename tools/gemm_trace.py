@@ -13,7 +13,7 @@ import paper_2011_04130_b200 as q
 
 NAMES = ["mma_wait_a_full", "mma_wait_b_full", "mma_wait_acc_empty", "mma_total", "xf_wait_a_empty",
          "xf_expand_st", "xf_total", "bgen_wait_b_empty", "bgen_total", "epi_wait_acc_full", "epi_total",
-         "stages", "", "", "", ""]
+         "stages", "mma_wait_acc_empty_nt1", "prologue", "", "", "mma_issue_blocks", "mma_tile_setup"]
 
 
 def main():
@@ -30,13 +30,21 @@ def main():
     out = q.toeplitz_extract(raw, w.n_blocks, w.n, w.m, seed)
     torch.cuda.synchronize()
     q.gemm_trace(True)
+    q.kernel_timing(True)
+    q.kernel_time_ms()
     out = q.toeplitz_extract(raw, w.n_blocks, w.n, w.m, seed, out=out)
+    torch.cuda.synchronize()
+    kms, _ = q.kernel_time_ms()
+    q.kernel_timing(False)
     c = q.gemm_trace(True)
     ctas = 148
-    res = {"workload": w.name, "karatsuba": args.karatsuba}
+    res = {"workload": w.name, "karatsuba": args.karatsuba, "gemm_kernel_ms": kms}
     for i, n in enumerate(NAMES):
         if n:
             res[n] = int(c[i]) / (1 if n == "stages" else ctas)
+    res["cta_span_us"] = (int(c[14]) - (~int(c[15]) & (2**64 - 1))) / 1e3
+    # SM clock during the kernel: MMA-role cycles per CTA over the global span (a lower bound)
+    res["sm_ghz_est"] = res["mma_total"] / (res["cta_span_us"] * 1e3) if res["cta_span_us"] > 0 else None
     # per-warp normalisation: xform counters are summed over 4*XF_PAR warps, b-gen 3, epilogue 8
     print(json.dumps(res))
 
