@@ -269,6 +269,12 @@ QRNG_API qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies,
  * counts the same 160 butterflies per iteration, so the rate is directly
  * comparable with qrng_debug_butterfly_rate. */
 QRNG_API qrng_status qrng_debug_pass_rate(int iters, uint64_t *butterflies, cudaStream_t stream);
+/* TEST ONLY: the same product on kind::mxf4 (E2M1 0/1 operands, both in shared
+ * memory, unit UE8M0 block scales, FP32 accumulation): D (128 x N float,
+ * row-major, device).  hi_first selects the nibble order of the packed
+ * operands.  N in [16, 256] multiple of 16, K in [64, 1024] multiple of 64. */
+QRNG_API qrng_status qrng_debug_mxf4_probe(const uint8_t *d_A, const uint8_t *d_h, float *d_D, int N, int K,
+                                           int hi_first, cudaStream_t stream);
 QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D,
                                            int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);

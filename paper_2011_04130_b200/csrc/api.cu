@@ -217,9 +217,16 @@ qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_
     if (st != QRNG_OK) return st;
     return gemm::probe(d_A, d_h, d_D, N, K, stream);
 }
+qrng_status qrng_debug_mxf4_probe(const uint8_t *d_A, const uint8_t *d_h, float *d_D, int N, int K, int hi_first,
+                                  cudaStream_t stream) {
+    if (!d_A || !d_h || !d_D) { set_error("NULL buffer"); return QRNG_E_INVALID; }
+    qrng_status st = device_ready();
+    if (st != QRNG_OK) return st;
+    return gemm::mxf4_probe(d_A, d_h, d_D, N, K, hi_first, stream);
+}
 qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream) {
     const int n0 = n & 511, n1 = n >> 9;  // form 3: two N tiles (n1 = 0: same as n0)
-    if (!macs || iters <= 0 || n0 < 16 || n0 > 256 || n0 % 16 || n1 > 192 || n1 % 16 || ((form % 16) != 3 && n1)) {
+    if (!macs || iters <= 0 || n0 < 16 || n0 > 256 || n0 % 16 || n1 > 192 || n1 % 16 || ((form % 16) != 3 && (form % 16) != 5 && n1)) {
         set_error("bad arguments");
         return QRNG_E_INVALID;
     }

@@ -41,7 +41,20 @@ namespace gemm {
 constexpr int BM = 128;        // blocks per tile (TMEM lanes)
 constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
 constexpr int KS = 128;        // K per A stage
-constexpr int A_STAGES = QRNG_GEMM_ASTAGES;  // A ring slots in TMEM (32 columns each)
+// Operand format.  FP4 (default): tcgen05.mma kind::mxf4 -- E2M1 0/1 operands
+// (0x0 / 0x2 = 0.0 / 1.0, two per byte) with unit UE8M0 block scales, both
+// operands in shared memory, FP32 accumulators (exact: every product is 0 or 1
+// and every partial sum an integer <= n <= 2^16 < 2^24), twice the int8 MMA
+// rate.  Otherwise kind::i8 with A in TMEM and S32 accumulators.
+#ifndef QRNG_GEMM_FP4
+#define QRNG_GEMM_FP4 1
+#endif
+constexpr bool FP4 = QRNG_GEMM_FP4 != 0;
+#ifndef QRNG_GEMM_ASTAGES_FP4
+#define QRNG_GEMM_ASTAGES_FP4 6
+#endif
+constexpr int A_STAGES = FP4 ? QRNG_GEMM_ASTAGES_FP4 : QRNG_GEMM_ASTAGES;  // A ring slots (FP4: smem; i8: TMEM, 32 columns each)
+constexpr int A_STAGE_BYTES = 128 * 128 / 2;  // FP4 A stage in smem: BM rows x KS nibbles
 constexpr int KC = 1024;       // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
 constexpr int B_SLOTS = 3;
@@ -51,9 +64,10 @@ constexpr int ACC_BUFS = QRNG_GEMM_ACCBUFS;
 constexpr int CM_PER_CHUNK = KC / 8 + NT * BN / 8 - 1;  // core matrices per chunk
 constexpr int CHUNK_BYTES = CM_PER_CHUNK * 128;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t A_COL0 = 0;    // A stages: columns [0, 32 A_STAGES)
-constexpr uint32_t ACC_COL0 = 32 * A_STAGES;  // accumulator sets (buffer x N tile) follow
-static_assert(A_STAGES * 32 + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
+constexpr uint32_t A_COL0 = 0;    // i8: A stages in columns [0, 32 A_STAGES)
+constexpr uint32_t ACC_COL0 = FP4 ? 0u : 32u * A_STAGES;  // accumulator sets (buffer x N tile)
+constexpr uint32_t SF_COL = ACC_COL0 + ACC_BUFS * NT * BN;  // FP4: unit block scales (16 columns of 0x7F)
+static_assert((FP4 ? 16 : A_STAGES * 32) + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
 static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (NT = 1) or one per N tile");
 // Deferred second N tile (NT = 2, one accumulator set): the epilogue drains
 // N tile 0 and then N tile 1 (all 8 warps, half the columns each); the next
@@ -62,6 +76,7 @@ static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (N
 constexpr bool DEFER_ON = QRNG_GEMM_DEFER > 0 && NT == 2 && ACC_BUFS == 1 && BN == 192;
 constexpr int DEFER = QRNG_GEMM_DEFER > 0 ? QRNG_GEMM_DEFER : 1;
 static_assert(!DEFER_ON || (DEFER < A_STAGES && DEFER < KC / KS), "deferred stages stay resident in one chunk");
+static_assert(!FP4 || DEFER_ON, "the FP4 operand path is implemented for the deferred NT = 2, BN = 192 geometry");
 constexpr int ACC_EMPTY = DEFER_ON ? 2 : ACC_BUFS;
 // Warp roles.  The A transform uses XF_PAR warps per TMEM lane quadrant, each
 // taking every XF_PAR-th stage, so the per-stage latency chain (wait slot ->
@@ -210,6 +225,23 @@ __device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr, uint32_t lbo, ui
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool is_signed = true) {
     return (2u << 4) | ((is_signed ? 1u : 0u) << 7) | ((is_signed ? 1u : 0u) << 10) |
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_mxf4_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t sfa, uint32_t sfb, bool acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"((uint32_t)acc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+// 32 E2M1 elements (one core-matrix row, 16 bytes) from a 32-bit window v:
+// slot 8i + j (word i, nibble j) takes bit 4j + i of v as 0x0 / 0x2.  A and B
+// use the same slot order, so the K permutation cancels in the dot product.
+__device__ __forceinline__ uint4 e2m1_row(uint32_t v) {
+    return make_uint4((v << 1) & 0x22222222u, v & 0x22222222u, (v >> 1) & 0x22222222u, (v >> 2) & 0x22222222u);
 }
 
 // prmt.b32 with sign-replicate selectors: each output byte is 0x00 or 0xFF,
@@ -378,7 +410,8 @@ template <bool GROUPED>
 __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *chunks = smem;
-    uint32_t *seed_s = reinterpret_cast<uint32_t *>(smem + B_SLOTS * CHUNK_BYTES);
+    uint8_t *a_ring = smem + B_SLOTS * CHUNK_BYTES;  // FP4: A stages (core-matrix layout, LBO 128, SBO 512)
+    uint32_t *seed_s = reinterpret_cast<uint32_t *>(a_ring + (FP4 ? A_STAGES * A_STAGE_BYTES : 0));
     // plain mode: the seed words; grouped mode: the leaf table (leaf seeds stay in global / L1)
     const uint32_t seed_stage = GROUPED ? a.n_leaves * 8u : a.seed_words_n;
     uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
@@ -424,6 +457,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (FP4) {
+        // unit block scales: UE8M0 127 = 2^0 in every byte of the scale-factor columns
+        if (warp >= W_EPI0 && warp < W_EPI0 + 4) {
+            uint32_t v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = 0x7F7F7F7Fu;
+            tmem_st16(tmem + (((uint32_t)(warp & 3) * 32) << 16) + SF_COL, v);
+            tmem_wait_st();
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: total over leaves in grouped mode
     uint32_t cur = 0;                                 // leaf cursor of this role
     TRACE_T0(t_role);
@@ -435,7 +481,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             TRACE_T0(tsetup);
             const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
-            const uint32_t idesc_full = idesc_i8(BM, BN), idesc_last = idesc_i8(BM, (int)ti.nlast);
+            const uint32_t idesc_full = FP4 ? idesc_mxf4(BM, BN) : idesc_i8(BM, BN);
+            const uint32_t idesc_last = FP4 ? idesc_mxf4(BM, (int)ti.nlast) : idesc_i8(BM, (int)ti.nlast);
             const uint32_t ph = (it & 1) ^ 1;
             if (lane == 0) TRACE_ADD(17, tsetup);
             { TRACE_T0(tw); mbar_wait(&acc_empty[0], ph); if (lane == 0) TRACE_ADD(2, tw); }
@@ -463,12 +510,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     if (elect_one()) {
 #pragma unroll
                         for (int d = 0; d < DEFER; ++d) {
+                            if constexpr (FP4) {
+                                const uint32_t abase = smem_u32(a_ring + dslot[d] * A_STAGE_BYTES);
 #pragma unroll
-                            for (uint32_t kk = 0; kk < 4; ++kk) {
-                                const uint32_t koff = d * KS + kk * 32;
-                                const uint64_t bdesc = desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 256, 128);
-                                mma_i8_ts(tmem + ACC_COL0 + BN, tmem + A_COL0 + dslot[d] * 32 + kk * 8, bdesc,
-                                          idesc_last, (d | kk) != 0);
+                                for (uint32_t kk = 0; kk < 2; ++kk) {
+                                    const uint32_t koff = d * KS + kk * 64;
+                                    mma_mxf4_ss(tmem + ACC_COL0 + BN, desc_kmajor(abase + kk * 256, 128, 512),
+                                                desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
+                                                tmem + SF_COL, tmem + SF_COL + 8, (d | kk) != 0);
+                                }
+                            } else {
+#pragma unroll
+                                for (uint32_t kk = 0; kk < 4; ++kk) {
+                                    const uint32_t koff = d * KS + kk * 32;
+                                    const uint64_t bdesc = desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 256, 128);
+                                    mma_i8_ts(tmem + ACC_COL0 + BN, tmem + A_COL0 + dslot[d] * 32 + kk * 8, bdesc,
+                                              idesc_last, (d | kk) != 0);
+                                }
                             }
                             mma_commit(&a_empty[dslot[d]]);
                         }
@@ -479,6 +537,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 const uint32_t a_tmem = tmem + A_COL0 + as * 32;
                 TRACE_T0(tiss);
                 if (elect_one()) {
+                    if constexpr (FP4) {
+                        const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+#pragma unroll
+                        for (uint32_t kk = 0; kk < 2; ++kk) {
+                            const uint32_t koff = kin * KS + kk * 64;
+                            const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, 512);
+                            mma_mxf4_ss(tmem + ACC_COL0, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128),
+                                        ti.ntc == 1 ? idesc_last : idesc_full, tmem + SF_COL, tmem + SF_COL + 8,
+                                        (ks | kk) != 0);
+                            if (nt1_on && ti.ntc == 2)
+                                mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc,
+                                            desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
+                                            tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                        }
+                    } else {
 #pragma unroll
                     for (uint32_t kk = 0; kk < 4; ++kk) {
                         const uint32_t koff = kin * KS + kk * 32;
@@ -489,6 +562,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                             const uint64_t bdesc1 = desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 256, 128);
                             mma_i8_ts(tmem + ACC_COL0 + BN, a_tmem + kk * 8, bdesc1, idesc_last, (ks | kk) != 0);
                         }
+                    }
                     }
                     if (nt1_on) mma_commit(&a_empty[as]);
                     if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
@@ -581,10 +655,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     else { w0 = ti.seed[p >> 5]; w1 = ti.seed[(p >> 5) + 1]; }
                     const uint32_t v = __funnelshift_l(w1, w0, p & 31);
                     uint4 o;
-                    o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
-                    o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
-                    o.z = prmt_sign<0xFEBA>(v << 3, v << 2);
-                    o.w = prmt_sign<0xFEBA>(v << 1, v);
+                    if constexpr (FP4) {
+                        o = e2m1_row(v);  // 32 elements: seed bits p .. p + 31
+                    } else {
+                        o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
+                        o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
+                        o.z = prmt_sign<0xFEBA>(v << 3, v << 2);
+                        o.w = prmt_sign<0xFEBA>(v << 1, v);
+                    }
                     *reinterpret_cast<uint4 *>(cb + (r >> 3) * 128 + (r & 7) * 16) = o;
                 }
                 fence_proxy_async();
@@ -653,8 +731,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     tc_fence_after();
                     TRACE_T0(tx);
 #if !(QRNG_GEMM_EXP == 2 || (QRNG_GEMM_EXP >= 16 && (QRNG_GEMM_EXP & 2)))  // experiment 2: no A expansion/TMEM store
-                    xform_stage(lane_addr + A_COL0 + as * 32, cur4);
-                    tmem_wait_st();
+                    if constexpr (FP4) {
+                        // K group g (32 elements, K reversed) = memory word 3 - g, element c = bit c
+                        // of its big-endian value: bit-reverse so that bit b holds element 31 - b
+                        // as in the B rows, then the same nibble spread
+                        const uint32_t M4[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
+                        uint8_t *arow = a_ring + as * A_STAGE_BYTES + (row >> 3) * 512 + (row & 7) * 16;
+#pragma unroll
+                        for (int gk = 0; gk < 4; ++gk)
+                            *reinterpret_cast<uint4 *>(arow + gk * 128) =
+                                e2m1_row(__brev(__byte_perm(M4[3 - gk], 0, 0x0123)));
+                        fence_proxy_async();
+                    } else {
+                        xform_stage(lane_addr + A_COL0 + as * 32, cur4);
+                        tmem_wait_st();
+                    }
 #else
                     if (cur4.x == 0x12345678u) __nanosleep(1);
 #endif
@@ -694,16 +785,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #pragma unroll
                     for (int k = 0; k < 16; ++k) u[k] = row ^ k;
 #else
-                    tmem_ld32_pack16(quad + nt * BN, v);
-                    tmem_ld16_pack16(quad + nt * BN + 64, u);
-                    tmem_wait_ld();
+                    if constexpr (FP4) {
+                        // FP32 sums are exact integers < 2^23: adding 2^23 puts their
+                        // parity in the lowest mantissa bit
+                        uint32_t v2[32];
+                        tmem_ld32(quad + nt * BN, v);
+                        tmem_ld32(quad + nt * BN + 32, v2);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            words[0] = (words[0] << 1) | (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            words[1] = (words[1] << 1) | (__float_as_uint(__uint_as_float(v2[k]) + 8388608.0f) & 1u);
+                        tmem_ld32(quad + nt * BN + 64, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            words[2] = (words[2] << 1) | (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u);
+                    } else {
+                        tmem_ld32_pack16(quad + nt * BN, v);
+                        tmem_ld16_pack16(quad + nt * BN + 64, u);
+                        tmem_wait_ld();
+                    }
 #endif
+                    if constexpr (!FP4) {
 #pragma unroll
                     for (int k = 0; k < 16; ++k) words[0] = (words[0] << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
 #pragma unroll
                     for (int k = 16; k < 32; ++k) words[1] = (words[1] << 2) | ((v[k] & 1u) << 1) | ((v[k] >> 16) & 1u);
 #pragma unroll
                     for (int k = 0; k < 16; ++k) words[2] = (words[2] << 2) | ((u[k] & 1u) << 1) | ((u[k] >> 16) & 1u);
+                    }
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -1303,6 +1416,33 @@ __global__ void __cluster_dims__(FORM == 2 ? 2 : 1, 1, 1) __launch_bounds__(128,
         const uint32_t idesc = idesc_i8(FORM == 2 ? 256 : 128, n);
         const uint64_t bdesc = desc_kmajor(smem_u32(smem), 256, 128);
         const uint64_t adesc = desc_kmajor(smem_u32(smem + 32768), 128, 1024);
+        if (FORM == 4 || FORM == 5) {
+            // kind::mxf4 (E2M1, both operands in shared memory, unit scales in TMEM
+            // columns [448, 464)): form 4 = back-to-back M128 N=n K64; form 5 = the
+            // stage shape, 2 K64 steps x two N tiles (N0 = n & 511, N1 = n >> 9)
+            const uint32_t n0 = n & 511, n1 = (n >> 9) ? (n >> 9) : n0;
+            const uint32_t id0 = idesc_mxf4(128, n0), id1 = idesc_mxf4(128, n1);
+            const uint32_t cb = smem_u32(smem);
+            for (int it = 0; it < iters; ++it) {
+                if (elect_one()) {
+                    if (FORM == 4) {
+                        mma_mxf4_ss(tmem + 128, desc_kmajor(cb + 32768, 128, 1024), desc_kmajor(cb, 512, 128), id0,
+                                    tmem + 448, tmem + 456, 1);
+                    } else {
+#pragma unroll
+                        for (uint32_t kk = 0; kk < 2; ++kk) {
+                            const uint64_t ad = desc_kmajor(cb + 32768 + (it & 3) * 2048 + kk * 256, 128, 512);
+                            mma_mxf4_ss(tmem, ad, desc_kmajor(cb + ((it & 3) * 16 + kk * 8) * 128, 512, 128), id0,
+                                        tmem + 448, tmem + 456, 1);
+                            mma_mxf4_ss(tmem + 192, ad, desc_kmajor(cb + ((it & 3) * 16 + kk * 8 + 24) * 128, 512, 128),
+                                        id1, tmem + 448, tmem + 456, 1);
+                        }
+                        mma_commit(&bar + 1);
+                    }
+                }
+                __syncwarp();
+            }
+        } else
         if (FORM == 3) {
             // the kernels' stage shape: 4 K32 steps x 2 N tiles (N0 = n & 511,
             // N1 = n >> 9) and one commit per stage, runtime descriptors
@@ -1383,6 +1523,8 @@ qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s)
         case 0: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<0>)); mma_rate_kernel<0><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
         case 1: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<1>)); mma_rate_kernel<1><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
         case 3: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<3>)); mma_rate_kernel<3><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
+        case 4: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<4>)); mma_rate_kernel<4><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
+        case 5: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<5>)); mma_rate_kernel<5><<<grid, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
 #if QRNG_GEMM_2CTA
         case 2: allow_max_smem(reinterpret_cast<const void *>(mma_rate_kernel<2>)); mma_rate_kernel<2><<<grid & ~1u, 128, smem, s>>>(iters, n, nullptr, commit_every); break;
 #endif
@@ -1391,6 +1533,10 @@ qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s)
     QRNG_CUDA_TRY(cudaGetLastError());
     if (form == 3)
         *macs = (uint64_t)grid * iters * 4ull * 128ull * (uint64_t)((n & 511) + ((n >> 9) ? (n >> 9) : (n & 511))) * 32ull;
+    else if (form == 4)
+        *macs = (uint64_t)grid * iters * 128ull * (uint64_t)n * 64ull;
+    else if (form == 5)
+        *macs = (uint64_t)grid * iters * 2ull * 128ull * (uint64_t)((n & 511) + ((n >> 9) ? (n >> 9) : (n & 511))) * 64ull;
     else
         *macs = (uint64_t)(form == 2 ? (grid & ~1u) : grid) * (uint64_t)iters * 128ull * (uint64_t)n * 32ull;
     return QRNG_OK;
@@ -1460,6 +1606,101 @@ __global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, co
     }
 }
 
+// ---- FP4 (kind::mxf4) probe (test only) ------------------------------------------
+// E2M1 operands, 0 -> 0x0 and 1 -> 0x2 (1.0), two per byte (`hi_first`: element
+// 2i in the high nibble), unit block scales (UE8M0 127 = 2^0) in a TMEM region
+// filled with 0x7F, FP32 accumulation.  D = A * B^T, B[i][k] = h[i + k] through
+// the same overlapping core-matrix windows as the int8 B operand (a core-matrix
+// row now holds 32 elements, so the K-direction byte offset LBO is 4 x 128).
+__device__ __forceinline__ uint8_t pack_e2m1(uint8_t lo_elem, uint8_t hi_elem, bool hi_first) {
+    const uint8_t a = lo_elem ? 2 : 0, b = hi_elem ? 2 : 0;  // element 2i, element 2i + 1
+    return hi_first ? (uint8_t)((a << 4) | b) : (uint8_t)((b << 4) | a);
+}
+__global__ void __launch_bounds__(128, 1) mxf4_probe_kernel(const uint8_t *A, const uint8_t *h, float *D, int N,
+                                                           int K, int hi_first) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(smem + 8);
+    uint8_t *acm = smem + 1024;                   // A: core matrix (rg, kg) at (rg * K/32 + kg) * 128
+    uint8_t *bcm = acm + 128 * (K / 2);           // B windows: core matrix tau row rr = h[8 tau + rr + c], c < 32
+    const int warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int ncm = K / 8 + N / 8 - 1;
+    for (int r = tid; r < ncm * 8; r += 128) {
+        const int tau = r >> 3, rr = r & 7;
+        for (int c = 0; c < 16; ++c)
+            bcm[tau * 128 + rr * 16 + c] = pack_e2m1(h[8 * tau + rr + 2 * c], h[8 * tau + rr + 2 * c + 1], hi_first);
+    }
+    for (int kg = 0; kg < K / 32; ++kg)
+        for (int c = 0; c < 16; ++c) {
+            const int r = tid;
+            acm[((r >> 3) * (K / 32) + kg) * 128 + (r & 7) * 16 + c] =
+                pack_e2m1(A[r * K + kg * 32 + 2 * c], A[r * K + kg * 32 + 2 * c + 1], hi_first);
+        }
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_proxy_async();
+    if (warp == 0) tmem_alloc(slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    {
+        uint32_t v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = 0x7F7F7F7Fu;
+        tmem_st16(lane_addr + 256, v);  // scale-factor region, columns [256, 272)
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+        if (elect_one()) {
+            const uint32_t idesc = idesc_mxf4(128, N);
+            for (int k = 0; k < K; k += 64) {
+                const uint64_t adesc = desc_kmajor(smem_u32(acm) + (k / 32) * 128, 128, (K / 32) * 128);
+                const uint64_t bdesc = desc_kmajor(smem_u32(bcm) + (k / 8) * 128, 512, 128);
+                mma_mxf4_ss(tmem, adesc, bdesc, idesc, tmem + 256, tmem + 264, k != 0);
+            }
+            mma_commit(bar);
+        }
+        __syncwarp();
+    }
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    for (int c0 = 0; c0 < N; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(lane_addr + c0, v);
+        tmem_wait_ld();
+        for (int c = 0; c < 32 && c0 + c < N; ++c) D[tid * N + c0 + c] = __uint_as_float(v[c]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int K, int hi_first, cudaStream_t s) {
+    if (N < 16 || N > 256 || N % 16 || K < 64 || K > 1024 || K % 64) {
+        set_error("mxf4 probe: N in [16, 256] multiple of 16, K in [64, 1024] multiple of 64");
+        return QRNG_E_INVALID;
+    }
+    const size_t smem = 1024 + 128 * (K / 2) + (size_t)(K / 8 + N / 8) * 128;
+    {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(mxf4_probe_kernel));
+        if (st != QRNG_OK) return st;
+    }
+    count_launch();
+    mxf4_probe_kernel<<<1, 128, smem, s>>>(A, h, D, N, K, hi_first);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
 // ---- host ------------------------------------------------------------------------
 bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n; }
 
@@ -1473,7 +1714,7 @@ uint32_t seed_words_needed(uint64_t n, uint64_t m) {
 }
 
 static size_t smem_bytes(uint32_t seed_words_n) {
-    return (size_t)B_SLOTS * CHUNK_BYTES + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + ACC_BUFS + ACC_EMPTY) * 8 + 16;
+    return (size_t)B_SLOTS * CHUNK_BYTES + (FP4 ? (size_t)A_STAGES * A_STAGE_BYTES : 0) + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + ACC_BUFS + ACC_EMPTY) * 8 + 16;
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L
