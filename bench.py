@@ -112,7 +112,7 @@ def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool, modifi
     """Roofline numerators, per step of the main kernel(s)."""
     import paper_2011_04130_b200 as q
     if path == q.PATH_GEMM:
-        # int8 ops the tensor cores run: 2 x the leaf MACs of the Karatsuba
+        # tensor-core ops (E2M1 or int8): 2 x the leaf MACs of the Karatsuba
         # decomposition (= 2 m n per block for the dense product, depth 0)
         return 2.0 * (macs_per_block or w.m * w.n) * n_blocks, "tensor", "TOPS"
     L = (w.n - 1) if modified else (w.n + w.m - 1)
@@ -312,11 +312,19 @@ def run_ours(args):
         per_step_s = kern_ms / args.steps * 1e-3
         if bound == "tensor":
             achieved = work / per_step_s / 1e12
-            peak = pk["bf16_tflops"] * 2.0  # int8 dense = 2x bf16 (guide's nominal ratio)
+            fp4 = q.gemm_operand_bits() == 4
+            # the contraction's own dtype: E2M1 dense = 4 x bf16, int8 = 2 x bf16
+            # (nominal ratios 9 / 4.5 / 2.25 PFLOP/s)
+            ratio = 4.0 if fp4 else 2.0
+            peak = pk["bf16_tflops"] * ratio
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
-                    "peak_kind": f"{pk_kind} bf16 x 2 (int8 nominal ratio)"}
+                    "peak_kind": f"{pk_kind} bf16 x {ratio:g} ({'E2M1 kind::mxf4' if fp4 else 'int8'} nominal ratio)"}
             clk_mhz = pk.get("sm_max_mhz", 1965.0)
-            roof["peak_at_sm_max_clock"] = 148 * 8192 * 2 * clk_mhz * 1e6 / 1e12
+            macs_per_clk = 16384 if fp4 else 8192
+            roof["peak_at_sm_max_clock"] = 148 * macs_per_clk * 2 * clk_mhz * 1e6 / 1e12
+            # the tensor pipe measured live in the kernel's own stage shape (2 N tiles
+            # of 192 per elected issue, back to back, no data movement)
+            roof["peak_mma_microbench"] = 2 * q.mma_rate(5 if fp4 else 3, 192 | (192 << 9)) / 1e12
             roof["frac_of_clock_peak"] = achieved / roof["peak_at_sm_max_clock"]
             roof["ops_per_step"] = work
             roof["dense_ops_per_step"] = 2.0 * w.m * w.n * B  # the O(mn) product without Karatsuba
@@ -363,7 +371,9 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8 bits; int32 mod-p NTT" if path == 2 else "u8 bits; int8 x int8 -> int32 tensor core",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8 bits; int32 mod-p NTT" if path == 2 else (
+            "u8 bits; E2M1 0/1 x E2M1 -> fp32 tensor core (kind::mxf4, unit scales, exact)"
+            if q.gemm_operand_bits() == 4 else "u8 bits; int8 x int8 -> int32 tensor core"),
         "data": "synthetic: uint8 ADC samples clip(rint(N(128,sigma^2))) from PCG64 (qrng_synth); seeded uniform seed",
         "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_per_gpu": B, "seed_bits": w.seed_bits,
                    "raw_bits_per_gpu": w.raw_bits, "path": {1: "gemm", 2: "ntt"}[path],

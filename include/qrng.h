@@ -269,6 +269,10 @@ QRNG_API qrng_status qrng_debug_butterfly_rate(int iters, uint64_t *butterflies,
  * counts the same 160 butterflies per iteration, so the rate is directly
  * comparable with qrng_debug_butterfly_rate. */
 QRNG_API qrng_status qrng_debug_pass_rate(int iters, uint64_t *butterflies, cudaStream_t stream);
+/* BENCH ONLY: operand width of the tensor-core path this library was built
+ * with: 4 = tcgen05 kind::mxf4 (E2M1 0/1 operands, FP32 accumulation, the
+ * default), 8 = kind::i8 (S32 accumulation, -DQRNG_GEMM_FP4=0). */
+QRNG_API int         qrng_debug_gemm_operand_bits(void);
 /* TEST ONLY: the same product on kind::mxf4 (E2M1 0/1 operands, both in shared
  * memory, unit UE8M0 block scales, FP32 accumulation): D (128 x N float,
  * row-major, device).  hi_first selects the nibble order of the packed

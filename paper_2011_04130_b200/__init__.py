@@ -34,7 +34,7 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_plan_create_modified", "qrng_modified_toeplitz_extract_async",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
-           "qrng_debug_butterfly_rate", "qrng_debug_pass_rate", "qrng_debug_mxf4_probe", "qrng_debug_set_karatsuba", "qrng_plan_info",
+           "qrng_debug_butterfly_rate", "qrng_debug_pass_rate", "qrng_debug_mxf4_probe", "qrng_debug_gemm_operand_bits", "qrng_debug_set_karatsuba", "qrng_plan_info",
            "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
            "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split",
            "qrng_debug_mma_rate"]
@@ -116,6 +116,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_debug_butterfly_rate": ([i32, ctypes.POINTER(u64), vp], i32),
         "qrng_debug_pass_rate": ([i32, ctypes.POINTER(u64), vp], i32),
         "qrng_debug_mxf4_probe": ([vp, vp, vp, i32, i32, i32, vp], i32),
+        "qrng_debug_gemm_operand_bits": ([], i32),
         "qrng_debug_kernel_timing": ([i32], None),
         "qrng_debug_kernel_time_ms": ([ctypes.POINTER(u64)], ctypes.c_double),
         "qrng_debug_set_karatsuba": ([i32], None),
@@ -244,7 +245,7 @@ def kernel_time_split() -> tuple[float, int, float, int]:
 
 
 def mma_rate(form: int, n: int, iters: int = 20000, stream=None) -> float:
-    """PROFILING ONLY: int8 MAC/s of back-to-back MMAs of one form (see qrng.h)."""
+    """PROFILING ONLY: MAC/s of back-to-back MMAs of one form (see qrng.h)."""
     import torch
     macs = ctypes.c_uint64()
     s = torch.cuda.current_stream() if stream is None else stream
@@ -271,6 +272,11 @@ def butterfly_rate(iters: int = 2000, stream=None, with_twiddles: bool = False) 
     b.record(s)
     b.synchronize()
     return n.value / (a.elapsed_time(b) * 1e-3)
+
+
+def gemm_operand_bits() -> int:
+    """4: the tensor-core path runs kind::mxf4 (E2M1, FP32 accumulate); 8: kind::i8."""
+    return int(load_library().qrng_debug_gemm_operand_bits())
 
 
 def mxf4_probe(A, h, N: int, K: int, hi_first: bool = False, stream=None):

@@ -217,6 +217,7 @@ qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_
     if (st != QRNG_OK) return st;
     return gemm::probe(d_A, d_h, d_D, N, K, stream);
 }
+int qrng_debug_gemm_operand_bits(void) { return gemm::operand_bits(); }
 qrng_status qrng_debug_mxf4_probe(const uint8_t *d_A, const uint8_t *d_h, float *d_D, int N, int K, int hi_first,
                                   cudaStream_t stream) {
     if (!d_A || !d_h || !d_D) { set_error("NULL buffer"); return QRNG_E_INVALID; }

@@ -40,21 +40,27 @@ namespace gemm {
 
 constexpr int BM = 128;        // blocks per tile (TMEM lanes)
 constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
-constexpr int KS = 128;        // K per A stage
 // Operand format.  FP4 (default): tcgen05.mma kind::mxf4 -- E2M1 0/1 operands
 // (0x0 / 0x2 = 0.0 / 1.0, two per byte) with unit UE8M0 block scales, both
 // operands in shared memory, FP32 accumulators (exact: every product is 0 or 1
 // and every partial sum an integer <= n <= 2^16 < 2^24), twice the int8 MMA
 // rate.  Otherwise kind::i8 with A in TMEM and S32 accumulators.
 #ifndef QRNG_GEMM_FP4
+#if QRNG_GEMM_2CTA
+#define QRNG_GEMM_FP4 0  // the 2-SM variant is int8 only
+#else
 #define QRNG_GEMM_FP4 1
 #endif
+#endif
 constexpr bool FP4 = QRNG_GEMM_FP4 != 0;
+constexpr int KS = FP4 ? 256 : 128;  // K per A stage (FP4: 4 MMAs of K64 per N tile per stage)
+constexpr int KS128 = KS / 128;      // 128-bit raw chunks per A stage
 #ifndef QRNG_GEMM_ASTAGES_FP4
-#define QRNG_GEMM_ASTAGES_FP4 6
+#define QRNG_GEMM_ASTAGES_FP4 4
 #endif
 constexpr int A_STAGES = FP4 ? QRNG_GEMM_ASTAGES_FP4 : QRNG_GEMM_ASTAGES;  // A ring slots (FP4: smem; i8: TMEM, 32 columns each)
-constexpr int A_STAGE_BYTES = 128 * 128 / 2;  // FP4 A stage in smem: BM rows x KS nibbles
+constexpr int A_STAGE_BYTES = 128 * KS / 2;  // FP4 A stage in smem: BM rows x KS nibbles
+constexpr int A_SBO = KS / 32 * 128;          // FP4 A stage: byte stride between 8-row core-matrix groups
 constexpr int KC = 1024;       // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
 constexpr int B_SLOTS = 3;
@@ -294,7 +300,8 @@ struct Args {
     const uint32_t *raw;       // packed raw stream (MSB-first bytes) as words
     uint64_t n_blocks;
     uint32_t n, m;
-    uint32_t kst;              // K stages per tile = n / 128
+    uint32_t kst;              // K stages per tile = ceil(n / KS)
+    uint32_t k128;             // 128-bit raw chunks per block = n / 128
     uint32_t nchunks;          // B chunks per tile = ceil(kst / SPC)
     uint32_t n_mtiles, n_npairs;  // M tiles; pairs of N tiles (NT = 2 per work tile)
     const uint32_t *seed_words;  // logical big-endian seed words, zero padded
@@ -315,7 +322,7 @@ struct Args {
 // at kernel start: the per-tile lookup is on the MMA issuer's critical path).
 struct TLeaf {
     uint32_t tile_base, tile_end;  // work tiles [tile_base, tile_end) of this leaf
-    uint32_t prows, kst, r;        // rows per N pair, K stages, output rows
+    uint32_t prows, k128, r;       // rows per N pair, 128-bit input chunks (w / 128), output rows
     uint32_t seed_off;             // leaf seed (word offset in the plan's seed buffer)
     uint32_t x_off_src;            // input word offset | (1 << 31) when it is in the X workspace
     uint32_t out_off;              // word offset of the leaf parities in a block's Y row
@@ -329,7 +336,8 @@ __device__ __forceinline__ uint32_t div_mtiles(const Args &a, uint32_t x) {
 // Geometry of one work tile (M tile of BM blocks x up to NT*BN output rows).
 struct Tile {
     uint32_t mt, n0;           // M tile; first output row of the N pair
-    uint32_t kst, nchunks;     // K stages of 128, B chunks of KC
+    uint32_t kst, nchunks;     // K stages of KS (the last one zero-padded), B chunks of KC
+    uint32_t k128;             // 128-bit input chunks per block row
     uint32_t r;                // valid output rows of the product this tile belongs to
     uint32_t ntc, nlast;       // N tiles used (1..NT); N of the last one (multiple of 16)
     const uint32_t *seed;      // seed words of the product (smem in plain mode)
@@ -355,6 +363,7 @@ __device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s,
         ti.mt = t % a.n_mtiles;
         ti.n0 = (t / a.n_mtiles) * (NT * BN);
         ti.kst = a.kst;
+        ti.k128 = a.k128;
         ti.nchunks = a.nchunks;
         ti.r = a.m;
         ti.seed = seed_s;
@@ -368,7 +377,8 @@ __device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s,
         const uint32_t tl = t - L.tile_base, q = div_mtiles(a, tl);
         ti.mt = tl - q * a.n_mtiles;
         ti.n0 = q * L.prows;
-        ti.kst = L.kst;
+        ti.k128 = L.k128;
+        ti.kst = (L.k128 + KS128 - 1) / KS128;
         ti.nchunks = (ti.kst + SPC - 1) / SPC;
         ti.r = L.r;
         ti.seed = a.seed_words + L.seed_off;
@@ -435,7 +445,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             o.tile_base = L.npair_base * a.n_mtiles;
             o.tile_end = (L.npair_base + L.npairs) * a.n_mtiles;
             o.prows = L.pair_rows;
-            o.kst = L.w / KS;
+            o.k128 = L.w / 128;
             o.r = L.r;
             o.seed_off = L.seed_off;
             o.x_off_src = L.x_off | (L.x_src ? 0x80000000u : 0u);
@@ -513,9 +523,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                             if constexpr (FP4) {
                                 const uint32_t abase = smem_u32(a_ring + dslot[d] * A_STAGE_BYTES);
 #pragma unroll
-                                for (uint32_t kk = 0; kk < 2; ++kk) {
+                                for (uint32_t kk = 0; kk < KS / 64; ++kk) {
                                     const uint32_t koff = d * KS + kk * 64;
-                                    mma_mxf4_ss(tmem + ACC_COL0 + BN, desc_kmajor(abase + kk * 256, 128, 512),
+                                    mma_mxf4_ss(tmem + ACC_COL0 + BN, desc_kmajor(abase + kk * 256, 128, A_SBO),
                                                 desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
                                                 tmem + SF_COL, tmem + SF_COL + 8, (d | kk) != 0);
                                 }
@@ -540,9 +550,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     if constexpr (FP4) {
                         const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
 #pragma unroll
-                        for (uint32_t kk = 0; kk < 2; ++kk) {
+                        for (uint32_t kk = 0; kk < KS / 64; ++kk) {
                             const uint32_t koff = kin * KS + kk * 64;
-                            const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, 512);
+                            const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
                             mma_mxf4_ss(tmem + ACC_COL0, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128),
                                         ti.ntc == 1 ? idesc_last : idesc_full, tmem + SF_COL, tmem + SF_COL + 8,
                                         (ks | kk) != 0);
@@ -694,23 +704,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         // Branch-free prefetch: always load from a valid address (clamped block,
         // stale tile past the end) and keep a validity flag, so every ring slot
         // stays in its own registers and the load latency is really hidden.
-        auto load = [&](bool &v) -> uint4 {
+        // K is reversed: stage lks, half hf (128 K each) reads 128-bit chunk
+        // k128 - 1 - KS128 lks - hf of the block row (FP4: the second half of the
+        // last stage may lie before the row start -> zeros)
+        auto load = [&](bool &v, uint32_t hf) -> uint4 {
             const uint64_t b = (uint64_t)lti.mt * BM + row;
-            v = lt < ntiles && b < a.n_blocks;
+            const int32_t ci = (int32_t)lti.k128 - 1 - (int32_t)(KS128 * lks + hf);
+            v = lt < ntiles && b < a.n_blocks && ci >= 0;
 #if QRNG_GEMM_EXP == 3  // experiment 3: every lane reads block 0 (coalesced broadcast loads)
             const uint64_t bc = 0;
 #else
             const uint64_t bc = b < a.n_blocks ? b : a.n_blocks - 1;
 #endif
-            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (lti.kst - 1 - lks));
+            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (ci >= 0 ? ci : 0));
         };
         for (uint32_t i = 0; i < par; ++i) step1();
-        uint4 pf[PF];
-        bool ok[PF], vd[PF];
+        uint4 pf[PF], pf2[FP4 ? PF : 1];
+        bool ok[PF], vd[PF], vd2[FP4 ? PF : 1];
 #pragma unroll
         for (int j = 0; j < PF; ++j) {
             ok[j] = lt < ntiles;
-            pf[j] = load(vd[j]);
+            pf[j] = load(vd[j], 0);
+            if constexpr (FP4) pf2[j] = load(vd2[j], 1);
 #pragma unroll
             for (int i = 0; i < XF_PAR; ++i) step1();
         }
@@ -722,8 +737,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 if (more && !ok[j]) more = false;
                 if (more) {
                     const uint4 cur4 = vd[j] ? pf[j] : make_uint4(0, 0, 0, 0);
+                    uint4 cur4b = make_uint4(0, 0, 0, 0);
+                    if constexpr (FP4) cur4b = vd2[j] ? pf2[j] : make_uint4(0, 0, 0, 0);
                     ok[j] = lt < ntiles;
-                    pf[j] = load(vd[j]);
+                    pf[j] = load(vd[j], 0);
+                    if constexpr (FP4) pf2[j] = load(vd2[j], 1);
 #pragma unroll
                     for (int i = 0; i < XF_PAR; ++i) step1();
                     const uint32_t as = g % A_STAGES, aph = (g / A_STAGES) & 1;
@@ -735,12 +753,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                         // K group g (32 elements, K reversed) = memory word 3 - g, element c = bit c
                         // of its big-endian value: bit-reverse so that bit b holds element 31 - b
                         // as in the B rows, then the same nibble spread
-                        const uint32_t M4[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
-                        uint8_t *arow = a_ring + as * A_STAGE_BYTES + (row >> 3) * 512 + (row & 7) * 16;
+                        const uint32_t M4[8] = {cur4.x, cur4.y, cur4.z, cur4.w, cur4b.x, cur4b.y, cur4b.z, cur4b.w};
+                        uint8_t *arow = a_ring + as * A_STAGE_BYTES + (row >> 3) * A_SBO + (row & 7) * 16;
 #pragma unroll
-                        for (int gk = 0; gk < 4; ++gk)
+                        for (int gk = 0; gk < KS / 32; ++gk)
                             *reinterpret_cast<uint4 *>(arow + gk * 128) =
-                                e2m1_row(__brev(__byte_perm(M4[3 - gk], 0, 0x0123)));
+                                e2m1_row(__brev(__byte_perm(M4[(gk >> 2) * 4 + 3 - (gk & 3)], 0, 0x0123)));
                         fence_proxy_async();
                     } else {
                         xform_stage(lane_addr + A_COL0 + as * 32, cur4);
@@ -1685,6 +1703,8 @@ __global__ void __launch_bounds__(128, 1) mxf4_probe_kernel(const uint8_t *A, co
     }
 }
 
+int operand_bits() { return FP4 ? 4 : 8; }
+
 qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int K, int hi_first, cudaStream_t s) {
     if (N < 16 || N > 256 || N % 16 || K < 64 || K > 1024 || K % 64) {
         set_error("mxf4 probe: N in [16, 256] multiple of 16, K in [64, 1024] multiple of 64");
@@ -1705,7 +1725,7 @@ qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int 
 bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n; }
 
 uint32_t seed_words_needed(uint64_t n, uint64_t m) {
-    const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = n / KS, nchunks = (kst + SPC - 1) / SPC;
+    const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = (n + KS - 1) / KS, nchunks = (kst + SPC - 1) / SPC;
     uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
     // 2-SM kernel: 256-row tiles, the second CTA's half starts 128 rows later
     const uint64_t nt2 = (m + 255) / 256, pmax2 = (nt2 - 1) * 256 + 128 + (nchunks - 1) * KC + 8 * (KC / 8 + 16 - 1) + 7;
@@ -1781,7 +1801,8 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.n_blocks = n_blocks;
     a.n = (uint32_t)n;
     a.m = (uint32_t)m;
-    a.kst = (uint32_t)(n / KS);
+    a.kst = (uint32_t)((n + KS - 1) / KS);
+    a.k128 = (uint32_t)(n / 128);
     a.nchunks = (a.kst + SPC - 1) / SPC;
     a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
     a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)

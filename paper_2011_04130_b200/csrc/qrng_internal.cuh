@@ -149,6 +149,7 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
                     uint64_t m, const OutStream &out, cudaStream_t s);
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
 qrng_status trace(uint64_t *h_out, int reset);
+int operand_bits();  // 4: kind::mxf4 (E2M1), 8: kind::i8
 qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int K, int hi_first, cudaStream_t s);
 qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s);  // 16 cycle counters (-DQRNG_GEMM_TRACE builds)
 }  // namespace gemm
