@@ -109,7 +109,7 @@ void KernelTimer::stop() {
 }
 
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
-static uint64_t g_gemm_max_n = 1ull << 17;  // profiles/sweep_r1b.jsonl: Karatsuba GEMM 52.9 vs NTT 42.6 Gbit/s at 2^17, 28.4 vs 42.7 at 2^18
+static uint64_t g_gemm_max_n = 1ull << 18;  // profiles/sweep_r1h.jsonl (FP4 operands): Karatsuba GEMM 60.0 vs NTT 47.8 Gbit/s at 2^18, 33.9 vs 47.5 at 2^19
 static std::atomic<int> g_debug_path{QRNG_PATH_AUTO};
 // Karatsuba depth over the GEMM path: -1 = the planner's cost model, 0 = plain
 // GEMM kernel, d > 0 = split whenever allowed down to depth d (tests).
