@@ -763,6 +763,56 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_pack_kernel(const uint32
     }
 }
 
+// Gather form of the same combine + pack: one thread per output word, no
+// shared memory.  Output word w covers key bits [32w, 32w + 32): at most two
+// blocks; for each, the (one or two) key-row words the bits come from are
+// XORed straight from the leaf-parity rows in L2 as the CSR lists them
+// (neighbouring threads read neighbouring words, so the gathers coalesce).
+// Every output word has exactly one writer.
+__device__ __forceinline__ uint32_t csr_word(const uint32_t *__restrict__ csr, uint32_t ywords,
+                                             const uint32_t *__restrict__ yr, uint32_t q) {
+    // the first 8 terms with independent (predicated) loads, so the gathers of
+    // one word are in flight together; deeper trees loop over the rest
+    const uint32_t c = __ldg(csr + q);
+    uint32_t idx[8];
+#pragma unroll
+    for (uint32_t e = 0; e < 8; ++e) idx[e] = e < c ? __ldg(csr + ywords + e * ywords + q) : 0u;
+    uint32_t v = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < 8; ++e)
+        if (e < c) v ^= __ldg(yr + idx[e]);
+    for (uint32_t e = 8; e < c; ++e) v ^= __ldg(yr + __ldg(csr + ywords + e * ywords + q));
+    return v;
+}
+__global__ void __launch_bounds__(256) csr_gather_pack_kernel(const uint32_t *__restrict__ csr,
+                                                              const uint32_t *__restrict__ yws, uint32_t y_stride,
+                                                              uint64_t n_blocks, uint32_t m, uint64_t m_magic,
+                                                              OutStream out) {
+    const uint32_t ywords = (m + 31) / 32;
+    const uint64_t gbits = n_blocks * m, gwords = (gbits + 31) / 32;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < gwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t G = w * 32, end = min(G + 32, gbits);
+        uint64_t b = m_magic ? __umul64hi(G, m_magic) : G;  // G / m
+        uint32_t i = (uint32_t)(G - b * m);
+        uint64_t pos = G;
+        uint32_t word = 0;
+        while (pos < end) {
+            const uint32_t len = (uint32_t)min((uint64_t)(m - i), end - pos);  // 1..32 bits of block b
+            const uint32_t *yr = yws + b * y_stride;
+            const uint32_t q = i >> 5, sft = i & 31;
+            const uint32_t c0 = csr_word(csr, ywords, yr, q);
+            const uint32_t c1 = (sft && q + 1 < ywords) ? csr_word(csr, ywords, yr, q + 1) : 0u;
+            const uint32_t bits = sft ? ((c0 << sft) | (c1 >> (32 - sft))) : c0;
+            word |= (bits >> (32 - len)) << (32 - len - (uint32_t)(pos - G));
+            pos += len;
+            ++b;
+            i = 0;
+        }
+        emit_word(out, w, word, true);
+    }
+}
+
 // ---- host entry points -----------------------------------------------------
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s) {
     const Tables *t = nullptr;
@@ -859,7 +909,28 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
     while (bpc < 8 && csr_bytes(2 * bpc) <= 72 * 1024) bpc *= 2;
     const size_t csr_smem = csr_bytes(bpc);
     uint32_t *zws = nullptr;
-    if (st == QRNG_OK && csr_smem <= 200 * 1024) {
+    // gather form for long key rows (measured: config 3, 1434 words, 146.2 ->
+    // 149.7 Gbit/s); the staged form for short ones (config 2, 180 words: 477
+    // vs 459 -- the gather form is load-instruction bound there)
+    static const int gather_env = [] {
+        const char *e = getenv("QRNG_CSR_GATHER");
+        return e ? atoi(e) : -1;
+    }();
+    const bool gather = gather_env >= 0 ? gather_env != 0 : ywords >= 1024;
+    if (st == QRNG_OK && gather) {
+        // one thread per output word, gathers from L2 (no staging)
+        const uint64_t gwords = ((uint64_t)n_blocks * m + 31) / 32;
+        const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const uint64_t want = (gwords + 255) / 256, cap = (uint64_t)sms * 16;
+        KernelTimer tc(s, true, 1);
+        csr_gather_pack_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, s>>>(t->csr, yws, H.y_stride, n_blocks,
+                                                                                   (uint32_t)m, m_magic, out);
+        tc.stop();
+        if (cudaGetLastError() != cudaSuccess) { set_error("csr_gather_pack_kernel launch failed"); st = QRNG_E_CUDA; }
+    } else if (st == QRNG_OK && csr_smem <= 200 * 1024) {
         // flattened tree over bpc blocks of leaf parities in shared memory
         if (csr_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_pack_kernel));
         KernelTimer tc(s, true, 1);
