@@ -26,6 +26,7 @@
 // (C4).  Exactness: every step is a GF(2) identity and each leaf is exact
 // int32 accumulation followed by & 1.
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <map>
 #include <mutex>
@@ -54,17 +55,30 @@ static int auto_max_depth(uint64_t n) { return n >= (1u << 17) ? 6 : 5; }
 // tensor cores; per-tile pipeline overhead and the workspace traffic of the
 // input / parity combinations are expressed in the same unit (calibrated on
 // B200).
+// Fitted on the int8 kernel.  Re-checked on the E2M1 kernel (which does the
+// row x K work in about half the tensor time) with a full depth scan,
+// profiles/kara_depths_r1j.jsonl: the same constants pick the measured best
+// depth at 2^12, 2^13, 2^14, 2^16, 2^17, 2^18 and one level too deep at 2^15
+// (223 vs 232 Gbit/s); halving the MAC weight would pick d0 at 2^13 (-6%) and
+// d4 at 2^16 (-3.5%).  QRNG_KARA_MAC_WEIGHT overrides it for calibration.
 constexpr double kTileOverhead = 186e3;  // per work tile (pipeline fill, accumulator drain; ~3.6k SM clocks)
 constexpr double kPrepPerBit = 180.0;    // forming x0 ^ x1 in the workspace, per input bit
 constexpr double kLeafRow = 250.0;       // leaf parities written by the GEMM and read by the combine, per row
 constexpr double kCombPerRow = 0.0;      // internal node row written and read back, per row
+static double mac_weight() {
+    static const double w = [] {
+        const char *e = getenv("QRNG_KARA_MAC_WEIGHT");  // calibration override
+        return e ? atof(e) : 1.0;
+    }();
+    return w;
+}
 
 static double leaf_cost(uint32_t r, uint32_t w) {
     double c = kLeafRow * r;
     for (uint32_t n0 = 0; n0 < r; n0 += gemm::kTileRows) {
         const uint32_t left = std::min<uint32_t>(gemm::kTileRows, r - n0);
         const uint32_t rows = std::max<uint32_t>((left + 15) & ~15u, 128);  // A expansion floor
-        c += (double)rows * w + kTileOverhead;
+        c += mac_weight() * (double)rows * w + kTileOverhead;
     }
     return c;
 }
