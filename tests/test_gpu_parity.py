@@ -59,6 +59,8 @@ SMALL_CASES = [
     (32, 1, 1), (32, 31, 3), (64, 7, 5), (96, 50, 7), (128, 127, 2), (256, 200, 9),
     (512, 300, 33), (1024, 716, 17), (1024, 1, 4), (2048, 1433, 10), (4096, 2867, 5),
     (8192, 5734, 7), (16384, 11468, 3), (16384, 16383, 2), (12288, 8000, 5),
+    # odd multiples of 128: the E2M1 kernel's last 256-K stage is half zero-filled
+    (384, 300, 7), (1152, 806, 9), (2432, 1702, 5), (65408, 45785, 2),
 ]
 
 
@@ -75,7 +77,7 @@ def test_random_small(q, oracle_mod, path, n, m, B):
 
 
 @pytest.mark.parametrize("path", PATHS)
-@pytest.mark.parametrize("n,m,B", [(1024, 716, 3), (8192, 5734, 3), (16384, 11468, 2), (96, 95, 5)])
+@pytest.mark.parametrize("n,m,B", [(1024, 716, 3), (8192, 5734, 3), (16384, 11468, 2), (96, 95, 5), (1152, 806, 3)])
 def test_all_ones_max_window(q, oracle_mod, path, n, m, B):
     if path == "gemm" and n % 128:
         pytest.skip("GEMM path needs n % 128 == 0")
