@@ -179,9 +179,14 @@ QRNG_API void        qrng_plan_destroy(qrng_plan *plan);
  * (PAPER.md:257), plus the last m raw bits (k_i = k'_i + r_{i+1}):
  *     y_t = XOR_{j<n-m} a'[(n-m+t-j) mod n] AND r_j  XOR  r_{n-m+t},  0 <= t < m.
  * d_seed holds the n seed bits (C2); raw/out layouts, alignment and errors as
- * qrng_toeplitz_extract (n % 32 == 0, n - 1 <= 2^23).  Runs on the NTT path
- * (transform length 2^ceil(log2(n-1)) instead of 2^ceil(log2(n+m-1))).  The
- * plan works with qrng_plan_extract / qrng_plan_destroy. */
+ * qrng_toeplitz_extract (n % 32 == 0, n - 1 <= 2^23).  Path: the tensor-core
+ * path when n - m <= 2^16 (each block's first n - m bits repacked, zero
+ * prefixed, to a multiple of 128 bits; C1 product with seed bits a_2..a_n;
+ * then XOR of the last m raw bits), else the NTT path (transform length
+ * 2^ceil(log2(n-1)) instead of 2^ceil(log2(n+m-1))); qrng_debug_set_path
+ * forces either (GEMM with n - m > 2^16: QRNG_E_UNSUPPORTED).  The GEMM path
+ * allocates an n_blocks x (n-m rounded up to 128)/8-byte workspace per call
+ * (stream-ordered).  The plan works with qrng_plan_extract / qrng_plan_destroy. */
 QRNG_API qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uint8_t *d_seed,
                                                cudaStream_t stream, qrng_plan **plan);
 QRNG_API qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks,

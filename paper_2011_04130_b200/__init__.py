@@ -315,7 +315,7 @@ def toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=
 
 
 def modified_toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=None):
-    """Modified Toeplitz [T | I_m] with an n-bit seed (NTT path)."""
+    """Modified Toeplitz [T | I_m] with an n-bit seed (tensor-core path for n - m <= 2^16, else NTT)."""
     import torch
     _need_cuda_u8(raw, "raw")
     _need_cuda_u8(seed, "seed")

@@ -174,6 +174,7 @@ struct qrng_plan {
     uint64_t n = 0, m = 0;
     int path = QRNG_PATH_NTT;
     bool kara_on = false;  // GEMM path through the Karatsuba decomposition
+    bool modified = false;  // modified Toeplitz [T | I_m] (n-bit seed)
     ntt::Plan ntt;
     gemm::Plan gemm;
     kara::Plan kara;
@@ -280,7 +281,7 @@ qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info) {
         info->macs_per_block = macs;
     } else {
         info->leaves = 1;
-        info->macs_per_block = plan->n * plan->m;
+        info->macs_per_block = plan->modified ? (plan->n - plan->m + 127) / 128 * 128 * plan->m : plan->n * plan->m;
     }
     return QRNG_OK;
 }
@@ -329,8 +330,12 @@ qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uint8_t *d_s
     if (n % 32 != 0) { set_error("n must be a multiple of 32"); return QRNG_E_UNSUPPORTED; }
     if (n - 1 > (1ull << ntt::kMaxLogP)) { set_error("n - 1 exceeds 2^23"); return QRNG_E_UNSUPPORTED; }
     if (!d_seed || !aligned16(d_seed)) { set_error("d_seed is NULL or not 16-byte aligned"); return QRNG_E_INVALID; }
-    if (g_debug_path.load() == QRNG_PATH_GEMM) {
-        set_error("the modified Toeplitz runs on the NTT path only");
+    int want = g_debug_path.load();
+    const uint64_t kprod = (n - m + 127) / 128 * 128;  // GEMM product length (n - m rounded up to 128)
+    if (want == QRNG_PATH_AUTO) want = (gemm::modified_supported(n, m) && kprod <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
+    if (want == QRNG_PATH_GEMM && !gemm::modified_supported(n, m)) {
+        set_error("GEMM path: the modified Toeplitz needs n %% 32 == 0 and n - m <= 2^16 (n=%llu, m=%llu)",
+                  (unsigned long long)n, (unsigned long long)m);
         return QRNG_E_UNSUPPORTED;
     }
     qrng_status st = device_ready();
@@ -339,8 +344,10 @@ qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uint8_t *d_s
     if (!p) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
     p->n = n;
     p->m = m;
-    p->path = QRNG_PATH_NTT;
-    st = ntt::plan_init(p->ntt, n - m, m, d_seed, 1, true, stream);
+    p->path = want;
+    p->modified = true;
+    st = want == QRNG_PATH_GEMM ? gemm::plan_init_modified(p->gemm, n, m, d_seed, stream)
+                                : ntt::plan_init(p->ntt, n - m, m, d_seed, 1, true, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
     *plan = p;
     return QRNG_OK;
@@ -395,7 +402,8 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
     if (!(plan->path == QRNG_PATH_GEMM && plan->kara_on)) QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
     qrng_status st = (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->kara_on ? kara::extract(plan->kara, d_raw_bits, n_blocks, n, m, o, stream)
-                                     : gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream);
+                     : plan->modified ? gemm::extract_modified(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
+                                      : gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream);
     if (st == QRNG_OK && o.tail) {
         cudaError_t e = cudaMemcpyAsync(d_out + (out_bytes / 4) * 4, o.tail, out_bytes % 4,
                                         cudaMemcpyDeviceToDevice, stream);

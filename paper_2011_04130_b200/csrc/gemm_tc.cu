@@ -1738,17 +1738,74 @@ static size_t smem_bytes(uint32_t seed_words_n) {
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L
-__global__ void seed_words_kernel(const uint8_t *seed, uint64_t L, uint32_t *words, uint64_t nwords) {
+// seed bits [off, off + L) of an MSB-first byte buffer (off = 1 drops a_1 for
+// the modified Toeplitz) -> logical big-endian words, zero past L
+__global__ void seed_words_kernel(const uint8_t *seed, uint64_t L, uint32_t off, uint32_t *words, uint64_t nwords) {
+    const uint64_t nbytes = (off + L + 7) / 8;
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t v = 0;
-        for (int k = 0; k < 4; ++k) {
-            const uint64_t byte = w * 4 + k;
-            const uint32_t bv = (byte * 8 < L) ? seed[byte] : 0u;
-            v |= bv << (24 - 8 * k);
-        }
+        const uint64_t pos = off + w * 32, b0 = pos / 8;
+        uint64_t v40 = 0;  // 40 bits starting at byte b0
+        for (int k = 0; k < 5; ++k) v40 = (v40 << 8) | (b0 + k < nbytes ? seed[b0 + k] : 0u);
+        uint32_t v = (uint32_t)(v40 >> (8 - (pos & 7)));
         const uint64_t lo = w * 32;
         if (lo + 32 > L) v &= (L > lo) ? (0xFFFFFFFFu << (32 - (L - lo))) : 0u;
         words[w] = v;
+    }
+}
+
+// Modified Toeplitz on this path (api.cu): block b's product input is
+// x''_b = [0^pad | x_b[0, n')] (n' = n - m, pad = K - n', K = n' rounded up to
+// 128), so the product is a C1 extraction with n = K on a repacked copy; the
+// zeros meet seed positions whose values do not matter.  One thread per
+// 32-bit word of x'' (memory byte order, like the raw stream).
+__global__ void modified_repack_kernel(const uint32_t *raw, uint64_t n_blocks, uint32_t n, uint32_t nprime, uint32_t K,
+                                       uint32_t *xws) {
+    const uint32_t kw = K / 32, pad = K - nprime;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_blocks * kw;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i / kw;
+        const int32_t o = (int32_t)((uint32_t)(i - b * kw) * 32u) - (int32_t)pad;  // first bit of x_b in this word
+        const uint32_t *row = raw + b * (n / 32);
+        const int32_t w0 = o >= 0 ? o / 32 : -((31 - o) / 32);                      // floor(o / 32)
+        const uint32_t sh = (uint32_t)(o - 32 * w0);
+        const uint32_t hi = w0 >= 0 ? bswap32(__ldg(row + w0)) : 0u;
+        const uint32_t lo = (sh && w0 + 1 >= 0) ? bswap32(__ldg(row + w0 + 1)) : 0u;
+        uint32_t v = sh ? ((hi << sh) | (lo >> (32 - sh))) : hi;
+        xws[i] = bswap32(v);
+    }
+}
+
+// y ^= the block's last m raw bits: output bit b m + i takes raw bit b n + n' + i.
+// One thread per logical output word; the final partial word lives in the tail scratch.
+__global__ void modified_xor_tail_kernel(const uint32_t *raw, uint64_t n_blocks, uint32_t n, uint32_t m,
+                                         uint64_t m_magic, OutStream out) {
+    const uint32_t nprime = n - m;
+    const uint64_t gbits = n_blocks * m, gwords = (gbits + 31) / 32;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < gwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t G = w * 32, end = min(G + 32, gbits);
+        uint64_t b = m_magic ? __umul64hi(G, m_magic) : G;  // G / m
+        uint32_t i = (uint32_t)(G - b * m);
+        uint64_t pos = G;
+        uint32_t word = 0;
+        while (pos < end) {
+            const uint32_t len = (uint32_t)min((uint64_t)(m - i), end - pos);  // 1..32 bits of block b
+            const uint64_t rb = b * n + nprime + i;                            // raw bit of y_i
+            const uint64_t wi = rb >> 5;
+            const uint32_t sh = (uint32_t)(rb & 31);
+            const uint32_t hi = bswap32(__ldg(raw + wi));
+            const uint32_t lo = (sh && len > 32 - sh) ? bswap32(__ldg(raw + wi + 1)) : 0u;  // inside block b
+            const uint32_t bits = sh ? ((hi << sh) | (lo >> (32 - sh))) : hi;
+            word |= (bits >> (32 - len)) << (32 - len - (uint32_t)(pos - G));
+            pos += len;
+            ++b;
+            i = 0;
+        }
+        if (w >= out.full_words) {
+            if (word) atomicXor(out.tail, bswap32(word));
+        } else {
+            out.words[w] ^= bswap32(word);
+        }
     }
 }
 
@@ -1760,7 +1817,7 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, c
     pl.seed_words_n = seed_words_needed(n, m);
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.seed_words, pl.seed_words_n * 4, s));
     count_launch();
-    seed_words_kernel<<<(unsigned)((pl.seed_words_n + 255) / 256), 256, 0, s>>>(d_seed, n + m - 1, pl.seed_words,
+    seed_words_kernel<<<(unsigned)((pl.seed_words_n + 255) / 256), 256, 0, s>>>(d_seed, n + m - 1, 0, pl.seed_words,
                                                                               pl.seed_words_n);
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
@@ -1874,6 +1931,68 @@ qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, 
     umma_probe_kernel<<<1, 128, smem, s>>>(A, h, D, N, K);
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
+}
+
+bool modified_supported(uint64_t n, uint64_t m) {
+    if (m == 0 || m >= n || n % 32) return false;
+    const uint64_t K = (n - m + 127) / 128 * 128;
+    return K <= MAX_N;
+}
+
+// Modified Toeplitz (api.cu): the C1 product with n = K (n' = n - m rounded up
+// to 128) of the repacked inputs, seed bits a_2 .. a_n (offset 1, n - 1 bits),
+// zero beyond -- the prepended zero inputs meet seed positions >= n - 1 or
+// values that do not matter.
+qrng_status plan_init_modified(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s) {
+    if (!modified_supported(n, m)) {
+        set_error("GEMM path: unsupported modified Toeplitz n=%llu m=%llu", (unsigned long long)n, (unsigned long long)m);
+        return QRNG_E_UNSUPPORTED;
+    }
+    const uint64_t K = (n - m + 127) / 128 * 128;
+    pl.seed_words_n = seed_words_needed(K, m);
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.seed_words, pl.seed_words_n * 4, s));
+    count_launch();
+    seed_words_kernel<<<(unsigned)((pl.seed_words_n + 255) / 256), 256, 0, s>>>(d_seed, n - 1, 1, pl.seed_words,
+                                                                              pl.seed_words_n);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+qrng_status extract_modified(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                             const OutStream &out, cudaStream_t s) {
+    const uint64_t nprime = n - m, K = (nprime + 127) / 128 * 128;
+    uint32_t *xws = nullptr;
+    const size_t xbytes = (size_t)n_blocks * (K / 8);
+    QRNG_CUDA_TRY(cudaMallocAsync(&xws, xbytes, s));
+    int dev = 0, sms = 148;
+    QRNG_CUDA_TRY(cudaGetDevice(&dev));
+    QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const auto grid_for = [&](uint64_t items) {
+        const uint64_t want = (items + 255) / 256, cap = (uint64_t)sms * 16;
+        return (unsigned)(want < cap ? want : cap);
+    };
+    const uint32_t *raw = reinterpret_cast<const uint32_t *>(d_raw);
+    {
+        KernelTimer t(s, true, 1);
+        modified_repack_kernel<<<grid_for(n_blocks * (K / 32)), 256, 0, s>>>(raw, n_blocks, (uint32_t)n,
+                                                                             (uint32_t)nprime, (uint32_t)K, xws);
+        t.stop();
+    }
+    cudaError_t e = cudaGetLastError();
+    qrng_status st = e == cudaSuccess ? extract(pl, reinterpret_cast<const uint8_t *>(xws), n_blocks, K, m, out, s)
+                                      : QRNG_E_CUDA;
+    if (e != cudaSuccess) set_error("modified_repack_kernel: %s", cudaGetErrorString(e));
+    if (st == QRNG_OK) {
+        const uint64_t gwords = (n_blocks * m + 31) / 32;
+        const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
+        KernelTimer t(s, true, 1);
+        modified_xor_tail_kernel<<<grid_for(gwords), 256, 0, s>>>(raw, n_blocks, (uint32_t)n, (uint32_t)m, m_magic, out);
+        t.stop();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { set_error("modified_xor_tail_kernel: %s", cudaGetErrorString(e)); st = QRNG_E_CUDA; }
+    }
+    cudaFreeAsync(xws, s);
+    return st;
 }
 
 }  // namespace gemm

@@ -144,6 +144,12 @@ qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t to
                             cudaStream_t s);
 bool supported(uint64_t n, uint64_t m);
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
+// modified Toeplitz [T | I_m] (n-bit seed): repack x_b[0, n-m) to a multiple of
+// 128 bits, the C1 product, then XOR the last m raw bits (api.cu)
+bool modified_supported(uint64_t n, uint64_t m);
+qrng_status plan_init_modified(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
+qrng_status extract_modified(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                             const OutStream &out, cudaStream_t s);
 void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
