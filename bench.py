@@ -208,7 +208,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def step():
-        if modified:  # [T | I_m] with an n-bit seed, NTT path
+        if modified:  # [T | I_m] with an n-bit seed
             q.modified_toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
         else:
             q.toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
@@ -375,7 +375,8 @@ def run_ours(args):
             "u8 bits; E2M1 0/1 x E2M1 -> fp32 tensor core (kind::mxf4, unit scales, exact)"
             if q.gemm_operand_bits() == 4 else "u8 bits; int8 x int8 -> int32 tensor core"),
         "data": "synthetic: uint8 ADC samples clip(rint(N(128,sigma^2))) from PCG64 (qrng_synth); seeded uniform seed",
-        "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_per_gpu": B, "seed_bits": w.seed_bits,
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_per_gpu": B,
+                   "seed_bits": w.n if modified else w.seed_bits,
                    "raw_bits_per_gpu": w.raw_bits, "path": {1: "gemm", 2: "ntt"}[path],
                    "two_blocks_per_transform": bool(pack and path == 2),
                    "karatsuba_depth": pinfo["karatsuba_depth"] if path == 1 else None,
@@ -390,16 +391,17 @@ def run_ours(args):
     if entropy_info:
         line["config"]["minentropy"] = entropy_info
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = cpu_baseline(w, budget_s=args.cpu_budget, modified=modified)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
-def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0):
-    """The oracle as it stands (word mode, OpenMP over blocks) on a bounded
-    sample of the same workload: consecutive blocks until ~budget_s."""
+def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modified: bool = False):
+    """The oracle as it stands (word mode, OpenMP over blocks; the modified
+    variant: its literal loop) on a bounded sample of the same workload:
+    consecutive blocks until ~budget_s."""
     import oracle
     oracle.build()
     if threads == 0:
@@ -407,13 +409,18 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0):
     cores = threads
     sample_blocks = min(w.n_blocks, 4096)
     raw, seed = S.workload_inputs(w, 0, sample_blocks)
+    if modified:
+        seed = S.uniform_bits(w.key, w.n, tag=9)
     blocks_done, t_total, nb, pos = 0, 0.0, max(1, min(cores, sample_blocks)), 0
     while t_total < budget_s:
         if pos + nb > sample_blocks:  # cycle over the sample
             pos = 0
         chunk = raw[pos * w.n // 8:(pos + nb) * w.n // 8]
         t0 = time.perf_counter()
-        oracle.extract(chunk, nb, w.n, w.m, seed, "words", threads)
+        if modified:
+            oracle.modified_extract(chunk, nb, w.n, w.m, seed, threads)
+        else:
+            oracle.extract(chunk, nb, w.n, w.m, seed, "words", threads)
         t_total += time.perf_counter() - t0
         blocks_done += nb
         pos += nb
@@ -421,8 +428,9 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0):
             nb = min(nb * 2, sample_blocks)
     return {"value": blocks_done * w.n / t_total / 1e9, "unit": "Gbit/s", "cores": cores,
             "kind": "oracle", "sample": f"{blocks_done} blocks (cycling over the first {sample_blocks} of "
-                                        f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, word-parallel "
-                                        f"mode, OpenMP over blocks"}
+                                        f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, "
+                                        + ("modified Toeplitz literal loop" if modified else "word-parallel mode")
+                                        + ", OpenMP over blocks"}
 
 
 def run_reference(args):
