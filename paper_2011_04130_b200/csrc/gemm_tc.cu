@@ -45,13 +45,6 @@ constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
 // operands in shared memory, FP32 accumulators (exact: every product is 0 or 1
 // and every partial sum an integer <= n <= 2^16 < 2^24), twice the int8 MMA
 // rate.  Otherwise kind::i8 with A in TMEM and S32 accumulators.
-#ifndef QRNG_GEMM_FP4
-#if QRNG_GEMM_2CTA
-#define QRNG_GEMM_FP4 0  // the 2-SM variant is int8 only
-#else
-#define QRNG_GEMM_FP4 1
-#endif
-#endif
 constexpr bool FP4 = QRNG_GEMM_FP4 != 0;
 constexpr int KS = FP4 ? 256 : 128;  // K per A stage (FP4: 4 MMAs of K64 per N tile per stage)
 constexpr int KS128 = KS / 128;      // 128-bit raw chunks per A stage
@@ -998,15 +991,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #if QRNG_GEMM_2CTA
 namespace two {
 constexpr int BM2 = 256, BH = 128;          // blocks per tile, per CTA
-constexpr int BN2 = 256;                    // output rows per tile (N of one MMA)
-constexpr int A2_STAGES = 4;                // A ring in shared memory (16 KB each)
-constexpr int A2_BYTES = BH * KS;           // 128 rows x 128 K-bytes
+// FP4 (kind::mxf4): 224-row tiles (whole 32-bit words, so leaf parities stay
+// word aligned) so that two FP32 accumulator sets (448 columns) and the
+// scale-factor columns fit in TMEM; 512-K stages (8 MMAs per handshake)
+constexpr int BN2 = FP4 ? 224 : 256;        // output rows per tile (N of one MMA)
+constexpr int KS2 = FP4 ? 512 : KS;         // K per A stage
+constexpr int KS2_128 = KS2 / 128;
+constexpr int SPC2 = KC / KS2;              // A stages per B chunk
+constexpr int A2_STAGES = FP4 ? 3 : 4;      // A ring in shared memory
+constexpr int A2_BYTES = FP4 ? BH * KS2 / 2 : BH * KS;  // 128 rows x the stage's K (nibbles / bytes)
+constexpr int A2_SBO = FP4 ? KS2 / 32 * 128 : 1024;     // bytes between 8-row core-matrix groups
+constexpr uint32_t SF2_COL = 2 * BN2;       // FP4: unit block scales after the two accumulator sets
+static_assert(!FP4 || 2 * BN2 + 16 <= (int)TMEM_COLS, "TMEM budget (2-SM)");
+constexpr int PF2 = FP4 ? 2 : PF;           // transform prefetch depth (stages)
 constexpr int CM2 = KC / 8 + (BN2 / 2) / 8 - 1;  // core matrices per B chunk per CTA
 constexpr int CHUNK2_BYTES = CM2 * 128;
 constexpr int W2_MMA = 0, W2_BGEN0 = 1, N2_BGEN = 3, W2_XF0 = 4, N2_XF = 8, W2_EPI0 = 12, N2_EPI = 8;
 constexpr int NTHREADS2 = 20 * 32;
 constexpr int XF2_PAR = 2;                  // transform warps per 32-row quarter, alternating stages
-static_assert(kTileRows == BN2, "leaf tables assume 256 rows per work tile");
+static_assert(kTileRows == BN2, "leaf tables assume BN2 rows per work tile");
 
 __device__ __forceinline__ uint32_t cta_rank() {
     uint32_t r;
@@ -1033,6 +1036,14 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, uint32_t parity) 
             : "=r"(done) : "r"(a), "r"(parity) : "memory");
     } while (!done);
 }
+__device__ __forceinline__ void mma2_mxf4_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+        : "memory");
+}
 __device__ __forceinline__ void mma2_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
     asm volatile(
@@ -1053,6 +1064,7 @@ __device__ __forceinline__ void mma2_commit_both(uint64_t *bar) {
 
 struct Tile2 {
     uint32_t mt, n0, kst, nchunks, r, ntile;  // ntile: rows of this tile (N, multiple of 16)
+    uint32_t k128;                            // 128-bit input chunks per block row
     const uint32_t *seed, *xb;
     uint32_t xs, out_off;
 };
@@ -1062,7 +1074,8 @@ __device__ __forceinline__ Tile2 tile2_info(const Args &a, const uint32_t *seed_
     Tile2 ti;
     uint32_t tl;
     if (!GROUPED) {
-        ti.kst = a.kst;
+        ti.k128 = a.n / 128;
+        ti.kst = (ti.k128 + KS2_128 - 1) / KS2_128;
         ti.r = a.m;
         ti.seed = seed_s;
         ti.xb = a.raw;
@@ -1074,7 +1087,8 @@ __device__ __forceinline__ Tile2 tile2_info(const Args &a, const uint32_t *seed_
             ++cur;
         const Leaf &L = a.leaves[cur];
         tl = t - __ldg(&L.npair_base) * a.n_mtiles;
-        ti.kst = __ldg(&L.w) / KS;
+        ti.k128 = __ldg(&L.w) / 128;
+        ti.kst = (ti.k128 + KS2_128 - 1) / KS2_128;
         ti.r = __ldg(&L.r);
         ti.seed = a.seed_words + __ldg(&L.seed_off);
         if (__ldg(&L.x_src) == 0) { ti.xb = a.raw + __ldg(&L.x_off); ti.xs = a.n >> 5; }
@@ -1083,7 +1097,7 @@ __device__ __forceinline__ Tile2 tile2_info(const Args &a, const uint32_t *seed_
     }
     ti.mt = tl % a.n_mtiles;
     ti.n0 = (tl / a.n_mtiles) * BN2;
-    ti.nchunks = (ti.kst + SPC - 1) / SPC;
+    ti.nchunks = (ti.kst + SPC2 - 1) / SPC2;
     const uint32_t left = ti.r > ti.n0 ? min((uint32_t)BN2, ti.r - ti.n0) : 16u;
     ti.ntile = (left + 15) & ~15u;
     return ti;
@@ -1126,6 +1140,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
     cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (FP4) {
+        // unit block scales (UE8M0 127) in this CTA's scale-factor columns
+        if (warp >= W2_EPI0 && warp < W2_EPI0 + 4) {
+            uint32_t v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = 0x7F7F7F7Fu;
+            tmem_st16(tmem + (((uint32_t)(warp & 3) * 32) << 16) + SF2_COL, v);
+            tmem_wait_st();
+        }
+        tc_fence_before();
+        cluster_sync();
+        tc_fence_after();
+    }
     const uint32_t pair = blockIdx.x >> 1, npairs_grid = gridDim.x >> 1;
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: N tiles of 256 rows (total over leaves)
     uint32_t cur = 0;
@@ -1135,12 +1162,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
             for (uint32_t t = pair; t < ntiles; t += npairs_grid, ++it) {
                 const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
-                const uint32_t idesc = idesc_i8(BM2, (int)ti.ntile);
+                const uint32_t idesc = FP4 ? idesc_mxf4(BM2, (int)ti.ntile) : idesc_i8(BM2, (int)ti.ntile);
                 const uint32_t ab = it & 1, acc = ab * BN2;
                 mbar_wait_cluster(&acc_empty[ab], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (uint32_t ks = 0; ks < ti.kst; ++ks) {
-                    const uint32_t kin = ks % SPC;
+                    const uint32_t kin = ks % SPC2;
                     if (kin == 0) {
                         mbar_wait_cluster(&b_full[bs], bph);
                         tc_fence_after();
@@ -1150,20 +1177,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
                     const uint32_t abase = smem_u32(abuf + as * A2_BYTES);
                     const uint32_t cbase = smem_u32(chunks + bs * CHUNK2_BYTES);
                     if (elect_one()) {
+                        if constexpr (FP4) {
 #pragma unroll
-                        for (uint32_t kk = 0; kk < 4; ++kk) {
-                            // A: core matrix (row group g, K chunk q) at g*1024 + q*128: SBO 1024, LBO 128
-                            const uint64_t adesc = desc_kmajor(abase + kk * 2 * 128, 128, 1024);
-                            const uint32_t koff = kin * KS + kk * 32;
-                            const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
-                            mma2_i8_ss(tmem + acc, adesc, bdesc, idesc, (ks | kk) != 0);
+                            for (uint32_t kk = 0; kk < KS2 / 64; ++kk) {
+                                // A: core matrix (row group g, K group q of 32) at g*A2_SBO + q*128
+                                const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A2_SBO);
+                                const uint32_t koff = kin * KS2 + kk * 64;
+                                const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 512, 128);
+                                mma2_mxf4_ss(tmem + acc, adesc, bdesc, idesc, tmem + SF2_COL, tmem + SF2_COL + 8,
+                                             (ks | kk) != 0);
+                            }
+                        } else {
+#pragma unroll
+                            for (uint32_t kk = 0; kk < 4; ++kk) {
+                                // A: core matrix (row group g, K chunk q) at g*1024 + q*128: SBO 1024, LBO 128
+                                const uint64_t adesc = desc_kmajor(abase + kk * 2 * 128, 128, 1024);
+                                const uint32_t koff = kin * KS + kk * 32;
+                                const uint64_t bdesc = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
+                                mma2_i8_ss(tmem + acc, adesc, bdesc, idesc, (ks | kk) != 0);
+                            }
                         }
                         mma2_commit_both(&a_empty[as]);
-                        if (kin == SPC - 1 || ks == ti.kst - 1) mma2_commit_both(&b_empty[bs]);
+                        if (kin == SPC2 - 1 || ks == ti.kst - 1) mma2_commit_both(&b_empty[bs]);
                     }
                     __syncwarp();
                     if (++as == A2_STAGES) { as = 0; aph ^= 1; }
-                    if (kin == SPC - 1 || ks == ti.kst - 1) {
+                    if (kin == SPC2 - 1 || ks == ti.kst - 1) {
                         if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
                     }
                 }
@@ -1203,10 +1242,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
                     else { w0 = ti.seed[p >> 5]; w1 = ti.seed[(p >> 5) + 1]; }
                     const uint32_t v = __funnelshift_l(w1, w0, p & 31);
                     uint4 o;
-                    o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
-                    o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
-                    o.z = prmt_sign<0xFEBA>(v << 3, v << 2);
-                    o.w = prmt_sign<0xFEBA>(v << 1, v);
+                    if constexpr (FP4) {
+                        o = e2m1_row(v);
+                    } else {
+                        o.x = prmt_sign<0xFEBA>(v << 7, v << 6);
+                        o.y = prmt_sign<0xFEBA>(v << 5, v << 4);
+                        o.z = prmt_sign<0xFEBA>(v << 3, v << 2);
+                        o.w = prmt_sign<0xFEBA>(v << 1, v);
+                    }
                     *reinterpret_cast<uint4 *>(cb + (r >> 3) * 128 + (r & 7) * 16) = o;
                 }
                 fence_proxy_async();
@@ -1232,19 +1275,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
                 if (lt < ntiles) lti = tile2_info<GROUPED>(a, seed_s, lt, lcur);
             }
         };
-        auto load = [&](bool &v) -> uint4 {
+        // K reversed: stage lks, part hf (128 K each) is 128-bit chunk
+        // k128 - 1 - KS2_128 lks - hf of the block row (zeros before the row start)
+        auto load = [&](bool &v, uint32_t hf) -> uint4 {
             const uint64_t b = (uint64_t)lti.mt * BM2 + rank * BH + row;
-            v = lt < ntiles && b < a.n_blocks;
+            const int32_t ci = (int32_t)lti.k128 - 1 - (int32_t)(KS2_128 * lks + hf);
+            v = lt < ntiles && b < a.n_blocks && ci >= 0;
             const uint64_t bc = b < a.n_blocks ? b : a.n_blocks - 1;
-            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (lti.kst - 1 - lks));
+            return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (ci >= 0 ? ci : 0));
         };
         for (uint32_t i = 0; i < par; ++i) step1();
-        uint4 pf[PF];
-        bool ok[PF], vd[PF];
+        uint4 pf[PF2][KS2_128];
+        bool ok[PF2], vd[PF2][KS2_128];
 #pragma unroll
-        for (int j = 0; j < PF; ++j) {
+        for (int j = 0; j < PF2; ++j) {
             ok[j] = lt < ntiles;
-            pf[j] = load(vd[j]);
+#pragma unroll
+            for (int hf = 0; hf < KS2_128; ++hf) pf[j][hf] = load(vd[j][hf], hf);
 #pragma unroll
             for (int i = 0; i < XF2_PAR; ++i) step1();
         }
@@ -1252,12 +1299,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
         bool more = true;
         while (more) {
 #pragma unroll
-            for (int j = 0; j < PF; ++j) {
+            for (int j = 0; j < PF2; ++j) {
                 if (more && !ok[j]) more = false;
                 if (more) {
-                    const uint4 cur4 = vd[j] ? pf[j] : make_uint4(0, 0, 0, 0);
+                    const uint4 cur4 = vd[j][0] ? pf[j][0] : make_uint4(0, 0, 0, 0);
                     const uint32_t as = g % A2_STAGES, aph = (g / A2_STAGES) & 1;
                     mbar_wait(&a_empty[as], aph ^ 1);
+                    if constexpr (FP4) {
+                        // 16 core-matrix rows of 32 E2M1 elements: K group gk of the stage is
+                        // word 3 - (gk & 3) of 128-bit part gk / 4 (same slot order as B)
+                        uint8_t *dst = abuf + as * A2_BYTES + (row >> 3) * A2_SBO + (row & 7) * 16;
+#pragma unroll
+                        for (int hf = 0; hf < KS2_128; ++hf) {
+                            const uint4 c4 = vd[j][hf] ? pf[j][hf] : make_uint4(0, 0, 0, 0);
+                            const uint32_t M4[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                *reinterpret_cast<uint4 *>(dst + (hf * 4 + q) * 128) =
+                                    e2m1_row(__brev(__byte_perm(M4[3 - q], 0, 0x0123)));
+                        }
+                    } else {
                     // expand the 16 raw bytes (same K order as the 1-SM kernel's TMEM stage)
                     const uint32_t M[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
                     uint8_t *dst = abuf + as * A2_BYTES + (row >> 3) * 1024 + (row & 7) * 16;
@@ -1279,12 +1340,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
                         *reinterpret_cast<uint4 *>(dst + G0 * 128) = lo;
                         *reinterpret_cast<uint4 *>(dst + (G0 + 1) * 128) = hi;
                     }
+                    }
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(rank == 0 ? &a_full[as] : &a_local[as]);
                     // refill this ring slot after the arrive
                     ok[j] = lt < ntiles;
-                    pf[j] = load(vd[j]);
+#pragma unroll
+                    for (int hf = 0; hf < KS2_128; ++hf) pf[j][hf] = load(vd[j][hf], hf);
 #pragma unroll
                     for (int i = 0; i < XF2_PAR; ++i) step1();
                     g += XF2_PAR;
@@ -1302,16 +1365,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
             const Tile2 ti = tile2_info<GROUPED>(a, seed_s, t, cur);
             mbar_wait(&acc_full[ab], it & 1);
             tc_fence_after();
-            uint32_t words[BN2 / 32];
+            constexpr int NW2 = (BN2 + 31) / 32;
+            uint32_t words[NW2];
 #pragma unroll
-            for (int c = 0; c < BN2 / 32; ++c) {
+            for (int c = 0; c < NW2; ++c) {
                 uint32_t w = 0;
                 if ((uint32_t)(32 * c) < ti.ntile) {
                     uint32_t v[32];
-                    tmem_ld32(lane_addr + 32 * c, v);
+                    tmem_ld32(lane_addr + 32 * c, v);  // FP4: the last load runs past BN2 (masked below)
                     tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) w = (w << 1) | (v[k] & 1u);
+                    for (int k = 0; k < 32; ++k)
+                        w = (w << 1) | (FP4 ? (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u) : (v[k] & 1u));
                 }
                 words[c] = w;
             }
@@ -1321,9 +1386,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
             const uint64_t b = (uint64_t)ti.mt * BM2 + rank * BH + row;
             const uint32_t n0 = ti.n0;
             if (b >= a.n_blocks || n0 >= ti.r) continue;
-            const uint32_t nvalid = min((uint32_t)BN2, ti.r - n0);
+            const uint32_t nvalid = min(min((uint32_t)BN2, ti.ntile), ti.r - n0);
 #pragma unroll
-            for (int c = 0; c < BN2 / 32; ++c) {
+            for (int c = 0; c < NW2; ++c) {
                 const int vb = (int)nvalid - 32 * c;
                 if (vb <= 0) words[c] = 0;
                 else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
@@ -1331,7 +1396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
             if (GROUPED) {
                 uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
 #pragma unroll
-                for (int c = 0; c < BN2 / 32; ++c)
+                for (int c = 0; c < NW2; ++c)
                     if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
                 continue;
             }
@@ -1340,8 +1405,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS2, 1) toepli
             const uint64_t W0 = G_lo >> 5;
             uint32_t prev = 0;
 #pragma unroll
-            for (int c = 0; c <= BN2 / 32; ++c) {
-                const uint32_t cw = (c < BN2 / 32) ? words[c] : 0u;
+            for (int c = 0; c <= NW2; ++c) {
+                const uint32_t cw = (c < NW2) ? words[c] : 0u;
                 const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
                 prev = cw;
                 const uint64_t W = W0 + c;
@@ -1728,7 +1793,8 @@ uint32_t seed_words_needed(uint64_t n, uint64_t m) {
     const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = (n + KS - 1) / KS, nchunks = (kst + SPC - 1) / SPC;
     uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
     // 2-SM kernel: 256-row tiles, the second CTA's half starts 128 rows later
-    const uint64_t nt2 = (m + 255) / 256, pmax2 = (nt2 - 1) * 256 + 128 + (nchunks - 1) * KC + 8 * (KC / 8 + 16 - 1) + 7;
+    const uint64_t T2 = QRNG_GEMM_FP4 ? 224 : 256;  // 2-SM tile rows (kTileRows of a -DQRNG_GEMM_2CTA build)
+    const uint64_t nt2 = (m + T2 - 1) / T2, pmax2 = (nt2 - 1) * T2 + T2 / 2 + (nchunks - 1) * KC + 8 * (KC / 8 + T2 / 16 - 1) + 7;
     if (pmax2 > pmax) pmax = pmax2;
     return (uint32_t)(pmax / 32 + 2);
 }

@@ -130,8 +130,15 @@ struct Leaf {
 #ifndef QRNG_GEMM_2CTA
 #define QRNG_GEMM_2CTA 0  // 1: the cta_group::2 kernel (256 x 256 tiles, A in smem, double-buffered accumulators)
 #endif
+#ifndef QRNG_GEMM_FP4
 #if QRNG_GEMM_2CTA
-constexpr int kTileRows = 256;  // output rows per work tile of the 2-SM kernel
+#define QRNG_GEMM_FP4 0  // 2-SM variant: int8 unless -DQRNG_GEMM_FP4=1
+#else
+#define QRNG_GEMM_FP4 1  // tcgen05 kind::mxf4 operands (gemm_tc.cu)
+#endif
+#endif
+#if QRNG_GEMM_2CTA
+constexpr int kTileRows = QRNG_GEMM_FP4 ? 224 : 256;  // output rows per work tile of the 2-SM kernel
 #else
 constexpr int kTileRows = QRNG_GEMM_BN * QRNG_GEMM_NT;  // output rows per work tile (NT * BN)
 #endif
