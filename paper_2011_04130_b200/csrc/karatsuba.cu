@@ -777,6 +777,96 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_pack_kernel(const uint32
     }
 }
 
+// Streaming form of the staged combine + pack: a persistent grid, each CTA
+// walks groups of bpc blocks; a group's leaf-parity rows are one contiguous
+// range of the workspace and arrive by a single TMA bulk copy
+// (cp.async.bulk, mbarrier completion) into one of two shared buffers, so the
+// next group's rows are in flight while this group is combined and packed.
+__device__ __forceinline__ uint32_t ksmem(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const uint32_t *csr, uint32_t csr_words,
+                                                                           const uint32_t *yws, uint32_t y_stride,
+                                                                           uint64_t n_blocks, uint32_t m, uint32_t bpc,
+                                                                           OutStream out) {
+    extern __shared__ uint4 sm4[];
+    const uint32_t ywords = (m + 31) / 32, rwords = ywords + 1;
+    const uint32_t ybuf_words = bpc * y_stride;
+    uint32_t *Y0 = reinterpret_cast<uint32_t *>(sm4);
+    uint32_t *Rs = Y0 + 2 * ybuf_words;
+    uint32_t *Cs = Rs + bpc * rwords;
+    const uint32_t bar_off = (2 * ybuf_words + bpc * rwords + csr_words + 1) & ~1u;  // 8-byte aligned
+    uint64_t *bar = reinterpret_cast<uint64_t *>(Y0 + bar_off);
+    const uint64_t n_groups = (n_blocks + bpc - 1) / bpc;
+    auto issue = [&](uint64_t g, uint32_t buf) {  // one thread
+        const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - g * bpc);
+        const uint32_t bytes = nb * y_stride * 4;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ksmem(bar + buf)), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                ksmem(Y0 + buf * ybuf_words)),
+            "l"(yws + g * bpc * y_stride), "r"(bytes), "r"(ksmem(bar + buf))
+            : "memory");
+    };
+    for (uint32_t i = threadIdx.x; i < csr_words; i += blockDim.x) Cs[i] = __ldg(csr + i);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar + 1)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (blockIdx.x < n_groups) issue(blockIdx.x, 0);
+        if (blockIdx.x + gridDim.x < n_groups) issue(blockIdx.x + gridDim.x, 1);
+    }
+    __syncthreads();
+    uint32_t k = 0;
+    for (uint64_t g = blockIdx.x; g < n_groups; g += gridDim.x, ++k) {
+        const uint32_t buf = k & 1, ph = (k >> 1) & 1;
+        {
+            uint32_t done = 0;
+            do {
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(done) : "r"(ksmem(bar + buf)), "r"(ph) : "memory");
+            } while (!done);
+        }
+        const uint64_t b0 = g * bpc;
+        const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
+        const uint32_t *Ys = Y0 + buf * ybuf_words;
+        for (uint32_t idx = threadIdx.x; idx < nb * rwords; idx += blockDim.x) {
+            const uint32_t bl = idx / rwords, j = idx - bl * rwords;
+            uint32_t v = 0;
+            if (j < ywords) {
+                const uint32_t *yr = Ys + bl * y_stride;
+                for (uint32_t e = 0, c = Cs[j]; e < c; ++e) v ^= yr[Cs[ywords + e * ywords + j]];
+            }
+            Rs[idx] = v;
+        }
+        __syncthreads();  // Rs complete; this buffer's rows are no longer read
+        if (threadIdx.x == 0 && g + 2 * (uint64_t)gridDim.x < n_groups) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(g + 2 * (uint64_t)gridDim.x, buf);
+        }
+        const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
+        for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
+            const uint32_t G = w * 32, end = min(G + 32, gbits);
+            uint32_t b = G / m, i = G - b * m, pos = G, word = 0;
+            while (pos < end) {
+                const uint32_t len = min(m - i, end - pos);  // 1..32 bits of block b
+                const uint32_t *row = Rs + b * rwords;
+                const uint32_t q = i >> 5, sft = i & 31;
+                const uint32_t bits = sft ? ((row[q] << sft) | (row[q + 1] >> (32 - sft))) : row[q];
+                word |= (bits >> (32 - len)) << (32 - len - (pos - G));
+                pos += len;
+                ++b;
+                i = 0;
+            }
+            emit_word(out, b0 * m / 32 + w, word, true);
+        }
+        __syncthreads();  // Rs is rewritten by the next group
+    }
+}
+
 // Gather form of the same combine + pack: one thread per output word, no
 // shared memory.  Output word w covers key bits [32w, 32w + 32): at most two
 // blocks; for each, the (one or two) key-row words the bits come from are
@@ -931,6 +1021,11 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         return e ? atoi(e) : -1;
     }();
     const bool gather = gather_env >= 0 ? gather_env != 0 : ywords >= 1024;
+    static const bool stream_form = [] {
+        const char *e = getenv("QRNG_CSR_STREAM");
+        return e ? atoi(e) != 0 : true;
+    }();
+    const size_t stream_smem = (((size_t)2 * bpc * H.y_stride + (size_t)bpc * (ywords + 1) + csr_words + 1) & ~(size_t)1) * 4 + 16;
     if (st == QRNG_OK && gather) {
         // one thread per output word, gathers from L2 (no staging)
         const uint64_t gwords = ((uint64_t)n_blocks * m + 31) / 32;
@@ -944,6 +1039,19 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
                                                                                    (uint32_t)m, m_magic, out);
         tc.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_gather_pack_kernel launch failed"); st = QRNG_E_CUDA; }
+    } else if (st == QRNG_OK && stream_smem <= 200 * 1024 && stream_form) {
+        // the same, persistent, with the next group's rows in flight (TMA bulk copies)
+        if (stream_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_stream_pack_kernel));
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_stream_pack_kernel, QRNG_CSR_THREADS, stream_smem);
+        const uint64_t groups = (n_blocks + bpc - 1) / bpc, cap = (uint64_t)sms * std::max(per_sm, 1);
+        KernelTimer tc(s, true, 1);
+        csr_stream_pack_kernel<<<(unsigned)(groups < cap ? groups : cap), QRNG_CSR_THREADS, stream_smem, s>>>(
+            t->csr, csr_words, yws, H.y_stride, n_blocks, (uint32_t)m, bpc, out);
+        tc.stop();
+        if (cudaGetLastError() != cudaSuccess) { set_error("csr_stream_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && csr_smem <= 200 * 1024) {
         // flattened tree over bpc blocks of leaf parities in shared memory
         if (csr_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_pack_kernel));
