@@ -427,7 +427,10 @@ __device__ __forceinline__ void run_levels(uint32_t *data, uint32_t *stage, cons
 // entirely in shared memory by ntt_segment_kernel (forward levels, pointwise
 // product, inverse levels); the global inverse passes follow, the last one
 // emitting parity bits.
-constexpr int kSegLog = 15;
+#ifndef QRNG_NTT_SEGLOG
+#define QRNG_NTT_SEGLOG 15
+#endif
+constexpr int kSegLog = QRNG_NTT_SEGLOG;  // words per segment-kernel CTA (log2)
 
 template <int LOGS, int MODE>
 __global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
