@@ -223,7 +223,9 @@ def run_ours(args):
     # timed region
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    q.kernel_timing(True)
+    # the main extraction kernel(s) timed inside the timed region (two event
+    # records per launch on their stream); the auxiliary kernels in a separate pass
+    q.kernel_timing(True, aux=False)
     q.kernel_time_ms()  # clear
     if world > 1:
         dist.barrier()
@@ -241,7 +243,7 @@ def run_ours(args):
         dist.barrier()
     ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_total = sum(ms_steps)
-    kern_ms, kern_n, aux_ms, aux_n = q.kernel_time_split()
+    kern_ms, kern_n, _, _ = q.kernel_time_split()
     q.kernel_timing(False)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -271,6 +273,16 @@ def run_ours(args):
     steady = {"value": bits_all / (float(t_ss.item()) * 1e-3) / 1e9, "unit": "Gbit/s",
               "ms_per_step": float(t_ss.item()) / args.steps,
               "step": "qrng_plan_extract with the plan created once (seed preparation excluded)"}
+
+    # auxiliary kernels (Karatsuba Q buffers + combine/pack, modified repack/XOR):
+    # timed in their own pass of the same steps, outside the timed region
+    q.kernel_timing(True, aux=True)
+    q.kernel_time_split()  # clear
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    _, _, aux_ms, aux_n = q.kernel_time_split()
+    q.kernel_timing(False)
 
     # ---- end to end from pinned HOST buffers through the public API ----
     # Streaming ingest (qrng_stream_*, the continuous-stream use of the paper):
@@ -384,8 +396,15 @@ def run_ours(args):
             # two halves and writes itself: 3 x the X workspace) and combine +
             # pack (leaf parities in, packed key out)
             aux_s = aux_ms / args.steps * 1e-3
-            aux_bytes = B * (3 * 4.0 * pinfo["x_words"] + 4.0 * pinfo["y_words"] + w.m / 8)
-            roof["aux"] = {"kernels": "qbuf_kernel + csr_pack_kernel", "ms_per_step": aux_ms / args.steps,
+            if modified:  # repack (n'/8 in, K/8 out) + XOR tail (m/8 raw, m/8 key read and written)
+                kprod = (w.n - w.m + 127) // 128 * 128
+                aux_bytes = B * ((w.n - w.m) / 8 + kprod / 8 + 3 * w.m / 8)
+                aux_kernels = "modified_repack_kernel + modified_xor_tail_kernel"
+            else:
+                aux_bytes = B * (3 * 4.0 * pinfo["x_words"] + 4.0 * pinfo["y_words"] + w.m / 8)
+                aux_kernels = "qbuf_kernel + combine/pack kernel"
+            roof["aux"] = {"kernels": aux_kernels + " (own pass, outside the timed region)",
+                           "ms_per_step": aux_ms / args.steps,
                            "launches_per_step": aux_n / args.steps, "bytes_per_step": aux_bytes,
                            "achieved_gbs": aux_bytes / aux_s / 1e9,
                            "frac_of_hbm": aux_bytes / aux_s / 1e9 / pk["hbm_gbs"]}

@@ -254,7 +254,9 @@ QRNG_API qrng_status qrng_debug_karatsuba_plan(uint64_t n, uint64_t m, int max_d
  * qrng_debug_launch_count: number of kernels this library has launched in the
  * process so far (plan preparation and extraction kernels alike).
  * qrng_debug_kernel_timing(1) makes every subsequent main extraction-kernel
- * launch record CUDA events on its own stream; qrng_debug_kernel_time_ms
+ * launch record CUDA events on its own stream, (2) also every auxiliary
+ * kernel (Karatsuba Q buffers / combine, modified-Toeplitz repack / XOR;
+ * read with qrng_debug_kernel_time_split), (0) none; qrng_debug_kernel_time_ms
  * synchronises those events, returns the summed device time in ms, stores the
  * number of timed launches in *launches (if not NULL) and clears the record. */
 QRNG_API uint64_t    qrng_debug_launch_count(void);

@@ -226,8 +226,9 @@ def launch_count() -> int:
     return int(load_library().qrng_debug_launch_count())
 
 
-def kernel_timing(enable: bool) -> None:
-    load_library().qrng_debug_kernel_timing(1 if enable else 0)
+def kernel_timing(enable, aux: bool = True) -> None:
+    """Time the main extraction kernel(s) with CUDA events (and, with aux, the auxiliary kernels)."""
+    load_library().qrng_debug_kernel_timing((2 if aux else 1) if enable else 0)
 
 
 def kernel_time_ms() -> tuple[float, int]:

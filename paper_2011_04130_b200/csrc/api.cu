@@ -95,7 +95,10 @@ static cudaEvent_t pooled_event() {
 
 KernelTimer::KernelTimer(cudaStream_t st, bool timed, int ch) : s(st), channel(ch) {
     count_launch();
-    if (!timed || !g_timing.load()) return;
+    // level 1: the main extraction kernel(s) (channel 0) only; level 2: also the
+    // auxiliary kernels (each timed launch adds two event records to the stream)
+    const int lvl = g_timing.load();
+    if (!timed || lvl < 1 || (ch != 0 && lvl < 2)) return;
     a = pooled_event();
     b = pooled_event();
     if (!a || !b) { a = b = nullptr; return; }
@@ -240,7 +243,7 @@ qrng_status qrng_debug_gemm_trace(uint64_t *h_counters32, int reset) {
     if (!h_counters32) { set_error("NULL buffer"); return QRNG_E_INVALID; }
     return gemm::trace(h_counters32, reset);
 }
-void qrng_debug_kernel_timing(int enable) { g_timing.store(enable ? 1 : 0); }
+void qrng_debug_kernel_timing(int enable) { g_timing.store(enable < 0 ? 0 : (enable > 2 ? 2 : enable)); }
 double qrng_debug_kernel_time_split(double *aux_ms, uint64_t *launches, uint64_t *aux_launches) {
     std::lock_guard<std::mutex> lk(g_tmu);
     double tot[2] = {0, 0};
