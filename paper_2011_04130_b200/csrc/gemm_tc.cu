@@ -29,6 +29,7 @@
 //    per word MSB-first and store them at bit b*m + i (C4).
 //  * Persistent grid (one CTA per SM), warp-specialised, mbarrier pipelines.
 #include <algorithm>
+#include <cstdlib>
 #include "qrng_internal.cuh"
 
 namespace qrng {
@@ -66,7 +67,18 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t A_COL0 = 0;    // i8: A stages in columns [0, 32 A_STAGES)
 constexpr uint32_t ACC_COL0 = FP4 ? 0u : 32u * A_STAGES;  // accumulator sets (buffer x N tile)
 constexpr uint32_t SF_COL = ACC_COL0 + ACC_BUFS * NT * BN;  // FP4: unit block scales (16 columns of 0x7F)
-static_assert((FP4 ? 16 : A_STAGES * 32) + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
+// FP4 packed-accumulator mode (tiles with K <= 2048, i.e. Karatsuba leaves of
+// w <= 2048): N tile 1's MMAs accumulate into N tile 0's FP32 accumulator with
+// B scaled by 2^PACK_SHIFT, so one 192-column set holds both sums exactly
+// (S0 + 2^12 S1 <= 2048 + 2^12 * 2048 < 2^24; every partial sum is an integer
+// of that form): bit 0 and bit 12 of the integer are the two parities.  Two such sets alternate between tiles, so
+// the drain -- half the TMEM reads -- overlaps the next tile's MMAs.
+constexpr int PACK_SHIFT = 12;
+constexpr uint32_t kMaxPackedK = 2048;
+constexpr uint32_t SF2_COL = SF_COL + 16;  // FP4: block scales 2^PACK_SHIFT (UE8M0 127 + 12)
+constexpr int ACC_FULL = FP4 ? 2 : ACC_BUFS;
+static_assert((FP4 ? 32 : A_STAGES * 32) + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
+static_assert(!FP4 || (NT == 2 && ACC_BUFS == 1), "packed mode alternates the two N-tile column sets");
 static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (NT = 1) or one per N tile");
 // Deferred second N tile (NT = 2, one accumulator set): the epilogue drains
 // N tile 0 and then N tile 1 (all 8 warps, half the columns each); the next
@@ -409,7 +421,7 @@ __device__ __forceinline__ void xform_stage(uint32_t taddr, uint4 w) {
     tmem_st32(taddr, v);
 }
 
-template <bool GROUPED>
+template <bool GROUPED, bool PACKED = false>
 __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *chunks = smem;
@@ -419,7 +431,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     const uint32_t seed_stage = GROUPED ? a.n_leaves * 8u : a.seed_words_n;
     uint64_t *bars = reinterpret_cast<uint64_t *>(seed_s + ((seed_stage + 3) & ~3u));
     uint64_t *a_full = bars, *a_empty = bars + A_STAGES, *b_full = bars + 2 * A_STAGES;
-    uint64_t *b_empty = b_full + B_SLOTS, *acc_full = b_empty + B_SLOTS, *acc_empty = acc_full + ACC_BUFS;
+    uint64_t *b_empty = b_full + B_SLOTS, *acc_full = b_empty + B_SLOTS, *acc_empty = acc_full + ACC_FULL;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + ACC_EMPTY);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -451,7 +463,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM / XF_PAR); mbar_init(&a_empty[s], 1); }
         for (int s = 0; s < B_SLOTS; ++s) { mbar_init(&b_full[s], N_BGEN); mbar_init(&b_empty[s], 1); }
-        for (int s = 0; s < ACC_BUFS; ++s) mbar_init(&acc_full[s], 1);
+        for (int s = 0; s < ACC_FULL; ++s) mbar_init(&acc_full[s], 1);
         for (int s = 0; s < ACC_EMPTY; ++s) mbar_init(&acc_empty[s], DEFER_ON ? N_EPI : N_EPI / ACC_BUFS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -467,6 +479,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #pragma unroll
             for (int c = 0; c < 16; ++c) v[c] = 0x7F7F7F7Fu;
             tmem_st16(tmem + (((uint32_t)(warp & 3) * 32) << 16) + SF_COL, v);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = (127u + PACK_SHIFT) * 0x01010101u;
+            tmem_st16(tmem + (((uint32_t)(warp & 3) * 32) << 16) + SF2_COL, v);
             tmem_wait_st();
         }
         tc_fence_before();
@@ -478,7 +493,49 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     TRACE_T0(t_role);
     TRACE_DECL;
 
-    if (DEFER_ON && warp == W_MMA) {
+    if (PACKED && warp == W_MMA) {
+        // packed mode: both N tiles into one of two alternating column sets
+        uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+            const uint32_t r = it & 1, acc = tmem + ACC_COL0 + r * BN;
+            const uint32_t idesc0 = idesc_mxf4(BM, ti.ntc == 1 ? (int)ti.nlast : BN), idesc1 = idesc_mxf4(BM, (int)ti.nlast);
+            { TRACE_T0(tw); mbar_wait(&acc_empty[r], ((it >> 1) & 1) ^ 1); if (lane == 0) TRACE_ADD(2, tw); }
+            tc_fence_after();
+            for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                const uint32_t kin = ks % SPC;
+                if (kin == 0) {
+                    { TRACE_T0(tw); mbar_wait(&b_full[bs], bph); if (lane == 0) TRACE_ADD(1, tw); }
+                    tc_fence_after();
+                }
+                { TRACE_T0(tw); mbar_wait(&a_full[as], aph); if (lane == 0) TRACE_ADD(0, tw); }
+                tc_fence_after();
+                const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+                if (elect_one()) {
+#pragma unroll
+                    for (uint32_t kk = 0; kk < KS / 64; ++kk) {
+                        const uint32_t koff = kin * KS + kk * 64;
+                        const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
+                        mma_mxf4_ss(acc, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128), idesc0,
+                                    tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                        if (ti.ntc == 2)  // N tile 1, B scaled by 2^PACK_SHIFT, same columns
+                            mma_mxf4_ss(acc, adesc, desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 512, 128), idesc1,
+                                        tmem + SF_COL, tmem + SF2_COL, true);
+                    }
+                    mma_commit(&a_empty[as]);
+                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                }
+                __syncwarp();
+                if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                if (kin == SPC - 1 || ks == ti.kst - 1) {
+                    if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                }
+            }
+            if (elect_one()) mma_commit(&acc_full[r]);
+            __syncwarp();
+        }
+    } else if (DEFER_ON && warp == W_MMA) {
         // converged warp, elected issue; N tile 1 of each tile is deferred DEFER stages
         uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -765,6 +822,79 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&a_full[as]);
                     g += XF_PAR;
+                }
+            }
+        }
+    } else if (PACKED) {
+        // Epilogue (packed mode): every warp drains columns [96 h, 96 h + 96) of
+        // the tile's column set once; bit 0 of each exact FP32 sum is N tile 0's
+        // parity, bit PACK_SHIFT N tile 1's.
+        const uint32_t h = (uint32_t)(warp - W_EPI0) >> 2;
+        const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
+        const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + 96 * h;
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+            const uint32_t r = it & 1;
+            { TRACE_T0(tw); mbar_wait(&acc_full[r], (it >> 1) & 1); if (lane == 0) TRACE_ADD(9, tw); }
+            tc_fence_after();
+            const uint64_t b = (uint64_t)ti.mt * BM + row;
+            const uint32_t ncols0 = ti.ntc == 1 ? ti.nlast : (uint32_t)BN, ncols1 = ti.ntc == 2 ? ti.nlast : 0u;
+            uint32_t w0[3] = {0u, 0u, 0u}, w1[3] = {0u, 0u, 0u};
+            if (96 * h < ncols0) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(quad + r * BN + 32 * c, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        // exact integer F < 2^24: with exponent 23 (F < 2^23 lifted by
+                        // 2^23) the mantissa is F mod 2^23, whose bits 0 and 12 we need
+                        const float f = __uint_as_float(v[k]);
+                        const uint32_t V = __float_as_uint(f < 8388608.0f ? f + 8388608.0f : f);
+                        w0[c] = (w0[c] << 1) | (V & 1u);
+                        w1[c] = (w1[c] << 1) | ((V >> PACK_SHIFT) & 1u);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[r]);
+            if (b >= a.n_blocks) continue;
+#pragma unroll
+            for (uint32_t nt = 0; nt < 2; ++nt) {
+                const uint32_t ncols = nt ? ncols1 : ncols0;
+                uint32_t *words = nt ? w1 : w0;
+                const uint32_t n0 = ti.n0 + nt * BN + 96 * h;
+                if (n0 >= ti.r || 96 * h >= ncols) continue;
+                const uint32_t nvalid = min(min(96u, ncols - 96 * h), ti.r - n0);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int vb = (int)nvalid - 32 * c;
+                    if (vb <= 0) words[c] = 0;
+                    else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
+                }
+                if (GROUPED) {
+                    uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
+                    continue;
+                }
+                const uint64_t G_lo = b * a.m + n0, G_hi = G_lo + nvalid;
+                const uint32_t off = (uint32_t)(G_lo & 31);
+                const uint64_t W0 = G_lo >> 5;
+                uint32_t prev = 0;
+#pragma unroll
+                for (int c = 0; c <= 3; ++c) {
+                    const uint32_t cw = (c < 3) ? words[c] : 0u;
+                    const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
+                    prev = cw;
+                    const uint64_t W = W0 + c;
+                    if (W * 32 >= G_hi) break;
+                    const bool excl = (W * 32 >= G_lo) && (W * 32 + 32 <= G_hi);
+                    emit_word(a.out, W, ow, excl);
                 }
             }
         }
@@ -1800,7 +1930,7 @@ uint32_t seed_words_needed(uint64_t n, uint64_t m) {
 }
 
 static size_t smem_bytes(uint32_t seed_words_n) {
-    return (size_t)B_SLOTS * CHUNK_BYTES + (FP4 ? (size_t)A_STAGES * A_STAGE_BYTES : 0) + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + ACC_BUFS + ACC_EMPTY) * 8 + 16;
+    return (size_t)B_SLOTS * CHUNK_BYTES + (FP4 ? (size_t)A_STAGES * A_STAGE_BYTES : 0) + ((seed_words_n + 3) & ~3u) * 4 + (2 * A_STAGES + 2 * B_SLOTS + ACC_FULL + ACC_EMPTY) * 8 + 16;
 }
 
 // seed bytes (MSB-first) -> logical big-endian words, zero past L
@@ -1894,7 +2024,7 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
-template <bool GROUPED>
+template <bool GROUPED, bool PACKED = false>
 static qrng_status launch(const Args &a, cudaStream_t s) {
     if ((uint64_t)a.n_mtiles * a.n_npairs > 0xFFFFFFFFull) {
         set_error("GEMM path: too many tiles");
@@ -1905,13 +2035,13 @@ static qrng_status launch(const Args &a, cudaStream_t s) {
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const size_t smem = smem_bytes(GROUPED ? a.n_leaves * 8u : a.seed_words_n);
     {
-        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel<GROUPED>));
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel<GROUPED, PACKED>));
         if (st != QRNG_OK) return st;
     }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
     KernelTimer tm(s, true);
-    toeplitz_gemm_kernel<GROUPED><<<grid, NTHREADS, smem, s>>>(a);
+    toeplitz_gemm_kernel<GROUPED, PACKED><<<grid, NTHREADS, smem, s>>>(a);
     tm.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
@@ -1943,7 +2073,7 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
 qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t total_npairs,
                             const uint32_t *d_seeds, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                             const uint32_t *xws, uint32_t x_stride, uint32_t *yws, uint32_t y_stride,
-                            cudaStream_t s) {
+                            uint32_t max_leaf_w, cudaStream_t s) {
     Args a{};
     a.raw = reinterpret_cast<const uint32_t *>(d_raw);
     a.n_blocks = n_blocks;
@@ -1960,9 +2090,15 @@ qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t to
     // q = floor(x / d) = umul64hi(x, ceil(2^64 / d)) exactly for x, d < 2^32
     a.mt_magic = a.n_mtiles > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / a.n_mtiles) + 1 : 0;
 #if QRNG_GEMM_2CTA
+    (void)max_leaf_w;
     return two::launch2<true>(a, s);
 #else
-    return launch<true>(a, s);
+    static const bool packed_ok = [] {
+        const char *e = getenv("QRNG_GEMM_PACKED");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (FP4 && packed_ok && max_leaf_w <= kMaxPackedK) return launch<true, true>(a, s);
+    return launch<true, false>(a, s);
 #endif
 }
 

@@ -360,6 +360,7 @@ struct Tables {
     uint32_t *csr = nullptr;       // device: root word -> Y-row words (counts, then column-major entries)
     uint32_t csr_words = 0;
     std::vector<gemm::Leaf> hleaves;
+    uint32_t max_leaf_w = 0;       // widest leaf (K) -- the packed-accumulator kernel takes w <= 2048
 };
 
 static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Tables **out) {
@@ -398,6 +399,7 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
         gemm::Leaf g{};
         g.w = L.w;
         g.r = L.r;
+        t->max_leaf_w = std::max(t->max_leaf_w, L.w);
         g.npairs = (L.r + gemm::kTileRows - 1) / gemm::kTileRows;
         // equal tiles (no narrow N = 64 tail MMA, which runs at ~60% of the pipe rate)
         g.pair_rows = ((L.r + g.npairs - 1) / g.npairs + 31) & ~31u;
@@ -1001,7 +1003,7 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
     }
     if (st == QRNG_OK)
         st = gemm::extract_grouped(t->leaves, (uint32_t)t->hleaves.size(), H.total_npairs, pl.seeds, d_raw, n_blocks,
-                                   n, xws, H.x_stride, yws, H.y_stride, s);
+                                   n, xws, H.x_stride, yws, H.y_stride, t->max_leaf_w, s);
     const uint32_t rw4 = (uint32_t)(((m + 31) / 32 + 3) / 4 + 1);
     const size_t fused_smem = (size_t)32 * (H.z_stride + 4 * rw4) * 4;
     const uint32_t ywords = (uint32_t)((m + 31) / 32), csr_words = t->csr_words;

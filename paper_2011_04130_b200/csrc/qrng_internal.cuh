@@ -148,7 +148,7 @@ uint32_t seed_words_needed(uint64_t n, uint64_t m);
 qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t total_npairs,
                             const uint32_t *d_seeds, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                             const uint32_t *xws, uint32_t x_stride, uint32_t *yws, uint32_t y_stride,
-                            cudaStream_t s);
+                            uint32_t max_leaf_w, cudaStream_t s);
 bool supported(uint64_t n, uint64_t m);
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
 // modified Toeplitz [T | I_m] (n-bit seed): repack x_b[0, n-m) to a multiple of
