@@ -96,6 +96,9 @@ static bool can_split(uint32_t w) { return w % 256 == 0 && w / 2 >= kMinLeafW; }
 struct Planner {
     std::map<std::tuple<uint32_t, uint32_t, int>, std::pair<double, int>> memo;
     bool forced;  // forced depth: split whenever allowed
+    // inside a tree (w below the root's), split leaves wider than the E2M1
+    // kernel's packed-accumulator limit so that the whole launch can use it
+    uint32_t root_w = 0, pack_w = 0;
 
     std::pair<double, int> best(uint32_t r, uint32_t w, int depth) {
         auto key = std::make_tuple(r, w, depth);
@@ -104,13 +107,14 @@ struct Planner {
         std::pair<double, int> res{leaf_cost(r, w), LEAF};
         if (depth > 0 && can_split(w)) {
             const uint32_t h = w / 2;
+            const bool pack_split = pack_w && w < root_w && w > pack_w;
             if (r > h) {
                 const double c = 2 * best(h, h, depth - 1).first + best(r - h, h, depth - 1).first +
                                  kPrepPerBit * h + kCombPerRow * r;
-                if (forced || c < res.first) res = {c, KARA};
+                if (forced || pack_split || c < res.first) res = {c, KARA};
             } else {
                 const double c = 2 * best(r, h, depth - 1).first + kCombPerRow * r;
-                if (forced || c < res.first) res = {c, COLS};
+                if (forced || pack_split || c < res.first) res = {c, COLS};
             }
         }
         memo[key] = res;
@@ -239,6 +243,10 @@ static bool plan_host(uint64_t n, uint64_t m, int max_depth, HostTables &T) {
 static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, HostTables &T) {
     Planner pl;
     pl.forced = forced;
+    pl.root_w = (uint32_t)n;
+#if !QRNG_GEMM_2CTA
+    if (gemm::operand_bits() == 4) pl.pack_w = 2048;  // gemm_tc.cu kMaxPackedK
+#endif
     std::vector<Node> nodes;
     pl.build((uint32_t)m, (uint32_t)n, depth, nodes);
     std::vector<int> leaf_of_node(nodes.size(), -1);
