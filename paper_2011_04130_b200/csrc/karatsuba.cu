@@ -245,7 +245,16 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
     pl.forced = forced;
     pl.root_w = (uint32_t)n;
 #if !QRNG_GEMM_2CTA
-    if (gemm::operand_bits() == 4) pl.pack_w = 2048;  // gemm_tc.cu kMaxPackedK
+    static const bool pack_split = [] {
+        const char *e = getenv("QRNG_KARA_PACK_SPLIT");  // calibration override
+        return e ? atoi(e) != 0 : true;
+    }();
+    // measured (profiles/sweep_r1n.jsonl, tools/ab_pack.sh): splitting for the
+    // packed accumulators pays at config 2 (2^13, 16384 blocks: 510 -> 528
+    // Gbit/s) and from 2^16 (2048-wide leaves: 156 -> 166), loses at 2^14 /
+    // 2^15 (398 -> 391, 226 -> 204)
+    const bool pack_here = n <= 8192 || n >= 65536;
+    if (pack_split && pack_here && gemm::operand_bits() == 4) pl.pack_w = 2048;  // gemm_tc.cu kMaxPackedK
 #endif
     std::vector<Node> nodes;
     pl.build((uint32_t)m, (uint32_t)n, depth, nodes);
