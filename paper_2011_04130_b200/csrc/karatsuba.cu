@@ -807,7 +807,7 @@ __device__ __forceinline__ uint32_t ksmem(const void *p) {
 __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const uint32_t *csr, uint32_t csr_words,
                                                                            const uint32_t *yws, uint32_t y_stride,
                                                                            uint64_t n_blocks, uint32_t m, uint32_t bpc,
-                                                                           OutStream out) {
+                                                                           uint64_t m_magic, OutStream out) {
     extern __shared__ uint4 sm4[];
     const uint32_t ywords = (m + 31) / 32, rwords = ywords + 1;
     const uint32_t ybuf_words = bpc * y_stride;
@@ -852,14 +852,30 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
         const uint64_t b0 = g * bpc;
         const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
         const uint32_t *Ys = Y0 + buf * ybuf_words;
-        for (uint32_t idx = threadIdx.x; idx < nb * rwords; idx += blockDim.x) {
-            const uint32_t bl = idx / rwords, j = idx - bl * rwords;
-            uint32_t v = 0;
-            if (j < ywords) {
-                const uint32_t *yr = Ys + bl * y_stride;
-                for (uint32_t e = 0, c = Cs[j]; e < c; ++e) v ^= yr[Cs[ywords + e * ywords + j]];
+        {
+            // thread (set, j): key word j of blocks set, set + sets, ...; the word's
+            // CSR entries are read once and reused for every block of the group
+            const uint32_t sets = max(1u, blockDim.x / rwords);
+            for (uint32_t u = threadIdx.x; u < sets * rwords; u += blockDim.x) {
+                const uint32_t set = u / rwords, j = u - set * rwords;
+                if (j < ywords) {
+                    const uint32_t c = Cs[j];
+                    uint32_t idx[8];
+#pragma unroll
+                    for (uint32_t e = 0; e < 8; ++e) idx[e] = e < c ? Cs[ywords + e * ywords + j] : 0u;
+                    for (uint32_t bl = set; bl < nb; bl += sets) {
+                        const uint32_t *yr = Ys + bl * y_stride;
+                        uint32_t v = 0;
+#pragma unroll
+                        for (uint32_t e = 0; e < 8; ++e)
+                            if (e < c) v ^= yr[idx[e]];
+                        for (uint32_t e = 8; e < c; ++e) v ^= yr[Cs[ywords + e * ywords + j]];
+                        Rs[bl * rwords + j] = v;
+                    }
+                } else {
+                    for (uint32_t bl = set; bl < nb; bl += sets) Rs[bl * rwords + j] = 0;
+                }
             }
-            Rs[idx] = v;
         }
         __syncthreads();  // Rs complete; this buffer's rows are no longer read
         if (threadIdx.x == 0 && g + 2 * (uint64_t)gridDim.x < n_groups) {
@@ -867,9 +883,11 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
             issue(g + 2 * (uint64_t)gridDim.x, buf);
         }
         const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
+        const uint64_t wbase = b0 * m / 32;
         for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
             const uint32_t G = w * 32, end = min(G + 32, gbits);
-            uint32_t b = G / m, i = G - b * m, pos = G, word = 0;
+            uint32_t b = m_magic ? (uint32_t)__umul64hi((uint64_t)G, m_magic) : G;  // G / m
+            uint32_t i = G - b * m, pos = G, word = 0;
             while (pos < end) {
                 const uint32_t len = min(m - i, end - pos);  // 1..32 bits of block b
                 const uint32_t *row = Rs + b * rwords;
@@ -880,7 +898,7 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
                 ++b;
                 i = 0;
             }
-            emit_word(out, b0 * m / 32 + w, word, true);
+            emit_word(out, wbase + w, word, true);
         }
         __syncthreads();  // Rs is rewritten by the next group
     }
@@ -1067,8 +1085,9 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_stream_pack_kernel, QRNG_CSR_THREADS, stream_smem);
         const uint64_t groups = (n_blocks + bpc - 1) / bpc, cap = (uint64_t)sms * std::max(per_sm, 1);
         KernelTimer tc(s, true, 1);
+        const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
         csr_stream_pack_kernel<<<(unsigned)(groups < cap ? groups : cap), QRNG_CSR_THREADS, stream_smem, s>>>(
-            t->csr, csr_words, yws, H.y_stride, n_blocks, (uint32_t)m, bpc, out);
+            t->csr, csr_words, yws, H.y_stride, n_blocks, (uint32_t)m, bpc, m_magic, out);
         tc.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_stream_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && csr_smem <= 200 * 1024) {
