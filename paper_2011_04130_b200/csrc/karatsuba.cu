@@ -884,6 +884,36 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
         }
         const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
         const uint64_t wbase = b0 * m / 32;
+        if (m >= 64) {
+            // per block row: the words inside block bl are its key row shifted by
+            // a constant (bl m mod 32); the one word straddling bl and bl + 1 is
+            // assembled by the thread that owns it.  No division per word.
+            const uint32_t wpb = (m + 31) / 32 + 1;  // >= words starting in one block
+            const uint32_t sets = max(1u, blockDim.x / wpb);
+            for (uint32_t u = threadIdx.x; u < sets * wpb; u += blockDim.x) {
+                const uint32_t set = u / wpb, k = u - set * wpb;
+                for (uint32_t bl = set; bl < nb; bl += sets) {
+                    const uint32_t s0 = bl * m, s1 = s0 + m;  // bit range of block bl in the group
+                    const uint32_t W = (s0 + 31) / 32 + k;    // k-th word starting inside block bl
+                    if (32 * W >= s1) continue;  // block bl has fewer words (other blocks may not)
+                    const uint32_t *row = Rs + bl * rwords;
+                    const uint32_t i0 = 32 * W - s0, q = i0 >> 5, sft = i0 & 31;
+                    uint32_t word;
+                    if (32 * W + 32 <= s1) {
+                        word = sft ? ((row[q] << sft) | (row[q + 1] >> (32 - sft))) : row[q];
+                    } else {
+                        // tail of block bl (len1 bits), then the head of block bl + 1
+                        const uint32_t len1 = s1 - 32 * W;
+                        const uint32_t hi = sft ? ((row[q] << sft) | (row[q + 1] >> (32 - sft))) : row[q];
+                        word = hi & ~(0xFFFFFFFFu >> len1);
+                        if (bl + 1 < nb) word |= Rs[(bl + 1) * rwords] >> len1;
+                    }
+                    emit_word(out, wbase + W, word, true);
+                }
+            }
+            __syncthreads();
+            continue;
+        }
         for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
             const uint32_t G = w * 32, end = min(G + 32, gbits);
             uint32_t b = m_magic ? (uint32_t)__umul64hi((uint64_t)G, m_magic) : G;  // G / m
