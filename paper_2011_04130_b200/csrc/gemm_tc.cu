@@ -38,6 +38,9 @@ namespace gemm {
 #ifndef QRNG_GEMM_DEFER
 #define QRNG_GEMM_DEFER 2  // MMAs of N tile 1 of the next tile start this many A stages late (0: off)
 #endif
+#ifndef QRNG_GEMM_KS_FP4
+#define QRNG_GEMM_KS_FP4 512  // K per A stage of the E2M1 kernel (256 or 512; 512 measured faster)
+#endif
 
 constexpr int BM = 128;        // blocks per tile (TMEM lanes)
 constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
@@ -47,10 +50,10 @@ constexpr int BN = QRNG_GEMM_BN;  // output rows per N tile
 // and every partial sum an integer <= n <= 2^16 < 2^24), twice the int8 MMA
 // rate.  Otherwise kind::i8 with A in TMEM and S32 accumulators.
 constexpr bool FP4 = QRNG_GEMM_FP4 != 0;
-constexpr int KS = FP4 ? 256 : 128;  // K per A stage (FP4: 4 MMAs of K64 per N tile per stage)
+constexpr int KS = FP4 ? QRNG_GEMM_KS_FP4 : 128;  // K per A stage (FP4: KS/64 MMAs of K64 per N tile per stage)
 constexpr int KS128 = KS / 128;      // 128-bit raw chunks per A stage
 #ifndef QRNG_GEMM_ASTAGES_FP4
-#define QRNG_GEMM_ASTAGES_FP4 4
+#define QRNG_GEMM_ASTAGES_FP4 3
 #endif
 constexpr int A_STAGES = FP4 ? QRNG_GEMM_ASTAGES_FP4 : QRNG_GEMM_ASTAGES;  // A ring slots (FP4: smem; i8: TMEM, 32 columns each)
 constexpr int A_STAGE_BYTES = 128 * KS / 2;  // FP4 A stage in smem: BM rows x KS nibbles
@@ -85,7 +88,7 @@ static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (N
 // tile's MMAs start on N tile 0 as soon as it is drained and catch up N tile 1
 // after QRNG_GEMM_DEFER A stages, so half of the drain overlaps the MMAs.
 constexpr bool DEFER_ON = QRNG_GEMM_DEFER > 0 && NT == 2 && ACC_BUFS == 1 && BN == 192;
-constexpr int DEFER = QRNG_GEMM_DEFER > 0 ? QRNG_GEMM_DEFER : 1;
+constexpr int DEFER = QRNG_GEMM_DEFER > 0 ? (QRNG_GEMM_DEFER < KC / KS ? QRNG_GEMM_DEFER : KC / KS - 1) : 1;
 static_assert(!DEFER_ON || (DEFER < A_STAGES && DEFER < KC / KS), "deferred stages stay resident in one chunk");
 static_assert(!FP4 || DEFER_ON, "the FP4 operand path is implemented for the deferred NT = 2, BN = 192 geometry");
 constexpr int ACC_EMPTY = DEFER_ON ? 2 : ACC_BUFS;
@@ -100,7 +103,7 @@ constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4 * XF
               N_EPI = 8;
 constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
 static_assert(A_STAGES % XF_PAR == 0, "each transform warp owns fixed ring slots");
-constexpr int PF = 4;          // A-transform prefetch depth (stages)
+constexpr int PF = KS > 256 ? 2 : 4;  // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
 #if !QRNG_GEMM_2CTA
 static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile");
@@ -512,6 +515,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 tc_fence_after();
                 const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
                 const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+                if (lane == 0) TRACE_ADDV(11, 1);
+                TRACE_T0(tiss);
                 if (elect_one()) {
 #pragma unroll
                     for (uint32_t kk = 0; kk < KS / 64; ++kk) {
@@ -527,6 +532,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
                 }
                 __syncwarp();
+                if (lane == 0) TRACE_ADD(16, tiss);
                 if (++as == A_STAGES) { as = 0; aph ^= 1; }
                 if (kin == SPC - 1 || ks == ti.kst - 1) {
                     if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
@@ -769,13 +775,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (ci >= 0 ? ci : 0));
         };
         for (uint32_t i = 0; i < par; ++i) step1();
-        uint4 pf[PF], pf2[FP4 ? PF : 1];
-        bool ok[PF], vd[PF], vd2[FP4 ? PF : 1];
+        uint4 pf[PF][KS128];
+        bool ok[PF], vd[PF][KS128];
 #pragma unroll
         for (int j = 0; j < PF; ++j) {
             ok[j] = lt < ntiles;
-            pf[j] = load(vd[j], 0);
-            if constexpr (FP4) pf2[j] = load(vd2[j], 1);
+#pragma unroll
+            for (int hf = 0; hf < KS128; ++hf) pf[j][hf] = load(vd[j][hf], hf);
 #pragma unroll
             for (int i = 0; i < XF_PAR; ++i) step1();
         }
@@ -786,12 +792,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             for (int j = 0; j < PF; ++j) {
                 if (more && !ok[j]) more = false;
                 if (more) {
-                    const uint4 cur4 = vd[j] ? pf[j] : make_uint4(0, 0, 0, 0);
-                    uint4 cur4b = make_uint4(0, 0, 0, 0);
-                    if constexpr (FP4) cur4b = vd2[j] ? pf2[j] : make_uint4(0, 0, 0, 0);
+                    uint4 cur[KS128];
+#pragma unroll
+                    for (int hf = 0; hf < KS128; ++hf) cur[hf] = vd[j][hf] ? pf[j][hf] : make_uint4(0, 0, 0, 0);
+                    const uint4 cur4 = cur[0];
                     ok[j] = lt < ntiles;
-                    pf[j] = load(vd[j], 0);
-                    if constexpr (FP4) pf2[j] = load(vd2[j], 1);
+#pragma unroll
+                    for (int hf = 0; hf < KS128; ++hf) pf[j][hf] = load(vd[j][hf], hf);
 #pragma unroll
                     for (int i = 0; i < XF_PAR; ++i) step1();
                     const uint32_t as = g % A_STAGES, aph = (g / A_STAGES) & 1;
@@ -803,12 +810,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                         // K group g (32 elements, K reversed) = memory word 3 - g, element c = bit c
                         // of its big-endian value: bit-reverse so that bit b holds element 31 - b
                         // as in the B rows, then the same nibble spread
-                        const uint32_t M4[8] = {cur4.x, cur4.y, cur4.z, cur4.w, cur4b.x, cur4b.y, cur4b.z, cur4b.w};
                         uint8_t *arow = a_ring + as * A_STAGE_BYTES + (row >> 3) * A_SBO + (row & 7) * 16;
 #pragma unroll
-                        for (int gk = 0; gk < KS / 32; ++gk)
-                            *reinterpret_cast<uint4 *>(arow + gk * 128) =
-                                e2m1_row(__brev(__byte_perm(M4[(gk >> 2) * 4 + 3 - (gk & 3)], 0, 0x0123)));
+                        for (int hf = 0; hf < KS128; ++hf) {
+                            const uint32_t M4[4] = {cur[hf].x, cur[hf].y, cur[hf].z, cur[hf].w};
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4)
+                                *reinterpret_cast<uint4 *>(arow + (hf * 4 + q4) * 128) =
+                                    e2m1_row(__brev(__byte_perm(M4[3 - q4], 0, 0x0123)));
+                        }
                         fence_proxy_async();
                     } else {
                         xform_stage(lane_addr + A_COL0 + as * 32, cur4);
