@@ -496,7 +496,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     TRACE_T0(t_role);
     TRACE_DECL;
 
-    if (PACKED && warp == W_MMA) {
+#ifndef QRNG_GEMM_SOLO
+#define QRNG_GEMM_SOLO 1  // one elected lane runs the whole MMA loop (no per-stage warp reconvergence)
+#endif
+    if (PACKED && QRNG_GEMM_SOLO && warp == W_MMA) {
+        if (elect_one()) {
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+                const uint32_t r = it & 1, acc = tmem + ACC_COL0 + r * BN;
+                const uint32_t idesc0 = idesc_mxf4(BM, ti.ntc == 1 ? (int)ti.nlast : BN), idesc1 = idesc_mxf4(BM, (int)ti.nlast);
+                mbar_wait(&acc_empty[r], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                    const uint32_t kin = ks % SPC;
+                    if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
+                    mbar_wait(&a_full[as], aph);
+                    tc_fence_after();
+                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                    const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < KS / 64; ++kk) {
+                        const uint32_t koff = kin * KS + kk * 64;
+                        const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
+                        mma_mxf4_ss(acc, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128), idesc0,
+                                    tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                        if (ti.ntc == 2)
+                            mma_mxf4_ss(acc, adesc, desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 512, 128), idesc1,
+                                        tmem + SF_COL, tmem + SF2_COL, true);
+                    }
+                    mma_commit(&a_empty[as]);
+                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    if (kin == SPC - 1 || ks == ti.kst - 1) {
+                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                    }
+                }
+                mma_commit(&acc_full[r]);
+            }
+        }
+        __syncwarp();
+    } else if (PACKED && warp == W_MMA) {
         // packed mode: both N tiles into one of two alternating column sets
         uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -541,6 +581,113 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             if (elect_one()) mma_commit(&acc_full[r]);
             __syncwarp();
         }
+    } else if (DEFER_ON && FP4 && QRNG_GEMM_SOLO && warp == W_MMA) {
+        // the same loop run by one elected lane (no per-stage warp reconvergence)
+        if (elect_one()) {
+            // converged warp, elected issue; N tile 1 of each tile is deferred DEFER stages
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                TRACE_T0(tsetup);
+                const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+                const uint32_t idesc_full = FP4 ? idesc_mxf4(BM, BN) : idesc_i8(BM, BN);
+                const uint32_t idesc_last = FP4 ? idesc_mxf4(BM, (int)ti.nlast) : idesc_i8(BM, (int)ti.nlast);
+                const uint32_t ph = (it & 1) ^ 1;
+                if (lane == 0) TRACE_ADD(17, tsetup);
+                { TRACE_T0(tw); mbar_wait(&acc_empty[0], ph); if (lane == 0) TRACE_ADD(2, tw); }
+                const bool defer = ti.ntc == 2 && ti.kst > (uint32_t)DEFER;
+                if (!defer) { TRACE_T0(tw); mbar_wait(&acc_empty[1], ph); if (lane == 0) TRACE_ADD(12, tw); }
+                tc_fence_after();
+                bool nt1_on = !defer;
+                uint32_t dslot[DEFER];
+                uint32_t cb0 = 0;
+                for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                    const uint32_t kin = ks % SPC;
+                    if (kin == 0) {
+                        { TRACE_T0(tw); mbar_wait(&b_full[bs], bph); if (lane == 0) TRACE_ADD(1, tw); }
+                        tc_fence_after();
+                    }
+                    { TRACE_T0(tw); mbar_wait(&a_full[as], aph); if (lane == 0) TRACE_ADD(0, tw); }
+                    if (lane == 0) TRACE_ADDV(11, 1);
+                    tc_fence_after();
+                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                    if (ks == 0) cb0 = cbase;
+                    if (!nt1_on && ks == (uint32_t)DEFER) {
+                        // N tile 1 drained: its MMAs for the held stages, then release them
+                        { TRACE_T0(tw); mbar_wait(&acc_empty[1], ph); if (lane == 0) TRACE_ADD(12, tw); }
+                        tc_fence_after();
+                        {
+    #pragma unroll
+                            for (int d = 0; d < DEFER; ++d) {
+                                if constexpr (FP4) {
+                                    const uint32_t abase = smem_u32(a_ring + dslot[d] * A_STAGE_BYTES);
+    #pragma unroll
+                                    for (uint32_t kk = 0; kk < KS / 64; ++kk) {
+                                        const uint32_t koff = d * KS + kk * 64;
+                                        mma_mxf4_ss(tmem + ACC_COL0 + BN, desc_kmajor(abase + kk * 256, 128, A_SBO),
+                                                    desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
+                                                    tmem + SF_COL, tmem + SF_COL + 8, (d | kk) != 0);
+                                    }
+                                } else {
+    #pragma unroll
+                                    for (uint32_t kk = 0; kk < 4; ++kk) {
+                                        const uint32_t koff = d * KS + kk * 32;
+                                        const uint64_t bdesc = desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 256, 128);
+                                        mma_i8_ts(tmem + ACC_COL0 + BN, tmem + A_COL0 + dslot[d] * 32 + kk * 8, bdesc,
+                                                  idesc_last, (d | kk) != 0);
+                                    }
+                                }
+                                mma_commit(&a_empty[dslot[d]]);
+                            }
+                        }
+                    
+                        nt1_on = true;
+                    }
+                    const uint32_t a_tmem = tmem + A_COL0 + as * 32;
+                    TRACE_T0(tiss);
+                    {
+                        if constexpr (FP4) {
+                            const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+    #pragma unroll
+                            for (uint32_t kk = 0; kk < KS / 64; ++kk) {
+                                const uint32_t koff = kin * KS + kk * 64;
+                                const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
+                                mma_mxf4_ss(tmem + ACC_COL0, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128),
+                                            ti.ntc == 1 ? idesc_last : idesc_full, tmem + SF_COL, tmem + SF_COL + 8,
+                                            (ks | kk) != 0);
+                                if (nt1_on && ti.ntc == 2)
+                                    mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc,
+                                                desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
+                                                tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                            }
+                        } else {
+    #pragma unroll
+                        for (uint32_t kk = 0; kk < 4; ++kk) {
+                            const uint32_t koff = kin * KS + kk * 32;
+                            const uint64_t bdesc0 = desc_kmajor(cbase + (koff / 8) * 128, 256, 128);
+                            mma_i8_ts(tmem + ACC_COL0, a_tmem + kk * 8, bdesc0, ti.ntc == 1 ? idesc_last : idesc_full,
+                                      (ks | kk) != 0);
+                            if (nt1_on && ti.ntc == 2) {
+                                const uint64_t bdesc1 = desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 256, 128);
+                                mma_i8_ts(tmem + ACC_COL0 + BN, a_tmem + kk * 8, bdesc1, idesc_last, (ks | kk) != 0);
+                            }
+                        }
+                        }
+                        if (nt1_on) mma_commit(&a_empty[as]);
+                        if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                    }
+                
+                    if (lane == 0) TRACE_ADD(16, tiss);
+                    if (!nt1_on) dslot[ks] = as;
+                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    if (kin == SPC - 1 || ks == ti.kst - 1) {
+                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                    }
+                }
+                mma_commit(&acc_full[0]);
+            
+            }
+        }
+        __syncwarp();
     } else if (DEFER_ON && warp == W_MMA) {
         // converged warp, elected issue; N tile 1 of each tile is deferred DEFER stages
         uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
