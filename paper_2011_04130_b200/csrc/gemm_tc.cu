@@ -53,14 +53,17 @@ constexpr bool FP4 = QRNG_GEMM_FP4 != 0;
 constexpr int KS = FP4 ? QRNG_GEMM_KS_FP4 : 128;  // K per A stage (FP4: KS/64 MMAs of K64 per N tile per stage)
 constexpr int KS128 = KS / 128;      // 128-bit raw chunks per A stage
 #ifndef QRNG_GEMM_ASTAGES_FP4
-#define QRNG_GEMM_ASTAGES_FP4 3
+#define QRNG_GEMM_ASTAGES_FP4 2
 #endif
 constexpr int A_STAGES = FP4 ? QRNG_GEMM_ASTAGES_FP4 : QRNG_GEMM_ASTAGES;  // A ring slots (FP4: smem; i8: TMEM, 32 columns each)
 constexpr int A_STAGE_BYTES = 128 * KS / 2;  // FP4 A stage in smem: BM rows x KS nibbles
 constexpr int A_SBO = KS / 32 * 128;          // FP4 A stage: byte stride between 8-row core-matrix groups
 constexpr int KC = 1024;       // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
-constexpr int B_SLOTS = 3;
+#ifndef QRNG_GEMM_BSLOTS
+#define QRNG_GEMM_BSLOTS 3
+#endif
+constexpr int B_SLOTS = QRNG_GEMM_BSLOTS;  // B chunk ring slots
 constexpr int NT = QRNG_GEMM_NT;  // N tiles per A stage (A reuse factor)
 // accumulator sets in TMEM (2 lets the MMAs of tile k+1 overlap the drain of tile k; needs NT = 1)
 constexpr int ACC_BUFS = QRNG_GEMM_ACCBUFS;
