@@ -507,9 +507,17 @@ __device__ __forceinline__ uint32_t bswap(uint32_t x) { return __byte_perm(x, 0,
 __device__ __forceinline__ uint32_t seed_window32(const uint8_t *seed, uint64_t L, uint64_t pos) {
     if (pos >= L) return 0u;
     const uint64_t b = pos >> 3, nbytes = (L + 7) / 8;
-    uint64_t v = 0;
-    for (int i = 0; i < 5; ++i) v = (v << 8) | (b + i < nbytes ? seed[b + i] : 0u);
-    uint32_t r = (uint32_t)(v >> (8 - (pos & 7)));
+    uint32_t r;
+    const uint64_t w = pos >> 5;  // two aligned words hold bits [32w, 32w + 64) (the seed is 16-byte aligned)
+    if ((w + 2) * 4 <= nbytes) {
+        const uint32_t *s32 = reinterpret_cast<const uint32_t *>(seed);
+        const uint32_t hi = __byte_perm(__ldg(s32 + w), 0, 0x0123), lo = __byte_perm(__ldg(s32 + w + 1), 0, 0x0123);
+        r = __funnelshift_l(lo, hi, (uint32_t)(pos & 31));
+    } else {
+        uint64_t v = 0;
+        for (int i = 0; i < 5; ++i) v = (v << 8) | (b + i < nbytes ? seed[b + i] : 0u);
+        r = (uint32_t)(v >> (8 - (pos & 7)));
+    }
     if (pos + 32 > L) r &= 0xFFFFFFFFu << (32 - (uint32_t)(L - pos));
     return r;
 }
@@ -522,7 +530,8 @@ __global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms
     const uint32_t len = Lf.r + Lf.w - 1;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < Lf.seed_n; q += gridDim.x * blockDim.x) {
         uint32_t v = 0;
-        for (uint32_t k = 0; k < Lf.sterm_n; ++k) v ^= seed_window32(seed, L, terms[Lf.sterm_base + k] + 32ull * q);
+#pragma unroll 8
+        for (uint32_t k = 0; k < Lf.sterm_n; ++k) v ^= seed_window32(seed, L, __ldg(terms + Lf.sterm_base + k) + 32ull * q);
         const uint32_t lo = 32 * q;
         if (lo + 32 > len) v &= (len > lo) ? (0xFFFFFFFFu << (32 - (len - lo))) : 0u;
         seeds[Lf.seed_off + q] = v;
