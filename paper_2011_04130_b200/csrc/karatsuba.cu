@@ -1067,9 +1067,15 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
     QRNG_CUDA_TRY(cudaMallocAsync(&yws, (size_t)n_blocks * H.y_stride * 4, s));
     qrng_status st = QRNG_OK;
     if (!H.qbufs.empty()) {  // Q buffers, generation by generation, bpc blocks per CTA
-        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / 296));
+#ifndef QRNG_QBUF_U
+#define QRNG_QBUF_U 4      // 16-byte units in flight per thread
+#endif
+#ifndef QRNG_QBUF_DIV
+#define QRNG_QBUF_DIV 296  // target CTA count (blocks per CTA = n_blocks / this, at most 32)
+#endif
+        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / QRNG_QBUF_DIV));
         KernelTimer tq(s, true, 1);
-        qbuf_kernel<4><<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, 0, s>>>(
+        qbuf_kernel<QRNG_QBUF_U><<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, 0, s>>>(
             t->qbufs, t->qgen_dev, (uint32_t)t->qgen.size() - 1, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
             (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc);
         tq.stop();
