@@ -84,7 +84,7 @@ constexpr uint32_t kMaxPackedK = 2048;
 constexpr uint32_t SF2_COL = SF_COL + 16;  // FP4: block scales 2^PACK_SHIFT (UE8M0 127 + 12)
 constexpr int ACC_FULL = FP4 ? 2 : ACC_BUFS;
 static_assert((FP4 ? 32 : A_STAGES * 32) + ACC_BUFS * NT * BN <= (int)TMEM_COLS, "TMEM budget");
-static_assert(!FP4 || (NT == 2 && ACC_BUFS == 1), "packed mode alternates the two N-tile column sets");
+constexpr bool PACK_OK = FP4 && NT == 2 && ACC_BUFS == 1;  // packed mode alternates the two N-tile column sets
 static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (NT = 1) or one per N tile");
 // Deferred second N tile (NT = 2, one accumulator set): the epilogue drains
 // N tile 0 and then N tile 1 (all 8 warps, half the columns each); the next
@@ -93,7 +93,8 @@ static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (N
 constexpr bool DEFER_ON = QRNG_GEMM_DEFER > 0 && NT == 2 && ACC_BUFS == 1 && BN == 192;
 constexpr int DEFER = QRNG_GEMM_DEFER > 0 ? (QRNG_GEMM_DEFER < KC / KS ? QRNG_GEMM_DEFER : KC / KS - 1) : 1;
 static_assert(!DEFER_ON || (DEFER < A_STAGES && DEFER < KC / KS), "deferred stages stay resident in one chunk");
-static_assert(!FP4 || DEFER_ON, "the FP4 operand path is implemented for the deferred NT = 2, BN = 192 geometry");
+static_assert(!FP4 || DEFER_ON || (NT == 1 && ACC_BUFS == 2),
+              "the FP4 operand path: deferred NT = 2 / BN = 192, or one N tile with double-buffered accumulators");
 constexpr int ACC_EMPTY = DEFER_ON ? 2 : ACC_BUFS;
 // Warp roles.  The A transform uses XF_PAR warps per TMEM lane quadrant, each
 // taking every XF_PAR-th stage, so the per-stage latency chain (wait slot ->
@@ -794,6 +795,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             if (elect_one()) mma_commit(&acc_full[0]);
             __syncwarp();
         }
+    } else if (FP4 && warp == W_MMA) {
+        // E2M1, double-buffered accumulator sets (NT = 1): one elected lane runs the loop
+        if (elect_one()) {
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+                const uint32_t idesc_full = idesc_mxf4(BM, BN), idesc_last = idesc_mxf4(BM, (int)ti.nlast);
+                const uint32_t ab = it % ACC_BUFS, acc0 = ACC_COL0 + ab * NT * BN;
+                mbar_wait(&acc_empty[ab], ((it / ACC_BUFS) & 1) ^ 1);
+                tc_fence_after();
+                for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                    const uint32_t kin = ks % SPC;
+                    if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
+                    mbar_wait(&a_full[as], aph);
+                    tc_fence_after();
+                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                    const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < KS / 64; ++kk) {
+                        const uint32_t koff = kin * KS + kk * 64;
+                        const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
+#pragma unroll
+                        for (uint32_t nt = 0; nt < NT; ++nt)
+                            if (nt < ti.ntc)
+                                mma_mxf4_ss(tmem + acc0 + nt * BN, adesc,
+                                            desc_kmajor(cbase + (koff / 8 + nt * (BN / 8)) * 128, 512, 128),
+                                            nt + 1 == ti.ntc ? idesc_last : idesc_full, tmem + SF_COL, tmem + SF_COL + 8,
+                                            (ks | kk) != 0);
+                    }
+                    mma_commit(&a_empty[as]);
+                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    if (kin == SPC - 1 || ks == ti.kst - 1) {
+                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                    }
+                }
+                mma_commit(&acc_full[ab]);
+            }
+        }
+        __syncwarp();
     } else if (warp == W_MMA) {
         // the whole warp runs the issue loop converged (operands stay warp-uniform);
         // one elected lane issues each tcgen05.mma / commit
@@ -1171,6 +1212,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             const uint32_t ncols = nt < ti.ntc ? (nt + 1 == ti.ntc ? ti.nlast : (uint32_t)BN) : 0u;
             uint32_t words[BN / 32];
 #if QRNG_GEMM_PACK16
+            if constexpr (FP4) {
+                // FP32 sums: exact integers < 2^23, parity = lowest mantissa bit of F + 2^23
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t w = 0;
+                    if ((uint32_t)(32 * c) < ncols) {
+                        uint32_t v[32];
+                        tmem_ld32(lane_addr + 32 * c, v);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            w = (w << 1) | (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u);
+                    }
+                    words[c] = w;
+                }
+            } else
             // 64 columns per load: only the parity (bit 0) of each S32 sum is
             // needed and it survives truncation to 16 bits
 #pragma unroll
@@ -2257,7 +2314,9 @@ qrng_status extract_grouped(const Leaf *d_leaves, uint32_t n_leaves, uint32_t to
         const char *e = getenv("QRNG_GEMM_PACKED");
         return e ? atoi(e) != 0 : true;
     }();
-    if (FP4 && packed_ok && max_leaf_w <= kMaxPackedK) return launch<true, true>(a, s);
+    if constexpr (PACK_OK) {
+        if (packed_ok && max_leaf_w <= kMaxPackedK) return launch<true, true>(a, s);
+    }
     return launch<true, false>(a, s);
 #endif
 }
