@@ -90,7 +90,11 @@ static_assert(ACC_BUFS == 1 || NT == 1, "epilogue warp groups: one per buffer (N
 // N tile 0 and then N tile 1 (all 8 warps, half the columns each); the next
 // tile's MMAs start on N tile 0 as soon as it is drained and catch up N tile 1
 // after QRNG_GEMM_DEFER A stages, so half of the drain overlaps the MMAs.
-constexpr bool DEFER_ON = QRNG_GEMM_DEFER > 0 && NT == 2 && ACC_BUFS == 1 && BN == 192;
+constexpr bool DEFER_ON = QRNG_GEMM_DEFER > 0 && NT == 2 && ACC_BUFS == 1 && (BN == 192 || (FP4 && BN == 224));
+// deferred / packed epilogues: warp group h drains columns [GC_LO(h), GC_LO(h) + GC_N(h))
+// of an N tile (BN = 192: 96 + 96; BN = 224: 128 + 96), at most NWG words each
+constexpr uint32_t GC0 = 32 * ((BN / 32 + 1) / 2);
+constexpr int NWG = GC0 / 32;
 constexpr int DEFER = QRNG_GEMM_DEFER > 0 ? (QRNG_GEMM_DEFER < KC / KS ? QRNG_GEMM_DEFER : KC / KS - 1) : 1;
 static_assert(!DEFER_ON || (DEFER < A_STAGES && DEFER < KC / KS), "deferred stages stay resident in one chunk");
 static_assert(!FP4 || DEFER_ON || (NT == 1 && ACC_BUFS == 2),
@@ -1032,7 +1036,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         // parity, bit PACK_SHIFT N tile 1's.
         const uint32_t h = (uint32_t)(warp - W_EPI0) >> 2;
         const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
-        const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + 96 * h;
+        const uint32_t col_lo = h ? GC0 : 0u, col_n = h ? (uint32_t)BN - GC0 : GC0;
+        const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + col_lo;
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
@@ -1041,10 +1046,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             tc_fence_after();
             const uint64_t b = (uint64_t)ti.mt * BM + row;
             const uint32_t ncols0 = ti.ntc == 1 ? ti.nlast : (uint32_t)BN, ncols1 = ti.ntc == 2 ? ti.nlast : 0u;
-            uint32_t w0[3] = {0u, 0u, 0u}, w1[3] = {0u, 0u, 0u};
-            if (96 * h < ncols0) {
+            uint32_t w0[NWG], w1[NWG];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
+            for (int c = 0; c < NWG; ++c) w0[c] = w1[c] = 0u;
+            if (col_lo < ncols0) {
+#pragma unroll
+                for (int c = 0; c < NWG; ++c) {
+                    if ((uint32_t)(32 * c) >= col_n) continue;
                     uint32_t v[32];
                     tmem_ld32(quad + r * BN + 32 * c, v);
                     tmem_wait_ld();
@@ -1067,11 +1075,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             for (uint32_t nt = 0; nt < 2; ++nt) {
                 const uint32_t ncols = nt ? ncols1 : ncols0;
                 uint32_t *words = nt ? w1 : w0;
-                const uint32_t n0 = ti.n0 + nt * BN + 96 * h;
-                if (n0 >= ti.r || 96 * h >= ncols) continue;
-                const uint32_t nvalid = min(min(96u, ncols - 96 * h), ti.r - n0);
+                const uint32_t n0 = ti.n0 + nt * BN + col_lo;
+                if (n0 >= ti.r || col_lo >= ncols) continue;
+                const uint32_t nvalid = min(min(col_n, ncols - col_lo), ti.r - n0);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
+                for (int c = 0; c < NWG; ++c) {
                     const int vb = (int)nvalid - 32 * c;
                     if (vb <= 0) words[c] = 0;
                     else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
@@ -1079,7 +1087,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 if (GROUPED) {
                     uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
 #pragma unroll
-                    for (int c = 0; c < 3; ++c)
+                    for (int c = 0; c < NWG; ++c)
                         if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
                     continue;
                 }
@@ -1088,8 +1096,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 const uint64_t W0 = G_lo >> 5;
                 uint32_t prev = 0;
 #pragma unroll
-                for (int c = 0; c <= 3; ++c) {
-                    const uint32_t cw = (c < 3) ? words[c] : 0u;
+                for (int c = 0; c <= NWG; ++c) {
+                    const uint32_t cw = (c < NWG) ? words[c] : 0u;
                     const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
                     prev = cw;
                     const uint64_t W = W0 + c;
@@ -1107,7 +1115,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         // OR-ed (the output is pre-zeroed in the plain mode).
         const uint32_t h = (uint32_t)(warp - W_EPI0) >> 2;
         const uint32_t row = (uint32_t)(warp & 3) * 32 + lane;
-        const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + 96 * h;
+        const uint32_t col_lo = h ? GC0 : 0u, col_n = h ? (uint32_t)BN - GC0 : GC0;
+        const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + col_lo;
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
@@ -1117,8 +1126,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #pragma unroll
             for (uint32_t nt = 0; nt < 2; ++nt) {
                 const uint32_t ncols = nt < ti.ntc ? (nt + 1 == ti.ntc ? ti.nlast : (uint32_t)BN) : 0u;
-                uint32_t words[3] = {0u, 0u, 0u};
-                if (96 * h < ncols) {
+                uint32_t words[NWG];
+#pragma unroll
+                for (int c = 0; c < NWG; ++c) words[c] = 0u;
+                if (col_lo < ncols) {
                     uint32_t v[32];
                     uint32_t u[16];
 #if QRNG_GEMM_EXP == 4 || (QRNG_GEMM_EXP >= 16 && (QRNG_GEMM_EXP & 4))  // experiment 4: no accumulator reads
@@ -1129,22 +1140,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 #else
                     if constexpr (FP4) {
                         // FP32 sums are exact integers < 2^23: adding 2^23 puts their
-                        // parity in the lowest mantissa bit
-                        uint32_t v2[32];
-                        tmem_ld32(quad + nt * BN, v);
-                        tmem_ld32(quad + nt * BN + 32, v2);
-                        tmem_wait_ld();
+                        // parity in the lowest mantissa bit; two 32-column loads in flight
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            words[0] = (words[0] << 1) | (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u);
+                        for (int c = 0; c < NWG; c += 2) {
+                            uint32_t v2[32];
+                            if ((uint32_t)(32 * c) < col_n) tmem_ld32(quad + nt * BN + 32 * c, v);
+                            if (c + 1 < NWG && (uint32_t)(32 * (c + 1)) < col_n) tmem_ld32(quad + nt * BN + 32 * (c + 1), v2);
+                            tmem_wait_ld();
+                            if ((uint32_t)(32 * c) < col_n) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            words[1] = (words[1] << 1) | (__float_as_uint(__uint_as_float(v2[k]) + 8388608.0f) & 1u);
-                        tmem_ld32(quad + nt * BN + 64, v);
-                        tmem_wait_ld();
+                                for (int k = 0; k < 32; ++k)
+                                    words[c] = (words[c] << 1) | (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u);
+                            }
+                            if (c + 1 < NWG && (uint32_t)(32 * (c + 1)) < col_n) {
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            words[2] = (words[2] << 1) | (__float_as_uint(__uint_as_float(v[k]) + 8388608.0f) & 1u);
+                                for (int k = 0; k < 32; ++k)
+                                    words[c + 1] = (words[c + 1] << 1) |
+                                                   (__float_as_uint(__uint_as_float(v2[k]) + 8388608.0f) & 1u);
+                            }
+                        }
                     } else {
                         tmem_ld32_pack16(quad + nt * BN, v);
                         tmem_ld16_pack16(quad + nt * BN + 64, u);
@@ -1163,11 +1177,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[nt]);
-                const uint32_t n0 = ti.n0 + nt * BN + 96 * h;  // first row of these 3 words
-                if (b >= a.n_blocks || n0 >= ti.r || 96 * h >= ncols) continue;
-                const uint32_t nvalid = min(min(96u, ncols - 96 * h), ti.r - n0);  // tile end, then leaf end
+                const uint32_t n0 = ti.n0 + nt * BN + col_lo;  // first row of these words
+                if (b >= a.n_blocks || n0 >= ti.r || col_lo >= ncols) continue;
+                const uint32_t nvalid = min(min(col_n, ncols - col_lo), ti.r - n0);  // tile end, then leaf end
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
+                for (int c = 0; c < NWG; ++c) {
                     const int vb = (int)nvalid - 32 * c;
                     if (vb <= 0) words[c] = 0;
                     else if (vb < 32) words[c] &= ~(0xFFFFFFFFu >> vb);
@@ -1175,7 +1189,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 if (GROUPED) {
                     uint32_t *dst = a.yws + b * a.y_stride + ti.out_off + n0 / 32;
 #pragma unroll
-                    for (int c = 0; c < 3; ++c)
+                    for (int c = 0; c < NWG; ++c)
                         if ((uint32_t)(32 * c) < nvalid) dst[c] = words[c];
                     continue;
                 }
@@ -1184,8 +1198,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                 const uint64_t W0 = G_lo >> 5;
                 uint32_t prev = 0;
 #pragma unroll
-                for (int c = 0; c <= 3; ++c) {
-                    const uint32_t cw = (c < 3) ? words[c] : 0u;
+                for (int c = 0; c <= NWG; ++c) {
+                    const uint32_t cw = (c < NWG) ? words[c] : 0u;
                     const uint32_t ow = off ? ((prev << (32 - off)) | (cw >> off)) : cw;
                     prev = cw;
                     const uint64_t W = W0 + c;

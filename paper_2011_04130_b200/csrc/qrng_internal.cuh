@@ -115,9 +115,7 @@ struct Leaf {
 };
 // tcgen05 kernel geometry (build-time; gemm_tc.cu): rows per N tile, N tiles per
 // A stage, A ring slots, accumulator sets.
-#ifndef QRNG_GEMM_BN
-#define QRNG_GEMM_BN 192
-#endif
+
 #ifndef QRNG_GEMM_NT
 #define QRNG_GEMM_NT 2
 #endif
@@ -135,6 +133,13 @@ struct Leaf {
 #define QRNG_GEMM_FP4 0  // 2-SM variant: int8 unless -DQRNG_GEMM_FP4=1
 #else
 #define QRNG_GEMM_FP4 1  // tcgen05 kind::mxf4 operands (gemm_tc.cu)
+#endif
+#endif
+#ifndef QRNG_GEMM_BN
+#if QRNG_GEMM_FP4 && !QRNG_GEMM_2CTA
+#define QRNG_GEMM_BN 224  // E2M1: N tiles of 224 rows (448 per A stage; measured faster than 192)
+#else
+#define QRNG_GEMM_BN 192
 #endif
 #endif
 #if QRNG_GEMM_2CTA
