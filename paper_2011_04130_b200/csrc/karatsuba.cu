@@ -234,9 +234,19 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
 
 static bool plan_host(uint64_t n, uint64_t m, int max_depth, HostTables &T) {
     if (n % 128 || m == 0 || m >= n || n > (1u << 22)) return false;
-    // auto: the cost model's best tree with at most kMaxLeaves leaves
+    // auto: the cost model's best tree with at most kMaxLeaves leaves picks the
+    // depth; the tree itself is then the uniform one (every node split down to
+    // that depth), measured at least as fast as the cost model's mixed trees
+    // (profiles/kara_depths_r1q.jsonl: 2^14 d3 484 vs 443 Gbit/s, 2^15 d4 273
+    // vs 259, equal elsewhere)
     for (int depth = max_depth >= 0 ? std::min(max_depth, kMaxDepth) : auto_max_depth(n); depth >= 0; --depth)
-        if (plan_host_depth(n, m, depth, max_depth >= 0, T)) return true;
+        if (plan_host_depth(n, m, depth, max_depth >= 0, T)) {
+            if (max_depth < 0 && T.depth > 0) {
+                HostTables U;
+                if (plan_host_depth(n, m, T.depth, true, U)) T = std::move(U);
+            }
+            return true;
+        }
     return false;
 }
 
