@@ -58,7 +58,10 @@ constexpr int KS128 = KS / 128;      // 128-bit raw chunks per A stage
 constexpr int A_STAGES = FP4 ? QRNG_GEMM_ASTAGES_FP4 : QRNG_GEMM_ASTAGES;  // A ring slots (FP4: smem; i8: TMEM, 32 columns each)
 constexpr int A_STAGE_BYTES = 128 * KS / 2;  // FP4 A stage in smem: BM rows x KS nibbles
 constexpr int A_SBO = KS / 32 * 128;          // FP4 A stage: byte stride between 8-row core-matrix groups
-constexpr int KC = 1024;       // K per B chunk
+#ifndef QRNG_GEMM_KC
+#define QRNG_GEMM_KC 1024
+#endif
+constexpr int KC = QRNG_GEMM_KC;  // K per B chunk
 constexpr int SPC = KC / KS;   // A stages per B chunk
 #ifndef QRNG_GEMM_BSLOTS
 #define QRNG_GEMM_BSLOTS 3
