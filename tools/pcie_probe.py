@@ -49,3 +49,24 @@ t1, t2, t3 = timed(h2d), timed(d2h), timed(both)
 print(json.dumps({"h2d_gbs": h_in.numel() / t1 / 1e6, "d2h_gbs": h_out.numel() / t2 / 1e6,
                   "both_ms": t3, "both_h2d_equiv_gbs": h_in.numel() / t3 / 1e6,
                   "cfg2_e2e_bound_gbit_s": 134217728 / (max(t1, t2, t3) * 1e-3) / 1e9}))
+
+
+# two concurrent H2D copies of half the batch each (two copy streams)
+half = h_in.numel() // 2
+
+
+def h2d2():
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    with torch.cuda.stream(s1):
+        d_in[:half].copy_(h_in[:half], non_blocking=True)
+    with torch.cuda.stream(s2):
+        d_in[half:].copy_(h_in[half:], non_blocking=True)
+    cur.wait_stream(s1)
+    cur.wait_stream(s2)
+
+
+t4 = timed(h2d2, reps=40)
+t5 = timed(h2d, reps=40)
+print(json.dumps({"h2d_two_streams_gbs": h_in.numel() / t4 / 1e6, "h2d_again_gbs": h_in.numel() / t5 / 1e6}))
