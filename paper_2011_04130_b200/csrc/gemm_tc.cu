@@ -504,6 +504,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: total over leaves in grouped mode
     uint32_t cur = 0;                                 // leaf cursor of this role
+    if (GROUPED) {
+        pdl_release();  // the combine kernel may be scheduled as CTAs finish
+        pdl_wait();     // the Q buffers (previous kernel) are complete
+    }
     TRACE_T0(t_role);
     TRACE_DECL;
 
@@ -2275,7 +2279,12 @@ static qrng_status launch(const Args &a, cudaStream_t s) {
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
     KernelTimer tm(s, true);
-    toeplitz_gemm_kernel<GROUPED, PACKED><<<grid, NTHREADS, smem, s>>>(a);
+    if (GROUPED) {
+        const cudaError_t e = launch_pdl(toeplitz_gemm_kernel<GROUPED, PACKED>, dim3(grid), dim3(NTHREADS), smem, s, a);
+        if (e != cudaSuccess) { set_error("grouped GEMM launch: %s", cudaGetErrorString(e)); return QRNG_E_CUDA; }
+    } else {
+        toeplitz_gemm_kernel<GROUPED, PACKED><<<grid, NTHREADS, smem, s>>>(a);
+    }
     tm.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;

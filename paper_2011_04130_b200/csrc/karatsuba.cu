@@ -558,6 +558,7 @@ template <int U>
 __global__ void __launch_bounds__(512) qbuf_kernel(const uint4 *units, const uint32_t *gen_start, uint32_t n_gen,
                                                    const uint4 *raw, uint64_t n_blocks, uint32_t n, uint4 *xws,
                                                    uint32_t x_stride, uint32_t bpc) {
+    pdl_release();  // the grouped GEMM may be scheduled as CTAs finish
     const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
     const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
     const uint32_t xs4 = x_stride / 4, rs4 = n / 128;
@@ -848,6 +849,7 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
             : "memory");
     };
     for (uint32_t i = threadIdx.x; i < csr_words; i += blockDim.x) Cs[i] = __ldg(csr + i);
+    pdl_wait();  // the leaf parities (previous kernel) are complete
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar)) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar + 1)) : "memory");
@@ -1141,8 +1143,10 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         const uint64_t groups = (n_blocks + bpc - 1) / bpc, cap = (uint64_t)sms * std::max(per_sm, 1);
         KernelTimer tc(s, true, 1);
         const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
-        csr_stream_pack_kernel<<<(unsigned)(groups < cap ? groups : cap), QRNG_CSR_THREADS, stream_smem, s>>>(
-            t->csr, csr_words, yws, H.y_stride, n_blocks, (uint32_t)m, bpc, m_magic, out);
+        const cudaError_t le = launch_pdl(csr_stream_pack_kernel, dim3((unsigned)(groups < cap ? groups : cap)),
+                                          dim3(QRNG_CSR_THREADS), stream_smem, s, t->csr, csr_words,
+                                          (const uint32_t *)yws, H.y_stride, n_blocks, (uint32_t)m, bpc, m_magic, out);
+        if (le != cudaSuccess) { set_error("csr_stream_pack_kernel: %s", cudaGetErrorString(le)); st = QRNG_E_CUDA; }
         tc.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_stream_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && csr_smem <= 200 * 1024) {

@@ -53,6 +53,40 @@ struct OutStream {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl() may start
+// (prologue) while the previous kernel in the stream finishes; pdl_wait() blocks
+// until that kernel has completed and its memory is visible.  pdl_release()
+// lets the next PDL-launched kernel be scheduled early.
+__device__ __forceinline__ void pdl_wait() {
+#ifndef QRNG_NO_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_release() {
+#ifndef QRNG_NO_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+#ifdef QRNG_NO_PDL
+    cfg.numAttrs = 0;  // plain stream order
+#else
+    cfg.numAttrs = 1;
+#endif
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Write logical word W.  `exclusive` = every bit of W belongs to the caller.
 __device__ __forceinline__ void emit_word(const OutStream &o, uint64_t W, uint32_t logical,
                                           bool exclusive) {
