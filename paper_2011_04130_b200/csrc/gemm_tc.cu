@@ -114,7 +114,10 @@ constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4 * XF
               N_EPI = 8;
 constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
 static_assert(A_STAGES % XF_PAR == 0, "each transform warp owns fixed ring slots");
-constexpr int PF = KS > 256 ? 2 : 4;  // A-transform prefetch depth (stages)
+#ifndef QRNG_GEMM_PF
+#define QRNG_GEMM_PF (KS > 256 ? 2 : 4)
+#endif
+constexpr int PF = QRNG_GEMM_PF;  // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
 #if !QRNG_GEMM_2CTA
 static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile");
