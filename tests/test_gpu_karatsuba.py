@@ -151,3 +151,23 @@ def test_guard_bytes_untouched(q, oracle_mod):
         q.set_karatsuba(-1)
     assert_same(got[:nb], oracle_mod.extract(raw, B, n, m, seed), m)
     assert (got[nb:] == 0xEE).all()
+
+
+def test_back_to_back_mixed_plans_one_stream(q, oracle_mod):
+    """Karatsuba extractions of different shapes queued back to back on one
+    stream without synchronisation (the Q-buffer, leaf-GEMM and combine kernels
+    are chained with programmatic dependent launch): every key is still exact."""
+    shapes = [(8192, 5734, 33), (16384, 11468, 7), (4096, 2867, 65), (8192, 5734, 17), (32768, 22937, 3)]
+    jobs = []
+    for k, (n, m, B) in enumerate(shapes):
+        raw = S.random_bytes(9000 + k, B * n // 8)
+        seed = S.random_bytes(9000 + k, (n + m - 1 + 7) // 8, tag=4)
+        jobs.append((n, m, B, raw, seed, dev(raw), dev(seed)))
+    q.set_debug_path(q.PATH_GEMM)
+    try:
+        outs = [q.toeplitz_extract(dr, B, n, m, ds) for n, m, B, raw, seed, dr, ds in jobs]
+        torch.cuda.synchronize()
+    finally:
+        q.set_debug_path(q.PATH_AUTO)
+    for (n, m, B, raw, seed, _, _), out in zip(jobs, outs):
+        assert_same(out.cpu().numpy(), oracle_mod.extract(raw, B, n, m, seed), m)
