@@ -531,17 +531,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
                     mbar_wait(&a_full[as], aph);
                     tc_fence_after();
-                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
-                    const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+                    // descriptors of the stage's first MMA; the others differ only in the
+                    // start-address field (addr >> 4, no carry: shared memory < 256 KB)
+                    const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + as * A_STAGE_BYTES), 128, A_SBO);
+                    const uint64_t bdesc0 =
+                        desc_kmajor(smem_u32(chunks + bs * CHUNK_BYTES) + (kin * KS / 8) * 128, 512, 128);
 #pragma unroll
                     for (uint32_t kk = 0; kk < KS / 64; ++kk) {
-                        const uint32_t koff = kin * KS + kk * 64;
-                        const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
-                        mma_mxf4_ss(acc, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128), idesc0,
-                                    tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                        const uint64_t adesc = adesc0 + kk * 16;      // + kk * 256 bytes
+                        const uint64_t bdesc = bdesc0 + kk * 64;      // + kk * 8 core matrices
+                        mma_mxf4_ss(acc, adesc, bdesc, idesc0, tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
                         if (ti.ntc == 2)
-                            mma_mxf4_ss(acc, adesc, desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 512, 128), idesc1,
-                                        tmem + SF_COL, tmem + SF2_COL, true);
+                            mma_mxf4_ss(acc, adesc, bdesc + BN, idesc1, tmem + SF_COL, tmem + SF2_COL, true);  // + BN/8 cm
                     }
                     mma_commit(&a_empty[as]);
                     if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
@@ -637,14 +638,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
     #pragma unroll
                             for (int d = 0; d < DEFER; ++d) {
                                 if constexpr (FP4) {
-                                    const uint32_t abase = smem_u32(a_ring + dslot[d] * A_STAGE_BYTES);
+                                    const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + dslot[d] * A_STAGE_BYTES), 128, A_SBO);
+                                    const uint64_t bdesc0 = desc_kmajor(cb0 + (d * KS / 8 + BN / 8) * 128, 512, 128);
     #pragma unroll
-                                    for (uint32_t kk = 0; kk < KS / 64; ++kk) {
-                                        const uint32_t koff = d * KS + kk * 64;
-                                        mma_mxf4_ss(tmem + ACC_COL0 + BN, desc_kmajor(abase + kk * 256, 128, A_SBO),
-                                                    desc_kmajor(cb0 + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
+                                    for (uint32_t kk = 0; kk < KS / 64; ++kk)
+                                        mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc0 + kk * 16, bdesc0 + kk * 64, idesc_last,
                                                     tmem + SF_COL, tmem + SF_COL + 8, (d | kk) != 0);
-                                    }
                                 } else {
     #pragma unroll
                                     for (uint32_t kk = 0; kk < 4; ++kk) {
@@ -664,18 +663,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     TRACE_T0(tiss);
                     {
                         if constexpr (FP4) {
-                            const uint32_t abase = smem_u32(a_ring + as * A_STAGE_BYTES);
+                            // first MMA's descriptors; the others add to the start-address field
+                            const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + as * A_STAGE_BYTES), 128, A_SBO);
+                            const uint64_t bdesc0 = desc_kmajor(cbase + (kin * KS / 8) * 128, 512, 128);
     #pragma unroll
                             for (uint32_t kk = 0; kk < KS / 64; ++kk) {
-                                const uint32_t koff = kin * KS + kk * 64;
-                                const uint64_t adesc = desc_kmajor(abase + kk * 256, 128, A_SBO);
-                                mma_mxf4_ss(tmem + ACC_COL0, adesc, desc_kmajor(cbase + (koff / 8) * 128, 512, 128),
-                                            ti.ntc == 1 ? idesc_last : idesc_full, tmem + SF_COL, tmem + SF_COL + 8,
-                                            (ks | kk) != 0);
+                                const uint64_t adesc = adesc0 + kk * 16, bdesc = bdesc0 + kk * 64;
+                                mma_mxf4_ss(tmem + ACC_COL0, adesc, bdesc, ti.ntc == 1 ? idesc_last : idesc_full,
+                                            tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
                                 if (nt1_on && ti.ntc == 2)
-                                    mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc,
-                                                desc_kmajor(cbase + (koff / 8 + BN / 8) * 128, 512, 128), idesc_last,
-                                                tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                                    mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc, bdesc + BN, idesc_last, tmem + SF_COL,
+                                                tmem + SF_COL + 8, (ks | kk) != 0);
                             }
                         } else {
     #pragma unroll
