@@ -386,6 +386,7 @@ struct Tables {
     uint32_t *unit_node = nullptr; // device: unit -> node per level
     uint32_t *csr = nullptr;       // device: root word -> Y-row words (counts, then column-major entries)
     uint32_t csr_words = 0;
+    uint32_t csr_kmax = 0;         // most entries of one key word
     std::vector<gemm::Leaf> hleaves;
     uint32_t max_leaf_w = 0;       // widest leaf (K) -- the packed-accumulator kernel takes w <= 2048
 };
@@ -472,6 +473,7 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
             for (uint32_t q = 0; q < cm[j]; ++q) cm[yw + (size_t)q * yw + j] = H.comb_idx[H.comb_ptr[j] + q];
         }
         t->csr_words = (uint32_t)cm.size();
+        t->csr_kmax = kmax;
         if (e == cudaSuccess) e = cudaMalloc(&t->csr, cm.size() * 4);
         if (e == cudaSuccess) e = cudaMemcpy(t->csr, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice);
     }
@@ -824,6 +826,20 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_pack_kernel(const uint32
 __device__ __forceinline__ uint32_t ksmem(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
+// 32-bit shared-window accesses from precomputed addresses (the generic
+// pointer form re-derived the window base for every load: ~6 instructions per
+// combined word instead of an add, a load and a fused and-xor)
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// KU: CSR entries per key word handled branch-free (the table's maximum when
+// it is <= 8; padded entries are masked); entries past KU take a loop
+template <int KU>
 __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const uint32_t *csr, uint32_t csr_words,
                                                                            const uint32_t *yws, uint32_t y_stride,
                                                                            uint64_t n_blocks, uint32_t m, uint32_t bpc,
@@ -873,28 +889,32 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
         const uint64_t b0 = g * bpc;
         const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
         const uint32_t *Ys = Y0 + buf * ybuf_words;
+        const uint32_t ys_sa = ksmem(Ys), rs_sa = ksmem(Rs);
         {
             // thread (set, j): key word j of blocks set, set + sets, ...; the word's
             // CSR entries are read once and reused for every block of the group
             const uint32_t sets = max(1u, blockDim.x / rwords);
             for (uint32_t u = threadIdx.x; u < sets * rwords; u += blockDim.x) {
                 const uint32_t set = u / rwords, j = u - set * rwords;
+                const uint32_t rstep = sets * y_stride * 4, dstep = sets * rwords * 4;
+                uint32_t row = ys_sa + set * y_stride * 4, dst = rs_sa + (set * rwords + j) * 4;
                 if (j < ywords) {
                     const uint32_t c = Cs[j];
-                    uint32_t idx[8];
+                    uint32_t off[KU], msk[KU];
 #pragma unroll
-                    for (uint32_t e = 0; e < 8; ++e) idx[e] = e < c ? Cs[ywords + e * ywords + j] : 0u;
-                    for (uint32_t bl = set; bl < nb; bl += sets) {
-                        const uint32_t *yr = Ys + bl * y_stride;
+                    for (int e = 0; e < KU; ++e) {
+                        off[e] = (uint32_t)e < c ? 4 * Cs[ywords + e * ywords + j] : 0u;
+                        msk[e] = (uint32_t)e < c ? ~0u : 0u;
+                    }
+                    for (uint32_t bl = set; bl < nb; bl += sets, row += rstep, dst += dstep) {
                         uint32_t v = 0;
 #pragma unroll
-                        for (uint32_t e = 0; e < 8; ++e)
-                            if (e < c) v ^= yr[idx[e]];
-                        for (uint32_t e = 8; e < c; ++e) v ^= yr[Cs[ywords + e * ywords + j]];
-                        Rs[bl * rwords + j] = v;
+                        for (int e = 0; e < KU; ++e) v ^= lds32(row + off[e]) & msk[e];
+                        for (uint32_t e = KU; e < c; ++e) v ^= lds32(row + 4 * Cs[ywords + e * ywords + j]);
+                        sts32(dst, v);
                     }
                 } else {
-                    for (uint32_t bl = set; bl < nb; bl += sets) Rs[bl * rwords + j] = 0;
+                    for (uint32_t bl = set; bl < nb; bl += sets, dst += dstep) sts32(dst, 0);
                 }
             }
         }
@@ -917,17 +937,15 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
                     const uint32_t s0 = bl * m, s1 = s0 + m;  // bit range of block bl in the group
                     const uint32_t W = (s0 + 31) / 32 + k;    // k-th word starting inside block bl
                     if (32 * W >= s1) continue;  // block bl has fewer words (other blocks may not)
-                    const uint32_t *row = Rs + bl * rwords;
-                    const uint32_t i0 = 32 * W - s0, q = i0 >> 5, sft = i0 & 31;
-                    uint32_t word;
-                    if (32 * W + 32 <= s1) {
-                        word = sft ? ((row[q] << sft) | (row[q + 1] >> (32 - sft))) : row[q];
-                    } else {
+                    const uint32_t i0 = 32 * W - s0, sft = i0 & 31;
+                    const uint32_t ra = rs_sa + (bl * rwords + (i0 >> 5)) * 4;
+                    // row[q + 1] exists (rwords = ywords + 1, the pad word is 0)
+                    uint32_t word = __funnelshift_l(lds32(ra + 4), lds32(ra), sft);
+                    if (32 * W + 32 > s1) {
                         // tail of block bl (len1 bits), then the head of block bl + 1
                         const uint32_t len1 = s1 - 32 * W;
-                        const uint32_t hi = sft ? ((row[q] << sft) | (row[q + 1] >> (32 - sft))) : row[q];
-                        word = hi & ~(0xFFFFFFFFu >> len1);
-                        if (bl + 1 < nb) word |= Rs[(bl + 1) * rwords] >> len1;
+                        word &= ~(0xFFFFFFFFu >> len1);
+                        if (bl + 1 < nb) word |= lds32(rs_sa + (bl + 1) * rwords * 4) >> len1;
                     }
                     emit_word(out, wbase + W, word, true);
                 }
@@ -1135,15 +1153,18 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_gather_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && stream_smem <= 200 * 1024 && stream_form) {
         // the same, persistent, with the next group's rows in flight (TMA bulk copies)
-        if (stream_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_stream_pack_kernel));
+        auto kern = t->csr_kmax <= 2 ? csr_stream_pack_kernel<2>
+                    : t->csr_kmax <= 4 ? csr_stream_pack_kernel<4>
+                                       : csr_stream_pack_kernel<8>;
+        if (stream_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(kern));
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_stream_pack_kernel, QRNG_CSR_THREADS, stream_smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QRNG_CSR_THREADS, stream_smem);
         const uint64_t groups = (n_blocks + bpc - 1) / bpc, cap = (uint64_t)sms * std::max(per_sm, 1);
         KernelTimer tc(s, true, 1);
         const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
-        const cudaError_t le = launch_pdl(csr_stream_pack_kernel, dim3((unsigned)(groups < cap ? groups : cap)),
+        const cudaError_t le = launch_pdl(kern, dim3((unsigned)(groups < cap ? groups : cap)),
                                           dim3(QRNG_CSR_THREADS), stream_smem, s, t->csr, csr_words,
                                           (const uint32_t *)yws, H.y_stride, n_blocks, (uint32_t)m, bpc, m_magic, out);
         if (le != cudaSuccess) { set_error("csr_stream_pack_kernel: %s", cudaGetErrorString(le)); st = QRNG_E_CUDA; }
