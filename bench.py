@@ -220,31 +220,41 @@ def run_ours(args):
         path = pl.path
         pinfo = pl.info()
     pack = ntt_two_blocks(w, modified)
-    # timed region
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    # the main extraction kernel(s) timed inside the timed region (two event
-    # records per launch on their stream); the auxiliary kernels in a separate pass
-    q.kernel_timing(True, aux=False)
-    q.kernel_time_ms()  # clear
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = q.launch_count()
-    with ClockSampler(local) as clk:
+    def timed_pass(kernel_events):
+        """K steps, L2 flushed between them outside the step events.  With
+        kernel_events the main extraction kernel(s) are also bracketed by CUDA
+        event records on their own launching stream inside libqrng; those
+        records sit between the chained kernels of a step (Q buffers -> leaf
+        GEMM -> combine, programmatic dependent launch) and cost the chain its
+        overlap (measured +9 us per config-2 step), so the headline pass runs
+        without them and an identical second pass times the kernel."""
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        q.kernel_timing(kernel_events, aux=False)
+        q.kernel_time_ms()  # clear
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = q.launch_count()
         for i in range(args.steps):
             flush.zero_()  # L2 flush, outside the events
             starts[i].record(stream)
             step()
             ends[i].record(stream)
         torch.cuda.synchronize()
-    launches = q.launch_count() - launches0
-    if world > 1:
-        dist.barrier()
-    ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    ms_total = sum(ms_steps)
-    kern_ms, kern_n, _, _ = q.kernel_time_split()
-    q.kernel_timing(False)
+        nl = q.launch_count() - l0
+        if world > 1:
+            dist.barrier()
+        ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+        km, kn, _, _ = q.kernel_time_split()
+        q.kernel_timing(False)
+        return ms, nl, km, kn
+
+    # timed region
+    with ClockSampler(local) as clk:
+        ms_total, launches, _, _ = timed_pass(False)
+    # the same K steps again with the main kernel(s) timed live (roofline)
+    ms_total_kt, _, kern_ms, kern_n = timed_pass(True)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -369,9 +379,9 @@ def run_ours(args):
             # multi-pass batches overlap on two streams: the summed per-launch
             # times then exceed the step, so the butterflies are divided by the
             # device time of the whole step instead
-            share = (kern_ms / args.steps) / (ms_total / args.steps)
+            share = (kern_ms / args.steps) / (ms_total_kt / args.steps)
             if share > 1.0:
-                per_step_s = ms_total / args.steps * 1e-3
+                per_step_s = ms_total_kt / args.steps * 1e-3
             achieved = work / per_step_s / 1e9
             peak = q.butterfly_rate() / 1e9
             roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
@@ -388,7 +398,10 @@ def run_ours(args):
         roof["traffic"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
         roof["kernel_ms_per_step"] = kern_ms / args.steps  # summed per-launch device times
         roof["kernel_launches_per_step"] = kern_n / args.steps
-        roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total / args.steps)
+        roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total_kt / args.steps)
+        roof["kernel_timing"] = ("CUDA events on the kernel's launching stream, in a second pass of the same "
+                                 "K steps (same inputs, same L2 flushes) right after the timed region")
+        roof["ms_per_step_with_kernel_events"] = ms_total_kt / args.steps
         hbm_bytes = B * w.n / 8 + B * w.m / 8
         roof["hbm_gbs_algorithmic"] = hbm_bytes / per_step_s / 1e9
         if aux_n:
