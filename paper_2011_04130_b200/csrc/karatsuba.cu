@@ -838,8 +838,16 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 // KU: CSR entries per key word handled branch-free (the table's maximum when
-// it is <= 8; padded entries are masked); entries past KU take a loop
-template <int KU>
+// it is <= 8; padded entries are masked); entries past KU take a loop.
+// FUSED (m >= 64): combine and pack in one pass -- lane l of a warp combines
+// key word 31w + l of a block and takes word + 1 from lane l + 1 by a shuffle
+// (lane 31 only feeds lane 30), so the shifted output word is formed in
+// registers; only each block's word 0 (the low part of the word straddling
+// into it) goes through shared memory.
+#ifndef QRNG_CSR_NBUF
+#define QRNG_CSR_NBUF 2  // leaf-parity group buffers in flight per CTA
+#endif
+template <int KU, bool FUSED>
 __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const uint32_t *csr, uint32_t csr_words,
                                                                            const uint32_t *yws, uint32_t y_stride,
                                                                            uint64_t n_blocks, uint32_t m, uint32_t bpc,
@@ -848,9 +856,9 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
     const uint32_t ywords = (m + 31) / 32, rwords = ywords + 1;
     const uint32_t ybuf_words = bpc * y_stride;
     uint32_t *Y0 = reinterpret_cast<uint32_t *>(sm4);
-    uint32_t *Rs = Y0 + 2 * ybuf_words;
+    uint32_t *Rs = Y0 + QRNG_CSR_NBUF * ybuf_words;
     uint32_t *Cs = Rs + bpc * rwords;
-    const uint32_t bar_off = (2 * ybuf_words + bpc * rwords + csr_words + 1) & ~1u;  // 8-byte aligned
+    const uint32_t bar_off = (QRNG_CSR_NBUF * ybuf_words + bpc * rwords + csr_words + 1) & ~1u;  // 8-byte aligned
     uint64_t *bar = reinterpret_cast<uint64_t *>(Y0 + bar_off);
     const uint64_t n_groups = (n_blocks + bpc - 1) / bpc;
     auto issue = [&](uint64_t g, uint32_t buf) {  // one thread
@@ -867,17 +875,17 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
     for (uint32_t i = threadIdx.x; i < csr_words; i += blockDim.x) Cs[i] = __ldg(csr + i);
     pdl_wait();  // the leaf parities (previous kernel) are complete
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar)) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar + 1)) : "memory");
+        for (int i = 0; i < QRNG_CSR_NBUF; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ksmem(bar + i)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (blockIdx.x < n_groups) issue(blockIdx.x, 0);
-        if (blockIdx.x + gridDim.x < n_groups) issue(blockIdx.x + gridDim.x, 1);
+        for (uint32_t i = 0; i < QRNG_CSR_NBUF; ++i)
+            if (blockIdx.x + (uint64_t)i * gridDim.x < n_groups) issue(blockIdx.x + (uint64_t)i * gridDim.x, i);
     }
     __syncthreads();
     uint32_t k = 0;
     for (uint64_t g = blockIdx.x; g < n_groups; g += gridDim.x, ++k) {
-        const uint32_t buf = k & 1, ph = (k >> 1) & 1;
+        const uint32_t buf = k % QRNG_CSR_NBUF, ph = (k / QRNG_CSR_NBUF) & 1;
         {
             uint32_t done = 0;
             do {
@@ -890,6 +898,56 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
         const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
         const uint32_t *Ys = Y0 + buf * ybuf_words;
         const uint32_t ys_sa = ksmem(Ys), rs_sa = ksmem(Rs);
+        if (FUSED && m >= 64) {
+            const uint32_t c0 = Cs[0];
+            for (uint32_t bl = threadIdx.x; bl < nb; bl += blockDim.x) {  // heads: key word 0 of each block
+                const uint32_t row = ys_sa + bl * y_stride * 4;
+                uint32_t v = 0;
+                for (uint32_t e = 0; e < c0; ++e) v ^= lds32(row + 4 * Cs[ywords + e * ywords]);
+                sts32(rs_sa + bl * 4, v);
+            }
+            __syncthreads();
+            const uint32_t lane = threadIdx.x & 31, wpb = ywords + 1;  // >= words starting in one block
+            const uint32_t tps = 32 * ((wpb + 30) / 31);                // threads per block set (whole warps)
+            const uint32_t sets = max(1u, blockDim.x / tps);
+            const uint64_t wbase = b0 * m / 32;
+            for (uint32_t u = threadIdx.x; u < sets * tps; u += blockDim.x) {  // warp-uniform bounds
+                const uint32_t set = u / tps, kk = 31 * ((u - set * tps) >> 5) + lane;
+                const uint32_t c = kk < ywords ? Cs[kk] : 0u;
+                uint32_t off[KU], msk[KU];
+#pragma unroll
+                for (int e = 0; e < KU; ++e) {
+                    off[e] = (uint32_t)e < c ? 4 * Cs[ywords + e * ywords + kk] : 0u;
+                    msk[e] = (uint32_t)e < c ? ~0u : 0u;
+                }
+                const uint32_t rstep = sets * y_stride * 4;
+                uint32_t row = ys_sa + set * y_stride * 4;
+                for (uint32_t bl = set; bl < nb; bl += sets, row += rstep) {
+                    uint32_t r0 = 0;
+#pragma unroll
+                    for (int e = 0; e < KU; ++e) r0 ^= lds32(row + off[e]) & msk[e];
+                    for (uint32_t e = KU; e < c; ++e) r0 ^= lds32(row + 4 * Cs[ywords + e * ywords + kk]);
+                    const uint32_t r1 = __shfl_down_sync(0xFFFFFFFFu, r0, 1);  // key word kk + 1
+                    if (lane == 31 || kk >= wpb) continue;
+                    const uint32_t s0 = bl * m, s1 = s0 + m, Wf = (s0 + 31) / 32;
+                    const uint32_t W = Wf + kk;  // kk-th word starting inside block bl
+                    if (32 * W >= s1) continue;
+                    uint32_t word = __funnelshift_l(r1, r0, 32 * Wf - s0);
+                    if (32 * W + 32 > s1) {  // tail of block bl, then the head of block bl + 1
+                        const uint32_t len1 = s1 - 32 * W;
+                        word &= ~(0xFFFFFFFFu >> len1);
+                        if (bl + 1 < nb) word |= lds32(rs_sa + (bl + 1) * 4) >> len1;
+                    }
+                    emit_word(out, wbase + W, word, true);
+                }
+            }
+            __syncthreads();  // this buffer's rows and the heads are no longer read
+            if (threadIdx.x == 0 && g + QRNG_CSR_NBUF * (uint64_t)gridDim.x < n_groups) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(g + QRNG_CSR_NBUF * (uint64_t)gridDim.x, buf);
+            }
+            continue;
+        }
         {
             // thread (set, j): key word j of blocks set, set + sets, ...; the word's
             // CSR entries are read once and reused for every block of the group
@@ -919,9 +977,9 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
             }
         }
         __syncthreads();  // Rs complete; this buffer's rows are no longer read
-        if (threadIdx.x == 0 && g + 2 * (uint64_t)gridDim.x < n_groups) {
+        if (threadIdx.x == 0 && g + QRNG_CSR_NBUF * (uint64_t)gridDim.x < n_groups) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(g + 2 * (uint64_t)gridDim.x, buf);
+            issue(g + QRNG_CSR_NBUF * (uint64_t)gridDim.x, buf);
         }
         const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
         const uint64_t wbase = b0 * m / 32;
@@ -1137,7 +1195,7 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         const char *e = getenv("QRNG_CSR_STREAM");
         return e ? atoi(e) != 0 : true;
     }();
-    const size_t stream_smem = (((size_t)2 * bpc * H.y_stride + (size_t)bpc * (ywords + 1) + csr_words + 1) & ~(size_t)1) * 4 + 16;
+    const size_t stream_smem = (((size_t)QRNG_CSR_NBUF * bpc * H.y_stride + (size_t)bpc * (ywords + 1) + csr_words + 1) & ~(size_t)1) * 4 + 8 * QRNG_CSR_NBUF;
     if (st == QRNG_OK && gather) {
         // one thread per output word, gathers from L2 (no staging)
         const uint64_t gwords = ((uint64_t)n_blocks * m + 31) / 32;
@@ -1153,9 +1211,16 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_gather_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && stream_smem <= 200 * 1024 && stream_form) {
         // the same, persistent, with the next group's rows in flight (TMA bulk copies)
-        auto kern = t->csr_kmax <= 2 ? csr_stream_pack_kernel<2>
-                    : t->csr_kmax <= 4 ? csr_stream_pack_kernel<4>
-                                       : csr_stream_pack_kernel<8>;
+        static const bool fused = [] {  // QRNG_CSR_FUSED=0: separate combine and pack phases
+            const char *e = getenv("QRNG_CSR_FUSED");
+            return e ? atoi(e) != 0 : true;
+        }();
+        auto kern = fused ? (t->csr_kmax <= 2   ? csr_stream_pack_kernel<2, true>
+                             : t->csr_kmax <= 4 ? csr_stream_pack_kernel<4, true>
+                                                : csr_stream_pack_kernel<8, true>)
+                          : (t->csr_kmax <= 2   ? csr_stream_pack_kernel<2, false>
+                             : t->csr_kmax <= 4 ? csr_stream_pack_kernel<4, false>
+                                                : csr_stream_pack_kernel<8, false>);
         if (stream_smem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(kern));
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
