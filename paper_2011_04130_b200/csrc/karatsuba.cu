@@ -857,8 +857,10 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
     const uint32_t ybuf_words = bpc * y_stride;
     uint32_t *Y0 = reinterpret_cast<uint32_t *>(sm4);
     uint32_t *Rs = Y0 + QRNG_CSR_NBUF * ybuf_words;
-    uint32_t *Cs = Rs + bpc * rwords;
-    const uint32_t bar_off = (QRNG_CSR_NBUF * ybuf_words + bpc * rwords + csr_words + 1) & ~1u;  // 8-byte aligned
+    // fused form: Rs holds only each block's word 0 (the straddle heads)
+    const uint32_t rs_words = (FUSED && m >= 64) ? bpc : bpc * rwords;
+    uint32_t *Cs = Rs + rs_words;
+    const uint32_t bar_off = (QRNG_CSR_NBUF * ybuf_words + rs_words + csr_words + 1) & ~1u;  // 8-byte aligned
     uint64_t *bar = reinterpret_cast<uint64_t *>(Y0 + bar_off);
     const uint64_t n_groups = (n_blocks + bpc - 1) / bpc;
     auto issue = [&](uint64_t g, uint32_t buf) {  // one thread
@@ -1195,7 +1197,13 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         const char *e = getenv("QRNG_CSR_STREAM");
         return e ? atoi(e) != 0 : true;
     }();
-    const size_t stream_smem = (((size_t)QRNG_CSR_NBUF * bpc * H.y_stride + (size_t)bpc * (ywords + 1) + csr_words + 1) & ~(size_t)1) * 4 + 8 * QRNG_CSR_NBUF;
+    static const bool fused = [] {  // QRNG_CSR_FUSED=0: separate combine and pack phases
+        const char *e = getenv("QRNG_CSR_FUSED");
+        return e ? atoi(e) != 0 : true;
+    }();
+    // (the fused form stages only each block's word 0 of the key rows)
+    const size_t rs_words = (fused && m >= 64) ? (size_t)bpc : (size_t)bpc * (ywords + 1);
+    const size_t stream_smem = (((size_t)QRNG_CSR_NBUF * bpc * H.y_stride + rs_words + csr_words + 1) & ~(size_t)1) * 4 + 8 * QRNG_CSR_NBUF;
     if (st == QRNG_OK && gather) {
         // one thread per output word, gathers from L2 (no staging)
         const uint64_t gwords = ((uint64_t)n_blocks * m + 31) / 32;
@@ -1211,10 +1219,6 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         if (cudaGetLastError() != cudaSuccess) { set_error("csr_gather_pack_kernel launch failed"); st = QRNG_E_CUDA; }
     } else if (st == QRNG_OK && stream_smem <= 200 * 1024 && stream_form) {
         // the same, persistent, with the next group's rows in flight (TMA bulk copies)
-        static const bool fused = [] {  // QRNG_CSR_FUSED=0: separate combine and pack phases
-            const char *e = getenv("QRNG_CSR_FUSED");
-            return e ? atoi(e) != 0 : true;
-        }();
         auto kern = fused ? (t->csr_kmax <= 2   ? csr_stream_pack_kernel<2, true>
                              : t->csr_kmax <= 4 ? csr_stream_pack_kernel<4, true>
                                                 : csr_stream_pack_kernel<8, true>)
