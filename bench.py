@@ -2,23 +2,33 @@
 """Benchmark: Toeplitz-extraction raw Gbit/s on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+                    [--scaling weak|strong] [--configs all|none|LIST] [--dry-run]
 
 One step = one pass of the whole hot path over one
 batch: the one-shot C-ABI call qrng_toeplitz_extract_async on the rank's
-blocks (seed preparation, output clear, extraction kernel, tail fix-up), with
-raw bits and seed already resident in HBM.  The default workload is
-BASELINE.json configs[1] (n = 8192, m = 5734, 16384 blocks).
+blocks (seed preparation, output clear, extraction kernel(s), tail fix-up),
+with raw bits and seed already resident in HBM.  The headline workload is
+BASELINE.json configs[1] (config 2: n = 8192, m = 5734, 16384 blocks), the
+configuration the metric is quoted on; the default line also carries a
+`configs` object with every other config (1, 3, 4a, 4b and the config-5
+block-length sweep points over the full 2^30-bit stream), each timed the same
+way, checked against the oracle and with its own roofline and CPU baseline.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): blocks are independent, so
-each rank extracts its own batch of the config's size ("scaling": "weak"); the
-seed is broadcast once from rank 0 (NCCL), nothing is exchanged in the timed
-loop, and the time is the max over ranks of the summed CUDA-event step times.
+Multi-GPU: `--gpus N` without torchrun re-launches this script under
+`torch.distributed.run` with N local ranks (NCCL; gloo when the box has fewer
+GPUs than ranks, and for --dry-run).  Under torchrun it reads
+RANK/LOCAL_RANK/WORLD_SIZE.  Blocks are independent, so a
+fixed stream of B_total blocks is split into contiguous ranges, rank r owning
+[floor(r B_total / W), floor((r+1) B_total / W)) (SURVEY 8(e),
+paper_2011_04130_b200.dist.shard_range):
+  * weak   (default for configs 1-4): B_total = W x the config's blocks
+           (per-GPU work fixed);
+  * strong (default for config 5):    B_total = the config's blocks (the one
+           fixed 2^30-bit sequence cut W ways).
+The seed is broadcast once from rank 0 (NCCL), nothing is exchanged in the
+timed loop, and the time is the max over ranks of the summed CUDA-event step
+times; every rank checks its own shard against the oracle afterwards.
 L2 is flushed (256 MiB write) between timed steps, outside the events.
-
-Also reported: the dominant kernel's roofline (CUDA events on its own stream
-inside libqrng), the end-to-end number through the host-buffer C-ABI call,
-the CPU oracle as cpu_baseline (rank 0, N=1), clocks sampled during the timed
-region, and the number of libqrng kernel launches in the timed region.
 """
 from __future__ import annotations
 
@@ -26,6 +36,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,6 +51,10 @@ sys.path.insert(0, ROOT)
 import qrng_synth as S  # noqa: E402
 
 METRIC = "Toeplitz extraction raw Gbit/s (1/2/4/8 B200), fraction of roofline"
+# the default line's `configs` object: (label, --config code)
+EXTRA_CONFIGS = [("cfg1", 1), ("cfg3", 3), ("cfg4a", 4), ("cfg4b", 41),
+                 ("cfg5_n2^10", 10), ("cfg5_n2^13", 13), ("cfg5_n2^16", 16), ("cfg5_n2^18", 18),
+                 ("cfg5_n2^19", 19), ("cfg5_n2^22", 22)]
 
 
 def peaks():
@@ -50,14 +65,32 @@ def peaks():
                 "sm_max_mhz": 1965.0}, "fallback"
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
 def workload(cfg: int) -> S.Workload:
-    if cfg == 41:  # config 4b: m from qrng_minentropy, resolved in run_ours / run_reference
+    if cfg == 41:  # config 4b: m from qrng_minentropy, resolved at run time
         return S.CONFIGS[4]
     if cfg in S.CONFIGS:
         return S.CONFIGS[cfg]
     if cfg >= 10:  # sweep point: --config 10..22 means config 5 at n = 2^cfg
         return S.sweep_workload(cfg)
     raise SystemExit(f"unknown config {cfg}")
+
+
+def default_scaling(cfg: int) -> str:
+    return "strong" if cfg >= 10 else "weak"
 
 
 class ClockSampler:
@@ -107,10 +140,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False,
+def algorithmic_work(q, path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False,
                      macs_per_block: int = 0):
     """Roofline numerators, per step of the main kernel(s)."""
-    import paper_2011_04130_b200 as q
     if path == q.PATH_GEMM:
         # tensor-core ops (E2M1 or int8): 2 x the leaf MACs of the Karatsuba
         # decomposition (= 2 m n per block for the dense product, depth 0)
@@ -124,12 +156,13 @@ def algorithmic_work(path: int, w: S.Workload, n_blocks: int, pack: bool, modifi
 
 def ncu_traffic(workload_name: str, path_name: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
+    kernel from a committed ncu --set full capture (profiles/ncu_traffic.json)."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return t.get(f"{workload_name}/{path_name}", {}).get("bytes_per_launch")
+        e = t.get(f"{workload_name}/{path_name}", {})
+        return e.get("bytes_per_launch"), e.get("source")
     except Exception:
-        return None
+        return None, None
 
 
 def ntt_two_blocks(w: S.Workload, modified: bool) -> bool:
@@ -147,63 +180,183 @@ def alu_peak_gbfly(pk):
     return 148 * 128 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 7 / 1e9
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-    import paper_2011_04130_b200 as q
+# ---------------------------------------------------------------------------
+# process group
+# ---------------------------------------------------------------------------
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one process per GPU; QRNG_BENCH_BACKEND=gloo lets the multi-rank plumbing be
-    # smoke-tested with fewer GPUs than ranks (ranks never wait on each other)
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    if world > 1:
-        backend = os.environ.get("QRNG_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    q.load_library()
-    w = workload(args.config)
-    B = w.n_blocks
-    # rank r owns blocks [r*B, (r+1)*B) of a world*B-block stream (weak scaling)
-    raw_np = S.adc_samples(w.key, B * w.n // 8, w.mu, w.sigma, start=rank * B * w.n // 8)
+class Ctx:
+    def __init__(self, args):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dry = args.dry_run
+        self.backend = None
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            self.dist = dist
+            self.backend = os.environ.get("QRNG_BENCH_BACKEND", "gloo" if self.dry else "nccl")
+        if not self.dry:
+            import torch
+            # one process per GPU; with QRNG_BENCH_BACKEND=gloo several ranks may
+            # share a GPU (plumbing check) -- ranks never wait on each other in a kernel
+            self.local = self.local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(self.local)
+        if self.world > 1:
+            import torch
+            if self.backend == "nccl":
+                self.dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                self.dist.init_process_group(self.backend)
+
+    @property
+    def coll_device(self):
+        return "cuda" if self.backend == "nccl" else "cpu"
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def allreduce(self, vals, op="max"):
+        """All-reduce a list of floats (max or sum) over ranks."""
+        if self.world == 1:
+            return list(vals)
+        import torch
+        t = torch.tensor(vals, dtype=torch.float64, device=self.coll_device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return [float(v) for v in t.cpu().tolist()]
+
+    def broadcast_seed(self, seed_np):
+        """The seed drawn on rank 0 reaches every rank by one broadcast (N1)."""
+        import torch
+        dev = "cuda" if not self.dry else "cpu"
+        seed = torch.empty(seed_np.size, dtype=torch.uint8, device=dev)
+        if self.rank == 0:
+            seed.copy_(torch.from_numpy(seed_np))
+        if self.world > 1:
+            from paper_2011_04130_b200 import dist as qd
+            if self.coll_device == "cpu" and seed.device.type != "cpu":
+                tmp = seed.cpu()
+                qd.broadcast_seed(tmp, 0)
+                seed.copy_(tmp)
+            else:
+                qd.broadcast_seed(seed, 0)
+        return seed
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def launch_ranks(args) -> int:
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run
+    with N local ranks on 127.0.0.1 (one process per GPU)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    if args.dry_run:
+        env["QRNG_BENCH_BACKEND"] = "gloo"
+    else:
+        try:
+            import torch
+            if torch.cuda.device_count() < args.gpus:
+                env.setdefault("QRNG_BENCH_BACKEND", "gloo")
+                print(f"bench: {torch.cuda.device_count()} GPU(s) for {args.gpus} ranks: gloo process group, "
+                      "ranks share GPUs (no rank waits on another in a kernel)", file=sys.stderr)
+        except Exception:
+            pass
+    env.setdefault("NCCL_DEBUG", "INFO")           # rank count visible in the NCCL init log
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+# ---------------------------------------------------------------------------
+# one workload
+# ---------------------------------------------------------------------------
+
+_RAW_CACHE: dict = {}
+
+
+def shard_samples(w: S.Workload, b0: int, b1: int) -> np.ndarray:
+    key = (w.key, w.mu, w.sigma, b0 * w.n // 8, (b1 - b0) * w.n // 8)
+    if key not in _RAW_CACHE:
+        _RAW_CACHE.clear()  # one stream at a time (config 5's points share theirs)
+        _RAW_CACHE[key] = S.adc_samples(w.key, (b1 - b0) * w.n // 8, w.mu, w.sigma, start=b0 * w.n // 8)
+    return _RAW_CACHE[key]
+
+
+def parity_check(q, out_np: np.ndarray, raw_np: np.ndarray, seed_np: np.ndarray, w: S.Workload, B: int,
+                 b_first: int, modified: bool, rows_per_block: int = 64, seed: int = 0):
+    """The keys produced by the timed steps against the CPU oracle (after the
+    timed region): first / last / middle / random blocks of this rank's shard,
+    first and last rows plus random rows of each, bit for bit.  Returns
+    (checked bits, mismatches, description)."""
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(seed)
+    blocks = sorted({0, B - 1, B // 2, *rng.integers(0, B, 3).tolist()})
+    bl, rw = [], []
+    for b in blocks:
+        rows = np.unique(np.concatenate([[0, w.m - 1], rng.integers(0, w.m, rows_per_block)]))
+        bl += [b] * rows.size
+        rw += rows.tolist()
+    bl, rw = np.array(bl, np.uint64), np.array(rw, np.uint64)
+    if modified:
+        ref = oracle.modified_rows(raw_np, bl, rw, w.n, w.m, seed_np)
+    else:
+        ref = oracle.extract_rows(raw_np, bl, rw, w.n, w.m, seed_np)
+    pos = (bl * w.m + rw).astype(np.int64)
+    got = (out_np[pos >> 3] >> (7 - (pos & 7))) & 1
+    bad = int(np.count_nonzero(got != ref))
+    gblocks = [b_first + b for b in blocks]
+    return int(pos.size), bad, f"{pos.size} sampled key bits of blocks {gblocks}"
+
+
+def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
+    """Time one workload on this rank's shard; returns the JSON-able dict
+    (rank 0's view, times max-reduced over ranks)."""
+    import torch
+    w = workload(cfg)
+    scaling = args.scaling or default_scaling(cfg)
+    W, r = ctx.world, ctx.rank
+    from paper_2011_04130_b200 import dist as qd
     entropy_info = None
-    if args.config == 41:
-        # config 4b: m from the corrected min-entropy of the samples,
-        # s = 0; under torchrun the 256 counts of every rank's shard are summed
+    if cfg == 41:
+        # config 4b (SURVEY A8): m from the corrected min-entropy of config 4's
+        # samples (s = 0); each rank histograms its share, the counts are summed
+        c4 = S.CONFIGS[4]
+        lo, hi = qd.shard_range(c4.n_blocks, r, W)
+        samples = torch.from_numpy(shard_samples(c4, lo, hi)).cuda()
         counts = torch.zeros(256, dtype=torch.int64, device="cuda")
-        samples = torch.from_numpy(raw_np).cuda()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         q.hist256_async(samples, counts)
         e1.record()
-        if world > 1:
-            from paper_2011_04130_b200 import dist as qd
-            qd.allreduce_counts(counts)
-        rep = q.entropy_from_counts(counts.cpu().numpy().astype(np.uint64), 8, w.n, 0)
         torch.cuda.synchronize()
+        if W > 1:
+            c = counts.to(ctx.coll_device)
+            qd.allreduce_counts(c)
+            counts.copy_(c)
+        rep = q.entropy_from_counts(counts.cpu().numpy().astype(np.uint64), 8, c4.n, 0)
         w = S.config4b(rep.m)
         entropy_info = {"m_from_minentropy": int(rep.m), "h_min_hist": rep.h_min_hist,
                         "h_min_ideal": rep.h_min_ideal, "stat_dist": rep.stat_dist,
                         "delta_h_m": rep.delta_h_m, "h_min_mod": rep.h_min_mod,
                         "hist_ms": e0.elapsed_time(e1)}
         del samples
+    B_total = w.n_blocks * W if scaling == "weak" else w.n_blocks
+    b0, b1 = qd.shard_range(B_total, r, W)
+    B = b1 - b0
     modified = args.variant == "modified"
+    raw_np = shard_samples(w, b0, b1)
     seed_np = S.uniform_bits(w.key, w.n, tag=9) if modified else S.workload_inputs(w, 0, 1)[1]
-    seed = torch.empty(seed_np.size, dtype=torch.uint8, device="cuda")
-    if rank == 0:
-        seed.copy_(torch.from_numpy(seed_np))
-    if world > 1:
-        from paper_2011_04130_b200 import dist as qd
-        qd.broadcast_seed(seed, 0)  # N1: the one collective, outside the timed loop
+    seed = ctx.broadcast_seed(seed_np)
     raw = torch.from_numpy(raw_np).cuda()
     out = torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8, device="cuda")
-    if args.path != "auto":
-        q.set_debug_path({"gemm": q.PATH_GEMM, "ntt": q.PATH_NTT}[args.path])
-    q.set_karatsuba(args.karatsuba)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -220,6 +373,7 @@ def run_ours(args):
         path = pl.path
         pinfo = pl.info()
     pack = ntt_two_blocks(w, modified)
+
     def timed_pass(kernel_events):
         """K steps, L2 flushed between them outside the step events.  With
         kernel_events the main extraction kernel(s) are also bracketed by CUDA
@@ -232,8 +386,7 @@ def run_ours(args):
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         q.kernel_timing(kernel_events, aux=False)
         q.kernel_time_ms()  # clear
-        if world > 1:
-            dist.barrier()
+        ctx.barrier()
         torch.cuda.synchronize()
         l0 = q.launch_count()
         for i in range(args.steps):
@@ -243,23 +396,20 @@ def run_ours(args):
             ends[i].record(stream)
         torch.cuda.synchronize()
         nl = q.launch_count() - l0
-        if world > 1:
-            dist.barrier()
-        ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+        ctx.barrier()
+        per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         km, kn, _, _ = q.kernel_time_split()
         q.kernel_timing(False)
-        return ms, nl, km, kn
+        return sum(per), per, nl, km, kn
 
     # timed region
-    with ClockSampler(local) as clk:
-        ms_total, launches, _, _ = timed_pass(False)
+    with ClockSampler(ctx.local) as clk:
+        ms_total, per_step, launches, _, _ = timed_pass(False)
+    out_np = out.cpu().numpy()  # the keys of the last timed step (checked below)
     # the same K steps again with the main kernel(s) timed live (roofline)
-    ms_total_kt, _, kern_ms, kern_n = timed_pass(True)
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    bits_all = float(w.raw_bits) * world * args.steps
+    ms_total_kt, _, _, kern_ms, kern_n = timed_pass(True)
+    ms_max, = ctx.allreduce([ms_total], "max")
+    bits_all = float(B_total) * w.n * args.steps
     value = bits_all / (ms_max * 1e-3) / 1e9
 
     # ---- steady state: the plan (seed preparation) reused ----
@@ -268,8 +418,7 @@ def run_ours(args):
             pl.extract(raw, B, out=out, stream=stream)
         ss0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ss1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        if world > 1:
-            dist.barrier()
+        ctx.barrier()
         torch.cuda.synchronize()
         for i in range(args.steps):
             flush.zero_()
@@ -277,11 +426,8 @@ def run_ours(args):
             pl.extract(raw, B, out=out, stream=stream)
             ss1[i].record(stream)
         torch.cuda.synchronize()
-    t_ss = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ss0, ss1))], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_ss, op=dist.ReduceOp.MAX)
-    steady = {"value": bits_all / (float(t_ss.item()) * 1e-3) / 1e9, "unit": "Gbit/s",
-              "ms_per_step": float(t_ss.item()) / args.steps,
+    t_ss, = ctx.allreduce([sum(a.elapsed_time(b) for a, b in zip(ss0, ss1))], "max")
+    steady = {"value": bits_all / (t_ss * 1e-3) / 1e9, "unit": "Gbit/s", "ms_per_step": t_ss / args.steps,
               "step": "qrng_plan_extract with the plan created once (seed preparation excluded)"}
 
     # auxiliary kernels (Karatsuba Q buffers + combine/pack, modified repack/XOR):
@@ -294,167 +440,178 @@ def run_ours(args):
     _, _, aux_ms, aux_n = q.kernel_time_split()
     q.kernel_timing(False)
 
-    # ---- end to end from pinned HOST buffers through the public API ----
-    # Streaming ingest (qrng_stream_*, the continuous-stream use of the paper):
-    # every step copies its batch host->device, extracts it with the plan and
-    # copies the key back; three steps in flight on their own streams.  Timed
-    # on the host clock with full synchronisation on both sides (the work runs
-    # on the library's internal streams), max over ranks.  Also reported: the
-    # one-shot synchronous call (plan creation + chunked pipeline per step).
+    # ---- the keys of the timed steps against the oracle (every rank, own shard) ----
+    parity = None
+    if not args.no_parity:
+        t0 = time.perf_counter()
+        nbits, bad, what = parity_check(q, out_np, raw_np, seed_np, w, B, b0, modified, seed=cfg * 131 + r)
+        tot_bits, tot_bad = ctx.allreduce([nbits, bad], "sum")
+        parity = {"status": "bit-exact" if tot_bad == 0 else f"MISMATCH ({int(tot_bad)} bits)",
+                  "checked_bits": int(tot_bits), "mismatches": int(tot_bad),
+                  "what": (f"every rank: {what.split(' of blocks')[0]} of its own shard (rank 0: "
+                           f"{what.split('sampled key bits of ')[1]}) from the last timed step, "
+                           "vs oracle_extract_rows" + (" (modified)" if modified else "")),
+                  "check_s": time.perf_counter() - t0}
+
+    # ---- end to end from pinned HOST buffers through the public API (headline) ----
     e2e = None
-    if not args.no_e2e and not modified:
-        h_raw = torch.from_numpy(raw_np).pin_memory()
-        h_seed = seed.cpu().pin_memory()
-        depth = 3
-        h_outs = [torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8).pin_memory() for _ in range(depth)]
-        hr, hs = h_raw.numpy(), h_seed.numpy()
-        hos = [h.numpy() for h in h_outs]
-        with q.Plan(w.n, w.m, seed) as splan, q.Stream(splan, B, depth=depth) as qs:
-            for i in range(depth + 1):
-                qs.submit(hr, B, hos[i % depth])
-            qs.synchronize()
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            for i in range(args.steps):
-                qs.submit(hr, B, hos[i % depth])
-            qs.synchronize()
-            t_stream = time.perf_counter() - t0
-        torch.cuda.synchronize()
-        # one-shot synchronous host-buffer call (plan + chunked H2D/extract/D2H per step)
-        for _ in range(2):
-            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, hos[0], stream=stream)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        for a, b in ev:
-            flush.zero_()
-            a.record(stream)
-            q.toeplitz_extract_host(hr, B, w.n, w.m, hs, hos[0], stream=stream)
-            b.record(stream)
-        torch.cuda.synchronize()
-        e_t = torch.tensor([t_stream * 1e3, sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-        e2e = {"value": bits_all / (float(e_t[0].item()) * 1e-3) / 1e9, "unit": "Gbit/s",
-               "h2d_bytes_per_step": int(h_raw.numel()), "d2h_bytes_per_step": int(h_outs[0].numel()),
-               "api": f"qrng_stream_submit (pinned host buffers, plan reused, {depth} batches in flight; "
-                      "host clock, synchronised)",
-               "oneshot_value": bits_all / (float(e_t[1].item()) * 1e-3) / 1e9,
-               "oneshot_api": "qrng_toeplitz_extract_host per step (plan incl. seed prep, chunked pipeline; "
-                              "CUDA events)",
-               "oneshot_h2d_bytes_per_step": int(h_raw.numel() + h_seed.numel())}
+    if headline and not args.no_e2e and not modified:
+        e2e = measure_e2e(q, ctx, args, w, B, raw_np, seed, bits_all, flush, stream)
 
     # ---- roofline of the dominant kernel ----
-    pk, pk_kind = peaks()
-    work, bound, unit = algorithmic_work(path, w, B, pack, modified, pinfo["macs_per_block"])
-    roof = None
-    if kern_n:
-        # the path's extraction kernel(s) of one step (GEMM and fused NTT: one
-        # launch; multi-pass NTT: passes + segment kernels), CUDA events on the
-        # launching stream inside libqrng
-        per_step_s = kern_ms / args.steps * 1e-3
-        if bound == "tensor":
-            achieved = work / per_step_s / 1e12
-            fp4 = q.gemm_operand_bits() == 4
-            # the contraction's own dtype: E2M1 dense = 4 x bf16, int8 = 2 x bf16
-            # (nominal ratios 9 / 4.5 / 2.25 PFLOP/s)
-            ratio = 4.0 if fp4 else 2.0
-            peak = pk["bf16_tflops"] * ratio
-            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
-                    "peak_kind": f"{pk_kind} bf16 x {ratio:g} ({'E2M1 kind::mxf4' if fp4 else 'int8'} nominal ratio)"}
-            clk_mhz = pk.get("sm_max_mhz", 1965.0)
-            macs_per_clk = 16384 if fp4 else 8192
-            roof["peak_at_sm_max_clock"] = 148 * macs_per_clk * 2 * clk_mhz * 1e6 / 1e12
-            # the tensor pipe measured live in the kernel's own stage shape (2 N tiles
-            # of 192 per elected issue, back to back, no data movement)
-            roof["peak_mma_microbench"] = 2 * q.mma_rate(5 if fp4 else 3, 192 | (192 << 9)) / 1e12
-            roof["frac_of_clock_peak"] = achieved / roof["peak_at_sm_max_clock"]
-            # the measured bf16 x nominal-ratio peak undershoots what the E2M1 pipe
-            # sustains (frac can exceed 1 on long-K leaves); against the pipe's own
-            # live rate in the kernel's stage shape:
-            roof["frac_of_mma_microbench"] = achieved / roof["peak_mma_microbench"]
-            roof["ops_per_step"] = work
-            roof["dense_ops_per_step"] = 2.0 * w.m * w.n * B  # the O(mn) product without Karatsuba
-            # the same kernel time credited with the dense product's ops (> 1 = the
-            # Karatsuba decomposition saved tensor work)
-            roof["dense_equivalent_frac"] = roof["dense_ops_per_step"] / per_step_s / 1e12 / peak
-        else:
-            # multi-pass batches overlap on two streams: the summed per-launch
-            # times then exceed the step, so the butterflies are divided by the
-            # device time of the whole step instead
-            share = (kern_ms / args.steps) / (ms_total_kt / args.steps)
-            if share > 1.0:
-                per_step_s = ms_total_kt / args.steps * 1e-3
-            achieved = work / per_step_s / 1e9
-            peak = q.butterfly_rate() / 1e9
-            roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
-                    "peak_kind": "measured live: register-resident radix-32 fwd+inv modular butterflies on all SMs "
-                                 "(qrng_debug_butterfly_rate, the kernels' own butterfly code)",
-                    "peak_derived_issue_bound": alu_peak_gbfly(pk)}
-            # the same butterflies with the inter-pass twiddle chains included
-            # (the passes' whole register-resident instruction mix): the part of
-            # the gap to `peak` the twiddles explain; the rest is shared-memory /
-            # global traffic, barriers and occupancy
-            roof["pass_rate_peak"] = q.butterfly_rate(with_twiddles=True) / 1e9
-            roof["frac_of_pass_rate"] = achieved / roof["pass_rate_peak"]
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
-        roof["kernel_ms_per_step"] = kern_ms / args.steps  # summed per-launch device times
-        roof["kernel_launches_per_step"] = kern_n / args.steps
-        roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total_kt / args.steps)
-        roof["kernel_timing"] = ("CUDA events on the kernel's launching stream, in a second pass of the same "
-                                 "K steps (same inputs, same L2 flushes) right after the timed region")
-        roof["ms_per_step_with_kernel_events"] = ms_total_kt / args.steps
-        hbm_bytes = B * w.n / 8 + B * w.m / 8
-        roof["hbm_gbs_algorithmic"] = hbm_bytes / per_step_s / 1e9
-        if aux_n:
-            # Karatsuba auxiliary stages (HBM/L2-bound): Q buffers (each reads its
-            # two halves and writes itself: 3 x the X workspace) and combine +
-            # pack (leaf parities in, packed key out)
-            aux_s = aux_ms / args.steps * 1e-3
-            if modified:  # repack (n'/8 in, K/8 out) + XOR tail (m/8 raw, m/8 key read and written)
-                kprod = (w.n - w.m + 127) // 128 * 128
-                aux_bytes = B * ((w.n - w.m) / 8 + kprod / 8 + 3 * w.m / 8)
-                aux_kernels = "modified_repack_kernel + modified_xor_tail_kernel"
-            else:
-                aux_bytes = B * (3 * 4.0 * pinfo["x_words"] + 4.0 * pinfo["y_words"] + w.m / 8)
-                aux_kernels = "qbuf_kernel + combine/pack kernel"
-            roof["aux"] = {"kernels": aux_kernels + " (own pass, outside the timed region)",
-                           "ms_per_step": aux_ms / args.steps,
-                           "launches_per_step": aux_n / args.steps, "bytes_per_step": aux_bytes,
-                           "achieved_gbs": aux_bytes / aux_s / 1e9,
-                           "frac_of_hbm": aux_bytes / aux_s / 1e9 / pk["hbm_gbs"]}
+    roof = roofline(q, args, w, B, path, pack, modified, pinfo, kern_ms, kern_n, ms_total_kt, aux_ms, aux_n)
 
-    line = {
-        "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8 bits; int32 mod-p NTT" if path == 2 else (
+    res = {
+        "value": value, "unit": "Gbit/s", "ms_per_step": ms_max / args.steps,
+        "ms_per_step_median_rank0": statistics.median(per_step), "ms_per_step_min_rank0": min(per_step),
+        "ms_per_step_max_rank0": max(per_step),
+        "steady_state": steady, "roofline": roof, "parity": parity, "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "dtype": "u8 bits; int32 mod-p NTT" if path == q.PATH_NTT else (
             "u8 bits; E2M1 0/1 x E2M1 -> fp32 tensor core (kind::mxf4, unit scales, exact)"
             if q.gemm_operand_bits() == 4 else "u8 bits; int8 x int8 -> int32 tensor core"),
-        "data": "synthetic: uint8 ADC samples clip(rint(N(128,sigma^2))) from PCG64 (qrng_synth); seeded uniform seed",
-        "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_per_gpu": B,
-                   "seed_bits": w.n if modified else w.seed_bits,
-                   "raw_bits_per_gpu": w.raw_bits, "path": {1: "gemm", 2: "ntt"}[path],
-                   "two_blocks_per_transform": bool(pack and path == 2),
-                   "karatsuba_depth": pinfo["karatsuba_depth"] if path == 1 else None,
-                   "karatsuba_leaves": pinfo["leaves"] if path == 1 else None,
+        "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_total": B_total,
+                   "blocks_per_gpu": w.n_blocks if scaling == "weak" else f"~{w.n_blocks / W:g}",
+                   "blocks_rank0": B, "seed_bits": w.n if modified else w.seed_bits,
+                   "raw_bits_total": B_total * w.n, "path": {1: "gemm", 2: "ntt"}[path],
+                   "two_blocks_per_transform": bool(pack and path == q.PATH_NTT),
+                   "karatsuba_depth": pinfo["karatsuba_depth"] if path == q.PATH_GEMM else None,
+                   "karatsuba_leaves": pinfo["leaves"] if path == q.PATH_GEMM else None,
+                   "ntt_log2_transform": pinfo["log2_transform"] if path == q.PATH_NTT else None,
                    "l2": "flushed between timed steps (256 MiB write, outside events)",
                    "variant": args.variant,
                    "step": ("one-shot qrng_modified_toeplitz_extract_async" if modified else
                             "one-shot qrng_toeplitz_extract_async") + " (seed prep + clear + extract)",
-                   "parallelism": f"block-sharded x{world}"},
-        "steady_state": steady,
-        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+                   "scaling": scaling,
+                   "partition": (f"rank r of {W} owns blocks [floor(r*{B_total}/{W}), floor((r+1)*{B_total}/{W})) "
+                                 f"of one {B_total}-block stream"),
+                   "parallelism": f"block-sharded x{W}"},
+        "e2e": e2e,
     }
     if entropy_info:
-        line["config"]["minentropy"] = entropy_info
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w, budget_s=args.cpu_budget, modified=modified)
-    if rank == 0:
-        print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+        res["config"]["minentropy"] = entropy_info
+    if ctx.rank == 0 and ctx.world == 1 and cpu_budget > 0:
+        res["cpu_baseline"] = cpu_baseline(w, budget_s=cpu_budget, modified=modified)
+    del raw, out, flush
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_e2e(q, ctx, args, w, B, raw_np, seed, bits_all, flush, stream):
+    """Streaming ingest (qrng_stream_*, the continuous-stream use of the paper):
+    every step copies its batch host->device, extracts it with the plan and
+    copies the key back; three steps in flight on their own streams.  Timed
+    on the host clock with full synchronisation on both sides (the work runs
+    on the library's internal streams), max over ranks.  Also reported: the
+    one-shot synchronous call (plan creation + chunked pipeline per step)."""
+    import torch
+    h_raw = torch.from_numpy(raw_np).pin_memory()
+    h_seed = seed.cpu().pin_memory()
+    depth = 3
+    h_outs = [torch.empty(q.out_bytes(B, w.m), dtype=torch.uint8).pin_memory() for _ in range(depth)]
+    hr, hs = h_raw.numpy(), h_seed.numpy()
+    hos = [h.numpy() for h in h_outs]
+    with q.Plan(w.n, w.m, seed) as splan, q.Stream(splan, B, depth=depth) as qs:
+        for i in range(depth + 1):
+            qs.submit(hr, B, hos[i % depth])
+        qs.synchronize()
+        torch.cuda.synchronize()
+        ctx.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            qs.submit(hr, B, hos[i % depth])
+        qs.synchronize()
+        t_stream = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    for _ in range(2):
+        q.toeplitz_extract_host(hr, B, w.n, w.m, hs, hos[0], stream=stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record(stream)
+        q.toeplitz_extract_host(hr, B, w.n, w.m, hs, hos[0], stream=stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    t_s, t_o = ctx.allreduce([t_stream * 1e3, sum(a.elapsed_time(b) for a, b in ev)], "max")
+    return {"value": bits_all / (t_s * 1e-3) / 1e9, "unit": "Gbit/s",
+            "h2d_bytes_per_step": int(h_raw.numel()), "d2h_bytes_per_step": int(h_outs[0].numel()),
+            "api": f"qrng_stream_submit (pinned host buffers, plan reused, {depth} batches in flight; "
+                   "host clock, synchronised)",
+            "oneshot_value": bits_all / (t_o * 1e-3) / 1e9,
+            "oneshot_api": "qrng_toeplitz_extract_host per step (plan incl. seed prep, chunked pipeline; "
+                           "CUDA events)",
+            "oneshot_h2d_bytes_per_step": int(h_raw.numel() + h_seed.numel())}
+
+
+def roofline(q, args, w, B, path, pack, modified, pinfo, kern_ms, kern_n, ms_total_kt, aux_ms, aux_n):
+    pk, pk_kind = peaks()
+    work, bound, unit = algorithmic_work(q, path, w, B, pack, modified, pinfo["macs_per_block"])
+    if not kern_n:
+        return None
+    # the path's extraction kernel(s) of one step (GEMM and fused NTT: one
+    # launch; multi-pass NTT: passes + segment kernels), CUDA events on the
+    # launching stream inside libqrng
+    per_step_s = kern_ms / args.steps * 1e-3
+    if bound == "tensor":
+        achieved = work / per_step_s / 1e12
+        fp4 = q.gemm_operand_bits() == 4
+        # the contraction's own dtype: E2M1 dense = 4 x bf16, int8 = 2 x bf16
+        # (nominal ratios 9 / 4.5 / 2.25 PFLOP/s)
+        ratio = 4.0 if fp4 else 2.0
+        peak = pk["bf16_tflops"] * ratio
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS",
+                "peak_kind": f"{pk_kind} bf16 x {ratio:g} ({'E2M1 kind::mxf4' if fp4 else 'int8'} nominal ratio)"}
+        clk_mhz = pk.get("sm_max_mhz", 1965.0)
+        macs_per_clk = 16384 if fp4 else 8192
+        roof["peak_at_sm_max_clock"] = 148 * macs_per_clk * 2 * clk_mhz * 1e6 / 1e12
+        # the tensor pipe measured live in the kernel's own stage shape (2 N tiles
+        # of 192 per elected issue, back to back, no data movement)
+        roof["peak_mma_microbench"] = 2 * q.mma_rate(5 if fp4 else 3, 192 | (192 << 9)) / 1e12
+        roof["frac_of_clock_peak"] = achieved / roof["peak_at_sm_max_clock"]
+        roof["frac_of_mma_microbench"] = achieved / roof["peak_mma_microbench"]
+        roof["ops_per_step"] = work
+        roof["dense_ops_per_step"] = 2.0 * w.m * w.n * B  # the O(mn) product without Karatsuba
+        roof["dense_equivalent_frac"] = roof["dense_ops_per_step"] / per_step_s / 1e12 / peak
+    else:
+        # multi-pass batches overlap on two streams: the summed per-launch
+        # times then exceed the step, so the butterflies are divided by the
+        # device time of the whole step instead
+        share = (kern_ms / args.steps) / (ms_total_kt / args.steps)
+        if share > 1.0:
+            per_step_s = ms_total_kt / args.steps * 1e-3
+        achieved = work / per_step_s / 1e9
+        peak = q.butterfly_rate() / 1e9
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": unit,
+                "peak_kind": "measured live: register-resident radix-32 fwd+inv modular butterflies on all SMs "
+                             "(qrng_debug_butterfly_rate, the kernels' own butterfly code)",
+                "peak_derived_issue_bound": alu_peak_gbfly(pk)}
+        roof["pass_rate_peak"] = q.butterfly_rate(with_twiddles=True) / 1e9
+        roof["frac_of_pass_rate"] = achieved / roof["pass_rate_peak"]
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
+    roof["kernel_ms_per_step"] = kern_ms / args.steps  # summed per-launch device times
+    roof["kernel_launches_per_step"] = kern_n / args.steps
+    roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total_kt / args.steps)
+    roof["kernel_timing"] = ("CUDA events on the kernel's launching stream, in a second pass of the same "
+                             "K steps (same inputs, same L2 flushes) right after the timed region")
+    roof["ms_per_step_with_kernel_events"] = ms_total_kt / args.steps
+    hbm_bytes = B * w.n / 8 + B * w.m / 8
+    roof["hbm_gbs_algorithmic"] = hbm_bytes / per_step_s / 1e9
+    if aux_n:
+        aux_s = aux_ms / args.steps * 1e-3
+        if modified:  # repack (n'/8 in, K/8 out) + XOR tail (m/8 raw, m/8 key read and written)
+            kprod = (w.n - w.m + 127) // 128 * 128
+            aux_bytes = B * ((w.n - w.m) / 8 + kprod / 8 + 3 * w.m / 8)
+            aux_kernels = "modified_repack_kernel + modified_xor_tail_kernel"
+        else:
+            aux_bytes = B * (3 * 4.0 * pinfo["x_words"] + 4.0 * pinfo["y_words"] + w.m / 8)
+            aux_kernels = "qbuf_kernel + combine/pack kernel"
+        roof["aux"] = {"kernels": aux_kernels + " (own pass, outside the timed region)",
+                       "ms_per_step": aux_ms / args.steps,
+                       "launches_per_step": aux_n / args.steps, "bytes_per_step": aux_bytes,
+                       "achieved_gbs": aux_bytes / aux_s / 1e9,
+                       "frac_of_hbm": aux_bytes / aux_s / 1e9 / pk["hbm_gbs"]}
+    return roof
 
 
 def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modified: bool = False):
@@ -463,9 +620,7 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modifi
     consecutive blocks until ~budget_s."""
     import oracle
     oracle.build()
-    if threads == 0:
-        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else oracle.max_threads()
-    cores = threads
+    cores = threads or host_cores()
     sample_blocks = min(w.n_blocks, 4096)
     raw, seed = S.workload_inputs(w, 0, sample_blocks)
     if modified:
@@ -477,19 +632,90 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modifi
         chunk = raw[pos * w.n // 8:(pos + nb) * w.n // 8]
         t0 = time.perf_counter()
         if modified:
-            oracle.modified_extract(chunk, nb, w.n, w.m, seed, threads)
+            oracle.modified_extract(chunk, nb, w.n, w.m, seed, cores)
         else:
-            oracle.extract(chunk, nb, w.n, w.m, seed, "words", threads)
+            oracle.extract(chunk, nb, w.n, w.m, seed, "words", cores)
         t_total += time.perf_counter() - t0
         blocks_done += nb
         pos += nb
         if t_total < budget_s / 8:
             nb = min(nb * 2, sample_blocks)
     return {"value": blocks_done * w.n / t_total / 1e9, "unit": "Gbit/s", "cores": cores,
-            "kind": "oracle", "sample": f"{blocks_done} blocks (cycling over the first {sample_blocks} of "
-                                        f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, "
-                                        + ("modified Toeplitz literal loop" if modified else "word-parallel mode")
-                                        + ", OpenMP over blocks"}
+            "cpu_model": cpu_model(), "kind": "oracle",
+            "sample": f"{blocks_done} blocks (cycling over the first {sample_blocks} of "
+                      f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, "
+                      + ("modified Toeplitz literal loop" if modified else "word-parallel mode")
+                      + ", OpenMP over blocks"}
+
+
+def run_ours(args):
+    ctx = Ctx(args)
+    if ctx.dry:
+        return dry_run(ctx, args)
+    import paper_2011_04130_b200 as q
+    q.load_library()
+    if args.path != "auto":
+        q.set_debug_path({"gemm": q.PATH_GEMM, "ntt": q.PATH_NTT}[args.path])
+    q.set_karatsuba(args.karatsuba)
+    head = measure(q, ctx, args, args.config, headline=True,
+                   cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget)
+    line = {"metric": METRIC, "value": head["value"], "unit": "Gbit/s", "n_gpus": ctx.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": head["config"]["scaling"], "vs_baseline": None,
+            "dtype": head["dtype"],
+            "data": "synthetic: uint8 ADC samples clip(rint(N(128,sigma^2))) from PCG64 (qrng_synth); "
+                    "seeded uniform seed",
+            "headline": (f"{head['config']['workload']} (BASELINE.json configs[1], the configuration the metric "
+                         "is quoted on)" if args.config == 2 else head["config"]["workload"]),
+            "config": head["config"]}
+    for k in ("steady_state", "roofline", "e2e", "parity", "gpu_launches", "clocks", "cpu_baseline",
+              "ms_per_step_median_rank0", "ms_per_step_min_rank0", "ms_per_step_max_rank0"):
+        if k in head:
+            line[k] = head[k]
+    extra = []
+    if args.configs == "all":
+        extra = [c for c in EXTRA_CONFIGS if c[1] != args.config]
+    elif args.configs not in ("none", ""):
+        want = args.configs.split(",")
+        extra = [c for c in EXTRA_CONFIGS if c[0] in want or str(c[1]) in want]
+    if extra:
+        t0 = time.perf_counter()
+        line["configs"] = {}
+        for label, code in extra:
+            d = measure(q, ctx, args, code, headline=False,
+                        cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget_extra)
+            line["configs"][label] = d
+        line["configs_wall_s"] = time.perf_counter() - t0
+    pars = [line.get("parity")] + [d.get("parity") for d in line.get("configs", {}).values()]
+    if all(p is not None for p in pars):
+        bad = sum(p["mismatches"] for p in pars)
+        line["parity_all"] = ("bit-exact" if bad == 0 else f"MISMATCH ({bad} bits)") + \
+            f" ({sum(p['checked_bits'] for p in pars)} sampled key bits over {len(pars)} workloads, every rank)"
+    if ctx.rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+
+
+def dry_run(ctx: Ctx, args):
+    """--dry-run: the multi-rank plumbing without CUDA work (CPU test): shard
+    ranges, the seed broadcast and the max-over-ranks reduction."""
+    from paper_2011_04130_b200 import dist as qd
+    w = workload(args.config)
+    scaling = args.scaling or default_scaling(args.config)
+    B_total = w.n_blocks * ctx.world if scaling == "weak" else w.n_blocks
+    b0, b1 = qd.shard_range(B_total, ctx.rank, ctx.world)
+    seed_np = S.workload_inputs(w, 0, 1)[1]
+    seed = ctx.broadcast_seed(seed_np if ctx.rank == 0 else np.zeros_like(seed_np))
+    seed_ok = bool(np.array_equal(seed.numpy(), seed_np))
+    shard_all = ctx.allreduce([0.0] * (2 * ctx.rank) + [b0, b1] + [0.0] * (2 * (ctx.world - ctx.rank - 1)), "sum")
+    ok, = ctx.allreduce([1.0 if seed_ok else 0.0], "sum")
+    t, = ctx.allreduce([float(ctx.rank + 1)], "max")
+    if ctx.rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": ctx.world, "backend": ctx.backend,
+                          "scaling": scaling, "config": {"workload": w.name, "blocks_total": B_total},
+                          "shards": [[int(shard_all[2 * i]), int(shard_all[2 * i + 1])] for i in range(ctx.world)],
+                          "seed_broadcast_ok_ranks": int(ok), "max_over_ranks": t}))
+    ctx.close()
 
 
 def run_reference(args):
@@ -505,12 +731,14 @@ def run_reference(args):
         from oracle import entropy as E
         w = S.config4b(E.report(S.workload_inputs(w)[0], 8, w.n, 0).m)
     # all host cores (torchrun sets OMP_NUM_THREADS=1 for its workers)
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else oracle.max_threads()
+    cores = host_cores()
     per_step_blocks = max(cores, min(w.n_blocks, int(os.environ.get("QRNG_REF_BLOCKS", "0")) or
                                      _ref_blocks(w, cores)))
+    per_step_blocks = min(per_step_blocks, w.n_blocks)
     raw, seed = S.workload_inputs(w, 0, per_step_blocks)
     for _ in range(args.warmup):
-        oracle.extract(raw[:cores * w.n // 8], cores, w.n, w.m, seed, "words", cores)
+        nb = min(cores, per_step_blocks)
+        oracle.extract(raw[:nb * w.n // 8], nb, w.n, w.m, seed, "words", cores)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -525,7 +753,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 bit words",
         "data": "synthetic (qrng_synth)", "config": {"workload": w.name, "n": w.n, "m": w.m,
                                                      "blocks_per_step": per_step_blocks},
-        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": cores, "cpu_model": cpu_model(),
+                         "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -541,7 +770,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=2,
+                    help="1..4 = BASELINE configs, 41 = config 4b, 10..22 = config 5 at n = 2^k")
+    ap.add_argument("--configs", default="all",
+                    help="extra workloads in the line's `configs` object: all | none | comma list "
+                         "(labels or codes, e.g. cfg3,22)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="multi-GPU partition (default: weak for configs 1-4, strong for config 5)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--path", choices=["auto", "gemm", "ntt"], default="auto")
     ap.add_argument("--variant", choices=["standard", "modified"], default="standard",
@@ -550,12 +785,18 @@ def main():
                     help="GEMM path: GF(2) Karatsuba depth (-1 = the library's cost model, 0 = dense)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget-extra", type=float, default=3.0,
+                    help="oracle seconds per workload of the `configs` object")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only, no CUDA work")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     else:
         run_ours(args)
 

@@ -93,7 +93,9 @@ QRNG_API qrng_status qrng_minentropy(const uint8_t *d_samples, uint64_t n_sample
 /* Building blocks of qrng_minentropy for sharded samples (one process per
  * GPU): each rank ACCUMULATES its shard's counts into d_counts (uint64[256],
  * device, caller-zeroed) asynchronously, the caller all-reduces the 256
- * counts, then any rank finalises on the host.  h_counts is a host pointer. */
+ * counts, then any rank finalises on the host.  h_counts is a host pointer.
+ * d_samples may have any alignment (e.g. a shard slice samples[lo:hi]); the
+ * same holds for qrng_minentropy. */
 QRNG_API qrng_status qrng_hist256_async(const uint8_t *d_samples, uint64_t n_samples,
                                uint64_t *d_counts, cudaStream_t stream);
 QRNG_API qrng_status qrng_entropy_from_counts(const uint64_t *h_counts, uint32_t bit_depth,

@@ -167,6 +167,30 @@ def out_bytes(n_blocks: int, m: int) -> int:
     return (n_blocks * m + 7) // 8
 
 
+def _need_bytes(t, nbytes: int, name: str):
+    """The C ABI cannot see buffer sizes: refuse short buffers before any
+    device read or write past their end (tensor numel or numpy size)."""
+    size = t.numel() if hasattr(t, "numel") and not isinstance(t, np.ndarray) else t.size
+    if size < nbytes:
+        raise ValueError(f"{name} holds {size} bytes, needs at least {nbytes}")
+
+
+def _same_device(*ts):
+    devs = {t.device for t in ts}
+    if len(devs) != 1:
+        raise ValueError(f"tensors on different devices: {sorted(map(str, devs))}")
+
+
+def _check_extract_buffers(raw, n_blocks: int, n: int, m: int, seed, seed_bits: int, out):
+    """raw >= n_blocks*n/8 bytes, seed >= ceil(seed_bits/8), out >= ceil(n_blocks*m/8)."""
+    if n_blocks < 0 or n < 0 or m < 0:
+        raise ValueError("negative size")
+    _need_bytes(raw, (n_blocks * n + 7) // 8, "raw")
+    if seed is not None:
+        _need_bytes(seed, (seed_bits + 7) // 8, "seed")
+    _need_bytes(out, out_bytes(n_blocks, m), "out")
+
+
 def version() -> str:
     return load_library().qrng_version().decode()
 
@@ -310,6 +334,8 @@ def toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None, stream=
     if out is None:
         out = torch.empty(out_bytes(n_blocks, m), dtype=torch.uint8, device=raw.device)
     _need_cuda_u8(out, "out")
+    _same_device(raw, seed, out)
+    _check_extract_buffers(raw, n_blocks, n, m, seed, n + m - 1, out)
     _check(load_library().qrng_toeplitz_extract_async(_ptr(raw), n_blocks, n, m, _ptr(seed), _ptr(out),
                                                       _stream_handle(stream)))
     return out
@@ -323,6 +349,8 @@ def modified_toeplitz_extract(raw, n_blocks: int, n: int, m: int, seed, out=None
     if out is None:
         out = torch.empty(out_bytes(n_blocks, m), dtype=torch.uint8, device=raw.device)
     _need_cuda_u8(out, "out")
+    _same_device(raw, seed, out)
+    _check_extract_buffers(raw, n_blocks, n, m, seed, n, out)
     _check(load_library().qrng_modified_toeplitz_extract_async(_ptr(raw), n_blocks, n, m, _ptr(seed), _ptr(out),
                                                                _stream_handle(stream)))
     return out
@@ -334,8 +362,7 @@ def toeplitz_extract_host(raw: np.ndarray, n_blocks: int, n: int, m: int, seed: 
     for a in (raw, seed, out):
         if not (isinstance(a, np.ndarray) and a.dtype == np.uint8 and a.flags.c_contiguous):
             raise TypeError("host buffers must be contiguous uint8 numpy arrays")
-    if out.size < out_bytes(n_blocks, m):
-        raise ValueError("out too small")
+    _check_extract_buffers(raw, n_blocks, n, m, seed, n + m - 1, out)
     _check(load_library().qrng_toeplitz_extract_host(raw.ctypes.data, n_blocks, n, m, seed.ctypes.data,
                                                      out.ctypes.data, _stream_handle(stream)))
     return out
@@ -346,7 +373,9 @@ class Plan:
 
     def __init__(self, n: int, m: int, seed, stream=None, modified: bool = False):
         _need_cuda_u8(seed, "seed")
+        _need_bytes(seed, ((n if modified else n + m - 1) + 7) // 8, "seed")
         self.n, self.m = n, m
+        self.device = seed.device
         h = ctypes.c_void_p()
         create = load_library().qrng_plan_create_modified if modified else load_library().qrng_plan_create
         _check(create(n, m, _ptr(seed), _stream_handle(stream), ctypes.byref(h)))
@@ -368,6 +397,9 @@ class Plan:
         if out is None:
             out = torch.empty(out_bytes(n_blocks, self.m), dtype=torch.uint8, device=raw.device)
         _need_cuda_u8(out, "out")
+        if raw.device != self.device or out.device != self.device:
+            raise ValueError(f"plan lives on {self.device}; raw on {raw.device}, out on {out.device}")
+        _check_extract_buffers(raw, n_blocks, self.n, self.m, None, 0, out)
         _check(load_library().qrng_plan_extract(self._h, _ptr(raw), n_blocks, _ptr(out),
                                                 _stream_handle(stream)))
         return out
@@ -465,6 +497,7 @@ def hist256_async(samples, counts, stream=None):
     _need_cuda_u8(samples, "samples")
     if counts.dtype not in (torch.int64, torch.uint64) or counts.numel() != 256 or counts.device.type != "cuda":
         raise TypeError("counts must be a 256-element 64-bit CUDA tensor")
+    _same_device(samples, counts)
     _check(load_library().qrng_hist256_async(_ptr(samples), samples.numel(), _ptr(counts),
                                              _stream_handle(stream)))
     return counts

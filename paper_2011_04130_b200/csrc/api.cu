@@ -112,7 +112,7 @@ void KernelTimer::stop() {
 }
 
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
-static uint64_t g_gemm_max_n = 1ull << 18;  // profiles/sweep_r1h.jsonl (FP4 operands): Karatsuba GEMM 60.0 vs NTT 47.8 Gbit/s at 2^18, 33.9 vs 47.5 at 2^19
+static uint64_t g_gemm_max_n = 1ull << 18;  // profiles/sweep_r1u.jsonl (E2M1 operands): Karatsuba GEMM 68.5 vs NTT 48.5 Gbit/s at 2^18, 40.6 vs 47.5 at 2^19
 static std::atomic<int> g_debug_path{QRNG_PATH_AUTO};
 // Karatsuba depth over the GEMM path: -1 = the planner's cost model, 0 = plain
 // GEMM kernel, d > 0 = split whenever allowed down to depth d (tests).
@@ -302,9 +302,13 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     p->n = n;
     p->m = m;
     int want = g_debug_path.load();
+    const bool automatic = want == QRNG_PATH_AUTO;
     const int kd = g_kara_depth.load();
-    if (want == QRNG_PATH_AUTO) want = (n % 128 == 0 && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
+    if (automatic) want = (n % 128 == 0 && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
     if (want == QRNG_PATH_GEMM) p->kara_on = kara::choose(n, m, kd);
+    // AUTO: a shape the planner leaves undecomposed (small m at large n) that the
+    // dense kernel cannot take runs on the NTT path, which accepts every valid (n, m)
+    if (automatic && want == QRNG_PATH_GEMM && !p->kara_on && !gemm::supported(n, m)) want = QRNG_PATH_NTT;
     if (want == QRNG_PATH_GEMM && !p->kara_on && !gemm::supported(n, m)) {
         set_error("GEMM path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
         delete p;
@@ -479,10 +483,18 @@ qrng_status qrng_toeplitz_extract_host(const uint8_t *h_raw_bits, uint64_t n_blo
     const uint64_t raw_bytes = n_blocks * n / 8, seed_bytes = (n + m - 1 + 7) / 8,
                    out_bytes = (n_blocks * m + 7) / 8;
     uint8_t *d_raw = nullptr, *d_seed = nullptr, *d_out = nullptr;
-    QRNG_CUDA_TRY(cudaMallocAsync(&d_raw, raw_bytes, stream));
-    QRNG_CUDA_TRY(cudaMallocAsync(&d_seed, seed_bytes, stream));
-    QRNG_CUDA_TRY(cudaMallocAsync(&d_out, out_bytes, stream));
-    QRNG_CUDA_TRY(cudaMemcpyAsync(d_seed, h_seed, seed_bytes, cudaMemcpyHostToDevice, stream));
+    {  // on any failure here, free what was already allocated (no early return past an allocation)
+        cudaError_t e = cudaMallocAsync(&d_raw, raw_bytes, stream);
+        if (e == cudaSuccess) e = cudaMallocAsync(&d_seed, seed_bytes, stream);
+        if (e == cudaSuccess) e = cudaMallocAsync(&d_out, out_bytes, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_seed, h_seed, seed_bytes, cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) {
+            set_error("host path setup: %s", cudaGetErrorString(e));
+            for (uint8_t *ptr : {d_raw, d_seed, d_out})
+                if (ptr) cudaFreeAsync(ptr, stream);
+            return e == cudaErrorMemoryAllocation ? QRNG_E_NOMEM : QRNG_E_CUDA;
+        }
+    }
     qrng_plan *plan = nullptr;
     st = qrng_plan_create(n, m, d_seed, stream, &plan);
     // Pipeline over chunks of whole 32-block granules: every chunk's key starts

@@ -2156,7 +2156,12 @@ qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int 
 }
 
 // ---- host ------------------------------------------------------------------------
-bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n; }
+static size_t smem_bytes(uint32_t seed_words_n);
+// The non-grouped kernel stages all seed words it reads in shared memory next
+// to the operand rings, so (n, m) is also bounded by the 227 KB per CTA.
+static bool fits_smem(uint64_t n, uint64_t m) { return smem_bytes(seed_words_needed(n, m)) <= 227u * 1024u; }
+
+bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m >= 1 && m < n && fits_smem(n, m); }
 
 uint32_t seed_words_needed(uint64_t n, uint64_t m) {
     const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = (n + KS - 1) / KS, nchunks = (kst + SPC - 1) / SPC;
@@ -2384,7 +2389,7 @@ qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, 
 bool modified_supported(uint64_t n, uint64_t m) {
     if (m == 0 || m >= n || n % 32) return false;
     const uint64_t K = (n - m + 127) / 128 * 128;
-    return K <= MAX_N;
+    return K <= MAX_N && fits_smem(K, m);  // m can be far larger than K: the seed window grows with m
 }
 
 // Modified Toeplitz (api.cu): the C1 product with n = K (n' = n - m rounded up

@@ -6,7 +6,8 @@
 // sub-histograms in shared memory (Gaussian ADC data concentrates on a few
 // bins, so a single CTA histogram would serialise on the hot bins), then one
 // 64-bit global atomic per bin per CTA.  Counts are exact (uint32 in smem per
-// CTA chunk, uint64 in HBM).
+// CTA chunk, uint64 in HBM).  d_samples may have any alignment (head bytes up
+// to the first 16-byte boundary are counted with scalar loads).
 #include "qrng_internal.cuh"
 
 namespace qrng {
@@ -28,10 +29,17 @@ __global__ void __launch_bounds__(kThreads) hist256_kernel(const uint8_t *__rest
     for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&h[0][0])[i] = 0;
     __syncthreads();
     uint32_t *mine = h[threadIdx.x >> 5];
-    const uint64_t nvec = n / 16;
-    const uint4 *v = reinterpret_cast<const uint4 *>(x);
     const uint64_t tid = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
     const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
+    // any alignment: the bytes before the first 16-byte boundary are counted
+    // one by one (a shard slice samples[lo:hi] starts anywhere), then vectors
+    uint64_t head = (16u - ((uintptr_t)x & 15u)) & 15u;
+    if (head > n) head = n;
+    if (tid < head) atomicAdd(&mine[x[tid]], 1u);
+    x += head;
+    n -= head;
+    const uint64_t nvec = n / 16;
+    const uint4 *v = reinterpret_cast<const uint4 *>(x);
     for (uint64_t i = tid; i < nvec; i += nthr) {
         uint4 q = __ldcs(v + i);  // streamed once
         add4(mine, q.x);

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <array>
+#include <list>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -389,20 +390,37 @@ struct Tables {
     uint32_t csr_kmax = 0;         // most entries of one key word
     std::vector<gemm::Leaf> hleaves;
     uint32_t max_leaf_w = 0;       // widest leaf (K) -- the packed-accumulator kernel takes w <= 2048
+    ~Tables() {
+        // the last owner is the cache or a plan; cudaFree waits for the work that reads them
+        for (void *ptr : {(void *)leaves, (void *)terms, (void *)qbufs, (void *)qgen_dev, (void *)inner,
+                          (void *)levels, (void *)unit_node, (void *)csr})
+            if (ptr) cudaFree(ptr);
+    }
 };
 
-static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Tables **out) {
+// Device tables are shared by every plan of the same (device, n, m, depth) and
+// cached so that one-shot calls do not re-plan.  The cache is bounded (LRU,
+// kTableCacheCap entries): a long-running process that re-derives m from live
+// min-entropy creates a new (n, m) per re-plan, and evicted tables are freed
+// once the last plan holding them is destroyed (shared ownership).
+constexpr size_t kTableCacheCap = 16;
+
+static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, std::shared_ptr<const Tables> *out) {
+    using Key = std::tuple<int, uint64_t, uint64_t, int>;
     static std::mutex mu;
-    static std::map<std::tuple<int, uint64_t, uint64_t, int>, Tables *> cache;
+    static std::list<std::pair<Key, std::shared_ptr<const Tables>>> lru;  // front = most recent
     int dev = 0;
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(dev, n, m, max_depth);
-    auto it = cache.find(key);
-    if (it != cache.end()) { *out = it->second; return QRNG_OK; }
-    Tables *t = new Tables;
+    const Key key = std::make_tuple(dev, n, m, max_depth);
+    for (auto it = lru.begin(); it != lru.end(); ++it)
+        if (it->first == key) {
+            lru.splice(lru.begin(), lru, it);
+            *out = lru.front().second;
+            return QRNG_OK;
+        }
+    auto t = std::make_shared<Tables>();
     if (!plan_host(n, m, max_depth, t->host)) {
-        delete t;
         set_error("Karatsuba planner: no decomposition for n=%llu m=%llu", (unsigned long long)n,
                   (unsigned long long)m);
         return QRNG_E_UNSUPPORTED;
@@ -483,12 +501,11 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, const Table
         e = cudaMemcpy(t->levels, H.levels.data(), H.levels.size() * 16, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         set_error("Karatsuba tables: %s", cudaGetErrorString(e));
-        cudaFree(t->leaves); cudaFree(t->terms); cudaFree(t->inner); cudaFree(t->qbufs); cudaFree(t->levels); cudaFree(t->unit_node); cudaFree(t->csr); cudaFree(t->qgen_dev);
-        delete t;
-        return QRNG_E_CUDA;
+        return QRNG_E_CUDA;  // t's destructor frees what was allocated
     }
-    cache[key] = t;
-    *out = t;
+    lru.emplace_front(key, t);
+    while (lru.size() > kTableCacheCap) lru.pop_back();
+    *out = lru.front().second;
     return QRNG_OK;
 }
 
@@ -1085,7 +1102,7 @@ __global__ void __launch_bounds__(256) csr_gather_pack_kernel(const uint32_t *__
 
 // ---- host entry points -----------------------------------------------------
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s) {
-    const Tables *t = nullptr;
+    std::shared_ptr<const Tables> t;
     qrng_status st = get_tables(n, m, max_depth, &t);
     if (st != QRNG_OK) return st;
     pl.tab = t;
@@ -1150,7 +1167,7 @@ void describe(const Plan &pl, int *depth, int *n_leaves, uint64_t *macs_per_bloc
 
 static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                                  const OutStream &out, cudaStream_t s) {
-    const Tables *t = pl.tab;
+    const Tables *t = pl.tab.get();
     const HostTables &H = t->host;
     uint32_t *xws = nullptr, *yws = nullptr;
     if (H.x_stride) QRNG_CUDA_TRY(cudaMallocAsync(&xws, (size_t)n_blocks * H.x_stride * 4, s));

@@ -2,6 +2,7 @@
 // Product code (sm_100a).  Nothing here is shared with oracle/.
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <cuda_runtime.h>
 #include "../../include/qrng.h"
 
@@ -210,7 +211,7 @@ qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s)
 namespace kara {
 struct Tables;  // device-resident leaf / term / combine tables, cached per (n, m, depth)
 struct Plan {
-    const Tables *tab = nullptr;
+    std::shared_ptr<const Tables> tab;  // shared with the LRU table cache
     uint32_t *seeds = nullptr;  // leaf seeds (logical big-endian words)
 };
 // Chooses the decomposition for (n, m); returns false if no leaf split pays off

@@ -97,3 +97,26 @@ def test_no_decomposition_rejected():
         q.karatsuba_plan(8192 + 32, 100, 2)  # n % 128 != 0
     with pytest.raises(q.QrngError):
         q.karatsuba_plan(1024, 1024, 2)      # m >= n
+
+
+def test_adversarial_packed_precondition():
+    """tests/test_gpu_edges.py's packed-accumulator case really drives
+    S1 = 2048 next to odd S0 in leaf 0 (CPU arithmetic on the plan's own
+    leaf table; the GPU test then checks the kernel against the oracle)."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_edges import adversarial_packed_inputs
+    import paper_2011_04130_b200 as q
+    n, m, h, s, X = adversarial_packed_inputs()
+    plan = q.karatsuba_plan(n, m, 1)
+    assert plan.depth == 1
+    r, w, _, sterms, iterms = plan.leaves[0]
+    assert (r, w, sterms, sorted(iterms)) == (2048, 2048, [h], [0, h])
+    d = s[h:h + r + w - 1].astype(np.int64)
+    xq = (X[0, :h] ^ X[0, h:]).astype(np.int64)
+    # S(i) = sum_j d[i - j + w - 1] x_j
+    S0 = np.array([int(np.dot(d[i:i + w][::-1], xq)) for i in range(r)])
+    assert np.all(S0[224:] == 2048)
+    assert np.sum(S0[:224] % 2 == 1) >= 100
+    F = S0[:192] + 4096 * S0[224:224 + 192]     # a packed pair: rows c and 224 + c
+    assert np.all(F >= 1 << 23) and np.any(F % 2 == 1)

@@ -86,3 +86,22 @@ def test_two_rank_gloo_plumbing(oracle_mod):
     assert sorted(r[0] for r in res) == [0, 1]
     assert all(r[1] for r in res), "concatenated shards differ from the single-process key"
     assert all(r[2] for r in res), "all-reduced histogram differs"
+
+
+@pytest.mark.parametrize("cfg,scaling,blocks", [(2, "weak", 2 * 16384), (16, "strong", 16384)])
+def test_bench_launcher_spawns_ranks(cfg, scaling, blocks):
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks
+    (torch.distributed.run, gloo for --dry-run): the line reports n_gpus 2,
+    the SURVEY 8(e) contiguous partition and the seed broadcast on every rank."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--config", str(cfg)], capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["dry_run"] and line["scaling"] == scaling
+    assert line["config"]["blocks_total"] == blocks
+    assert line["shards"] == [list(qd.shard_range(blocks, k, 2)) for k in range(2)]
+    assert line["seed_broadcast_ok_ranks"] == 2 and line["max_over_ranks"] == 2.0
