@@ -621,6 +621,13 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modifi
     import oracle
     oracle.build()
     cores = threads or host_cores()
+    # word-mode cost ~ m*n/64 word operations per block at ~1e9 per core-second:
+    # when even one block per core would blow the budget (config 5 at n >= 2^20:
+    # 1.9e11 word operations per block at 2^22), time a subset of the rows of one
+    # block (OpenMP over rows) and extrapolate to whole blocks -- labelled so
+    est_batch_s = w.m * w.n / 64 / 1e9
+    if not modified and est_batch_s > budget_s / 2:
+        return cpu_baseline_rows(w, budget_s, cores)
     sample_blocks = min(w.n_blocks, 4096)
     raw, seed = S.workload_inputs(w, 0, sample_blocks)
     if modified:
@@ -646,6 +653,28 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modifi
                       f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, "
                       + ("modified Toeplitz literal loop" if modified else "word-parallel mode")
                       + ", OpenMP over blocks"}
+
+
+def cpu_baseline_rows(w: S.Workload, budget_s: float, cores: int):
+    """Oracle timing for blocks too large to finish within the budget: rows
+    [0, R) of block 0 (oracle_extract_rows, the same word-parallel formula,
+    OpenMP over rows), extrapolated to m rows per block."""
+    import oracle
+    raw, seed = S.workload_inputs(w, 0, 1)
+    R, t = max(cores, 64), 0.0
+    while True:
+        rows = np.arange(R, dtype=np.uint64)
+        t0 = time.perf_counter()
+        oracle.extract_rows(raw, np.zeros(R, np.uint64), rows, w.n, w.m, seed, cores)
+        t = time.perf_counter() - t0
+        if t > budget_s / 4 or R * 2 > w.m:
+            break
+        R *= 2
+    per_block_s = t * w.m / R
+    return {"value": w.n / per_block_s / 1e9, "unit": "Gbit/s", "cores": cores, "cpu_model": cpu_model(),
+            "kind": "oracle", "extrapolated": True,
+            "sample": f"rows [0, {R}) of block 0 of {w.name} in {t:.2f} s (word-parallel oracle_extract_rows, "
+                      f"OpenMP over rows), EXTRAPOLATED to the block's {w.m} rows"}
 
 
 def run_ours(args):
@@ -682,8 +711,10 @@ def run_ours(args):
         t0 = time.perf_counter()
         line["configs"] = {}
         for label, code in extra:
+            t1 = time.perf_counter()
             d = measure(q, ctx, args, code, headline=False,
                         cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget_extra)
+            d["wall_s"] = time.perf_counter() - t1
             line["configs"][label] = d
         line["configs_wall_s"] = time.perf_counter() - t0
     pars = [line.get("parity")] + [d.get("parity") for d in line.get("configs", {}).values()]
@@ -732,6 +763,23 @@ def run_reference(args):
         w = S.config4b(E.report(S.workload_inputs(w)[0], 8, w.n, 0).m)
     # all host cores (torchrun sets OMP_NUM_THREADS=1 for its workers)
     cores = host_cores()
+    if w.m * w.n / 64 / 1e9 > 10.0:
+        # blocks too large for whole-block steps (config 5 at n >= 2^20): each
+        # step times a subset of one block's rows, extrapolated (labelled)
+        ts, cb = [], None
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            cb = cpu_baseline_rows(w, 8.0, cores)
+            ts.append(time.perf_counter() - t0)
+        value = cb["value"]
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": w.n / (value * 1e9) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 bit words",
+            "data": "synthetic (qrng_synth)", "config": {"workload": w.name, "n": w.n, "m": w.m},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
     per_step_blocks = max(cores, min(w.n_blocks, int(os.environ.get("QRNG_REF_BLOCKS", "0")) or
                                      _ref_blocks(w, cores)))
     per_step_blocks = min(per_step_blocks, w.n_blocks)

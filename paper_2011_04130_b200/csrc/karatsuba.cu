@@ -255,7 +255,6 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
     Planner pl;
     pl.forced = forced;
     pl.root_w = (uint32_t)n;
-#if !QRNG_GEMM_2CTA
     static const bool pack_split = [] {
         const char *e = getenv("QRNG_KARA_PACK_SPLIT");  // calibration override
         return e ? atoi(e) != 0 : true;
@@ -265,8 +264,7 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
     // Gbit/s) and from 2^16 (2048-wide leaves: 156 -> 166), loses at 2^14 /
     // 2^15 (398 -> 391, 226 -> 204)
     const bool pack_here = n <= 8192 || n >= 65536;
-    if (pack_split && pack_here && gemm::operand_bits() == 4) pl.pack_w = 2048;  // gemm_tc.cu kMaxPackedK
-#endif
+    if (pack_split && pack_here) pl.pack_w = 2048;  // gemm_tc.cu kMaxPackedK
     std::vector<Node> nodes;
     pl.build((uint32_t)m, (uint32_t)n, depth, nodes);
     std::vector<int> leaf_of_node(nodes.size(), -1);
@@ -449,7 +447,7 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, std::shared
         g.npairs = (L.r + gemm::kTileRows - 1) / gemm::kTileRows;
         // equal tiles (no narrow N = 64 tail MMA, which runs at ~60% of the pipe rate)
         g.pair_rows = ((L.r + g.npairs - 1) / g.npairs + 31) & ~31u;
-        if (g.pair_rows > gemm::kTileRows || QRNG_GEMM_2CTA) g.pair_rows = gemm::kTileRows;
+        if (g.pair_rows > gemm::kTileRows) g.pair_rows = gemm::kTileRows;
         g.npair_base = npb;
         npb += g.npairs;
         g.seed_off = so;

@@ -127,7 +127,7 @@ int choose_pack_shift(uint64_t n, int logP);
 qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s, bool with_twiddles);
 }  // namespace ntt
 
-// GEMM path (gemm_tc.cu): tcgen05 kind::i8 batched Toeplitz product.
+// GEMM path (gemm_tc.cu): tcgen05 kind::mxf4 batched Toeplitz product.
 namespace gemm {
 struct Plan {
     uint32_t *seed_words = nullptr;  // seed as logical big-endian words, zero padded
@@ -148,40 +148,8 @@ struct Leaf {
     uint32_t iterm_base, iterm_n;  // input terms (bit offsets into the raw block)
     uint32_t pair_rows;         // rows per N pair (<= NT*BN, multiple of 32): r split evenly over npairs
 };
-// tcgen05 kernel geometry (build-time; gemm_tc.cu): rows per N tile, N tiles per
-// A stage, A ring slots, accumulator sets.
-
-#ifndef QRNG_GEMM_NT
-#define QRNG_GEMM_NT 2
-#endif
-#ifndef QRNG_GEMM_ASTAGES
-#define QRNG_GEMM_ASTAGES 4
-#endif
-#ifndef QRNG_GEMM_ACCBUFS
-#define QRNG_GEMM_ACCBUFS 1
-#endif
-#ifndef QRNG_GEMM_2CTA
-#define QRNG_GEMM_2CTA 0  // 1: the cta_group::2 kernel (256 x 256 tiles, A in smem, double-buffered accumulators)
-#endif
-#ifndef QRNG_GEMM_FP4
-#if QRNG_GEMM_2CTA
-#define QRNG_GEMM_FP4 0  // 2-SM variant: int8 unless -DQRNG_GEMM_FP4=1
-#else
-#define QRNG_GEMM_FP4 1  // tcgen05 kind::mxf4 operands (gemm_tc.cu)
-#endif
-#endif
-#ifndef QRNG_GEMM_BN
-#if QRNG_GEMM_FP4 && !QRNG_GEMM_2CTA
-#define QRNG_GEMM_BN 224  // E2M1: N tiles of 224 rows (448 per A stage; measured faster than 192)
-#else
-#define QRNG_GEMM_BN 192
-#endif
-#endif
-#if QRNG_GEMM_2CTA
-constexpr int kTileRows = QRNG_GEMM_FP4 ? 224 : 256;  // output rows per work tile of the 2-SM kernel
-#else
-constexpr int kTileRows = QRNG_GEMM_BN * QRNG_GEMM_NT;  // output rows per work tile (NT * BN)
-#endif
+// Output rows per work tile of the tcgen05 kernel (gemm_tc.cu: 2 N tiles x 224).
+constexpr int kTileRows = 448;
 uint32_t seed_words_needed(uint64_t n, uint64_t m);
 // Grouped launch over the leaf table (Karatsuba): parities of leaf l, block b,
 // row i go to bit 31 - (i & 31) of yws[b * y_stride + out_off + i / 32] (logical words).
@@ -202,9 +170,10 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
                     uint64_t m, const OutStream &out, cudaStream_t s);
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
 qrng_status trace(uint64_t *h_out, int reset);
-int operand_bits();  // 4: kind::mxf4 (E2M1), 8: kind::i8
+int operand_bits();  // 4: kind::mxf4 (E2M1 operands)
 qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int K, int hi_first, cudaStream_t s);
-qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s);  // 16 cycle counters (-DQRNG_GEMM_TRACE builds)
+// instruments (gemm_probe.cu)
+qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s);
 }  // namespace gemm
 
 // Karatsuba decomposition over the GEMM path (karatsuba.cu).
