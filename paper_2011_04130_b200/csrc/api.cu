@@ -178,6 +178,7 @@ struct qrng_plan {
     int path = QRNG_PATH_NTT;
     bool kara_on = false;  // GEMM path through the Karatsuba decomposition
     bool modified = false;  // modified Toeplitz [T | I_m] (n-bit seed)
+    const uint8_t *direct_seed = nullptr;  // one-shot dense GEMM: the caller's seed, read by the kernel itself
     ntt::Plan ntt;
     gemm::Plan gemm;
     kara::Plan kara;
@@ -289,6 +290,27 @@ qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info) {
     return QRNG_OK;
 }
 
+// The block scheduler's path choice (row a2): the tensor-core path for n a
+// multiple of 128 up to the measured crossover (Karatsuba tree if the planner
+// decomposes (n, m)), the NTT path above it and for every shape the dense
+// kernel cannot take.
+static qrng_status resolve_path(uint64_t n, uint64_t m, int *path, bool *kara_on) {
+    int want = g_debug_path.load();
+    const bool automatic = want == QRNG_PATH_AUTO;
+    *kara_on = false;
+    if (automatic) want = (n % 128 == 0 && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
+    if (want == QRNG_PATH_GEMM) *kara_on = kara::choose(n, m, g_kara_depth.load());
+    // AUTO: a shape the planner leaves undecomposed (small m at large n) that the
+    // dense kernel cannot take runs on the NTT path, which accepts every valid (n, m)
+    if (automatic && want == QRNG_PATH_GEMM && !*kara_on && !gemm::supported(n, m)) want = QRNG_PATH_NTT;
+    if (want == QRNG_PATH_GEMM && !*kara_on && !gemm::supported(n, m)) {
+        set_error("GEMM path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
+        return QRNG_E_UNSUPPORTED;
+    }
+    *path = want;
+    return QRNG_OK;
+}
+
 qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
                              qrng_plan **plan) {
     if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
@@ -297,24 +319,16 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     if (st != QRNG_OK) return st;
     if (!d_seed || !aligned16(d_seed)) { set_error("d_seed is NULL or not 16-byte aligned"); return QRNG_E_INVALID; }
     if ((st = device_ready()) != QRNG_OK) return st;
+    int want = 0;
+    bool kara_on = false;
+    if ((st = resolve_path(n, m, &want, &kara_on)) != QRNG_OK) return st;
     qrng_plan *p = new (std::nothrow) qrng_plan;
     if (!p) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
     p->n = n;
     p->m = m;
-    int want = g_debug_path.load();
-    const bool automatic = want == QRNG_PATH_AUTO;
-    const int kd = g_kara_depth.load();
-    if (automatic) want = (n % 128 == 0 && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
-    if (want == QRNG_PATH_GEMM) p->kara_on = kara::choose(n, m, kd);
-    // AUTO: a shape the planner leaves undecomposed (small m at large n) that the
-    // dense kernel cannot take runs on the NTT path, which accepts every valid (n, m)
-    if (automatic && want == QRNG_PATH_GEMM && !p->kara_on && !gemm::supported(n, m)) want = QRNG_PATH_NTT;
-    if (want == QRNG_PATH_GEMM && !p->kara_on && !gemm::supported(n, m)) {
-        set_error("GEMM path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
-        delete p;
-        return QRNG_E_UNSUPPORTED;
-    }
+    p->kara_on = kara_on;
     p->path = want;
+    const int kd = g_kara_depth.load();
     st = (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
          : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream)
                                  : gemm::plan_init(p->gemm, n, m, d_seed, stream);
@@ -410,6 +424,7 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
     qrng_status st = (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->kara_on ? kara::extract(plan->kara, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->modified ? gemm::extract_modified(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
+                     : plan->direct_seed ? gemm::extract_direct(plan->direct_seed, d_raw_bits, n_blocks, n, m, o, stream)
                                       : gemm::extract(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream);
     if (st == QRNG_OK && o.tail) {
         cudaError_t e = cudaMemcpyAsync(d_out + (out_bytes / 4) * 4, o.tail, out_bytes % 4,
@@ -430,6 +445,22 @@ qrng_status qrng_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_bl
         overlap(d_seed, (n + m - 1 + 7) / 8, d_out, (n_blocks * m + 7) / 8)) {
         set_error("d_out overlaps d_seed");
         return QRNG_E_INVALID;
+    }
+    if (!aligned16(d_seed)) { set_error("d_seed must be 16-byte aligned"); return QRNG_E_INVALID; }
+    if ((st = device_ready()) != QRNG_OK) return st;
+    int path = 0;
+    bool kara_on = false;
+    if ((st = resolve_path(n, m, &path, &kara_on)) != QRNG_OK) return st;
+    if (path == QRNG_PATH_GEMM && !kara_on) {
+        // dense tensor-core product: no plan buffers or seed kernel; the GEMM
+        // kernel forms the seed words from d_seed in its prologue (small batches
+        // are latency-bound: this removes an allocation, a launch and a free)
+        qrng_plan direct;
+        direct.n = n;
+        direct.m = m;
+        direct.path = QRNG_PATH_GEMM;
+        direct.direct_seed = d_seed;
+        return qrng_plan_extract(&direct, d_raw_bits, n_blocks, d_out, stream);
     }
     qrng_plan *p = nullptr;
     if ((st = qrng_plan_create(n, m, d_seed, stream, &p)) != QRNG_OK) return st;

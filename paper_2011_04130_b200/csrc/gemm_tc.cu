@@ -107,6 +107,8 @@ struct Args {
     uint32_t n_mtiles, n_npairs;  // M tiles; pairs of N tiles (NT = 2 per work tile)
     const uint32_t *seed_words;  // logical big-endian seed words, zero padded
     uint32_t seed_words_n;
+    const uint8_t *seed_bytes;   // plain mode, one-shot calls: the caller's MSB-first seed (seed_words unused)
+    uint64_t seed_bits;          // L = n + m - 1 (seed_bytes mode)
     OutStream out;
     // grouped (Karatsuba leaf) mode only: tiles walk the leaf table, operands
     // come from per-leaf inputs and parities go to a word-aligned workspace
@@ -258,7 +260,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
             reinterpret_cast<TLeaf *>(seed_s)[i] = o;
         }
     } else {
-        for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
+        if (a.seed_bytes) {
+            // one-shot calls: the seed words are formed here from the caller's
+            // bytes (word w = seed bits [32w, 32w + 32), big-endian, zero at and
+            // past L) -- no plan buffer, no separate seed kernel
+            const uint64_t nbytes = (a.seed_bits + 7) / 8;
+            for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) {
+                uint32_t v = 0;
+                const uint64_t b0 = 4ull * i;
+                if (b0 + 4 <= nbytes) {
+                    v = __byte_perm(__ldg(reinterpret_cast<const uint32_t *>(a.seed_bytes) + i), 0, 0x0123);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v = (v << 8) | (b0 + k < nbytes ? (uint32_t)a.seed_bytes[b0 + k] : 0u);
+                }
+                const uint64_t lo = 32ull * i;
+                if (lo + 32 > a.seed_bits) v &= a.seed_bits > lo ? (0xFFFFFFFFu << (32 - (uint32_t)(a.seed_bits - lo))) : 0u;
+                seed_s[i] = v;
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < seed_stage; i += NTHREADS) seed_s[i] = a.seed_words[i];
+        }
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < A_STAGES; ++s) { mbar_init(&a_full[s], N_XFORM); mbar_init(&a_empty[s], 1); }
@@ -766,6 +788,33 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
     a.seed_words = pl.seed_words;
     a.seed_words_n = (uint32_t)pl.seed_words_n;
+    a.out = out;
+    return launch<false>(a, s);
+}
+
+// One-shot dense product without a plan: the kernel forms the seed words from
+// the caller's seed bytes in its prologue (d_seed must stay valid until the
+// kernel has run: stream order on `s`).
+qrng_status extract_direct(const uint8_t *d_seed, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                           const OutStream &out, cudaStream_t s) {
+    if (!supported(n, m)) {
+        set_error("GEMM path: unsupported n=%llu m=%llu", (unsigned long long)n, (unsigned long long)m);
+        return QRNG_E_UNSUPPORTED;
+    }
+    Args a{};
+    a.raw = reinterpret_cast<const uint32_t *>(d_raw);
+    a.n_blocks = n_blocks;
+    a.n = (uint32_t)n;
+    a.m = (uint32_t)m;
+    a.kst = (uint32_t)((n + KS - 1) / KS);
+    a.k128 = (uint32_t)(n / 128);
+    a.nchunks = (a.kst + SPC - 1) / SPC;
+    a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
+    a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));
+    a.seed_words = nullptr;
+    a.seed_words_n = seed_words_needed(n, m);
+    a.seed_bytes = d_seed;
+    a.seed_bits = n + m - 1;
     a.out = out;
     return launch<false>(a, s);
 }

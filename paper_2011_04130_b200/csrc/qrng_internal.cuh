@@ -168,6 +168,9 @@ qrng_status extract_modified(const Plan &pl, const uint8_t *d_raw, uint64_t n_bl
 void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
+// one-shot dense product straight from the caller's seed bytes (no plan)
+qrng_status extract_direct(const uint8_t *d_seed, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                           const OutStream &out, cudaStream_t s);
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
 qrng_status trace(uint64_t *h_out, int reset);
 int operand_bits();  // 4: kind::mxf4 (E2M1 operands)
