@@ -113,8 +113,11 @@ QRNG_API qrng_status qrng_entropy_from_counts(const uint64_t *h_counts, uint32_t
  * Errors: E_INVALID if a pointer is NULL or misaligned (d_raw_bits / d_seed 16 bytes,
  *         d_out 4 bytes), n == 0, m == 0,
  *         m >= n, n_blocks == 0, or d_out overlaps d_raw_bits or d_seed;
- *         E_UNSUPPORTED if n % 32 != 0 or L > 2^23 (2-adic limit of the NTT prime
- *         p = 119*2^23 + 1);  E_CUDA / E_NOMEM on device failures.
+ *         E_UNSUPPORTED if n % 32 != 0 or L > 2^26;  E_CUDA / E_NOMEM on device failures.
+ *         L <= 2^23 runs the tensor-core path or the NTT modulo p = 119*2^23 + 1;
+ *         2^23 < L <= 2^26 (n around 2^24..2^25, past the 2-adic limit of that
+ *         prime) runs the four-step NTT of qrng_dist_* below with world = 1,
+ *         block by block, modulo p = 7*2^26 + 1.
  * The one-shot calls build a temporary plan (seed preparation included) and
  * release it stream-ordered; _async returns once the work is enqueued.
  */
@@ -162,6 +165,42 @@ QRNG_API qrng_status qrng_stream_submit(qrng_stream *stream, const uint8_t *h_ra
 QRNG_API qrng_status qrng_stream_synchronize(qrng_stream *stream);
 QRNG_API qrng_status qrng_stream_counts(qrng_stream *stream, uint64_t *h_counts256);
 QRNG_API void        qrng_stream_destroy(qrng_stream *stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-4: ONE block across `world` GPUs -- a distributed
+ * four-step NTT modulo p = 7*2^26 + 1 (2-adicity 26; P = 2^ceil(log2 L) <= 2^26,
+ * window sums <= n < p, so the result is exact as in C1; PAPER.md:213-241 for
+ * the circulant embedding, PAPER.md:273 for cutting the work of a long stream).
+ * With t = N2 n1 + n2 (N2 = P / world) and k = k1 + world k2, rank r owns the
+ * spectrum slice k1 = r: it forms it from the (replicated) block bits with no
+ * communication, multiplies by the seed spectrum slice of its plan, transforms
+ * back and twists; ONE all-to-all of N2 words per rank then gives each rank
+ * all slices of its columns, and qrng_dist_finish completes the radix-world
+ * inverse and ORs the window parities into the key.  One process per GPU; the
+ * all-to-all (equal chunks of N2/world words) and the final OR of the ranks'
+ * keys (their bits are disjoint, so a byte-wise SUM all-reduce is an OR) are
+ * the caller's collectives (torch.distributed / NCCL in the Python binding).
+ *
+ * qrng_dist_plan_create: world in {1, 2, 4, 8}, rank < world; d_seed as for
+ *   qrng_plan_create (read on `stream`, may be freed afterwards).
+ * qrng_dist_exchange_words: N2, the words of every rank's exchange buffer.
+ * qrng_dist_local: d_block_bits = the block's n bits (C2, ceil(n/8) bytes, any
+ *   alignment); d_buf = N2 uint32 words, 16-byte aligned, written completely;
+ *   words [r' N2/world, (r'+1) N2/world) go to rank r'.
+ * qrng_dist_finish: d_recv = N2 words, chunk k1 received from rank k1;
+ *   d_key = ceil(m/8) bytes, 4-byte aligned, ZEROED by the caller; this rank's
+ *   key bits are ORed in (bit i = y_i, C4); other bits stay 0.
+ * Errors: E_INVALID for NULL/misaligned pointers, bad world/rank, 0 < m < n
+ *   violated; E_UNSUPPORTED for n % 32 != 0 or L > 2^26; E_CUDA / E_NOMEM. */
+typedef struct qrng_dist_plan qrng_dist_plan;
+QRNG_API qrng_status qrng_dist_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t world,
+                                           uint32_t rank, cudaStream_t stream, qrng_dist_plan **plan);
+QRNG_API uint64_t    qrng_dist_exchange_words(const qrng_dist_plan *plan);
+QRNG_API qrng_status qrng_dist_local(const qrng_dist_plan *plan, const uint8_t *d_block_bits, uint32_t *d_buf,
+                                     cudaStream_t stream);
+QRNG_API qrng_status qrng_dist_finish(const qrng_dist_plan *plan, const uint32_t *d_recv, uint8_t *d_key,
+                                      cudaStream_t stream);
+QRNG_API void        qrng_dist_plan_destroy(qrng_dist_plan *plan);
 
 /* Plans: seed preparation (a3) once per (seed, n, m), reused over many batches.
  * qrng_plan_create reads d_seed on `stream` (the seed may be freed once that

@@ -37,7 +37,8 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_debug_butterfly_rate", "qrng_debug_pass_rate", "qrng_debug_mxf4_probe", "qrng_debug_gemm_operand_bits", "qrng_debug_set_karatsuba", "qrng_plan_info",
            "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
            "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split",
-           "qrng_debug_mma_rate"]
+           "qrng_debug_mma_rate", "qrng_dist_plan_create", "qrng_dist_exchange_words", "qrng_dist_local",
+           "qrng_dist_finish", "qrng_dist_plan_destroy"]
 
 
 class QrngError(RuntimeError):
@@ -131,6 +132,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_stream_destroy": ([vp], None),
         "qrng_plan_info": ([vp, vp], i32),
         "qrng_debug_karatsuba_plan": ([u64, u64, i32, vp, u32, vp, u32, vp, u32, vp], i32),
+        "qrng_dist_plan_create": ([u64, u64, vp, u32, u32, vp, ctypes.POINTER(vp)], i32),
+        "qrng_dist_exchange_words": ([vp], u64),
+        "qrng_dist_local": ([vp, vp, vp, vp], i32),
+        "qrng_dist_finish": ([vp, vp, vp, vp], i32),
+        "qrng_dist_plan_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -407,6 +413,67 @@ class Plan:
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             load_library().qrng_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class DistPlan:
+    """NEXT-4: this rank's share of ONE block's extraction across `world` GPUs
+    (qrng_dist_*, the distributed four-step NTT; see include/qrng.h).  The
+    collectives between local() and finish() are the caller's
+    (paper_2011_04130_b200.dist.extract_block_distributed)."""
+
+    def __init__(self, n: int, m: int, seed, world: int, rank: int, stream=None):
+        _need_cuda_u8(seed, "seed")
+        _need_bytes(seed, (n + m - 1 + 7) // 8, "seed")
+        self.n, self.m, self.world, self.rank = n, m, world, rank
+        self.device = seed.device
+        h = ctypes.c_void_p()
+        _check(load_library().qrng_dist_plan_create(n, m, _ptr(seed), world, rank, _stream_handle(stream),
+                                                     ctypes.byref(h)))
+        self._h = h
+        self.exchange_words = int(load_library().qrng_dist_exchange_words(self._h))
+
+    def new_buffer(self):
+        import torch
+        return torch.empty(self.exchange_words, dtype=torch.int32, device=self.device)
+
+    def local(self, block, buf, stream=None):
+        """Spectrum slice k1 = rank of the block, * seed slice, inverse, twist -> buf (send chunks)."""
+        import torch
+        _need_cuda_u8(block, "block")
+        _need_bytes(block, (self.n + 7) // 8, "block")
+        if buf.dtype != torch.int32 or buf.numel() != self.exchange_words or not buf.is_contiguous():
+            raise TypeError("buf must be a contiguous int32 tensor of exchange_words elements")
+        _same_device(block, buf)
+        _check(load_library().qrng_dist_local(self._h, _ptr(block), _ptr(buf), _stream_handle(stream)))
+        return buf
+
+    def finish(self, recv, key, stream=None):
+        """ORs this rank's key bits into key (uint8, ceil(m/8) bytes, zeroed by the caller)."""
+        import torch
+        if recv.dtype != torch.int32 or recv.numel() != self.exchange_words or not recv.is_contiguous():
+            raise TypeError("recv must be a contiguous int32 tensor of exchange_words elements")
+        _need_cuda_u8(key, "key")
+        _need_bytes(key, out_bytes(1, self.m), "key")
+        _same_device(recv, key)
+        _check(load_library().qrng_dist_finish(self._h, _ptr(recv), _ptr(key), _stream_handle(stream)))
+        return key
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load_library().qrng_dist_plan_destroy(self._h)
             self._h = ctypes.c_void_p()
 
     def __del__(self):

@@ -162,8 +162,8 @@ static qrng_status check_nm(uint64_t n, uint64_t m) {
         set_error("n must be a multiple of 32 (got %llu)", (unsigned long long)n);
         return QRNG_E_UNSUPPORTED;
     }
-    if (n + m - 1 > (1ull << ntt::kMaxLogP)) {
-        set_error("seed length n+m-1 = %llu exceeds 2^23", (unsigned long long)(n + m - 1));
+    if (n + m - 1 > (1ull << ntt::kMaxLogP2)) {
+        set_error("seed length n+m-1 = %llu exceeds 2^26", (unsigned long long)(n + m - 1));
         return QRNG_E_UNSUPPORTED;
     }
     return QRNG_OK;
@@ -179,6 +179,8 @@ struct qrng_plan {
     bool kara_on = false;  // GEMM path through the Karatsuba decomposition
     bool modified = false;  // modified Toeplitz [T | I_m] (n-bit seed)
     const uint8_t *direct_seed = nullptr;  // one-shot dense GEMM: the caller's seed, read by the kernel itself
+    bool four_step = false;  // NTT path with L > 2^23: the four-step NTT (world 1), block by block
+    ntt::DistPlan dist;
     ntt::Plan ntt;
     gemm::Plan gemm;
     kara::Plan kara;
@@ -194,6 +196,7 @@ static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
     fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.work);
     fr(p->gemm.seed_words);
     fr(p->kara.seeds);
+    ntt::dist_plan_free(p->dist, s, async);
     delete p;
 }
 
@@ -329,7 +332,9 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     p->kara_on = kara_on;
     p->path = want;
     const int kd = g_kara_depth.load();
-    st = (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
+    p->four_step = want == QRNG_PATH_NTT && n + m - 1 > (1ull << ntt::kMaxLogP);
+    st = p->four_step            ? ntt::dist_plan_init(p->dist, n, m, d_seed, 1, 0, stream)
+         : (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
          : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream)
                                  : gemm::plan_init(p->gemm, n, m, d_seed, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
@@ -394,6 +399,21 @@ qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_bits, uint
 
 void qrng_plan_destroy(qrng_plan *plan) { plan_release(plan, 0, false); }
 
+// L > 2^23 on one GPU: the world-1 four-step NTT block by block (each block's
+// local transform fills the GPU: P up to 2^26 words).
+static qrng_status four_step_extract(const ntt::DistPlan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
+                                     uint64_t m, const OutStream &o, cudaStream_t stream) {
+    uint32_t *ws = nullptr;
+    QRNG_CUDA_TRY(cudaMallocAsync(&ws, (size_t)pl.N2 * 4, stream));
+    qrng_status st = QRNG_OK;
+    for (uint64_t b = 0; b < n_blocks && st == QRNG_OK; ++b) {
+        st = ntt::dist_local(pl, d_raw + b * (n / 8), ws, stream);
+        if (st == QRNG_OK) st = ntt::dist_finish(pl, ws, o, b * m, stream);
+    }
+    cudaFreeAsync(ws, stream);
+    return st;
+}
+
 qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, uint64_t n_blocks,
                               uint8_t *d_out, cudaStream_t stream) {
     if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
@@ -421,7 +441,8 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
     // the Karatsuba pack kernel writes every output word once; the other
     // epilogues OR the words they share with a neighbouring tile / CTA
     if (!(plan->path == QRNG_PATH_GEMM && plan->kara_on)) QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
-    qrng_status st = (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
+    qrng_status st = plan->four_step ? four_step_extract(plan->dist, d_raw_bits, n_blocks, n, m, o, stream)
+                     : (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->kara_on ? kara::extract(plan->kara, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->modified ? gemm::extract_modified(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->direct_seed ? gemm::extract_direct(plan->direct_seed, d_raw_bits, n_blocks, n, m, o, stream)
@@ -730,6 +751,84 @@ qrng_status qrng_stream_counts(qrng_stream *q, uint64_t *h_counts256) {
 }
 
 void qrng_stream_destroy(qrng_stream *q) { stream_release(q); }
+
+// ---- NEXT-4: one block across GPUs ----------------------------------------------
+struct qrng_dist_plan {
+    ntt::DistPlan d;
+};
+
+qrng_status qrng_dist_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t world, uint32_t rank,
+                                  cudaStream_t stream, qrng_dist_plan **plan) {
+    if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
+    *plan = nullptr;
+    qrng_status st = check_nm(n, m);
+    if (st != QRNG_OK) return st;
+    if (!d_seed || !aligned16(d_seed)) { set_error("d_seed is NULL or not 16-byte aligned"); return QRNG_E_INVALID; }
+    if (world == 0 || world > 8 || (world & (world - 1)) || rank >= world) {
+        set_error("world must be 1, 2, 4 or 8 and rank < world (got %u, %u)", world, rank);
+        return QRNG_E_INVALID;
+    }
+    if ((st = device_ready()) != QRNG_OK) return st;
+    qrng_dist_plan *p = new (std::nothrow) qrng_dist_plan;
+    if (!p) { set_error("host allocation failed"); return QRNG_E_NOMEM; }
+    st = ntt::dist_plan_init(p->d, n, m, d_seed, world, rank, stream);
+    if (st != QRNG_OK) {
+        ntt::dist_plan_free(p->d, stream, true);
+        delete p;
+        return st;
+    }
+    *plan = p;
+    return QRNG_OK;
+}
+
+uint64_t qrng_dist_exchange_words(const qrng_dist_plan *plan) { return plan ? plan->d.N2 : 0; }
+
+qrng_status qrng_dist_local(const qrng_dist_plan *plan, const uint8_t *d_block_bits, uint32_t *d_buf,
+                            cudaStream_t stream) {
+    if (!plan || !d_block_bits || !d_buf) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    if (!aligned16(d_buf)) { set_error("d_buf must be 16-byte aligned"); return QRNG_E_INVALID; }
+    if (overlap(d_block_bits, (plan->d.n + 7) / 8, d_buf, (uint64_t)plan->d.N2 * 4)) {
+        set_error("d_buf overlaps d_block_bits");
+        return QRNG_E_INVALID;
+    }
+    return ntt::dist_local(plan->d, d_block_bits, d_buf, stream);
+}
+
+qrng_status qrng_dist_finish(const qrng_dist_plan *plan, const uint32_t *d_recv, uint8_t *d_key,
+                             cudaStream_t stream) {
+    if (!plan || !d_recv || !d_key) { set_error("NULL argument"); return QRNG_E_INVALID; }
+    if (((uintptr_t)d_key & 3u) != 0) { set_error("d_key must be 4-byte aligned"); return QRNG_E_INVALID; }
+    const uint64_t m = plan->d.m, key_bytes = (m + 7) / 8;
+    if (overlap(d_recv, (uint64_t)plan->d.N2 * 4, d_key, key_bytes)) {
+        set_error("d_key overlaps d_recv");
+        return QRNG_E_INVALID;
+    }
+    OutStream o;
+    o.words = reinterpret_cast<uint32_t *>(d_key);
+    o.total_bits = m;
+    o.full_words = key_bytes / 4;
+    o.tail = nullptr;
+    if (key_bytes % 4) {  // the final partial word goes through a scratch word (nothing past key_bytes is touched)
+        cudaError_t e = cudaMallocAsync(&o.tail, 4, stream);
+        if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); return QRNG_E_NOMEM; }
+        QRNG_CUDA_TRY(cudaMemcpyAsync(o.tail, d_key + (key_bytes / 4) * 4, key_bytes % 4, cudaMemcpyDeviceToDevice,
+                                      stream));
+    }
+    qrng_status st = ntt::dist_finish(plan->d, d_recv, o, 0, stream);
+    if (st == QRNG_OK && o.tail) {
+        cudaError_t e = cudaMemcpyAsync(d_key + (key_bytes / 4) * 4, o.tail, key_bytes % 4, cudaMemcpyDeviceToDevice,
+                                        stream);
+        if (e != cudaSuccess) { set_error("tail copy: %s", cudaGetErrorString(e)); st = QRNG_E_CUDA; }
+    }
+    if (o.tail) cudaFreeAsync(o.tail, stream);
+    return st;
+}
+
+void qrng_dist_plan_destroy(qrng_dist_plan *plan) {
+    if (!plan) return;
+    ntt::dist_plan_free(plan->d, 0, false);
+    delete plan;
+}
 
 // ---- min-entropy ------------------------
 

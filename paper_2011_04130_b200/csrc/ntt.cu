@@ -24,56 +24,69 @@
 // final residue is made canonical before its parity is taken.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include "qrng_internal.cuh"
 
 namespace qrng {
 namespace ntt {
 
-constexpr uint32_t P = kP;
-constexpr uint32_t P2 = 2u * kP;
-constexpr uint32_t PINV = 3296722945u;  // p^-1 mod 2^32
+// The two NTT primes (both < 2^30, so lazy residues in [0, 2p) and sums < 4p
+// fit 32 bits; primitive root 3 for both):
+//   F = 0: p = 119 * 2^23 + 1 = 998244353 -- every single-GPU transform P <= 2^23;
+//   F = 1: p =   7 * 2^26 + 1 = 469762049 -- the distributed four-step NTT of
+//          one block (NEXT-4, ntt_dist.cu): roots of unity of order up to 2^26.
+template <int F> struct Fld;
+template <> struct Fld<0> { static constexpr uint32_t P = kP, PINV = 3296722945u; static constexpr int LOG2 = 23; };
+template <> struct Fld<1> { static constexpr uint32_t P = kP2, PINV = 3825205249u; static constexpr int LOG2 = 26; };
+static_assert(Fld<0>::P * Fld<0>::PINV == 1u && Fld<1>::P * Fld<1>::PINV == 1u, "PINV = p^-1 mod 2^32");
+static_assert(4ull * Fld<0>::P < (1ull << 32) && 4ull * Fld<1>::P < (1ull << 32), "lazy [0, 4p) sums fit 32 bits");
+constexpr uint32_t P = kP;  // the single-GPU prime (fused kernels, plans of ntt.cu's host code)
 
-constexpr uint64_t powmod_c(uint64_t b, uint64_t e) {
+constexpr uint64_t powmod_p(uint64_t b, uint64_t e, uint64_t p) {
     uint64_t r = 1;
-    b %= P;
+    b %= p;
     while (e) {
-        if (e & 1) r = r * b % P;
-        b = b * b % P;
+        if (e & 1) r = r * b % p;
+        b = b * b % p;
         e >>= 1;
     }
     return r;
 }
+constexpr uint64_t powmod_c(uint64_t b, uint64_t e) { return powmod_p(b, e, P); }
 
 struct RootTab {
     uint32_t w[64], wp[64], iw[64], iwp[64];  // w_64^e, Shoup companions, inverses
 };
-constexpr RootTab make_roots() {
+constexpr RootTab make_roots(uint64_t p) {
     RootTab t{};
-    uint64_t w64 = powmod_c(3, (P - 1) / 64), iw64 = powmod_c(w64, P - 2);
+    uint64_t w64 = powmod_p(3, (p - 1) / 64, p), iw64 = powmod_p(w64, p - 2, p);
     uint64_t a = 1, b = 1;
     for (int e = 0; e < 64; ++e) {
         t.w[e] = (uint32_t)a;
-        t.wp[e] = (uint32_t)((a << 32) / P);
+        t.wp[e] = (uint32_t)((a << 32) / p);
         t.iw[e] = (uint32_t)b;
-        t.iwp[e] = (uint32_t)((b << 32) / P);
-        a = a * w64 % P;
-        b = b * iw64 % P;
+        t.iwp[e] = (uint32_t)((b << 32) / p);
+        a = a * w64 % p;
+        b = b * iw64 % p;
     }
     return t;
 }
-__constant__ RootTab c_roots = make_roots();
+__constant__ RootTab c_roots[2] = {make_roots(Fld<0>::P), make_roots(Fld<1>::P)};
 
 // ---- modular arithmetic on lazy residues in [0, 2p) ------------------------
-__device__ __forceinline__ uint32_t red2(uint32_t x) { return min(x, x - P2); }  // [0,4p)->[0,2p)
+template <int F = 0>
+__device__ __forceinline__ uint32_t red2(uint32_t x) { return min(x, x - 2u * Fld<F>::P); }  // [0,4p)->[0,2p)
+template <int F = 0>
 __device__ __forceinline__ uint32_t shoup(uint32_t a, uint32_t w, uint32_t wp) {
     uint32_t q = __umulhi(a, wp);
-    return a * w - q * P;  // a*w mod p in [0, 2p), any 32-bit a
+    return a * w - q * Fld<F>::P;  // a*w mod p in [0, 2p), any 32-bit a
 }
 // Montgomery product a*b/2^32 mod p for a, b < 2p, result in (0, 2p):
 // t = a*b < 4p^2 < p 2^32; q = t_lo p^-1 mod 2^32 makes t - q p divisible by
 // 2^32, so (t - q p)/2^32 = t_hi - hi(q p) lies in (-p, p); add p.  Written as
 // mul.wide / mul.lo / mul.hi / sub so ptxas emits 4 instructions (IMAD.WIDE,
 // IMAD, IMAD.HI, IADD3) instead of fusing a 64-bit addend chain.
+template <int F = 0>
 __device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b) {
     uint32_t r;
     asm("{\n\t.reg .u64 t;\n\t.reg .u32 lo, hi, q, h;\n\t"
@@ -83,7 +96,7 @@ __device__ __forceinline__ uint32_t mont(uint32_t a, uint32_t b) {
         "mul.hi.u32 h, q, %4;\n\t"
         "sub.u32 %0, hi, h;\n\t"
         "add.u32 %0, %0, %4;\n\t}"
-        : "=r"(r) : "r"(a), "r"(b), "n"(PINV), "n"(P));
+        : "=r"(r) : "r"(a), "r"(b), "n"(Fld<F>::PINV), "n"(Fld<F>::P));
     return r;
 }
 
@@ -95,8 +108,9 @@ __host__ __device__ constexpr int brev(int x, int bits) {
 
 // Radix-2^R DIF on registers: natural order in, bit-reversed order out.
 // Every loop has a compile-time trip count so the array stays in registers.
-template <int R>
+template <int R, int F = 0>
 __device__ __forceinline__ void dft_fwd(uint32_t (&x)[1 << R]) {
+    constexpr uint32_t P2 = 2u * Fld<F>::P;
     constexpr int N = 1 << R;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
@@ -108,16 +122,17 @@ __device__ __forceinline__ void dft_fwd(uint32_t (&x)[1 << R]) {
             const int step = 64 / (2 * half);
             uint32_t a = x[i], b = x[i + half];
             uint32_t v = a - b + P2;
-            x[i] = red2(a + b);
-            x[i + half] = (e == 0) ? red2(v) : shoup(v, c_roots.w[e * step], c_roots.wp[e * step]);
+            x[i] = red2<F>(a + b);
+            x[i + half] = (e == 0) ? red2<F>(v) : shoup<F>(v, c_roots[F].w[e * step], c_roots[F].wp[e * step]);
         }
     }
 }
 
 // Radix-2^R DIT with inverse roots: bit-reversed order in, natural order out
 // (unscaled: returns N times the inverse DFT).
-template <int R>
+template <int R, int F = 0>
 __device__ __forceinline__ void dft_inv(uint32_t (&x)[1 << R]) {
+    constexpr uint32_t P2 = 2u * Fld<F>::P;
     constexpr int N = 1 << R;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
@@ -128,9 +143,9 @@ __device__ __forceinline__ void dft_inv(uint32_t (&x)[1 << R]) {
             const int i = ((k / half) * 2 * half) + e;
             const int step = 64 / (2 * half);
             uint32_t a = x[i], b = x[i + half];
-            uint32_t tb = (e == 0) ? b : shoup(b, c_roots.iw[e * step], c_roots.iwp[e * step]);
-            x[i] = red2(a + tb);
-            x[i + half] = red2(a - tb + P2);
+            uint32_t tb = (e == 0) ? b : shoup<F>(b, c_roots[F].iw[e * step], c_roots[F].iwp[e * step]);
+            x[i] = red2<F>(a + tb);
+            x[i + half] = red2<F>(a - tb + P2);
         }
     }
 }
@@ -139,18 +154,18 @@ __device__ __forceinline__ void dft_inv(uint32_t (&x)[1 << R]) {
 // (tauM = tau * 2^32 mod p, Montgomery form).  The powers come from four
 // independent chains tau^(j+1) * (tau^4)^i, so the Montgomery products are not
 // one serial dependency chain.
-template <int R>
+template <int R, int F = 0>
 __device__ __forceinline__ void twiddle(uint32_t (&x)[1 << R], uint32_t tauM) {
     constexpr int N = 1 << R;
     if constexpr (N <= 4) {
         uint32_t pw = tauM;
 #pragma unroll
         for (int k = 1; k < N; ++k) {
-            if (k > 1) pw = mont(pw, tauM);
-            x[brev(k, R)] = mont(x[brev(k, R)], pw);
+            if (k > 1) pw = mont<F>(pw, tauM);
+            x[brev(k, R)] = mont<F>(x[brev(k, R)], pw);
         }
     } else {
-        const uint32_t t2 = mont(tauM, tauM), t3 = mont(t2, tauM), t4 = mont(t2, t2);
+        const uint32_t t2 = mont<F>(tauM, tauM), t3 = mont<F>(t2, tauM), t4 = mont<F>(t2, t2);
         uint32_t c[4] = {tauM, t2, t3, t4};
 #pragma unroll
         for (int i = 0; i < N / 4; ++i)
@@ -158,8 +173,8 @@ __device__ __forceinline__ void twiddle(uint32_t (&x)[1 << R], uint32_t tauM) {
             for (int j = 0; j < 4; ++j) {
                 const int k = 4 * i + j + 1;
                 if (k < N) {
-                    if (i > 0) c[j] = mont(c[j], t4);
-                    x[brev(k, R)] = mont(x[brev(k, R)], c[j]);
+                    if (i > 0) c[j] = mont<F>(c[j], t4);
+                    x[brev(k, R)] = mont<F>(x[brev(k, R)], c[j]);
                 }
             }
     }
@@ -206,8 +221,9 @@ __device__ __forceinline__ uint32_t raw_bit(const uint32_t *raw, uint64_t b, uin
     return (bswap32(w) >> (31 - (idx & 31))) & 1u;
 }
 
-template <int LOGP, int LV, bool PACK, int MODE = FUSED>
+template <int LOGP, int LV, bool PACK, int MODE = FUSED, int F = 0>
 struct Level {
+    static constexpr uint32_t P = Fld<F>::P;
     static constexpr int R = radix_of(LOGP, LV);
     static constexpr int S = prefix_of(LOGP, LV);
     static constexpr int NPASS = np_of(LOGP);
@@ -350,10 +366,10 @@ struct Level {
         for (int u = threadIdx.x; u < NSUB; u += T) {
             uint32_t x[N1];
             load(x, u, data, a, b0, nb);
-            dft_fwd<R>(x);
+            dft_fwd<R, F>(x);
             if (!LAST) {
                 const int n2 = u % STRIDE;
-                if (n2) twiddle<R>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
+                if (n2) twiddle<R, F>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
 #pragma unroll
                 { const int pb = pbase(u);
 #pragma unroll
@@ -361,19 +377,19 @@ struct Level {
             } else if (MODE == SEGFWD) {
                 uint32_t *dst = const_cast<uint32_t *>(a.shat) + (size_t)u * N1;
 #pragma unroll
-                for (int q = 0; q < N1; ++q) dst[q] = mont(x[q], a.scaleM);  // * P^-1 * 2^32
+                for (int q = 0; q < N1; ++q) dst[q] = mont<F>(x[q], a.scaleM);  // * P^-1 * 2^32
             } else {
                 // pointwise product with the seed spectrum (DIF order: position u*N1+q)
                 const uint4 *sh = reinterpret_cast<const uint4 *>(a.shat + (size_t)u * N1);
 #pragma unroll
                 for (int q4 = 0; q4 < N1 / 4; ++q4) {
                     uint4 s4 = __ldg(sh + q4);
-                    x[4 * q4 + 0] = mont(x[4 * q4 + 0], s4.x);
-                    x[4 * q4 + 1] = mont(x[4 * q4 + 1], s4.y);
-                    x[4 * q4 + 2] = mont(x[4 * q4 + 2], s4.z);
-                    x[4 * q4 + 3] = mont(x[4 * q4 + 3], s4.w);
+                    x[4 * q4 + 0] = mont<F>(x[4 * q4 + 0], s4.x);
+                    x[4 * q4 + 1] = mont<F>(x[4 * q4 + 1], s4.y);
+                    x[4 * q4 + 2] = mont<F>(x[4 * q4 + 2], s4.z);
+                    x[4 * q4 + 3] = mont<F>(x[4 * q4 + 3], s4.w);
                 }
-                dft_inv<R>(x);
+                dft_inv<R, F>(x);
                 if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
                 else {
 #pragma unroll
@@ -395,8 +411,8 @@ struct Level {
 #pragma unroll
             for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
             const int n2 = u % STRIDE;
-            if (n2) twiddle<R>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
-            dft_inv<R>(x);
+            if (n2) twiddle<R, F>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
+            dft_inv<R, F>(x);
             if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
             else {
 #pragma unroll
@@ -409,13 +425,13 @@ struct Level {
     }
 };
 
-template <int LOGP, int LV, bool PACK, int MODE = FUSED>
+template <int LOGP, int LV, bool PACK, int MODE = FUSED, int F = 0>
 __device__ __forceinline__ void run_levels(uint32_t *data, uint32_t *stage, const FusedArgs &a,
                                            uint64_t b0, int nb, uint64_t wfirst) {
-    using L = Level<LOGP, LV, PACK, MODE>;
+    using L = Level<LOGP, LV, PACK, MODE, F>;
     L::fwd(data, stage, a, b0, nb, wfirst);
     if constexpr (!L::LAST) {
-        run_levels<LOGP, LV + 1, PACK, MODE>(data, stage, a, b0, nb, wfirst);
+        run_levels<LOGP, LV + 1, PACK, MODE, F>(data, stage, a, b0, nb, wfirst);
         if constexpr (MODE != SEGFWD) L::inv(data, stage, a, b0, nb, wfirst);
     }
 }
@@ -432,7 +448,7 @@ __device__ __forceinline__ void run_levels(uint32_t *data, uint32_t *stage, cons
 #endif
 constexpr int kSegLog = QRNG_NTT_SEGLOG;  // words per segment-kernel CTA (log2)
 
-template <int LOGS, int MODE>
+template <int LOGS, int MODE, int F = 0>
 __global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
     ntt_segment_kernel(FusedArgs a, uint32_t *ws, uint32_t logP) {
     extern __shared__ uint32_t smem[];
@@ -450,7 +466,7 @@ __global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
     __syncthreads();
     FusedArgs b = a;
     b.shat = a.shat + seg * NS;
-    run_levels<LOGS, 0, false, MODE>(data, nullptr, b, 0, 1, 0);
+    run_levels<LOGS, 0, false, MODE, F>(data, nullptr, b, 0, 1, 0);
     if (MODE == SEGFWD) return;
     for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4)
         *reinterpret_cast<uint4 *>(src + i) =
@@ -469,9 +485,10 @@ struct PassArgs {
 };
 enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4, PASS_INV_EMIT_XOR = 5 };
 
-template <int R, int MODE>
+template <int R, int MODE, int F = 0>
 __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
     constexpr int N1 = 1 << R;
+    constexpr uint32_t P = Fld<F>::P;
     const uint32_t logseg = a.logP - a.S, logstride = logseg - R;
     const uint32_t u = blockIdx.x * 256 + threadIdx.x;  // sub-transform within the block
     const uint64_t bb = blockIdx.y;
@@ -505,14 +522,14 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
         for (int q = 0; q < N1; ++q) x[q] = base[(size_t)q * STRIDE];
     }
     if (MODE <= PASS_FWD) {
-        dft_fwd<R>(x);
-        if (n2) twiddle<R>(x, __ldg(a.tw + ((uint64_t)n2 << a.S)));
+        dft_fwd<R, F>(x);
+        if (n2) twiddle<R, F>(x, __ldg(a.tw + ((uint64_t)n2 << a.S)));
 #pragma unroll
         for (int q = 0; q < N1; ++q) base[(size_t)q * STRIDE] = x[q];
         return;
     }
-    if (n2) twiddle<R>(x, __ldg(a.itw + ((uint64_t)n2 << a.S)));
-    dft_inv<R>(x);
+    if (n2) twiddle<R, F>(x, __ldg(a.itw + ((uint64_t)n2 << a.S)));
+    dft_inv<R, F>(x);
     if (MODE == PASS_INV) {
 #pragma unroll
         for (int q = 0; q < N1; ++q) base[(size_t)q * STRIDE] = x[q];
@@ -568,12 +585,14 @@ __global__ void __launch_bounds__(threads_of(LOGP), 1024 / threads_of(LOGP)) ntt
 }
 
 // ---- plan preparation kernels ----------------------------------------------
+template <int F = 0>
 __device__ uint32_t powmod_d(uint64_t b, uint64_t e) {
+    constexpr uint64_t PP = Fld<F>::P;
     uint64_t r = 1;
-    b %= P;
+    b %= PP;
     while (e) {
-        if (e & 1) r = r * b % P;
-        b = b * b % P;
+        if (e & 1) r = r * b % PP;
+        b = b * b % PP;
         e >>= 1;
     }
     return (uint32_t)r;
@@ -582,18 +601,20 @@ __device__ uint32_t powmod_d(uint64_t b, uint64_t e) {
 // tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P (Montgomery
 // form).  Each thread owns 64 consecutive exponents: one modular power for the
 // first, then a Montgomery chain (mont(x * R, w * R) = x w R), canonicalised.
+template <int F = 0>
 __global__ void twiddle_table_kernel(uint32_t *tw, uint32_t *itw, uint32_t Pn, uint32_t w, uint32_t iw) {
+    constexpr uint32_t P = Fld<F>::P;
     const uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) * 64u;
     if (e0 >= Pn) return;
     const uint32_t wM = (uint32_t)(((uint64_t)w << 32) % P), iwM = (uint32_t)(((uint64_t)iw << 32) % P);
-    uint32_t a = (uint32_t)(((uint64_t)powmod_d(w, e0) << 32) % P);
-    uint32_t b = (uint32_t)(((uint64_t)powmod_d(iw, e0) << 32) % P);
+    uint32_t a = (uint32_t)(((uint64_t)powmod_d<F>(w, e0) << 32) % P);
+    uint32_t b = (uint32_t)(((uint64_t)powmod_d<F>(iw, e0) << 32) % P);
     for (uint32_t k = 0; k < 64 && e0 + k < Pn; ++k) {
         tw[e0 + k] = a;
         itw[e0 + k] = b;
-        a = mont(a, wM);
+        a = mont<F>(a, wM);
         a = a >= P ? a - P : a;
-        b = mont(b, iwM);
+        b = mont<F>(b, iwM);
         b = b >= P ? b - P : b;
     }
 }
@@ -732,9 +753,9 @@ __global__ void __launch_bounds__(512, 2) pass_rate_kernel(uint32_t *sink, int i
     for (int q = 0; q < 32; ++q) x[q] = (threadIdx.x * 32u + q) % P;
     for (int it = 0; it < iters; ++it) {
         dft_fwd<5>(x);
-        twiddle<5>(x, c_roots.w[(it & 31) + 1]);
+        twiddle<5>(x, c_roots[0].w[(it & 31) + 1]);
         dft_inv<5>(x);
-        twiddle<5>(x, c_roots.iw[(it & 31) + 1]);
+        twiddle<5>(x, c_roots[0].iw[(it & 31) + 1]);
     }
     uint32_t acc = 0;
 #pragma unroll
@@ -770,13 +791,13 @@ static int global_radices(int logP, int r[2]) {
     return 2;
 }
 
-template <int MODE>
+template <int MODE, int F = 0>
 static qrng_status launch_pass(int R, const PassArgs &a, uint64_t nb, cudaStream_t s, bool timed) {
     const uint64_t nsub = 1ull << (a.logP - R);
     dim3 grid((unsigned)(nsub / 256), (unsigned)nb);
     KernelTimer t(s, timed);
     switch (R) {
-#define X(RR) case RR: ntt_pass_kernel<RR, MODE><<<grid, 256, 0, s>>>(a); break;
+#define X(RR) case RR: ntt_pass_kernel<RR, MODE, F><<<grid, 256, 0, s>>>(a); break;
         X(1) X(2) X(3) X(4) X(5) X(6)
 #undef X
         default:
@@ -788,17 +809,17 @@ static qrng_status launch_pass(int R, const PassArgs &a, uint64_t nb, cudaStream
     return QRNG_OK;
 }
 
-template <int MODE>
+template <int MODE, int F = 0, int LOGS = kSegLog>
 static qrng_status launch_segments(const FusedArgs &a, uint32_t *ws, int logP, uint64_t nb, cudaStream_t s,
                                    bool timed) {
-    const size_t smem = ((size_t)(1 << kSegLog) + (1 << kSegLog) / 32) * 4;
+    const size_t smem = ((size_t)(1 << LOGS) + (1 << LOGS) / 32) * 4;
     {
-        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(ntt_segment_kernel<kSegLog, MODE>));
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(ntt_segment_kernel<LOGS, MODE, F>));
         if (st != QRNG_OK) return st;
     }
-    dim3 grid((unsigned)(1u << (logP - kSegLog)), (unsigned)nb);
+    dim3 grid((unsigned)(1u << (logP - LOGS)), (unsigned)nb);
     KernelTimer t(s, timed);
-    ntt_segment_kernel<kSegLog, MODE><<<grid, threads_of(kSegLog), smem, s>>>(a, ws, (uint32_t)logP);
+    ntt_segment_kernel<LOGS, MODE, F><<<grid, threads_of(LOGS), smem, s>>>(a, ws, (uint32_t)logP);
     t.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
@@ -836,7 +857,7 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
     QRNG_CUDA_TRY(cudaMallocAsync(&seed_words, nwords * 4, s));
     const uint64_t w = powmod_h(3, (P - 1) >> logP), iw = powmod_h(w, P - 2);
     count_launch();
-    twiddle_table_kernel<<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
+    twiddle_table_kernel<0><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
                                                                      (uint32_t)w, (uint32_t)iw);
     QRNG_CUDA_TRY(cudaGetLastError());
     count_launch();
@@ -1007,6 +1028,265 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
             set_error("NTT path: unsupported P = 2^%d", pl.logP);
             return QRNG_E_UNSUPPORTED;
     }
+}
+
+
+// ---- NEXT-4: one block across W GPUs (distributed four-step NTT) -----------
+// ("cut the sequence into several blocks" is
+// the opposite move -- here one block too large for a fast single-GPU
+// transform is cut across GPUs instead.)  Prime F = 1 (p = 7 * 2^26 + 1,
+// P = W * N2 <= 2^26).  Index t = N2 n1 + n2 (n1 < W), k = k1 + W k2:
+//   X^[k1 + W k2] = NTT_N2( u_k1 )[k2],
+//   u_k1[n2] = w_P^(n2 k1) * sum_{n1<W} x[N2 n1 + n2] w_W^(n1 k1),
+// so rank r computes the spectrum slice k1 = r from the (small, replicated)
+// block bits with NO communication, multiplies by the matching slice of the
+// seed spectrum (plan, same permuted order), runs the local inverse and
+// twists:  v_r[n2] = w_P^(-n2 r) * INTT_N2(...)[n2].  Then
+//   z[N2 n1 + n2] = sum_{k1<W} w_W^(-n1 k1) v_k1[n2]      (P^-1 folded into S^)
+// needs every rank's v at the same n2: ONE all-to-all of N2 words per rank
+// (chunk r' = columns [r' N2/W, (r'+1) N2/W)), after which rank r' finishes
+// its columns for every n1 and ORs the window parities into the key.  W = 1
+// is the single-GPU path for 2^23 < L <= 2^26.
+
+// u[n2] = twist(n2) * sum_{n1 < W} bit(N2 n1 + n2) * c[n1]  (c canonical, sum < W p < 2^32)
+struct ColArgs {
+    const uint8_t *bits;       // MSB-first bit buffer (block or seed)
+    uint64_t len;              // bits that enter the product (n or L); bits past len read as 0
+    uint32_t N2, W;
+    uint32_t c[8];             // w_W^(n1 r), canonical
+    const uint32_t *twM;       // w_P^(n2 r) * 2^32 mod p (Montgomery form), null for r = 0
+    uint32_t *u;
+};
+__global__ void dist_col_dft_kernel(ColArgs a) {
+    constexpr uint32_t Pp = Fld<1>::P;
+    for (uint32_t n2 = blockIdx.x * blockDim.x + threadIdx.x; n2 < a.N2; n2 += gridDim.x * blockDim.x) {
+        uint32_t acc = 0;
+        for (uint32_t n1 = 0; n1 < a.W; ++n1) {
+            const uint64_t t = (uint64_t)a.N2 * n1 + n2;
+            if (t < a.len && ((__ldg(a.bits + (t >> 3)) >> (7 - (t & 7))) & 1u)) acc += a.c[n1];
+        }
+        acc %= Pp;
+        a.u[n2] = a.twM ? mont<1>(acc, __ldg(a.twM + n2)) : acc;
+    }
+}
+
+// v[n2] = mont(v[n2], itwM[n2]) = v * w_P^(-n2 r) (lazy)
+__global__ void dist_twist_kernel(uint32_t *v, const uint32_t *itwM, uint32_t N2) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N2; i += gridDim.x * blockDim.x)
+        v[i] = mont<1>(v[i], __ldg(itwM + i));
+}
+
+// Rank r' after the all-to-all: recv[k1 * C + j] = v_k1[r' C + j] (C = N2 / W).
+// z[N2 n1 + n2] = sum_k1 w_W^(-n1 k1) v_k1[n2]; window t in [len-1, len-1+m)
+// -> output bit g0 + t - (len - 1).  Lanes take consecutive j (consecutive t).
+struct FinishArgs {
+    const uint32_t *recv;
+    uint64_t len, m;           // product length (n) and outputs per block
+    uint32_t N2, W, rank;
+    uint32_t icM[8][8];        // w_W^(-n1 k1) * 2^32 mod p (Montgomery form)
+    OutStream out;
+    uint64_t g0;               // global output bit of y_0
+};
+__global__ void dist_finish_kernel(FinishArgs a) {
+    constexpr uint32_t Pp = Fld<1>::P;
+    const uint32_t C = a.N2 / a.W;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; j0 < C; j0 += gridDim.x * blockDim.x) {
+        const uint32_t j = j0 + lane;  // C % 32 == 0
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = k < (int)a.W ? __ldg(a.recv + (size_t)k * C + j) : 0u;
+        for (uint32_t n1 = 0; n1 < a.W; ++n1) {
+            uint32_t z = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < (int)a.W) z = red2<1>(z + mont<1>(v[k], a.icM[n1][k]));
+            z = z >= Pp ? z - Pp : z;
+            const uint64_t t = (uint64_t)a.N2 * n1 + (uint64_t)a.rank * C + j;
+            const int64_t i = (int64_t)t - (int64_t)(a.len - 1);
+            const bool valid = i >= 0 && i < (int64_t)a.m;
+            const uint32_t bal = __ballot_sync(0xffffffffu, valid && (z & 1u));
+            if (lane == 0 && bal) {
+                const int64_t G = (int64_t)a.g0 + ((int64_t)((uint64_t)a.N2 * n1 + (uint64_t)a.rank * C + j0) -
+                                                   (int64_t)(a.len - 1));
+                const uint32_t V = __brev(bal);  // lane L (output G + L) -> logical bit 31 - L
+                const int64_t W0 = G >= 0 ? (G >> 5) : -((31 - G) >> 5);
+                const int o = (int)(G - W0 * 32);
+                const uint32_t hi = V >> o, lo = o ? (V << (32 - o)) : 0u;
+                if (hi) emit_word(a.out, (uint64_t)W0, hi, false);
+                if (lo) emit_word(a.out, (uint64_t)(W0 + 1), lo, false);
+            }
+        }
+    }
+}
+
+static unsigned grid_of(uint64_t items, unsigned block = 256) {
+    const uint64_t g = (items + block - 1) / block;
+    return (unsigned)(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
+}
+
+// The local length-N2 transform chain on one buffer (in place): forward; then
+// either the scaled spectrum (seed: SEGFWD, written to shat) or the pointwise
+// product with shat and the inverse (data: SEG + inverse passes).
+static qrng_status dist_local_ntt(const DistPlan &pl, uint32_t *ws, bool seed, uint32_t scaleM, cudaStream_t s) {
+    const int logN2 = pl.logN2;
+    FusedArgs fa{};
+    fa.shat = pl.shat;
+    fa.tw = pl.tw;
+    fa.itw = pl.itw;
+    fa.scaleM = scaleM;
+    if (logN2 <= kSegLog) {
+        fa.tw_shift = 0;
+        switch (logN2) {
+#define X(LS)                                                                                               \
+    case LS:                                                                                                \
+        return seed ? launch_segments<SEGFWD, 1, LS>(fa, ws, LS, 1, s, false)                                \
+                    : launch_segments<SEG, 1, LS>(fa, ws, LS, 1, s, true);
+            X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)
+#undef X
+            default: set_error("distributed NTT: unsupported N2 = 2^%d", logN2); return QRNG_E_UNSUPPORTED;
+        }
+    }
+    int r[2];
+    const int np = global_radices(logN2, r);
+    PassArgs pa{};
+    pa.ws = ws;
+    pa.tw = pl.tw;
+    pa.itw = pl.itw;
+    pa.logP = (uint32_t)logN2;
+    pa.S = 0;
+    qrng_status st = launch_pass<PASS_FWD, 1>(r[0], pa, 1, s, !seed);
+    if (st == QRNG_OK && np == 2) {
+        pa.S = (uint32_t)r[0];
+        st = launch_pass<PASS_FWD, 1>(r[1], pa, 1, s, !seed);
+    }
+    fa.tw_shift = (uint32_t)(logN2 - kSegLog);
+    if (st == QRNG_OK) st = seed ? launch_segments<SEGFWD, 1>(fa, ws, logN2, 1, s, false)
+                                 : launch_segments<SEG, 1>(fa, ws, logN2, 1, s, true);
+    if (seed || st != QRNG_OK) return st;
+    if (np == 2) {
+        pa.S = (uint32_t)r[0];
+        st = launch_pass<PASS_INV, 1>(r[1], pa, 1, s, true);
+    }
+    if (st == QRNG_OK) {
+        pa.S = 0;
+        st = launch_pass<PASS_INV, 1>(r[0], pa, 1, s, true);
+    }
+    return st;
+}
+
+static qrng_status dist_col(const DistPlan &pl, const uint8_t *bits, uint64_t len, uint32_t *u, cudaStream_t s) {
+    ColArgs c{};
+    c.bits = bits;
+    c.len = len;
+    c.N2 = pl.N2;
+    c.W = pl.world;
+    for (uint32_t i = 0; i < 8; ++i) c.c[i] = i < pl.world ? pl.colw[i] : 0u;
+    c.twM = pl.twr;
+    c.u = u;
+    count_launch();
+    dist_col_dft_kernel<<<grid_of(pl.N2), 256, 0, s>>>(c);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
+}
+
+qrng_status dist_plan_init(DistPlan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t world,
+                           uint32_t rank, cudaStream_t s) {
+    if (world == 0 || world > 8 || (world & (world - 1)) || rank >= world) {
+        set_error("distributed NTT: world must be 1, 2, 4 or 8 and rank < world (got %u, %u)", world, rank);
+        return QRNG_E_INVALID;
+    }
+    const uint64_t L = n + m - 1;
+    int logP = 5;
+    while ((1ull << logP) < L) ++logP;
+    int logW = 0;
+    while ((1u << logW) < world) ++logW;
+    if (logP - logW < 10) logP = 10 + logW;  // N2 / W >= 32 columns per peer (warp-wide finish)
+    if (logP > kMaxLogP2) {
+        set_error("distributed NTT: L = %llu exceeds 2^26", (unsigned long long)L);
+        return QRNG_E_UNSUPPORTED;
+    }
+    constexpr uint64_t Pp = Fld<1>::P;
+    pl.n = n;
+    pl.m = m;
+    pl.world = world;
+    pl.rank = rank;
+    pl.logP = logP;
+    pl.logN2 = logP - logW;
+    pl.N2 = 1u << pl.logN2;
+    const uint64_t wP = powmod_p(3, (Pp - 1) >> logP, Pp);        // w_P
+    const uint64_t wN2 = powmod_p(wP, world, Pp);                  // w_N2 = w_P^W
+    const uint64_t wW = powmod_p(wP, 1ull << pl.logN2, Pp);        // w_W = w_P^N2
+    const uint64_t iwW = powmod_p(wW, Pp - 2, Pp);
+    const uint64_t R32 = (1ull << 32) % Pp;
+    for (uint32_t i = 0; i < 8; ++i) {
+        pl.colw[i] = (uint32_t)powmod_p(wW, (uint64_t)i * rank, Pp);
+        for (uint32_t k = 0; k < 8; ++k)
+            pl.icolM[i][k] = (uint32_t)(powmod_p(iwW, (uint64_t)i * k % world, Pp) * R32 % Pp);
+    }
+    const size_t bytes = (size_t)pl.N2 * 4;
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.shat, bytes, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.tw, bytes, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(&pl.itw, bytes, s));
+    count_launch();
+    twiddle_table_kernel<1><<<(unsigned)(((pl.N2 + 63) / 64 + 127) / 128), 128, 0, s>>>(
+        pl.tw, pl.itw, pl.N2, (uint32_t)wN2, (uint32_t)powmod_p(wN2, Pp - 2, Pp));
+    QRNG_CUDA_TRY(cudaGetLastError());
+    if (rank != 0) {  // twist tables w_P^(+-n2 r), Montgomery form
+        QRNG_CUDA_TRY(cudaMallocAsync(&pl.twr, bytes, s));
+        QRNG_CUDA_TRY(cudaMallocAsync(&pl.itwr, bytes, s));
+        const uint64_t wr = powmod_p(wP, rank, Pp);
+        count_launch();
+        twiddle_table_kernel<1><<<(unsigned)(((pl.N2 + 63) / 64 + 127) / 128), 128, 0, s>>>(
+            pl.twr, pl.itwr, pl.N2, (uint32_t)wr, (uint32_t)powmod_p(wr, Pp - 2, Pp));
+        QRNG_CUDA_TRY(cudaGetLastError());
+    }
+    // seed spectrum slice k1 = rank, scaled by P^-1 (and 2^32: Montgomery form
+    // for the pointwise product): scaleM = P^-1 * 2^64 mod p
+    uint32_t *u = nullptr;
+    QRNG_CUDA_TRY(cudaMallocAsync(&u, bytes, s));
+    qrng_status st = dist_col(pl, d_seed, L, u, s);
+    const uint64_t pinvP = powmod_p((1ull << logP) % Pp, Pp - 2, Pp);
+    const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * (((unsigned __int128)1 << 64) % Pp) % Pp);
+    if (st == QRNG_OK) st = dist_local_ntt(pl, u, true, scaleM, s);
+    cudaFreeAsync(u, s);
+    return st;
+}
+
+void dist_plan_free(DistPlan &pl, cudaStream_t s, bool async) {
+    for (uint32_t *p : {pl.shat, pl.tw, pl.itw, pl.twr, pl.itwr})
+        if (p) { if (async) cudaFreeAsync(p, s); else cudaFree(p); }
+    pl = DistPlan{};
+}
+
+qrng_status dist_local(const DistPlan &pl, const uint8_t *d_block_bits, uint32_t *d_buf, cudaStream_t s) {
+    qrng_status st = dist_col(pl, d_block_bits, pl.n, d_buf, s);
+    if (st == QRNG_OK) st = dist_local_ntt(pl, d_buf, false, 0, s);
+    if (st == QRNG_OK && pl.itwr) {
+        count_launch();
+        dist_twist_kernel<<<grid_of(pl.N2), 256, 0, s>>>(d_buf, pl.itwr, pl.N2);
+        QRNG_CUDA_TRY(cudaGetLastError());
+    }
+    return st;
+}
+
+qrng_status dist_finish(const DistPlan &pl, const uint32_t *d_recv, const OutStream &out, uint64_t g0,
+                        cudaStream_t s) {
+    FinishArgs f{};
+    f.recv = d_recv;
+    f.len = pl.n;
+    f.m = pl.m;
+    f.N2 = pl.N2;
+    f.W = pl.world;
+    f.rank = pl.rank;
+    memcpy(f.icM, pl.icolM, sizeof f.icM);
+    f.out = out;
+    f.g0 = g0;
+    KernelTimer t(s, true);
+    dist_finish_kernel<<<grid_of(pl.N2 / pl.world), 256, 0, s>>>(f);
+    t.stop();
+    QRNG_CUDA_TRY(cudaGetLastError());
+    return QRNG_OK;
 }
 
 }  // namespace ntt

@@ -103,7 +103,9 @@ __device__ __forceinline__ void emit_word(const OutStream &o, uint64_t W, uint32
 // NTT path (ntt.cu).  Prime p = 119 * 2^23 + 1, primitive root 3.
 namespace ntt {
 constexpr uint32_t kP = 998244353u;
+constexpr uint32_t kP2 = 469762049u;  // 7 * 2^26 + 1: the distributed (NEXT-4) transforms, P up to 2^26
 constexpr int kMaxLogP = 23;
+constexpr int kMaxLogP2 = 26;
 constexpr int kMaxFusedLogP = 15;  // one CTA holds the whole transform in smem
 
 struct Plan {
@@ -124,6 +126,29 @@ void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                     uint64_t m, const OutStream &out, cudaStream_t s);
 int choose_pack_shift(uint64_t n, int logP);
+// NEXT-4: one block across `world` GPUs, distributed four-step NTT with the
+// prime kP2 (P = world * N2 <= 2^26).  See ntt.cu "NEXT-4".
+struct DistPlan {
+    uint64_t n = 0, m = 0;
+    uint32_t world = 1, rank = 0;
+    int logP = 0, logN2 = 0;
+    uint32_t N2 = 0;                   // local transform length = words exchanged per rank
+    uint32_t colw[8] = {};             // w_W^(n1 rank), canonical
+    uint32_t icolM[8][8] = {};         // w_W^(-n1 k1), Montgomery form
+    uint32_t *shat = nullptr;          // seed spectrum slice k1 = rank (N2 words, scaled by P^-1, Montgomery)
+    uint32_t *tw = nullptr, *itw = nullptr;    // w_N2^(+-e), e < N2 (Montgomery)
+    uint32_t *twr = nullptr, *itwr = nullptr;  // w_P^(+-n2 rank) (null for rank 0)
+};
+qrng_status dist_plan_init(DistPlan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t world,
+                           uint32_t rank, cudaStream_t s);
+void dist_plan_free(DistPlan &pl, cudaStream_t s, bool async);
+// column DFT of the block bits for k1 = rank, local NTT, * S^, inverse, twist:
+// d_buf (N2 words) = this rank's send buffer, chunk r' for peer r'
+qrng_status dist_local(const DistPlan &pl, const uint8_t *d_block_bits, uint32_t *d_buf, cudaStream_t s);
+// after the all-to-all: radix-W inverse across the received chunks, window
+// parities ORed into `out` at global bit g0 + i (out pre-zeroed)
+qrng_status dist_finish(const DistPlan &pl, const uint32_t *d_recv, const OutStream &out, uint64_t g0,
+                        cudaStream_t s);
 qrng_status butterfly_rate(int iters, uint64_t *butterflies, cudaStream_t s, bool with_twiddles);
 }  // namespace ntt
 

@@ -8,7 +8,12 @@ data-path collective.  The collectives here are setup/teardown only:
 * ``allreduce_counts``  -- the 256 histogram counts of sharded samples, so any
                            rank can finalise ``qrng_entropy_from_counts``;
 * ``gather_keys``       -- optional assembly of the full key stream (C4) from
-                           per-rank packed shards at arbitrary bit offsets.
+                           per-rank packed shards at arbitrary bit offsets;
+* ``extract_block_distributed`` -- NEXT-4: ONE block across the group
+                           (distributed four-step NTT, qrng_dist_*): the one
+                           data-path exchange is a single all-to-all of N2
+                           words per rank, then an OR (byte SUM of disjoint
+                           bits) of the ranks' key bits.
 
 Everything takes a ``torch.distributed`` process group (NCCL on GPUs, gloo in
 the CPU tests).
@@ -71,3 +76,81 @@ def gather_keys(local_key, n_local_blocks: int, m: int, group=None) -> np.ndarra
     dist.all_gather(outs, pad, group=group)
     return concat_bitstreams([o.cpu().numpy()[:(s * m + 7) // 8] for o, s in zip(outs, sizes)],
                              [s * m for s in sizes])
+
+
+def four_step_exchange(ops, group=None):
+    """The NEXT-4 data movement, independent of where the local steps run.
+
+    ``ops.local()`` returns this rank's send buffer (N2 words; chunk r' of
+    N2/world words goes to rank r'), ``ops.finish(recv)`` takes the received
+    buffer (chunk k1 from rank k1) and returns this rank's key bytes (its bits
+    only, zeros elsewhere).  One all-to-all of equal chunks, then a byte-wise
+    SUM all-reduce of the keys -- the ranks' bits are disjoint, so the sum is
+    their OR.  Collectives run on the tensors' device for NCCL and on host
+    copies for gloo."""
+    import torch
+    import torch.distributed as dist
+    send = ops.local()
+    host = dist.get_backend(group) == "gloo" and send.device.type != "cpu"
+    s = send.cpu() if host else send
+    recv = torch.empty_like(s)
+    dist.all_to_all_single(recv, s, group=group)
+    key = ops.finish(recv.to(send.device) if host else recv)
+    k = key.cpu() if host and key.device.type != "cpu" else key
+    dist.all_reduce(k, op=dist.ReduceOp.SUM, group=group)
+    return k.to(key.device) if k is not key else key
+
+
+class _GpuOps:
+    """The product's local steps: qrng_dist_local / qrng_dist_finish on this rank's GPU."""
+
+    def __init__(self, plan, block, stream=None):
+        self.plan, self.block, self.stream = plan, block, stream
+
+    def local(self):
+        return self.plan.local(self.block, self.plan.new_buffer(), stream=self.stream)
+
+    def finish(self, recv):
+        import torch
+        from paper_2011_04130_b200 import out_bytes
+        key = torch.zeros((out_bytes(1, self.plan.m) + 3) // 4 * 4, dtype=torch.uint8, device=recv.device)
+        self.plan.finish(recv.contiguous(), key, stream=self.stream)
+        return key[:out_bytes(1, self.plan.m)]
+
+
+def extract_block_distributed(block, n: int, m: int, seed, group=None, plan=None, stream=None):
+    """NEXT-4: the m key bits of ONE n-bit block (block bits replicated on every
+    rank, seed on every rank -- broadcast_seed), computed across the group's
+    GPUs; returns the full key (ceil(m/8) bytes) on every rank."""
+    import torch.distributed as dist
+    from paper_2011_04130_b200 import DistPlan
+    own = plan is None
+    if own:
+        plan = DistPlan(n, m, seed, dist.get_world_size(group), dist.get_rank(group), stream=stream)
+    try:
+        return four_step_exchange(_GpuOps(plan, block, stream), group)
+    finally:
+        if own:
+            plan.close()
+
+
+def extract_block_emulated(block, n: int, m: int, seed, world: int):
+    """TEST / single-GPU check of NEXT-4: the `world` ranks' local steps run one
+    after another in this process on one GPU (no rank waits on another inside a
+    kernel), the all-to-all is a device copy of chunks, the OR a byte sum."""
+    import torch
+    from paper_2011_04130_b200 import DistPlan, out_bytes
+    plans = [DistPlan(n, m, seed, world, r) for r in range(world)]
+    try:
+        sends = [p.local(block, p.new_buffer()) for p in plans]
+        C = plans[0].exchange_words // world
+        key = torch.zeros(out_bytes(1, m), dtype=torch.int32, device=block.device)
+        for r, p in enumerate(plans):
+            recv = torch.cat([s[r * C:(r + 1) * C] for s in sends])
+            k = torch.zeros((out_bytes(1, m) + 3) // 4 * 4, dtype=torch.uint8, device=block.device)
+            p.finish(recv, k)
+            key += k[:out_bytes(1, m)].to(torch.int32)
+        return key.to(torch.uint8)
+    finally:
+        for p in plans:
+            p.close()

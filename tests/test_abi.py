@@ -3,6 +3,7 @@ header declares, rejects invalid arguments with the documented codes, refuses
 to run without an sm_100 device (no CPU fallback), and its host-side entropy
 finalisation (qrng_entropy_from_counts) agrees with the oracle."""
 import math
+import ctypes
 import os
 import re
 
@@ -64,7 +65,12 @@ def test_invalid_arguments_codes(lib):
     assert _call_extract(lib, 64, 32, 0) == q.QRNG_E_INVALID        # n_blocks = 0
     assert _call_extract(lib, 64, 32, 1, raw=0) == q.QRNG_E_INVALID  # NULL
     assert _call_extract(lib, 48, 32, 1) == q.QRNG_E_UNSUPPORTED    # n % 32
-    assert _call_extract(lib, 1 << 23, (1 << 22), 1) == q.QRNG_E_UNSUPPORTED  # L > 2^23
+    assert _call_extract(lib, 1 << 26, (1 << 22), 1) == q.QRNG_E_UNSUPPORTED  # L > 2^26
+    # NEXT-4 plans: bad world / rank are rejected before any device work
+    h = ctypes.c_void_p()
+    assert lib.qrng_dist_plan_create(1 << 24, 1 << 23, 16, 3, 0, None, ctypes.byref(h)) == q.QRNG_E_INVALID
+    assert lib.qrng_dist_plan_create(1 << 24, 1 << 23, 16, 4, 4, None, ctypes.byref(h)) == q.QRNG_E_INVALID
+    assert lib.qrng_dist_plan_create(1 << 26, 1 << 22, 16, 4, 0, None, ctypes.byref(h)) == q.QRNG_E_UNSUPPORTED
     assert "n=" in q.last_error() or "seed" in q.last_error() or "exceeds" in q.last_error()
     assert lib.qrng_minentropy(16, 0, 8, None, 1024, 0, 16, None) == q.QRNG_E_INVALID
     assert lib.qrng_minentropy(16, 10, 9, None, 1024, 0, 16, None) == q.QRNG_E_INVALID

@@ -105,3 +105,100 @@ def test_bench_launcher_spawns_ranks(cfg, scaling, blocks):
     assert line["config"]["blocks_total"] == blocks
     assert line["shards"] == [list(qd.shard_range(blocks, k, 2)) for k in range(2)]
     assert line["seed_broadcast_ok_ranks"] == 2 and line["max_over_ranks"] == 2.0
+
+
+# ---- NEXT-4: one block across ranks (distributed four-step NTT) ------------------
+# The data movement of paper_2011_04130_b200.dist.four_step_exchange (one
+# all-to-all of equal chunks, then an OR of the ranks' keys by byte SUM) is
+# checked here on CPU with gloo.  The local steps -- the CUDA kernels
+# qrng_dist_local / qrng_dist_finish on a GPU -- are modelled by a plain
+# numpy reading of the four-step decomposition (natural-order DFT matrices mod
+# p = 7*2^26 + 1), so a wrong twist exponent, chunk order or column range in
+# the decomposition fails against the oracle.
+
+P2 = 469762049  # 7 * 2^26 + 1, primitive root 3
+
+
+def _dft(vec, root):
+    """Natural-order DFT mod P2 by its matrix (small sizes)."""
+    N = vec.size
+    e = (np.arange(N)[:, None] * np.arange(N)[None, :]) % N
+    pw = np.array([pow(root, int(k), P2) for k in range(N)], dtype=np.int64)
+    return ((pw[e] * (vec % P2)[None, :]) % P2).sum(axis=1) % P2
+
+
+class _NumpyFourStep:
+    def __init__(self, x_bits, s_bits, n, m, world, rank):
+        L = n + m - 1
+        logW = world.bit_length() - 1
+        logP = max(int(np.ceil(np.log2(L))), 10 + logW)
+        self.P, self.N2, self.W, self.r, self.n, self.m = 1 << logP, 1 << (logP - logW), world, rank, n, m
+        self.wP = pow(3, (P2 - 1) >> logP, P2)
+        self.wW = pow(self.wP, self.N2, P2)
+        self.wN2 = pow(self.wP, world, P2)
+        self.x, self.s = x_bits, s_bits
+
+    def _u(self, bits):
+        N2, W, r = self.N2, self.W, self.r
+        full = np.zeros(self.P, np.int64)
+        full[:bits.size] = bits
+        cols = full.reshape(W, N2)  # [n1][n2] = t = N2 n1 + n2
+        c = np.array([pow(self.wW, n1 * r, P2) for n1 in range(W)], np.int64)
+        tw = np.array([pow(self.wP, n2 * r, P2) for n2 in range(N2)], np.int64)
+        return ((cols * c[:, None]).sum(axis=0) % P2) * tw % P2
+
+    def local(self):
+        import torch
+        X = _dft(self._u(self.x), self.wN2)
+        S = _dft(self._u(self.s), self.wN2)
+        v = _dft(X * S % P2, pow(self.wN2, P2 - 2, P2))
+        itw = np.array([pow(self.wP, (-(n2 * self.r)) % (P2 - 1), P2) for n2 in range(self.N2)], np.int64)
+        return torch.from_numpy((v * itw % P2).astype(np.int32))
+
+    def finish(self, recv):
+        import torch
+        W, N2, r = self.W, self.N2, self.r
+        C = N2 // W
+        V = recv.numpy().astype(np.int64).reshape(W, C)  # [k1][j]
+        pinv = pow(self.P, P2 - 2, P2)
+        key = np.zeros(self.m, np.uint8)
+        for n1 in range(W):
+            w = np.array([pow(self.wW, (-(n1 * k1)) % (P2 - 1), P2) for k1 in range(W)], np.int64)
+            z = (V * w[:, None] % P2).sum(axis=0) % P2 * pinv % P2
+            t = N2 * n1 + r * C + np.arange(C)
+            i = t - (self.n - 1)
+            ok = (i >= 0) & (i < self.m)
+            key[i[ok]] = (z[ok] & 1).astype(np.uint8)
+        return torch.from_numpy(np.packbits(key))
+
+
+def _four_step_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        n, m = 256, 179
+        x = np.unpackbits(S.random_bytes(31, n // 8))
+        s = np.unpackbits(S.random_bytes(31, (n + m - 1 + 7) // 8, tag=4))[:n + m - 1]
+        key = qd.four_step_exchange(_NumpyFourStep(x, s, n, m, world, rank))
+        ref = oracle.extract(np.packbits(x), 1, n, m, np.packbits(s))
+        q.put((rank, np.array_equal(key.numpy(), ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_four_step_exchange_gloo(oracle_mod, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_four_step_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert sorted(r[0] for r in res) == list(range(world))
+    assert all(r[1] for r in res), "distributed four-step key differs from the oracle"
