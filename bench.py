@@ -54,7 +54,7 @@ METRIC = "Toeplitz extraction raw Gbit/s (1/2/4/8 B200), fraction of roofline"
 # the default line's `configs` object: (label, --config code)
 EXTRA_CONFIGS = [("cfg1", 1), ("cfg3", 3), ("cfg4a", 4), ("cfg4b", 41),
                  ("cfg5_n2^10", 10), ("cfg5_n2^13", 13), ("cfg5_n2^16", 16), ("cfg5_n2^18", 18),
-                 ("cfg5_n2^19", 19), ("cfg5_n2^22", 22)]
+                 ("cfg5_n2^19", 19), ("cfg5_n2^22", 22), ("next4_n2^24", 124)]
 
 
 def peaks():
@@ -677,6 +677,116 @@ def cpu_baseline_rows(w: S.Workload, budget_s: float, cores: int):
                       f"OpenMP over rows), EXTRAPOLATED to the block's {w.m} rows"}
 
 
+def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int = 4):
+    """NEXT-4: ONE block across all ranks -- the distributed
+    four-step NTT (qrng_dist_local, one all_to_all_single of N2 words per rank,
+    qrng_dist_finish, an OR all-reduce of the key bytes) for `blocks` blocks of
+    n = 2^24 bits per step (m = floor(0.7 n), L > 2^23: past the single-GPU
+    prime's limit).  The exchange is a real data-path collective inside the
+    timed region (NCCL); at N = 1 it is the single-GPU world-1 four-step.
+    Block bits are replicated (2 MiB each); the seed is broadcast once."""
+    import torch
+    from paper_2011_04130_b200 import dist as qd
+    m = 7 * n // 10
+    W = ctx.world
+    raw_np = S.adc_samples(24, blocks * n // 8)
+    seed_np = S.uniform_bits(24, n + m - 1, tag=7)
+    seed = ctx.broadcast_seed(seed_np)
+    raw = torch.from_numpy(raw_np).cuda()
+    stream = torch.cuda.current_stream()
+    plan = q.DistPlan(n, m, seed, W, ctx.rank)
+    send = plan.new_buffer()
+    recv = torch.empty_like(send)
+    kbytes = q.out_bytes(1, m)
+    keys = torch.zeros(blocks, (kbytes + 3) // 4 * 4, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    gloo = ctx.backend == "gloo"
+
+    def step():
+        keys.zero_()
+        for b in range(blocks):
+            plan.local(raw[b * n // 8:(b + 1) * n // 8], send, stream=stream)
+            if W > 1:
+                if gloo:
+                    r_ = torch.empty(send.numel(), dtype=torch.int32)
+                    ctx.dist.all_to_all_single(r_, send.cpu())
+                    recv.copy_(r_)
+                else:
+                    ctx.dist.all_to_all_single(recv, send)
+            plan.finish(recv if W > 1 else send, keys[b], stream=stream)
+        if W > 1:
+            k = keys.cpu() if gloo else keys
+            ctx.dist.all_reduce(k, op=ctx.dist.ReduceOp.SUM)  # disjoint bits: SUM == OR
+            if gloo:
+                keys.copy_(k)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    q.kernel_timing(True, aux=False)
+    q.kernel_time_split()
+    ctx.barrier()
+    torch.cuda.synchronize()
+    l0 = q.launch_count()
+    t_wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    launches = q.launch_count() - l0
+    ctx.barrier()
+    km, kn, _, _ = q.kernel_time_split()
+    q.kernel_timing(False)
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    ms_max, = ctx.allreduce([ms], "max")
+    bits = float(blocks) * n * args.steps
+    value = bits / (ms_max * 1e-3) / 1e9
+    key_np = keys[-1, :kbytes].cpu().numpy()
+    parity = None
+    if not args.no_parity:
+        import oracle
+        oracle.build()
+        rng = np.random.default_rng(124)
+        rows = np.unique(np.concatenate([[0, 1, m - 2, m - 1], rng.integers(0, m, 256)])).astype(np.uint64)
+        b = blocks - 1
+        ref = oracle.extract_rows(raw_np, np.full(rows.size, b, np.uint64), rows, n, m, seed_np)
+        pos = rows.astype(np.int64)
+        got = (key_np[pos >> 3] >> (7 - (pos & 7))) & 1
+        bad, = ctx.allreduce([float(np.count_nonzero(got != ref))], "sum")
+        parity = {"status": "bit-exact" if bad == 0 else f"MISMATCH ({int(bad)} bits)",
+                  "checked_bits": int(rows.size) * W, "mismatches": int(bad),
+                  "what": f"{rows.size} sampled key bits of the last block on every rank, vs oracle_extract_rows"}
+    # ALU roofline: every rank runs one local length-N2 convolution transform per block
+    N2 = plan.exchange_words
+    bfly = blocks * (N2 * math.log2(N2) + N2)
+    per_step_s = (km / args.steps * 1e-3) if kn else ms_max / args.steps * 1e-3
+    peak = q.butterfly_rate() / 1e9
+    roof = {"bound": "alu", "achieved": bfly / per_step_s / 1e9, "peak": peak, "unit": "Gbutterfly/s per GPU",
+            "kernel_ms_per_step": km / args.steps, "kernel_share_of_step": (km / args.steps) / (ms / args.steps),
+            "exchange_bytes_per_rank_per_block": N2 * 4 * (W - 1) / W if W > 1 else 0}
+    roof["frac"] = roof["achieved"] / peak
+    plan.close()
+    res = {"value": value, "unit": "Gbit/s", "ms_per_step": ms_max / args.steps, "roofline": roof,
+           "parity": parity, "gpu_launches": int(launches), "wall_ms_per_step_rank0": t_wall / args.steps * 1e3,
+           "dtype": "u8 bits; int32 mod-p NTT (p = 7*2^26+1)",
+           "config": {"workload": f"next4_n2^{n.bit_length() - 1}", "n": n, "m": m, "blocks_per_step": blocks,
+                      "log2_transform": int(math.log2(N2 * W)), "world": W,
+                      "scaling": "strong (each block's transform split across the ranks)",
+                      "step": "per block: qrng_dist_local -> all_to_all_single (N2 words per rank) -> "
+                              "qrng_dist_finish; then one OR all-reduce of the keys",
+                      "backend": ctx.backend or "single GPU"}}
+    if ctx.rank == 0 and ctx.world == 1 and cpu_budget > 0:
+        res["cpu_baseline"] = cpu_baseline_rows(S.Workload("next4", 24, n, m, blocks, 20.0), cpu_budget, host_cores())
+    del raw, keys, flush, send, recv
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     ctx = Ctx(args)
     if ctx.dry:
@@ -712,8 +822,11 @@ def run_ours(args):
         line["configs"] = {}
         for label, code in extra:
             t1 = time.perf_counter()
-            d = measure(q, ctx, args, code, headline=False,
-                        cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget_extra)
+            if code == 124:
+                d = measure_next4(q, ctx, args, cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget_extra)
+            else:
+                d = measure(q, ctx, args, code, headline=False,
+                            cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget_extra)
             d["wall_s"] = time.perf_counter() - t1
             line["configs"][label] = d
         line["configs_wall_s"] = time.perf_counter() - t0

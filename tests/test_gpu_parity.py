@@ -317,7 +317,8 @@ def test_one_plan_two_streams_concurrently(q, oracle_mod):
 
 def test_max_seed_length_2_23(q, oracle_mod):
     """L = n + m - 1 = 2^23 exactly: the largest transform (P = 2^23, the 2-adic
-    limit of p = 119*2^23 + 1); one bit more is rejected."""
+    limit of p = 119*2^23 + 1); one bit more moves to the world-1 four-step
+    NTT modulo 7*2^26 + 1 (P = 2^24), also bit-exact."""
     n = 5033152  # multiple of 32
     m = (1 << 23) + 1 - n
     B = 2
@@ -325,9 +326,9 @@ def test_max_seed_length_2_23(q, oracle_mod):
     seed = S.random_bytes(123, (n + m - 1 + 7) // 8, tag=3)
     got = gpu_extract(q, raw, B, n, m, seed)
     sampled_check(oracle_mod, got, raw, seed, n, m, B, n_rows=200, key=23)
-    with pytest.raises(q.QrngError) as ei:
-        q.toeplitz_extract(dev(raw), 1, n, m + 1, dev(S.random_bytes(1, (n + m + 7) // 8)))
-    assert ei.value.status == q.QRNG_E_UNSUPPORTED
+    seed2 = S.random_bytes(124, (n + m + 7) // 8, tag=3)
+    got2 = gpu_extract(q, raw, B, n, m + 1, seed2)
+    sampled_check(oracle_mod, got2, raw, seed2, n, m + 1, B, n_rows=200, key=24)
 
 
 @pytest.mark.parametrize("path", PATHS)
