@@ -1,0 +1,38 @@
+#!/bin/bash
+# One GPU pass that refreshes the round's evidence (round 2 layout):
+# tests, smoke, the default bench line (headline + configs object), the bench
+# launch list under ncu, and one `ncu --set full` capture of the dominant
+# kernel of every workload (traffic = dram bytes per launch).
+#   bash tools/round2_evidence.sh TAG
+T=${1:-r2x}
+mkdir -p gpurun_out
+python -m paper_2011_04130_b200.build > /dev/null || exit 1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$T.txt 2>&1; tail -1 gpurun_out/pytest_gpu_$T.txt
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1200 python bench.py > gpurun_out/bench_default_$T.json 2> gpurun_out/bench_default_$T.err
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/${T}_launches_bench_cfg2.csv python bench.py --steps 3 --warmup 3 --configs none \
+    --no-e2e --no-cpu-baseline --no-parity > /dev/null 2>&1
+cap() {  # name config kernel-regex [source]
+  ncu --set full --clock-control none ${4:+--import-source on} -k regex:$3 -s 1 -c 1 -o gpurun_out/${T}_$1 \
+      python tools/one_extract.py --config $2 --reps 2 > gpurun_out/${T}_$1.log 2>&1
+  echo "$1 rc=$?"
+}
+cap gemm_cfg2 2 toeplitz_gemm_kernel src
+cap gemm_cfg1 1 toeplitz_gemm_kernel
+cap gemm_cfg3 3 toeplitz_gemm_kernel
+cap ntt_segment_cfg4 4 ntt_segment_kernel src
+cap ntt_pass_cfg4 4 ntt_pass_kernel
+cap gemm_cfg5_n2^10 10 toeplitz_gemm_kernel
+cap ntt_segment_cfg5_n2^19 19 ntt_segment_kernel
+cap ntt_segment_cfg5_n2^22 22 ntt_segment_kernel
+for f in gpurun_out/${T}_*.ncu-rep; do echo "== $f"; python tools/ncu_summary.py $f; done > gpurun_out/${T}_ncu_summaries.txt 2>&1
+python - gpurun_out/bench_default_$T.json <<'PY'
+import json, sys
+d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); r = d["roofline"]
+print("headline", round(d["value"], 1), "steady", round(d["steady_state"]["value"], 1), "e2e", round(d["e2e"]["value"], 1),
+      "frac", round(r["frac"], 3), d.get("parity_all"), d["clocks"])
+for k, v in d.get("configs", {}).items():
+    r = v.get("roofline") or {}
+    print(k, round(v["value"], 2), r.get("bound"), round(r.get("frac", 0), 3), (v.get("parity") or {}).get("status"))
+PY
