@@ -41,11 +41,11 @@ namespace kara {
 #ifndef QRNG_CSR_THREADS
 #define QRNG_CSR_THREADS 512  // threads of the combine+pack kernel
 #endif
-#ifndef QRNG_KARA_EXP
-#define QRNG_KARA_EXP 0  // timing experiments only (results wrong when != 0)
-#endif
 constexpr uint32_t kMinLeafW = 128;   // narrowest leaf the planner creates (one K stage)
-constexpr int kMaxLeaves = 1024;
+#ifndef QRNG_KARA_MAXLEAVES
+#define QRNG_KARA_MAXLEAVES 1024  // the leaf table is staged in the GEMM kernel's shared memory (32 B per leaf)
+#endif
+constexpr int kMaxLeaves = QRNG_KARA_MAXLEAVES;
 constexpr int kMaxDepth = 10;
 // auto mode: deeper trees spill the leaf parities out of L2 (measured: depth 6
 // loses at n = 2^16, wins at 2^17)
@@ -802,20 +802,12 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_pack_kernel(const uint32
         uint32_t v = 0;
         if (j < ywords) {
             const uint32_t *yr = Ys + bl * y_stride;
-#if QRNG_KARA_EXP == 1  // timing experiment: no combine
-            v = yr[j];
-#else
             for (uint32_t e = 0, c = Cs[j]; e < c; ++e) v ^= yr[Cs[ywords + e * ywords + j]];
-#endif
         }
         Rs[idx] = v;
     }
     __syncthreads();
     const uint32_t gbits = nb * m, gwords = (gbits + 31) / 32;
-#if QRNG_KARA_EXP == 2  // timing experiment: no packing
-    for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) emit_word(out, b0 * m / 32 + w, Rs[w], true);
-    return;
-#endif
     for (uint32_t w = threadIdx.x; w < gwords; w += blockDim.x) {
         const uint32_t G = w * 32, end = min(G + 32, gbits);
         uint32_t b = G / m, i = G - b * m, pos = G, word = 0;

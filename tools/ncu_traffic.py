@@ -1,0 +1,31 @@
+#!/usr/bin/env python
+"""dram__bytes_read.sum + dram__bytes_write.sum per launch of each captured
+dominant kernel (one `ncu --set full` capture per workload) as the JSON that
+bench.py reads for roofline.traffic (profiles/ncu_traffic.json).
+
+    python tools/ncu_traffic.py TAG gpurun_out/TAG_*.ncu-rep > traffic.json
+"""
+import csv, json, os, re, subprocess, sys
+
+WORKLOAD = {"cfg1": "cfg1_n1024", "cfg2": "cfg2_n8192", "cfg3": "cfg3_n65536", "cfg4": "cfg4a_n1048576"}
+tag, reps = sys.argv[1], sys.argv[2:]
+out = {}
+for rep in reps:
+    name = os.path.basename(rep)[len(tag) + 1:-len(".ncu-rep")]  # e.g. gemm_cfg2, ntt_segment_cfg5_n2^19
+    m = re.match(r"(gemm|ntt_segment|ntt_pass)_(cfg\d)(?:_(n2\^\d+))?$", name)
+    if not m:
+        continue
+    kind, cfg, pt = m.groups()
+    wl = f"cfg5_{pt}" if pt else WORKLOAD[cfg]
+    path = "gemm" if kind == "gemm" else "ntt"
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(txt.splitlines()))
+    h, v = r[0], r[2] if len(r) > 2 else r[1]
+    val = lambda k: float(v[h.index(k)].replace(",", "")) if k in h else None
+    rd, wr, t = val("dram__bytes_read.sum"), val("dram__bytes_write.sum"), val("gpu__time_duration.sum")
+    key = f"{wl}/{path}" if kind != "ntt_pass" else f"{wl}/ntt_pass"
+    out[key] = {"bytes_per_launch": (rd or 0) + (wr or 0), "dram_read": rd, "dram_write": wr,
+                "duration_ns_under_ncu": t, "kernel": kind,
+                "source": f"profiles/{tag}_{name} (ncu --set full, one launch, clocks not locked)"}
+json.dump(out, sys.stdout, indent=1)
+print()

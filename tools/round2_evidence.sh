@@ -21,12 +21,17 @@ cap() {  # name config kernel-regex [source]
 cap gemm_cfg2 2 toeplitz_gemm_kernel src
 cap gemm_cfg1 1 toeplitz_gemm_kernel
 cap gemm_cfg3 3 toeplitz_gemm_kernel
-cap ntt_segment_cfg4 4 ntt_segment_kernel src
+cap ntt_segment_cfg4 4 ntt_segment_kernel
 cap ntt_pass_cfg4 4 ntt_pass_kernel
 cap gemm_cfg5_n2^10 10 toeplitz_gemm_kernel
 cap ntt_segment_cfg5_n2^19 19 ntt_segment_kernel
 cap ntt_segment_cfg5_n2^22 22 ntt_segment_kernel
 for f in gpurun_out/${T}_*.ncu-rep; do echo "== $f"; python tools/ncu_summary.py $f; done > gpurun_out/${T}_ncu_summaries.txt 2>&1
+python tools/ncu_traffic.py $T gpurun_out/${T}_*.ncu-rep > gpurun_out/${T}_ncu_traffic.json
+# keep the headline capture (with source) and the NTT segment capture; the rest
+# live on as summaries + traffic (gpurun copies back at most 64 MiB)
+for f in gpurun_out/${T}_*.ncu-rep; do case $f in *gemm_cfg2*|*ntt_segment_cfg4*) ;; *) rm -f "$f";; esac; done
+ls -la gpurun_out/
 python - gpurun_out/bench_default_$T.json <<'PY'
 import json, sys
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); r = d["roofline"]
