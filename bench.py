@@ -99,10 +99,18 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
+    # nvidia-smi's start-up (NVML initialisation) can stall this process's CUDA
+    # calls for tens of ms -- measured as a single 36 ms step inside config 4's
+    # timed region (tools/oneshot_jitter.py --smi 1), the "one-shot swing" of
+    # round 1.  So the sampler is started before the warm-up, has delivered its
+    # first sample before the timed region begins, and the summary keeps the
+    # samples taken between mark_start() and mark_end().
+
     def __init__(self, gpu_index: int):
         self.idx, self.rows, self.proc = gpu_index, [], None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
@@ -110,34 +118,52 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.monotonic() + 5.0
+            while not self.rows and time.monotonic() < deadline:
+                time.sleep(0.02)
+            time.sleep(0.2)  # past nvidia-smi's start-up
         except Exception:
             self.proc = None
         return self
+
+    def mark_start(self):
+        self.t0 = time.monotonic()
+
+    def mark_end(self):
+        self.t1 = time.monotonic()
+        if self.proc:  # one more sample period after a short timed region
+            time.sleep(0.25)
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.monotonic(), parts))
 
-    def __exit__(self, *exc):
+    def stop(self):
         if self.proc:
-            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(2)
             except Exception:
                 self.proc.kill()
+            self.proc = None
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        if self.t0 is not None and self.t1 is not None:
+            inside = [r for r in rows if self.t0 <= r[0] <= self.t1]
+            # short regions hold no sample: the nearest ones within 0.3 s
+            rows = inside or [r for r in rows if self.t0 - 0.3 <= r[0] <= self.t1 + 0.3]
+        rows = [r[1] for r in rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 def algorithmic_work(q, path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False,
@@ -366,6 +392,7 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
         else:
             q.toeplitz_extract(raw, B, w.n, w.m, seed, out=out, stream=stream)
 
+    clk = ClockSampler(ctx.local).start()  # before the warm-up (see ClockSampler)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -403,8 +430,10 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
         return sum(per), per, nl, km, kn
 
     # timed region
-    with ClockSampler(ctx.local) as clk:
-        ms_total, per_step, launches, _, _ = timed_pass(False)
+    clk.mark_start()
+    ms_total, per_step, launches, _, _ = timed_pass(False)
+    clk.mark_end()
+    clk.stop()
     out_np = out.cpu().numpy()  # the keys of the last timed step (checked below)
     # the same K steps again with the main kernel(s) timed live (roofline)
     ms_total_kt, _, _, kern_ms, kern_n = timed_pass(True)

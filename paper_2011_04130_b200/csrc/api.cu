@@ -314,8 +314,19 @@ static qrng_status resolve_path(uint64_t n, uint64_t m, int *path, bool *kara_on
     return QRNG_OK;
 }
 
+static qrng_status plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
+                               qrng_plan **plan, bool oneshot);
+
 qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
                              qrng_plan **plan) {
+    return plan_create(n, m, d_seed, stream, plan, false);
+}
+
+// oneshot: the plan is extracted exactly once, on `stream`, by the caller
+// (qrng_toeplitz_extract_async): work that can ride on the extraction's own
+// launches (the Karatsuba leaf seeds) is deferred to them.
+static qrng_status plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t stream,
+                               qrng_plan **plan, bool oneshot) {
     if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
     *plan = nullptr;
     qrng_status st = check_nm(n, m);
@@ -335,7 +346,7 @@ qrng_status qrng_plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cuda
     p->four_step = want == QRNG_PATH_NTT && n + m - 1 > (1ull << ntt::kMaxLogP);
     st = p->four_step            ? ntt::dist_plan_init(p->dist, n, m, d_seed, 1, 0, stream)
          : (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
-         : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream)
+         : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream, oneshot)
                                  : gemm::plan_init(p->gemm, n, m, d_seed, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
     *plan = p;
@@ -484,7 +495,7 @@ qrng_status qrng_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_bl
         return qrng_plan_extract(&direct, d_raw_bits, n_blocks, d_out, stream);
     }
     qrng_plan *p = nullptr;
-    if ((st = qrng_plan_create(n, m, d_seed, stream, &p)) != QRNG_OK) return st;
+    if ((st = plan_create(n, m, d_seed, stream, &p, true)) != QRNG_OK) return st;
     st = qrng_plan_extract(p, d_raw_bits, n_blocks, d_out, stream);
     plan_release(p, stream, true);
     return st;

@@ -105,6 +105,7 @@ struct Args {
     uint32_t k128;             // 128-bit raw chunks per block = n / 128
     uint32_t nchunks;          // B chunks per tile = ceil(kst / SPC)
     uint32_t n_mtiles, n_npairs;  // M tiles; pairs of N tiles (NT = 2 per work tile)
+    uint32_t prows;            // plain mode: output rows per N pair (448, fewer for small batches)
     const uint32_t *seed_words;  // logical big-endian seed words, zero padded
     uint32_t seed_words_n;
     const uint8_t *seed_bytes;   // plain mode, one-shot calls: the caller's MSB-first seed (seed_words unused)
@@ -164,7 +165,7 @@ __device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s,
     Tile ti;
     if (!GROUPED) {
         ti.mt = t % a.n_mtiles;
-        ti.n0 = (t / a.n_mtiles) * (NT * BN);
+        ti.n0 = (t / a.n_mtiles) * a.prows;
         ti.kst = a.kst;
         ti.k128 = a.k128;
         ti.nchunks = a.nchunks;
@@ -173,6 +174,8 @@ __device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s,
         ti.xb = a.raw;
         ti.xs = a.n >> 5;
         ti.out_off = 0;
+        tile_rows(ti, a.prows);
+        return ti;
     } else {
         const TLeaf *lv = reinterpret_cast<const TLeaf *>(seed_s);  // shared-memory leaf table
         while (cur + 1 < a.n_leaves && t >= lv[cur].tile_end) ++cur;
@@ -647,6 +650,10 @@ bool supported(uint64_t n, uint64_t m) { return n % 128 == 0 && n <= MAX_N && m 
 uint32_t seed_words_needed(uint64_t n, uint64_t m) {
     const uint64_t n_npairs = (m + NT * BN - 1) / (NT * BN), kst = (n + KS - 1) / KS, nchunks = (kst + SPC - 1) / SPC;
     uint64_t pmax = (n_npairs - 1) * NT * BN + (nchunks - 1) * KC + 8 * (CM_PER_CHUNK - 1) + 7;
+    // plain launches with narrower N pairs (small batches, plain_prows) reach at
+    // most row m - 1 + 448 of the last chunk
+    const uint64_t pmax_narrow = (m - 1) + nchunks * KC + NT * BN + 7;
+    if (pmax_narrow > pmax) pmax = pmax_narrow;
     return (uint32_t)(pmax / 32 + 2);
 }
 
@@ -774,6 +781,22 @@ static qrng_status launch(const Args &a, cudaStream_t s) {
     return QRNG_OK;
 }
 
+// Rows per N pair of a plain launch: 448 (two full N tiles) unless the batch
+// has too few M tiles to fill the GPU -- then narrower pairs (multiples of 32)
+// give ~one work tile per SM (a small batch is latency-bound: more, shorter
+// tiles in parallel).
+static uint32_t plain_prows(uint32_t n_mtiles, uint64_t m) {
+    static const bool narrow = [] {  // QRNG_GEMM_NARROW=0: always 448 (A/B)
+        const char *e = getenv("QRNG_GEMM_NARROW");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (!narrow) return NT * BN;
+    const uint32_t want_pairs = 148u / std::max(1u, n_mtiles);
+    if (want_pairs <= (m + NT * BN - 1) / (NT * BN)) return NT * BN;
+    const uint64_t rows = (m + want_pairs - 1) / want_pairs;
+    return (uint32_t)std::min<uint64_t>(NT * BN, std::max<uint64_t>(32, (rows + 31) / 32 * 32));
+}
+
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s) {
     Args a{};
@@ -785,7 +808,8 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
     a.k128 = (uint32_t)(n / 128);
     a.nchunks = (a.kst + SPC - 1) / SPC;
     a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
-    a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
+    a.prows = plain_prows(a.n_mtiles, m);
+    a.n_npairs = (uint32_t)((m + a.prows - 1) / a.prows);  // work tile t = (N pair t / n_mtiles, M tile t % n_mtiles)
     a.seed_words = pl.seed_words;
     a.seed_words_n = (uint32_t)pl.seed_words_n;
     a.out = out;
@@ -810,7 +834,8 @@ qrng_status extract_direct(const uint8_t *d_seed, const uint8_t *d_raw, uint64_t
     a.k128 = (uint32_t)(n / 128);
     a.nchunks = (a.kst + SPC - 1) / SPC;
     a.n_mtiles = (uint32_t)((n_blocks + BM - 1) / BM);
-    a.n_npairs = (uint32_t)((m + NT * BN - 1) / (NT * BN));
+    a.prows = plain_prows(a.n_mtiles, m);
+    a.n_npairs = (uint32_t)((m + a.prows - 1) / a.prows);
     a.seed_words = nullptr;
     a.seed_words_n = seed_words_needed(n, m);
     a.seed_bytes = d_seed;

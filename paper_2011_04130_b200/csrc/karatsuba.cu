@@ -551,11 +551,10 @@ __device__ __forceinline__ uint32_t seed_window32(const uint8_t *seed, uint64_t 
 
 // Leaf seeds: word q of leaf l = XOR over its terms t of seed bits [t + 32q, t + 32q + 32)
 // (zero past n+m-1), zero at and past the leaf seed length r + w - 1.
-__global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms, const uint8_t *seed, uint64_t L,
-                                 uint32_t *seeds) {
-    const gemm::Leaf Lf = leaves[blockIdx.y];
+__device__ __forceinline__ void leaf_seed_words(const gemm::Leaf &Lf, const uint32_t *terms, const uint8_t *seed,
+                                                uint64_t L, uint32_t *seeds, uint32_t q0, uint32_t stride) {
     const uint32_t len = Lf.r + Lf.w - 1;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < Lf.seed_n; q += gridDim.x * blockDim.x) {
+    for (uint32_t q = q0; q < Lf.seed_n; q += stride) {
         uint32_t v = 0;
 #pragma unroll 8
         for (uint32_t k = 0; k < Lf.sterm_n; ++k) v ^= seed_window32(seed, L, __ldg(terms + Lf.sterm_base + k) + 32ull * q);
@@ -564,6 +563,24 @@ __global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms
         seeds[Lf.seed_off + q] = v;
     }
 }
+
+__global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms, const uint8_t *seed, uint64_t L,
+                                 uint32_t *seeds) {
+    leaf_seed_words(leaves[blockIdx.y], terms, seed, L, seeds, blockIdx.x * blockDim.x + threadIdx.x,
+                    gridDim.x * blockDim.x);
+}
+
+// One-shot calls: the leaf seeds of a fresh plan are formed by extra CTAs of
+// the Q-buffer launch (the two are independent), so plan preparation costs no
+// launch of its own; the grouped GEMM's programmatic wait covers both.
+struct SeedJob {
+    const gemm::Leaf *leaves;
+    const uint32_t *terms;
+    const uint8_t *seed;       // null: no seed work in this launch
+    uint64_t L;
+    uint32_t *seeds;
+    uint32_t n_leaves, q_ctas;  // CTAs [q_ctas, gridDim.x) do seed work
+};
 
 // All Q buffers of a few blocks, generation by generation (one launch):
 // X[b][dst] = S[b][x0] ^ S[b][x0 + h/32] per 16-byte unit (x0 ^ x1 of a
@@ -574,8 +591,13 @@ __global__ void leaf_seed_kernel(const gemm::Leaf *leaves, const uint32_t *terms
 template <int U>
 __global__ void __launch_bounds__(512) qbuf_kernel(const uint4 *units, const uint32_t *gen_start, uint32_t n_gen,
                                                    const uint4 *raw, uint64_t n_blocks, uint32_t n, uint4 *xws,
-                                                   uint32_t x_stride, uint32_t bpc) {
+                                                   uint32_t x_stride, uint32_t bpc, SeedJob sj) {
     pdl_release();  // the grouped GEMM may be scheduled as CTAs finish
+    if (blockIdx.x >= sj.q_ctas) {  // leaf-seed CTAs (one-shot calls)
+        for (uint32_t l = blockIdx.x - sj.q_ctas; l < sj.n_leaves; l += gridDim.x - sj.q_ctas)
+            leaf_seed_words(sj.leaves[l], sj.terms, sj.seed, sj.L, sj.seeds, threadIdx.x, blockDim.x);
+        return;
+    }
     const uint64_t b0 = (uint64_t)blockIdx.x * bpc;
     const uint32_t nb = (uint32_t)min((uint64_t)bpc, n_blocks - b0);
     const uint32_t xs4 = x_stride / 4, rs4 = n / 128;
@@ -1091,13 +1113,22 @@ __global__ void __launch_bounds__(256) csr_gather_pack_kernel(const uint32_t *__
 }
 
 // ---- host entry points -----------------------------------------------------
-qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s) {
+// two block-range chunks on two streams per extraction (measured slower; see extract())
+constexpr bool kTwoChunks = false;
+
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s,
+                      bool defer_seeds) {
     std::shared_ptr<const Tables> t;
     qrng_status st = get_tables(n, m, max_depth, &t);
     if (st != QRNG_OK) return st;
     pl.tab = t;
     const HostTables &H = t->host;
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.seeds, (size_t)H.seed_total * 4, s));
+    if (defer_seeds && !H.qbufs.empty() && !kTwoChunks) {  // formed inside the first extraction's Q-buffer launch
+        pl.pending_seed = d_seed;
+        pl.seed_L = n + m - 1;
+        return QRNG_OK;
+    }
     uint32_t maxw = 0;
     for (const auto &g : t->hleaves) maxw = std::max(maxw, g.seed_n);
     count_launch();
@@ -1122,7 +1153,6 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
 // Measured +1.6% at config 2 (324.7 vs 319.7 Gbit/s), but the overlapping GEMM
 // launches blur the per-kernel roofline timing and the host-buffer pipeline
 // (two compute streams of its own) then shares one side stream, so it is off.
-constexpr bool kTwoChunks = false;
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s) {
     if (!kTwoChunks || n_blocks < 2048) return extract_chunk(pl, d_raw, n_blocks, n, m, out, s);
@@ -1172,9 +1202,21 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
 #endif
         const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / QRNG_QBUF_DIV));
         KernelTimer tq(s, true, 1);
-        qbuf_kernel<QRNG_QBUF_U><<<(unsigned)((n_blocks + bpc - 1) / bpc), 512, 0, s>>>(
+        SeedJob sj{};
+        sj.q_ctas = (uint32_t)((n_blocks + bpc - 1) / bpc);
+        uint32_t seed_ctas = 0;
+        if (pl.pending_seed) {
+            sj.leaves = t->leaves;
+            sj.terms = t->terms;
+            sj.seed = pl.pending_seed;
+            sj.L = pl.seed_L;
+            sj.seeds = pl.seeds;
+            sj.n_leaves = (uint32_t)t->hleaves.size();
+            seed_ctas = std::min<uint32_t>(sj.n_leaves, 64);
+        }
+        qbuf_kernel<QRNG_QBUF_U><<<sj.q_ctas + seed_ctas, 512, 0, s>>>(
             t->qbufs, t->qgen_dev, (uint32_t)t->qgen.size() - 1, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
-            (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc);
+            (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc, sj);
         tq.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("qbuf_kernel launch failed"); st = QRNG_E_CUDA; }
     }

@@ -210,11 +210,16 @@ struct Tables;  // device-resident leaf / term / combine tables, cached per (n, 
 struct Plan {
     std::shared_ptr<const Tables> tab;  // shared with the LRU table cache
     uint32_t *seeds = nullptr;  // leaf seeds (logical big-endian words)
+    const uint8_t *pending_seed = nullptr;  // one-shot plans: seeds formed by the first Q-buffer launch
+    uint64_t seed_L = 0;
 };
 // Chooses the decomposition for (n, m); returns false if no leaf split pays off
 // (the plain GEMM kernel is then used).  max_depth < 0: cost model decides.
 bool choose(uint64_t n, uint64_t m, int max_depth);
-qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s);
+// defer_seeds (one-shot calls only: the plan is extracted once, on `s`): the
+// leaf seeds are formed by extra CTAs of the first extraction's Q-buffer launch
+qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, int max_depth, const uint8_t *d_seed, cudaStream_t s,
+                      bool defer_seeds = false);
 void plan_free(Plan &pl);
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s);

@@ -2,7 +2,7 @@ import csv, subprocess, sys
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
-h = r[0]; v = r[2] if len(r) > 2 else r[1]
+h = r[0]; units = r[1]; v = r[2] if len(r) > 2 else r[1]
 want = sys.argv[2:] or ['gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum',
  'sm__throughput.avg.pct_of_peak_sustained_elapsed','sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
  'sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active',
@@ -13,4 +13,4 @@ want = sys.argv[2:] or ['gpu__time_duration.sum','dram__bytes_read.sum','dram__b
 for w in want:
     for i, k in enumerate(h):
         if k == w:
-            print(f"{w:70s} {v[i]}")
+            print(f"{w:70s} {v[i]} {units[i]}")

@@ -20,8 +20,14 @@ for rep in reps:
     path = "gemm" if kind == "gemm" else "ntt"
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(txt.splitlines()))
-    h, v = r[0], r[2] if len(r) > 2 else r[1]
-    val = lambda k: float(v[h.index(k)].replace(",", "")) if k in h else None
+    h, u, v = r[0], r[1], r[2]  # names, units, values
+    SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}
+
+    def val(k):
+        if k not in h:
+            return None
+        i = h.index(k)
+        return float(v[i].replace(",", "")) * SCALE.get(u[i], 1)
     rd, wr, t = val("dram__bytes_read.sum"), val("dram__bytes_write.sum"), val("gpu__time_duration.sum")
     key = f"{wl}/{path}" if kind != "ntt_pass" else f"{wl}/ntt_pass"
     out[key] = {"bytes_per_launch": (rd or 0) + (wr or 0), "dram_read": rd, "dram_write": wr,
