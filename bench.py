@@ -300,6 +300,16 @@ def launch_ranks(args) -> int:
     return subprocess.call(cmd, env=env)
 
 
+def head_start(stream, cycles: int = 4_000_000):
+    """A ~2 ms device spin before the first timed step (outside every event):
+    the host enqueues the timed steps while it runs, so a host-side stall at
+    the start of the region (nvidia-smi's NVML queries take a driver lock,
+    measured at 10 ms) is not counted as device time of step 0."""
+    import torch
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(cycles)
+
+
 # ---------------------------------------------------------------------------
 # one workload
 # ---------------------------------------------------------------------------
@@ -415,6 +425,7 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
         q.kernel_time_ms()  # clear
         ctx.barrier()
         torch.cuda.synchronize()
+        head_start(stream)
         l0 = q.launch_count()
         for i in range(args.steps):
             flush.zero_()  # L2 flush, outside the events
@@ -449,6 +460,7 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
         ss1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ctx.barrier()
         torch.cuda.synchronize()
+        head_start(stream)
         for i in range(args.steps):
             flush.zero_()
             ss0[i].record(stream)
@@ -758,6 +770,7 @@ def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int
     q.kernel_time_split()
     ctx.barrier()
     torch.cuda.synchronize()
+    head_start(stream)
     l0 = q.launch_count()
     t_wall0 = time.perf_counter()
     for i in range(args.steps):
