@@ -335,11 +335,13 @@ QRNG_API void        qrng_debug_kernel_timing(int enable);
  * the library was built with -DQRNG_GEMM_TRACE.  reset != 0 clears them. */
 QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters32, int reset);
 /* PROFILING ONLY: back-to-back int8 MMAs on fixed operands, one CTA per SM
- * (form 0: cta_group::1 A in TMEM; 1: cta_group::1 A in SMEM; 2: cta_group::2
- * pair, A in SMEM, needs a -DQRNG_GEMM_2CTA build; 3: the GEMM kernel's stage
- * shape, 4 K steps x two N tiles per elected issue + one commit, N0 = n & 511,
- * N1 = n >> 9 or N0 if 0), N = n; *macs = work done.  form + 16k (forms 0-2):
- * a commit every k MMAs.
+ * (form 0: int8 cta_group::1 A in TMEM; 1: int8 cta_group::1 A in SMEM;
+ * 3: int8 stage shape, 4 K32 steps x two N tiles per elected issue + one
+ * commit; 4: kind::mxf4 M128 N=n K64 back to back; 5: the E2M1 kernel's stage
+ * shape, 2 K64 steps x two N tiles (N0 = n & 511 <= 224, N1 = n >> 9 or N0 if
+ * 0, <= 224) per elected issue + one commit; form 2 (cta_group::2) was removed
+ * with the 2-SM kernel and returns E_UNSUPPORTED); *macs = work done.
+ * form + 16k (forms 0-1): a commit every k MMAs.
  * Time with CUDA events on `stream`. */
 QRNG_API qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);

@@ -235,7 +235,8 @@ qrng_status qrng_debug_mxf4_probe(const uint8_t *d_A, const uint8_t *d_h, float 
 }
 qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream) {
     const int n0 = n & 511, n1 = n >> 9;  // form 3: two N tiles (n1 = 0: same as n0)
-    if (!macs || iters <= 0 || n0 < 16 || n0 > 256 || n0 % 16 || n1 > 192 || n1 % 16 || ((form % 16) != 3 && (form % 16) != 5 && n1)) {
+    if (!macs || iters <= 0 || n0 < 16 || n0 > 256 || n0 % 16 || n1 > 224 || n1 % 16 ||
+        ((form % 16) != 3 && (form % 16) != 5 && n1) || ((form % 16) == 5 && n0 > 224)) {
         set_error("bad arguments");
         return QRNG_E_INVALID;
     }

@@ -84,7 +84,7 @@ __global__ void __cluster_dims__(FORM == 2 ? 2 : 1, 1, 1) __launch_bounds__(128,
                             const uint64_t ad = desc_kmajor(cb + 32768 + (it & 3) * 2048 + kk * 256, 128, 512);
                             mma_mxf4_ss(tmem, ad, desc_kmajor(cb + ((it & 3) * 16 + kk * 8) * 128, 512, 128), id0,
                                         tmem + 448, tmem + 456, 1);
-                            mma_mxf4_ss(tmem + 192, ad, desc_kmajor(cb + ((it & 3) * 16 + kk * 8 + 24) * 128, 512, 128),
+                            mma_mxf4_ss(tmem + 224, ad, desc_kmajor(cb + ((it & 3) * 16 + kk * 8 + n0 / 8) * 128, 512, 128),
                                         id1, tmem + 448, tmem + 456, 1);
                         }
                         mma_commit(&bar + 1);

@@ -190,8 +190,11 @@ __host__ __device__ constexpr int prefix_of(int logP, int lv) {
     for (int i = 0; i < lv; ++i) s += radix_of(logP, i);
     return s;
 }
+#ifndef QRNG_NTT_MAXT
+#define QRNG_NTT_MAXT 1024  // threads per transform CTA (each thread takes P / 32 / T sub-DFTs per level)
+#endif
 __host__ __device__ constexpr int threads_of(int logP) {
-    return (1 << logP) / 32 < 32 ? 32 : ((1 << logP) / 32 > 1024 ? 1024 : (1 << logP) / 32);
+    return (1 << logP) / 32 < 32 ? 32 : ((1 << logP) / 32 > QRNG_NTT_MAXT ? QRNG_NTT_MAXT : (1 << logP) / 32);
 }
 __host__ __device__ constexpr int pidx(int i) { return i + (i >> 5); }
 
@@ -363,7 +366,10 @@ struct Level {
 
     __device__ static __forceinline__ void fwd(uint32_t *data, uint32_t *stage, const FusedArgs &a,
                                                uint64_t b0, int nb, uint64_t wfirst) {
-        for (int u = threadIdx.x; u < NSUB; u += T) {
+#pragma unroll
+        for (int it = 0; it < (NSUB + T - 1) / T; ++it) {  // independent sub-DFTs: unrolled so they interleave
+            const int u = (int)threadIdx.x + it * T;
+            if (NSUB % T != 0 && u >= NSUB) break;
             uint32_t x[N1];
             load(x, u, data, a, b0, nb);
             dft_fwd<R, F>(x);
@@ -404,7 +410,10 @@ struct Level {
 
     __device__ static __forceinline__ void inv(uint32_t *data, uint32_t *stage, const FusedArgs &a,
                                                uint64_t b0, int nb, uint64_t wfirst) {
-        for (int u = threadIdx.x; u < NSUB; u += T) {
+#pragma unroll
+        for (int it = 0; it < (NSUB + T - 1) / T; ++it) {  // independent sub-DFTs: unrolled so they interleave
+            const int u = (int)threadIdx.x + it * T;
+            if (NSUB % T != 0 && u >= NSUB) break;
             uint32_t x[N1];
 #pragma unroll
             { const int pb = pbase(u);
