@@ -15,6 +15,11 @@ namespace qrng {
 namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+#ifndef QRNG_HIST_COPIES
+#define QRNG_HIST_COPIES 1  // sub-histograms per warp (lane % copies picks one): fewer same-bin atomic collisions
+#endif
+constexpr int kCopies = QRNG_HIST_COPIES;
+constexpr int kSub = kWarps * kCopies;
 
 __device__ __forceinline__ void add4(uint32_t *h, uint32_t w) {
     atomicAdd(&h[w & 0xFF], 1u);
@@ -25,10 +30,10 @@ __device__ __forceinline__ void add4(uint32_t *h, uint32_t w) {
 
 __global__ void __launch_bounds__(kThreads) hist256_kernel(const uint8_t *__restrict__ x, uint64_t n,
                                                            unsigned long long *__restrict__ counts) {
-    __shared__ uint32_t h[kWarps][256];
-    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&h[0][0])[i] = 0;
+    extern __shared__ uint32_t hs[];  // [kSub][256]
+    for (int i = threadIdx.x; i < kSub * 256; i += kThreads) hs[i] = 0;
     __syncthreads();
-    uint32_t *mine = h[threadIdx.x >> 5];
+    uint32_t *mine = hs + ((threadIdx.x >> 5) * kCopies + (threadIdx.x & (kCopies - 1))) * 256;
     const uint64_t tid = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
     const uint64_t nthr = (uint64_t)gridDim.x * kThreads;
     // any alignment: the bytes before the first 16-byte boundary are counted
@@ -51,7 +56,7 @@ __global__ void __launch_bounds__(kThreads) hist256_kernel(const uint8_t *__rest
     __syncthreads();
     for (int b = threadIdx.x; b < 256; b += kThreads) {
         uint32_t s = 0;
-        for (int w = 0; w < kWarps; ++w) s += h[w][b];
+        for (int w = 0; w < kSub; ++w) s += hs[w * 256 + b];
         if (s) atomicAdd(counts + b, (unsigned long long)s);
     }
 }
@@ -69,7 +74,12 @@ qrng_status hist256_launch(const uint8_t *d_samples, uint64_t n, unsigned long l
     if (grid < min_grid) grid = min_grid;
     if (grid == 0) grid = 1;
     count_launch();
-    hist256_kernel<<<(unsigned)grid, kThreads, 0, s>>>(d_samples, n, d_counts);
+    const size_t smem = (size_t)kSub * 256 * 4;
+    if (smem > 48 * 1024) {
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(hist256_kernel));
+        if (st != QRNG_OK) return st;
+    }
+    hist256_kernel<<<(unsigned)grid, kThreads, smem, s>>>(d_samples, n, d_counts);
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
 }
