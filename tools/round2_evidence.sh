@@ -9,7 +9,9 @@ mkdir -p gpurun_out
 python -m paper_2011_04130_b200.build > /dev/null || exit 1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$T.txt 2>&1; tail -1 gpurun_out/pytest_gpu_$T.txt
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 1200 python bench.py > gpurun_out/bench_default_$T.json 2> gpurun_out/bench_default_$T.err
+S0=$SECONDS; timeout 1200 python bench.py > gpurun_out/bench_default_$T.json 2> gpurun_out/bench_default_$T.err
+echo "default bench wall $((SECONDS - S0)) s" | tee gpurun_out/bench_default_${T}_wall.txt
+timeout 900 python bench.py --gpus 2 --configs cfg4a,cfg5_n2^16,next4_n2^24 --no-e2e > gpurun_out/bench_g2gloo_$T.json 2> gpurun_out/bench_g2gloo_$T.err
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/${T}_launches_bench_cfg2.csv python bench.py --steps 3 --warmup 3 --configs none \
     --no-e2e --no-cpu-baseline --no-parity > /dev/null 2>&1
