@@ -533,6 +533,8 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
         res["config"]["minentropy"] = entropy_info
     if ctx.rank == 0 and ctx.world == 1 and cpu_budget > 0:
         res["cpu_baseline"] = cpu_baseline(w, budget_s=cpu_budget, modified=modified)
+        if headline and not modified:
+            res["cpu_baseline"]["paper_method"] = paper_method_baseline(w, budget_s=min(5.0, cpu_budget))
     del raw, out, flush
     torch.cuda.empty_cache()
     return res
@@ -694,6 +696,26 @@ def cpu_baseline(w: S.Workload, budget_s: float = 15.0, threads: int = 0, modifi
                       f"{w.n_blocks}) of {w.name}, {t_total:.1f} s, "
                       + ("modified Toeplitz literal loop" if modified else "word-parallel mode")
                       + ", OpenMP over blocks"}
+
+
+def paper_method_baseline(w: S.Workload, budget_s: float = 5.0):
+    """Context row: the paper's own method (double-precision FFT, round, mod 2;
+    Listing 2) in numpy on the host (oracle/paper_fft.py,
+    checked against the oracle by tests/test_oracle_paper_fft.py), on a
+    bounded sample of the workload -- like for like with the paper's Matlab
+    figure (about 0.05 Gbit/s)."""
+    from oracle import paper_fft
+    nb = max(1, min(w.n_blocks, 64))
+    raw, seed = S.workload_inputs(w, 0, nb)
+    done, t = 0, 0.0
+    while t < budget_s:
+        t0 = time.perf_counter()
+        paper_fft.extract(raw, nb, w.n, w.m, seed)
+        t += time.perf_counter() - t0
+        done += nb
+    return {"value": done * w.n / t / 1e9, "unit": "Gbit/s", "kind": "paper float-FFT method (numpy rfft, "
+            "Listing 2 with the prose window)", "threads": "numpy FFT (one core)",
+            "sample": f"{done} blocks of {w.name} in {t:.1f} s"}
 
 
 def cpu_baseline_rows(w: S.Workload, budget_s: float, cores: int):
