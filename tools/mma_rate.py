@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """tcgen05 int8 MMA issue-rate microbenchmark (qrng_debug_mma_rate): TOPS per form and N.
-Forms: 0 = 1-SM A in TMEM, 1 = 1-SM A in SMEM, 2 = 2-SM pair A in SMEM (needs a -DQRNG_GEMM_2CTA build)."""
+Forms (int8): 0 = A in TMEM, 1 = A in SMEM; see include/qrng.h qrng_debug_mma_rate (form 2, the 2-SM pair,
+was removed with the 2-SM kernel; tools/mma_shapes.py covers the E2M1 forms 4 and 5)."""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
