@@ -765,7 +765,12 @@ def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     gloo = ctx.backend == "gloo"
 
+    out1 = torch.empty(q.out_bytes(blocks, m), dtype=torch.uint8, device="cuda")
+
     def step():
+        if W == 1:  # one GPU: the single-GPU API (multi-pass NTT mod 7*2^26+1 for L > 2^23)
+            q.toeplitz_extract(raw, blocks, n, m, seed, out=out1, stream=stream)
+            return
         keys.zero_()
         for b in range(blocks):
             plan.local(raw[b * n // 8:(b + 1) * n // 8], send, stream=stream)
@@ -810,7 +815,11 @@ def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int
     ms_max, = ctx.allreduce([ms], "max")
     bits = float(blocks) * n * args.steps
     value = bits / (ms_max * 1e-3) / 1e9
-    key_np = keys[-1, :kbytes].cpu().numpy()
+    if W == 1:  # the last block's key from the batched output stream
+        allbits = np.unpackbits(out1.cpu().numpy())[(blocks - 1) * m:blocks * m]
+        key_np = np.packbits(allbits)
+    else:
+        key_np = keys[-1, :kbytes].cpu().numpy()
     parity = None
     if not args.no_parity:
         import oracle
@@ -826,7 +835,7 @@ def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int
                   "checked_bits": int(rows.size) * W, "mismatches": int(bad),
                   "what": f"{rows.size} sampled key bits of the last block on every rank, vs oracle_extract_rows"}
     # ALU roofline: every rank runs one local length-N2 convolution transform per block
-    N2 = plan.exchange_words
+    N2 = plan.exchange_words  # W = 1: the full transform length P
     bfly = blocks * (N2 * math.log2(N2) + N2)
     per_step_s = (km / args.steps * 1e-3) if kn else ms_max / args.steps * 1e-3
     peak = q.butterfly_rate() / 1e9
@@ -841,12 +850,14 @@ def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int
            "config": {"workload": f"next4_n2^{n.bit_length() - 1}", "n": n, "m": m, "blocks_per_step": blocks,
                       "log2_transform": int(math.log2(N2 * W)), "world": W,
                       "scaling": "strong (each block's transform split across the ranks)",
-                      "step": "per block: qrng_dist_local -> all_to_all_single (N2 words per rank) -> "
-                              "qrng_dist_finish; then one OR all-reduce of the keys",
+                      "step": ("one-shot qrng_toeplitz_extract_async on the batch (multi-pass NTT mod 7*2^26+1)"
+                               if W == 1 else
+                               "per block: qrng_dist_local -> all_to_all_single (N2 words per rank) -> "
+                               "qrng_dist_finish; then one OR all-reduce of the keys"),
                       "backend": ctx.backend or "single GPU"}}
     if ctx.rank == 0 and ctx.world == 1 and cpu_budget > 0:
         res["cpu_baseline"] = cpu_baseline_rows(S.Workload("next4", 24, n, m, blocks, 20.0), cpu_budget, host_cores())
-    del raw, keys, flush, send, recv
+    del raw, keys, flush, send, recv, out1
     torch.cuda.empty_cache()
     return res
 

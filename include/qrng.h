@@ -116,8 +116,8 @@ QRNG_API qrng_status qrng_entropy_from_counts(const uint64_t *h_counts, uint32_t
  *         E_UNSUPPORTED if n % 32 != 0 or L > 2^26;  E_CUDA / E_NOMEM on device failures.
  *         L <= 2^23 runs the tensor-core path or the NTT modulo p = 119*2^23 + 1;
  *         2^23 < L <= 2^26 (n around 2^24..2^25, past the 2-adic limit of that
- *         prime) runs the four-step NTT of qrng_dist_* below with world = 1,
- *         block by block, modulo p = 7*2^26 + 1.
+ *         prime) runs the same multi-pass NTT modulo p = 7*2^26 + 1 (the prime
+ *         of qrng_dist_* below).
  * The one-shot calls build a temporary plan (seed preparation included) and
  * release it stream-ordered; _async returns once the work is enqueued.
  */

@@ -179,8 +179,6 @@ struct qrng_plan {
     bool kara_on = false;  // GEMM path through the Karatsuba decomposition
     bool modified = false;  // modified Toeplitz [T | I_m] (n-bit seed)
     const uint8_t *direct_seed = nullptr;  // one-shot dense GEMM: the caller's seed, read by the kernel itself
-    bool four_step = false;  // NTT path with L > 2^23: the four-step NTT (world 1), block by block
-    ntt::DistPlan dist;
     ntt::Plan ntt;
     gemm::Plan gemm;
     kara::Plan kara;
@@ -196,7 +194,6 @@ static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
     fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.work);
     fr(p->gemm.seed_words);
     fr(p->kara.seeds);
-    ntt::dist_plan_free(p->dist, s, async);
     delete p;
 }
 
@@ -344,9 +341,7 @@ static qrng_status plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cu
     p->kara_on = kara_on;
     p->path = want;
     const int kd = g_kara_depth.load();
-    p->four_step = want == QRNG_PATH_NTT && n + m - 1 > (1ull << ntt::kMaxLogP);
-    st = p->four_step            ? ntt::dist_plan_init(p->dist, n, m, d_seed, 1, 0, stream)
-         : (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
+    st = (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
          : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream, oneshot)
                                  : gemm::plan_init(p->gemm, n, m, d_seed, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
@@ -411,21 +406,6 @@ qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_bits, uint
 
 void qrng_plan_destroy(qrng_plan *plan) { plan_release(plan, 0, false); }
 
-// L > 2^23 on one GPU: the world-1 four-step NTT block by block (each block's
-// local transform fills the GPU: P up to 2^26 words).
-static qrng_status four_step_extract(const ntt::DistPlan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
-                                     uint64_t m, const OutStream &o, cudaStream_t stream) {
-    uint32_t *ws = nullptr;
-    QRNG_CUDA_TRY(cudaMallocAsync(&ws, (size_t)pl.N2 * 4, stream));
-    qrng_status st = QRNG_OK;
-    for (uint64_t b = 0; b < n_blocks && st == QRNG_OK; ++b) {
-        st = ntt::dist_local(pl, d_raw + b * (n / 8), ws, stream);
-        if (st == QRNG_OK) st = ntt::dist_finish(pl, ws, o, b * m, stream);
-    }
-    cudaFreeAsync(ws, stream);
-    return st;
-}
-
 qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, uint64_t n_blocks,
                               uint8_t *d_out, cudaStream_t stream) {
     if (!plan) { set_error("plan is NULL"); return QRNG_E_INVALID; }
@@ -453,8 +433,7 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
     // the Karatsuba pack kernel writes every output word once; the other
     // epilogues OR the words they share with a neighbouring tile / CTA
     if (!(plan->path == QRNG_PATH_GEMM && plan->kara_on)) QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
-    qrng_status st = plan->four_step ? four_step_extract(plan->dist, d_raw_bits, n_blocks, n, m, o, stream)
-                     : (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
+    qrng_status st = (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->kara_on ? kara::extract(plan->kara, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->modified ? gemm::extract_modified(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->direct_seed ? gemm::extract_direct(plan->direct_seed, d_raw_bits, n_blocks, n, m, o, stream)

@@ -730,7 +730,6 @@ static qrng_status launch_seed(const uint32_t *seed_words, uint32_t L, const uin
 
 #define QRNG_LOGP_CASES(X) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)
 
-static uint64_t powmod_h(uint64_t b, uint64_t e) { return powmod_c(b, e); }
 
 // ---- butterfly-rate microbenchmark (the NTT roofline denominator) ----------
 // Register-resident radix-32 forward DIF + inverse DIT with the exact butterfly
@@ -841,6 +840,10 @@ static uint64_t batch_blocks(int logP, uint64_t n_blocks) {
     return cap < n_blocks ? cap : n_blocks;
 }
 
+template <int F>
+static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
+                                  int logP, uint32_t scaleM, cudaStream_t s);
+
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t seed_bit_offset,
                       bool xor_tail, cudaStream_t s) {
     // n here is the number of raw bits per block that enter the product
@@ -851,10 +854,14 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
     int logP = 0;
     while ((1ull << logP) < L) ++logP;
     if (logP < 5) logP = 5;
-    if (logP > kMaxLogP) {
-        set_error("NTT path: L = %llu exceeds 2^23", (unsigned long long)L);
+    // P <= 2^23: p = 119 * 2^23 + 1; 2^23 < P <= 2^26: p = 7 * 2^26 + 1 (its
+    // 2-adic limit), same kernels (multi-pass: P > 2^15 here)
+    pl.field = logP > kMaxLogP ? 1 : 0;
+    if (logP > kMaxLogP2) {
+        set_error("NTT path: L = %llu exceeds 2^26", (unsigned long long)L);
         return QRNG_E_UNSUPPORTED;
     }
+    const uint64_t Pf = pl.field ? (uint64_t)kP2 : (uint64_t)kP;
     pl.logP = logP;
     pl.pack_shift = logP <= kMaxFusedLogP ? choose_pack_shift(n, logP) : 0;  // window sums <= n
     const uint64_t Pn = 1ull << logP;
@@ -864,19 +871,23 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.tw, Pn * 4, s));
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.itw, Pn * 4, s));
     QRNG_CUDA_TRY(cudaMallocAsync(&seed_words, nwords * 4, s));
-    const uint64_t w = powmod_h(3, (P - 1) >> logP), iw = powmod_h(w, P - 2);
+    const uint64_t w = powmod_p(3, (Pf - 1) >> logP, Pf), iw = powmod_p(w, Pf - 2, Pf);
     count_launch();
-    twiddle_table_kernel<0><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
-                                                                     (uint32_t)w, (uint32_t)iw);
+    if (pl.field)
+        twiddle_table_kernel<1><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
+                                                                                       (uint32_t)w, (uint32_t)iw);
+    else
+        twiddle_table_kernel<0><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
+                                                                                       (uint32_t)w, (uint32_t)iw);
     QRNG_CUDA_TRY(cudaGetLastError());
     count_launch();
     seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_bit_offset, seed_words,
                                                                       nwords);
     QRNG_CUDA_TRY(cudaGetLastError());
     // scale = P^-1 * 2^64 mod p, so mont(v, scale) = v * P^-1 * 2^32 (Montgomery form for the pointwise product)
-    const uint64_t pinvP = powmod_h(Pn % P, P - 2);
-    const uint64_t r2 = (uint64_t)(((unsigned __int128)1 << 64) % P);
-    const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * r2 % P);
+    const uint64_t pinvP = powmod_p(Pn % Pf, Pf - 2, Pf);
+    const uint64_t r2 = (uint64_t)(((unsigned __int128)1 << 64) % Pf);
+    const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * r2 % Pf);
     qrng_status st = QRNG_E_UNSUPPORTED;
     if (logP <= kMaxFusedLogP) {
         switch (logP) {
@@ -886,7 +897,20 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
             default: break;
         }
     } else {
-        // seed spectrum through the same multi-pass decomposition, forward only
+        st = pl.field ? seed_multipass<1>(pl, seed_words, n, m, L, logP, scaleM, s)
+                      : seed_multipass<0>(pl, seed_words, n, m, L, logP, scaleM, s);
+    }
+    cudaFreeAsync(seed_words, s);
+    return st;
+}
+
+// seed spectrum through the multi-pass decomposition, forward only
+template <int F>
+static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
+                                  int logP, uint32_t scaleM, cudaStream_t s) {
+    const uint64_t Pn = 1ull << logP;
+    qrng_status st = QRNG_OK;
+    {
         uint32_t *ws = nullptr;
         QRNG_CUDA_TRY(cudaMallocAsync(&ws, Pn * 4, s));
         int r[2];
@@ -902,10 +926,10 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
         pa.itw = pl.itw;
         pa.logP = (uint32_t)logP;
         pa.S = 0;
-        st = launch_pass<PASS_FWD_SEED>(r[0], pa, 1, s, false);
+        st = launch_pass<PASS_FWD_SEED, F>(r[0], pa, 1, s, false);
         if (st == QRNG_OK && np == 2) {
             pa.S = (uint32_t)r[0];
-            st = launch_pass<PASS_FWD>(r[1], pa, 1, s, false);
+            st = launch_pass<PASS_FWD, F>(r[1], pa, 1, s, false);
         }
         if (st == QRNG_OK) {
             FusedArgs fa{};
@@ -914,11 +938,10 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
             fa.itw = pl.itw;
             fa.tw_shift = (uint32_t)(logP - kSegLog);
             fa.scaleM = scaleM;
-            st = launch_segments<SEGFWD>(fa, ws, logP, 1, s, false);
+            st = launch_segments<SEGFWD, F>(fa, ws, logP, 1, s, false);
         }
         cudaFreeAsync(ws, s);
     }
-    cudaFreeAsync(seed_words, s);
     return st;
 }
 
@@ -930,6 +953,7 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
+template <int F>
 static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n,
                                      uint64_t m, const OutStream &out, cudaStream_t s) {
     const int logP = pl.logP;
@@ -984,20 +1008,20 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
         pa.ws = ws;
         pa.b0 = b0;
         pa.S = 0;
-        st = launch_pass<PASS_FWD_BITS>(r[0], pa, nb, s, true);
+        st = launch_pass<PASS_FWD_BITS, F>(r[0], pa, nb, s, true);
         if (st == QRNG_OK && np == 2) {
             pa.S = (uint32_t)r[0];
-            st = launch_pass<PASS_FWD>(r[1], pa, nb, s, true);
+            st = launch_pass<PASS_FWD, F>(r[1], pa, nb, s, true);
         }
-        if (st == QRNG_OK) st = launch_segments<SEG>(fa, ws, logP, nb, s, true);
+        if (st == QRNG_OK) st = launch_segments<SEG, F>(fa, ws, logP, nb, s, true);
         if (st == QRNG_OK && np == 2) {
             pa.S = (uint32_t)r[0];
-            st = launch_pass<PASS_INV>(r[1], pa, nb, s, true);
+            st = launch_pass<PASS_INV, F>(r[1], pa, nb, s, true);
         }
         if (st == QRNG_OK) {
             pa.S = 0;
-            st = pl.xor_tail ? launch_pass<PASS_INV_EMIT_XOR>(r[0], pa, nb, s, true)
-                             : launch_pass<PASS_INV_EMIT>(r[0], pa, nb, s, true);
+            st = pl.xor_tail ? launch_pass<PASS_INV_EMIT_XOR, F>(r[0], pa, nb, s, true)
+                             : launch_pass<PASS_INV_EMIT, F>(r[0], pa, nb, s, true);
         }
     }
     if (two) {  // join the side stream back before the workspaces are released
@@ -1011,7 +1035,9 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
 
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s) {
-    if (pl.logP > kMaxFusedLogP) return extract_multipass(pl, d_raw, n_blocks, n, m, out, s);
+    if (pl.logP > kMaxFusedLogP)
+        return pl.field ? extract_multipass<1>(pl, d_raw, n_blocks, n, m, out, s)
+                        : extract_multipass<0>(pl, d_raw, n_blocks, n, m, out, s);
     FusedArgs a{};
     a.raw = reinterpret_cast<const uint32_t *>(d_raw);
     a.n_blocks = n_blocks;

@@ -113,6 +113,7 @@ struct Plan {
     uint32_t len = 0;            // raw bits per block entering the product
     bool xor_tail = false;       // modified Toeplitz identity block
     int pack_shift = 0;          // >0: two blocks share one transform (x1 + 2^shift x2)
+    int field = 0;               // 0: p = kP (P <= 2^23); 1: p = kP2 (2^23 < P <= 2^26, multi-pass)
     uint32_t *shat = nullptr;    // P words: NTT(seed) * P^-1 * 2^32 mod p, DIF order
     uint32_t *tw = nullptr;      // P words: w_P^e * 2^32 mod p
     uint32_t *itw = nullptr;     // P words: w_P^-e * 2^32 mod p
