@@ -55,27 +55,51 @@ def concat_bitstreams(parts: list[np.ndarray], nbits: list[int]) -> np.ndarray:
     return np.packbits(np.concatenate(bits)) if bits else np.zeros(0, np.uint8)
 
 
-def gather_keys(local_key, n_local_blocks: int, m: int, group=None) -> np.ndarray:
-    """All-gather per-rank packed keys and return the full key stream (C4).
+def _unpack_dev(t, nbits):
+    """MSB-first bits of a uint8 tensor (on its device)."""
+    import torch
+    shifts = torch.arange(7, -1, -1, device=t.device, dtype=torch.uint8)
+    return ((t[:, None] >> shifts) & 1).reshape(-1)[:nbits]
+
+
+def _pack_dev(bits):
+    import torch
+    pad = (-bits.numel()) % 8
+    if pad:
+        bits = torch.cat([bits, torch.zeros(pad, dtype=bits.dtype, device=bits.device)])
+    w = torch.tensor([128, 64, 32, 16, 8, 4, 2, 1], dtype=torch.uint8, device=bits.device)
+    return (bits.reshape(-1, 8) * w).sum(dim=1, dtype=torch.int32).to(torch.uint8)
+
+
+def gather_keys(local_key, n_local_blocks: int, m: int, group=None):
+    """All-gather per-rank packed keys and return the full key stream (C4) as a
+    tensor on the local key's device.
 
     Shards may hold different block counts (shard_range); each shard is a
-    self-contained packed stream of n_local_blocks*m bits.
+    self-contained packed stream of n_local_blocks*m bits.  When every shard
+    ends on a byte boundary (every config on 1/2/4/8 GPUs) the streams are
+    concatenated as bytes; otherwise bit-level on the device.  With gloo the
+    exchange itself goes through host copies.
     """
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     dev = local_key.device
-    cnt = torch.tensor([n_local_blocks], dtype=torch.int64, device=dev)
+    cdev = dev if dist.get_backend(group) != "gloo" else torch.device("cpu")
+    cnt = torch.tensor([n_local_blocks], dtype=torch.int64, device=cdev)
     cnts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(cnts, cnt, group=group)
     sizes = [int(c.item()) for c in cnts]
     maxbytes = max((s * m + 7) // 8 for s in sizes)
-    pad = torch.zeros(maxbytes, dtype=torch.uint8, device=dev)
-    pad[:local_key.numel()] = local_key
+    pad = torch.zeros(maxbytes, dtype=torch.uint8, device=cdev)
+    pad[:local_key.numel()] = local_key.to(cdev)
     outs = [torch.zeros_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad, group=group)
-    return concat_bitstreams([o.cpu().numpy()[:(s * m + 7) // 8] for o, s in zip(outs, sizes)],
-                             [s * m for s in sizes])
+    outs = [o.to(dev) for o in outs]
+    if all((s * m) % 8 == 0 for s in sizes[:-1]):
+        return torch.cat([o[:(s * m + 7) // 8] for o, s in zip(outs, sizes)])
+    bits = torch.cat([_unpack_dev(o[:(s * m + 7) // 8], s * m) for o, s in zip(outs, sizes)])
+    return _pack_dev(bits)
 
 
 def four_step_exchange(ops, group=None):

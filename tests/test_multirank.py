@@ -59,14 +59,22 @@ def _worker(rank, world, port, q):
         qd.broadcast_seed(seed)
         b0, b1 = qd.shard_range(B, rank, world)
         local = oracle.extract(raw_all[b0 * n // 8:b1 * n // 8], b1 - b0, n, m, seed.numpy())
-        full = qd.gather_keys(torch.from_numpy(local), b1 - b0, m)
+        full = qd.gather_keys(torch.from_numpy(local), b1 - b0, m).numpy()  # bit-level assembly
         ref = oracle.extract(raw_all, B, n, m, seed.numpy())
+        # byte-aligned shards (every config on 1/2/4/8 GPUs): byte concatenation
+        m2, B2 = 176, 16
+        c0, c1 = qd.shard_range(B2, rank, world)
+        raw2 = S.random_bytes(98, B2 * n // 8)
+        seed2 = S.random_bytes(98, (n + m2 - 1 + 7) // 8, tag=5)
+        loc2 = oracle.extract(raw2[c0 * n // 8:c1 * n // 8], c1 - c0, n, m2, seed2)
+        full2 = qd.gather_keys(torch.from_numpy(loc2), c1 - c0, m2).numpy()
+        ok2 = np.array_equal(full2, oracle.extract(raw2, B2, n, m2, seed2))
         # sharded histogram: each rank counts its share of the samples
         samples = S.adc_samples(7, 100_003, 128, 20)
         lo, hi = qd.shard_range(samples.size, rank, world)
         counts = torch.from_numpy(oracle.hist256(samples[lo:hi]).astype(np.int64))
         qd.allreduce_counts(counts)
-        q.put((rank, np.array_equal(full, ref),
+        q.put((rank, np.array_equal(full, ref) and ok2,
                np.array_equal(counts.numpy().astype(np.uint64), oracle.hist256(samples))))
     finally:
         dist.destroy_process_group()
