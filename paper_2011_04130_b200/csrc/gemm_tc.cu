@@ -56,12 +56,18 @@ constexpr int BN = 224;          // output rows per N tile
 constexpr int NT = 2;            // N tiles per A stage (A reuse factor)
 constexpr int KS = 512;          // K per A stage: KS / 64 MMAs of K64 per N tile
 constexpr int KS128 = KS / 128;  // 128-bit raw chunks per A stage
-constexpr int A_STAGES = 2;      // A ring slots (2 measured faster than 3 / 4: more L1 for the loads)
+#ifndef QRNG_GEMM_ASTAGES
+#define QRNG_GEMM_ASTAGES 2
+#endif
+constexpr int A_STAGES = QRNG_GEMM_ASTAGES;  // A ring slots (2 measured faster than 3 / 4: more L1 for the loads)
 constexpr int A_STAGE_BYTES = BM * KS / 2;  // A stage: BM rows x KS nibbles
 constexpr int A_SBO = KS / 32 * 128;        // A stage: byte stride between 8-row core-matrix groups
 constexpr int KC = 1024;         // K per B chunk
 constexpr int SPC = KC / KS;     // A stages per B chunk
-constexpr int B_SLOTS = 3;       // B chunk ring slots
+#ifndef QRNG_GEMM_BSLOTS
+#define QRNG_GEMM_BSLOTS 3
+#endif
+constexpr int B_SLOTS = QRNG_GEMM_BSLOTS;  // B chunk ring slots
 constexpr int CM_PER_CHUNK = KC / 8 + NT * BN / 8 - 1;  // core matrices per chunk
 constexpr int CHUNK_BYTES = CM_PER_CHUNK * 128;
 constexpr uint32_t TMEM_COLS = 512;
@@ -92,7 +98,10 @@ constexpr int NWG = GC0 / 32;
 // Warp roles.
 constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4, W_EPI0 = W_XFORM0 + N_XFORM, N_EPI = 8;
 constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
-constexpr int PF = 2;  // A-transform prefetch depth (stages)
+#ifndef QRNG_GEMM_PF
+#define QRNG_GEMM_PF 2
+#endif
+constexpr int PF = QRNG_GEMM_PF;  // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
 static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile");
 
