@@ -1112,6 +1112,73 @@ __global__ void __launch_bounds__(256) csr_gather_pack_kernel(const uint32_t *__
     }
 }
 
+// Long key rows, two phases.  (1) every key word once: Z[b][j] = XOR of its
+// CSR entries (one thread per (block, word), consecutive threads on
+// consecutive words: coalesced gathers); (2) the packed stream from the Z rows
+// (one thread per output word, <= 4 Z words each, L2 hits).  The one-phase
+// gather form forms most output words from two key words (m % 32 != 0), i.e.
+// computes every key word twice.
+__global__ void __launch_bounds__(256) csr_key_kernel(const uint32_t *__restrict__ csr, const uint32_t *__restrict__ yws,
+                                                      uint32_t y_stride, uint64_t n_blocks, uint32_t ywords,
+                                                      uint32_t *__restrict__ zws, uint32_t z_stride) {
+    const uint64_t total = n_blocks * ywords;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = t / ywords;
+        const uint32_t j = (uint32_t)(t - b * ywords);
+        zws[b * z_stride + j] = csr_word(csr, ywords, yws + b * y_stride, j);
+    }
+}
+
+// Phase (1), staged: one CTA per block copies the block's whole leaf-parity
+// row (y_stride words, coalesced 16-byte loads at streaming bandwidth) into
+// shared memory and forms every key word from there; the CSR table (shared by
+// all blocks) is read through L1 / L2.  The gather form above is bound by the
+// latency of its dependent index -> parity loads from DRAM.
+__global__ void __launch_bounds__(512) csr_stage_key_kernel(const uint32_t *__restrict__ csr,
+                                                            const uint32_t *__restrict__ yws, uint32_t y_stride,
+                                                            uint32_t ywords, uint32_t *__restrict__ zws,
+                                                            uint32_t z_stride) {
+    extern __shared__ uint4 ys4[];
+    const uint32_t *ys = reinterpret_cast<const uint32_t *>(ys4);
+    const uint64_t b = blockIdx.x;
+    const uint4 *src = reinterpret_cast<const uint4 *>(yws + b * y_stride);  // y_stride % 4 == 0
+    for (uint32_t i = threadIdx.x; i < y_stride / 4; i += blockDim.x) ys4[i] = __ldcs(src + i);
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < ywords; j += blockDim.x) {
+        const uint32_t c = __ldg(csr + j);
+        uint32_t v = 0;
+        for (uint32_t e = 0; e < c; ++e) v ^= ys[__ldg(csr + ywords + e * ywords + j)];
+        zws[b * z_stride + j] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) zpack_kernel(const uint32_t *__restrict__ zws, uint32_t z_stride,
+                                                    uint64_t n_blocks, uint32_t m, uint64_t m_magic, OutStream out) {
+    const uint32_t ywords = (m + 31) / 32;
+    const uint64_t gbits = n_blocks * m, gwords = (gbits + 31) / 32;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < gwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t G = w * 32, end = min(G + 32, gbits);
+        uint64_t b = m_magic ? __umul64hi(G, m_magic) : G;  // G / m
+        uint32_t i = (uint32_t)(G - b * m);
+        uint64_t pos = G;
+        uint32_t word = 0;
+        while (pos < end) {
+            const uint32_t len = (uint32_t)min((uint64_t)(m - i), end - pos);  // 1..32 bits of block b
+            const uint32_t *zr = zws + b * z_stride;
+            const uint32_t q = i >> 5, sft = i & 31;
+            const uint32_t c0 = __ldg(zr + q);
+            const uint32_t c1 = (sft && q + 1 < ywords) ? __ldg(zr + q + 1) : 0u;
+            const uint32_t bits = sft ? ((c0 << sft) | (c1 >> (32 - sft))) : c0;
+            word |= (bits >> (32 - len)) << (32 - len - (uint32_t)(pos - G));
+            pos += len;
+            ++b;
+            i = 0;
+        }
+        emit_word(out, w, word, true);
+    }
+}
+
 // ---- host entry points -----------------------------------------------------
 // two block-range chunks on two streams per extraction (measured slower; see extract())
 constexpr bool kTwoChunks = false;
@@ -1253,7 +1320,45 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
     // (the fused form stages only each block's word 0 of the key rows)
     const size_t rs_words = (fused && m >= 64) ? (size_t)bpc : (size_t)bpc * (ywords + 1);
     const size_t stream_smem = (((size_t)QRNG_CSR_NBUF * bpc * H.y_stride + rs_words + csr_words + 1) & ~(size_t)1) * 4 + 8 * QRNG_CSR_NBUF;
-    if (st == QRNG_OK && gather) {
+    static const bool zpack = [] {  // QRNG_CSR_ZPACK=0: the one-phase gather form (A/B)
+        const char *e = getenv("QRNG_CSR_ZPACK");
+        return e ? atoi(e) != 0 : true;
+    }();
+    if (st == QRNG_OK && gather && zpack) {
+        const uint64_t gwords = ((uint64_t)n_blocks * m + 31) / 32;
+        const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const uint32_t z_stride = (ywords + 3) & ~3u;
+        uint32_t *kz = nullptr;
+        cudaError_t e = cudaMallocAsync(&kz, (size_t)n_blocks * z_stride * 4, s);
+        if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); st = QRNG_E_NOMEM; }
+        if (st == QRNG_OK) {
+            const uint64_t items = (uint64_t)n_blocks * ywords, cap = (uint64_t)sms * 16;
+            const uint64_t w1 = (items + 255) / 256, w2 = (gwords + 255) / 256;
+            static const bool staged = [] {  // QRNG_CSR_STAGE=0: the gather key kernel (A/B)
+                const char *e = getenv("QRNG_CSR_STAGE");
+                return e ? atoi(e) != 0 : true;
+            }();
+            const size_t ysmem = (size_t)H.y_stride * 4;
+            KernelTimer tc(s, true, 1);
+            if (staged && ysmem <= 200 * 1024 && H.y_stride % 4 == 0) {
+                if (ysmem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_stage_key_kernel));
+                csr_stage_key_kernel<<<(unsigned)n_blocks, 512, ysmem, s>>>(t->csr, yws, H.y_stride, ywords, kz,
+                                                                            z_stride);
+            } else {
+                csr_key_kernel<<<(unsigned)(w1 < cap ? w1 : cap), 256, 0, s>>>(t->csr, yws, H.y_stride, n_blocks,
+                                                                              ywords, kz, z_stride);
+            }
+            zpack_kernel<<<(unsigned)(w2 < cap ? w2 : cap), 256, 0, s>>>(kz, z_stride, n_blocks, (uint32_t)m, m_magic,
+                                                                        out);
+            count_launch();
+            tc.stop();
+            if (cudaGetLastError() != cudaSuccess) { set_error("csr_key / zpack launch failed"); st = QRNG_E_CUDA; }
+            cudaFreeAsync(kz, s);
+        }
+    } else if (st == QRNG_OK && gather) {
         // one thread per output word, gathers from L2 (no staging)
         const uint64_t gwords = ((uint64_t)n_blocks * m + 31) / 32;
         const uint64_t m_magic = m > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / m) + 1 : 0;
