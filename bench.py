@@ -843,6 +843,7 @@ def measure_next4(q, ctx, args, cpu_budget: float, n: int = 1 << 24, blocks: int
             "kernel_ms_per_step": km / args.steps, "kernel_share_of_step": (km / args.steps) / (ms / args.steps),
             "exchange_bytes_per_rank_per_block": N2 * 4 * (W - 1) / W if W > 1 else 0}
     roof["frac"] = roof["achieved"] / peak
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(f"next4_n2^{n.bit_length() - 1}", "ntt")
     plan.close()
     res = {"value": value, "unit": "Gbit/s", "ms_per_step": ms_max / args.steps, "roofline": roof,
            "parity": parity, "gpu_launches": int(launches), "wall_ms_per_step_rank0": t_wall / args.steps * 1e3,

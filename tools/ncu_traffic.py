@@ -7,12 +7,13 @@ bench.py reads for roofline.traffic (profiles/ncu_traffic.json).
 """
 import csv, json, os, re, subprocess, sys
 
-WORKLOAD = {"cfg1": "cfg1_n1024", "cfg2": "cfg2_n8192", "cfg3": "cfg3_n65536", "cfg4": "cfg4a_n1048576"}
+WORKLOAD = {"cfg1": "cfg1_n1024", "cfg2": "cfg2_n8192", "cfg3": "cfg3_n65536", "cfg4": "cfg4a_n1048576",
+            "cfg41": "cfg4b_n1048576", "next4": "next4_n2^24"}
 tag, reps = sys.argv[1], sys.argv[2:]
 out = {}
 for rep in reps:
     name = os.path.basename(rep)[len(tag) + 1:-len(".ncu-rep")]  # e.g. gemm_cfg2, ntt_segment_cfg5_n2^19
-    m = re.match(r"(gemm|ntt_segment|ntt_pass)_(cfg\d)(?:_(n2\^\d+))?$", name)
+    m = re.match(r"(gemm|ntt_segment|ntt_pass)_(cfg\d+|next4)(?:_(n2\^\d+))?$", name)
     if not m:
         continue
     kind, cfg, pt = m.groups()

@@ -19,7 +19,12 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args()
     q.load_library()
-    w = S.CONFIGS[args.config] if args.config in S.CONFIGS else S.sweep_workload(args.config)
+    if args.config == 124:  # NEXT-4's block length on one GPU: n = 2^24, 4 blocks (multi-pass NTT mod 7*2^26+1)
+        w = S.Workload("next4_n2^24", 24, 1 << 24, 7 * (1 << 24) // 10, 4, 20.0)
+    elif args.config == 41:  # config 4b: m of the bench's qrng_minentropy run (s = 0)
+        w = S.config4b(594060)
+    else:
+        w = S.CONFIGS[args.config] if args.config in S.CONFIGS else S.sweep_workload(args.config)
     raw_np, seed_np = S.workload_inputs(w)
     raw, seed = torch.from_numpy(raw_np).cuda(), torch.from_numpy(seed_np).cuda()
     if args.path != "auto":

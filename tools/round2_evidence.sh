@@ -28,6 +28,11 @@ cap ntt_pass_cfg4 4 ntt_pass_kernel
 cap gemm_cfg5_n2^10 10 toeplitz_gemm_kernel
 cap ntt_segment_cfg5_n2^19 19 ntt_segment_kernel
 cap ntt_segment_cfg5_n2^22 22 ntt_segment_kernel
+cap gemm_cfg5_n2^13 13 toeplitz_gemm_kernel
+cap gemm_cfg5_n2^16 16 toeplitz_gemm_kernel
+cap gemm_cfg5_n2^18 18 toeplitz_gemm_kernel
+cap ntt_segment_cfg41 41 ntt_segment_kernel
+cap ntt_segment_next4 124 ntt_segment_kernel
 for f in gpurun_out/${T}_*.ncu-rep; do echo "== $f"; python tools/ncu_summary.py $f; done > gpurun_out/${T}_ncu_summaries.txt 2>&1
 python tools/ncu_traffic.py $T gpurun_out/${T}_*.ncu-rep > gpurun_out/${T}_ncu_traffic.json
 # keep the headline capture (with source) and the NTT segment capture; the rest
