@@ -1311,7 +1311,10 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         const char *e = getenv("QRNG_CSR_GATHER");
         return e ? atoi(e) : -1;
     }();
-    const bool gather = gather_env >= 0 ? gather_env != 0 : ywords >= 1024;
+    // (round 2: with the two-phase staged form the threshold is 512 words --
+    // 2^15, 717 words: 278 -> 310 Gbit/s; 2^14, 359 words: the staged stream
+    // form stays faster, 534 vs 489; tools/csr_key_ab.sh, QRNG_CSR_GATHER)
+    const bool gather = gather_env >= 0 ? gather_env != 0 : ywords >= 512;
     static const bool stream_form = [] {
         const char *e = getenv("QRNG_CSR_STREAM");
         return e ? atoi(e) != 0 : true;
