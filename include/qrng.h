@@ -330,10 +330,14 @@ QRNG_API qrng_status qrng_debug_mxf4_probe(const uint8_t *d_A, const uint8_t *d_
 QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_h, int32_t *d_D,
                                            int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);
-/* PROFILING ONLY: 32 clock64 counters summed over all CTAs of the tcgen05 kernel
- * (waits per warp role, see gemm_tc.cu "cycle tracing"); E_UNSUPPORTED unless
- * the library was built with -DQRNG_GEMM_TRACE.  reset != 0 clears them. */
-QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_counters32, int reset);
+/* PROFILING ONLY: the MMA-issue timeline of CTA 0 of the last packed-mode
+ * tcgen05 launches (gemm_tc.cu "MMA-issue timeline"): h_out receives 4096
+ * uint64 = 512 stages x {tile << 8 | stage, clock64 at the stage's start
+ * (stage 0: the tile's start), after the tile lookup, after the accumulator
+ * wait, after the B wait, after the A wait, after issue + commits, 0};
+ * E_UNSUPPORTED unless the library was built with -DQRNG_GEMM_TIMELINE.
+ * reset != 0 clears the record. */
+QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_out, int reset);
 /* PROFILING ONLY: back-to-back int8 MMAs on fixed operands, one CTA per SM
  * (form 0: int8 cta_group::1 A in TMEM; 1: int8 cta_group::1 A in SMEM;
  * 3: int8 stage shape, 4 K32 steps x two N tiles per elected issue + one

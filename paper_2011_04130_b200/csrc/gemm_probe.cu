@@ -361,13 +361,7 @@ qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, 
     return QRNG_OK;
 }
 
-// The cycle-trace build of round 1 was removed with the rejected kernel variants.
-qrng_status trace(uint64_t *h_out, int reset) {
-    (void)h_out;
-    (void)reset;
-    set_error("cycle tracing is not built into this library");
-    return QRNG_E_UNSUPPORTED;
-}
+qrng_status trace(uint64_t *h_out, int reset) { return timeline(h_out, reset); }
 
 }  // namespace gemm
 }  // namespace qrng

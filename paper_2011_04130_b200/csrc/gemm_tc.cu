@@ -105,6 +105,24 @@ constexpr int PF = QRNG_GEMM_PF;  // A-transform prefetch depth (stages)
 constexpr int MAX_N = 1 << 16;
 static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile");
 
+// ---- optional MMA-issue timeline (profiling builds: -DQRNG_GEMM_TIMELINE) ----------
+// The elected MMA lane of CTA 0 records, per stage, clock64 before its waits,
+// after its waits and after its issue + commits (tag = tile << 8 | stage);
+// read back with qrng_debug_gemm_trace.  Compiled out of the product build.
+#ifdef QRNG_GEMM_TIMELINE
+constexpr int kTimelineStages = 512;
+__device__ unsigned long long g_timeline[8 * kTimelineStages];
+#define TL_T(v) const unsigned long long v = clock64()
+#define TL_REC(idx, tag, a, b, c, d, e, f)                                                     \
+    if (blockIdx.x == 0 && (idx) < kTimelineStages) {                                         \
+        unsigned long long *g_ = g_timeline + 8 * (idx);                                      \
+        g_[0] = (tag); g_[1] = (a); g_[2] = (b); g_[3] = (c); g_[4] = (d); g_[5] = (e); g_[6] = (f); \
+    }
+#else
+#define TL_T(v)
+#define TL_REC(idx, tag, a, b, c, d, e, f)
+#endif
+
 // ---- the extraction kernel -----------------------------------------------------
 struct Args {
     const uint32_t *raw;       // packed raw stream (MSB-first bytes) as words
@@ -332,17 +350,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         // elected lane runs the whole loop (no per-stage warp reconvergence)
         if (elect_one()) {
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+#ifdef QRNG_GEMM_TIMELINE
+            uint32_t tl_i = 0;
+#endif
+            // the next tile's geometry is looked up while the current tile's first
+            // stage is in the tensor pipe (measured: the lookup cost ~400 cycles of
+            // pipe idle per tile when done at the tile boundary)
+            Tile nti{};
+            if (blockIdx.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, blockIdx.x, cur);
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-                const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+                TL_T(tl_tile);
+                const Tile ti = nti;
                 const uint32_t r = it & 1, acc = tmem + ACC_COL0 + r * BN;
                 const uint32_t idesc0 = idesc_mxf4(BM, ti.ntc == 1 ? (int)ti.nlast : BN), idesc1 = idesc_mxf4(BM, (int)ti.nlast);
+                TL_T(tl_info);
                 mbar_wait(&acc_empty[r], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
+                TL_T(tl_acc);
                 for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                    TL_T(tl0);
                     const uint32_t kin = ks % SPC;
                     if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
+                    TL_T(tlb);
                     mbar_wait(&a_full[as], aph);
                     tc_fence_after();
+                    TL_T(tl1);
                     // descriptors of the stage's first MMA; the others differ only in the
                     // start-address field (addr >> 4, no carry: shared memory < 256 KB)
                     const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + as * A_STAGE_BYTES), 128, A_SBO);
@@ -358,6 +390,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     }
                     mma_commit(&a_empty[as]);
                     if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                    if (ks == 0 && t + gridDim.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, t + gridDim.x, cur);
+                    TL_T(tl2);
+                    TL_REC(tl_i, ((unsigned long long)it << 8) | ks, ks ? tl0 : tl_tile, ks ? tl0 : tl_info,
+                           ks ? tl0 : tl_acc, tlb, tl1, tl2);
+#ifdef QRNG_GEMM_TIMELINE
+                    ++tl_i;
+#endif
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
                     if (kin == SPC - 1 || ks == ti.kst - 1) {
                         if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
@@ -372,8 +411,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
         // stages behind N tile 0; one elected lane runs the loop
         if (elect_one()) {
             uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            Tile nti{};  // next tile's geometry, looked up during the current tile (as above)
+            if (blockIdx.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, blockIdx.x, cur);
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-                const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+                const Tile ti = nti;
                 const uint32_t idesc_full = idesc_mxf4(BM, BN);
                 const uint32_t idesc_last = idesc_mxf4(BM, (int)ti.nlast);
                 const uint32_t ph = (it & 1) ^ 1;
@@ -421,6 +462,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
                     }
                     if (nt1_on) mma_commit(&a_empty[as]);
                     if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                    if (ks == 0 && t + gridDim.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, t + gridDim.x, cur);
                     if (!nt1_on) dslot[ks] = as;
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
                     if (kin == SPC - 1 || ks == ti.kst - 1) {
@@ -647,6 +689,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
 }
 
 int operand_bits() { return 4; }
+
+qrng_status timeline(uint64_t *h_out, int reset) {
+#ifdef QRNG_GEMM_TIMELINE
+    QRNG_CUDA_TRY(cudaDeviceSynchronize());
+    QRNG_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_timeline, sizeof(g_timeline)));
+    if (reset) {
+        static unsigned long long z[8 * kTimelineStages] = {};
+        QRNG_CUDA_TRY(cudaMemcpyToSymbol(g_timeline, z, sizeof z));
+    }
+    return QRNG_OK;
+#else
+    (void)h_out;
+    (void)reset;
+    set_error("built without -DQRNG_GEMM_TIMELINE");
+    return QRNG_E_UNSUPPORTED;
+#endif
+}
 
 // ---- host ------------------------------------------------------------------------
 static size_t smem_bytes(uint32_t seed_words_n);

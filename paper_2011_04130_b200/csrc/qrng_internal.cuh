@@ -198,7 +198,8 @@ qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uin
 qrng_status extract_direct(const uint8_t *d_seed, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                            const OutStream &out, cudaStream_t s);
 qrng_status probe(const uint8_t *A, const uint8_t *h, int32_t *D, int N, int K, cudaStream_t s);
-qrng_status trace(uint64_t *h_out, int reset);
+qrng_status trace(uint64_t *h_out, int reset);     // = timeline (gemm_tc.cu, -DQRNG_GEMM_TIMELINE builds)
+qrng_status timeline(uint64_t *h_out, int reset);
 int operand_bits();  // 4: kind::mxf4 (E2M1 operands)
 qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int K, int hi_first, cudaStream_t s);
 // instruments (gemm_probe.cu)
