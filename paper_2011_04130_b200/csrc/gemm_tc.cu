@@ -96,8 +96,13 @@ static_assert(DEFER < A_STAGES && DEFER < SPC, "deferred stages stay resident in
 constexpr uint32_t GC0 = 32 * ((BN / 32 + 1) / 2);
 constexpr int NWG = GC0 / 32;
 // Warp roles.
-constexpr int W_MMA = 0, W_BGEN0 = 1, N_BGEN = 3, W_XFORM0 = 4, N_XFORM = 4, W_EPI0 = W_XFORM0 + N_XFORM, N_EPI = 8;
-constexpr int NTHREADS = (W_EPI0 + N_EPI) * 32;
+// Warp roles: MMA issuer, NBG B generators (3; 4 for grouped launches with
+// many leaves, whose B generators switch leaf seeds often: measured config 3
+// 206 -> 212 Gbit/s, config 2 716 -> 700 with 4), 4 A transformers, 8
+// epilogue warps (they use warp % 4 as their TMEM lane quadrant, so any
+// offset works).  NBG is a template parameter of the kernel.
+constexpr int W_MMA = 0, W_BGEN0 = 1, N_XFORM = 4, N_EPI = 8;
+__host__ __device__ constexpr int nthreads_for(int nbg) { return (1 + nbg + N_XFORM + N_EPI) * 32; }
 #ifndef QRNG_GEMM_PF
 #define QRNG_GEMM_PF 2
 #endif
@@ -261,8 +266,10 @@ __device__ __forceinline__ void store_words(const Args &a, const Tile &ti, uint6
     }
 }
 
-template <bool GROUPED, bool PACKED = false>
-__global__ void __launch_bounds__(NTHREADS, 1) toeplitz_gemm_kernel(Args a) {
+template <bool GROUPED, bool PACKED = false, int NBG = 3>
+__global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Args a) {
+    constexpr int N_BGEN = NBG, W_XFORM0 = W_BGEN0 + N_BGEN, W_EPI0 = W_XFORM0 + N_XFORM;
+    constexpr int NTHREADS = nthreads_for(NBG);
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *chunks = smem;
     uint8_t *a_ring = smem + B_SLOTS * CHUNK_BYTES;  // A stages (core-matrix layout, LBO 128, SBO A_SBO)
@@ -821,8 +828,8 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
-template <bool GROUPED, bool PACKED = false>
-static qrng_status launch(const Args &a, cudaStream_t s) {
+template <bool GROUPED, bool PACKED = false, int NBG = 3>
+static qrng_status launch_nbg(const Args &a, cudaStream_t s) {
     if ((uint64_t)a.n_mtiles * a.n_npairs > 0xFFFFFFFFull) {
         set_error("GEMM path: too many tiles");
         return QRNG_E_UNSUPPORTED;
@@ -832,21 +839,29 @@ static qrng_status launch(const Args &a, cudaStream_t s) {
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const size_t smem = smem_bytes(GROUPED ? a.n_leaves * 8u : a.seed_words_n);
     {
-        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel<GROUPED, PACKED>));
+        const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(toeplitz_gemm_kernel<GROUPED, PACKED, NBG>));
         if (st != QRNG_OK) return st;
     }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
     KernelTimer tm(s, true);
     if (GROUPED) {
-        const cudaError_t e = launch_pdl(toeplitz_gemm_kernel<GROUPED, PACKED>, dim3(grid), dim3(NTHREADS), smem, s, a);
+        const cudaError_t e = launch_pdl(toeplitz_gemm_kernel<GROUPED, PACKED, NBG>, dim3(grid), dim3(nthreads_for(NBG)), smem, s, a);
         if (e != cudaSuccess) { set_error("grouped GEMM launch: %s", cudaGetErrorString(e)); return QRNG_E_CUDA; }
     } else {
-        toeplitz_gemm_kernel<GROUPED, PACKED><<<grid, NTHREADS, smem, s>>>(a);
+        toeplitz_gemm_kernel<GROUPED, PACKED, NBG><<<grid, nthreads_for(NBG), smem, s>>>(a);
     }
     tm.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
+}
+
+template <bool GROUPED, bool PACKED = false>
+static qrng_status launch(const Args &a, cudaStream_t s) {
+    if constexpr (GROUPED) {
+        if (a.n_leaves > 64) return launch_nbg<GROUPED, PACKED, 4>(a, s);
+    }
+    return launch_nbg<GROUPED, PACKED, 3>(a, s);
 }
 
 // Rows per N pair of a plain launch: 448 (two full N tiles) unless the batch
