@@ -345,7 +345,9 @@ QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_out, int reset);
  * shape, 2 K64 steps x two N tiles (N0 = n & 511 <= 224, N1 = n >> 9 or N0 if
  * 0, <= 224) per elected issue + one commit; form 2 (cta_group::2) was removed
  * with the 2-SM kernel and returns E_UNSUPPORTED); *macs = work done.
- * form + 16k (forms 0-1): a commit every k MMAs.
+ * form + 16k (forms 0-1): a commit every k MMAs; (form 5): a second warp
+ * stores k bytes per clock to other shared memory while the MMAs run
+ * (shared-memory contention probe).
  * Time with CUDA events on `stream`. */
 QRNG_API qrng_status qrng_debug_mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t stream);
 QRNG_API double      qrng_debug_kernel_time_ms(uint64_t *launches);

@@ -44,6 +44,7 @@ __global__ void __cluster_dims__(FORM == 2 ? 2 : 1, 1, 1) __launch_bounds__(128,
     for (int i = threadIdx.x; i < 64 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
     if (threadIdx.x == 0) {
+        *reinterpret_cast<volatile uint32_t *>(smem + 64 * 1024 + 32) = 0u;  // form 5 writer stop flag
         mbar_init(&bar, 1);
         mbar_init(&bar + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -143,8 +144,28 @@ __global__ void __cluster_dims__(FORM == 2 ? 2 : 1, 1, 1) __launch_bounds__(128,
         }
         __syncwarp();
     }
+    if (FORM == 5 && warp == 1 && commit_every > 0) {
+        // shared-memory contention (form 5 + 16k): this warp stores k bytes per
+        // clock on average (one 512-byte st.shared.v4 per 512/k clocks) into a
+        // region the MMAs do not read, until the MMAs have completed
+        const long long period = 512 / commit_every;
+        volatile uint32_t *stop = reinterpret_cast<volatile uint32_t *>(smem + 64 * 1024 + 32);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + 65 * 1024);
+        const int lane = threadIdx.x & 31;
+        uint32_t i = 0;
+        long long t = clock64();
+        while (!*stop) {
+            dst[(i & 63) * 32 + lane] = make_uint4(i, i + 1, i + 2, i + 3);
+            ++i;
+            t += period;
+            while (clock64() < t) {}
+        }
+    }
     if (FORM == 2 || rank == 0) {
-        if (threadIdx.x == 0) mbar_wait(&bar, 0);
+        if (threadIdx.x == 0) {
+            mbar_wait(&bar, 0);
+            *reinterpret_cast<volatile uint32_t *>(smem + 64 * 1024 + 32) = 1u;
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -162,7 +183,7 @@ qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s)
     int dev = 0, sms = 148;
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const size_t smem = 64 * 1024 + 64;
+    const size_t smem = 65 * 1024 + 32 * 1024;  // operands, barriers, form-5 writer region
     const unsigned grid = (unsigned)sms;
     count_launch();
     switch (form) {

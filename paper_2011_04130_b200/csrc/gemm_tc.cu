@@ -152,6 +152,7 @@ struct Args {
     uint32_t *yws;             // leaf parity workspace
     uint32_t y_stride;         // words per block in yws
     uint64_t mt_magic;         // ceil(2^64 / n_mtiles) (0 when n_mtiles == 1): q = umul64hi(x, magic)
+    uint32_t n_runs, run_q, run_rem;  // tile runs (work distribution, set at launch): count, ntiles / n_runs, ntiles % n_runs
 };
 
 // Leaf table row as the kernel reads it (grouped mode, staged in shared memory
@@ -229,6 +230,53 @@ __device__ __forceinline__ Tile tile_info(const Args &a, const uint32_t *seed_s,
     }
     tile_rows(ti);
     return ti;
+}
+
+// ---- work distribution ----------------------------------------------------------
+// The tiles [0, ntiles) are cut into a.n_runs contiguous runs of equal
+// length (+-1); CTA c takes runs c, c + G, c + 2G, ... (G = gridDim.x).  Runs of
+// consecutive tiles share their N pair (M tile varies fastest), so one B
+// operand set serves the whole run (see `same_b`); a few runs per CTA keep the
+// CTAs working on nearby tiles (A-operand reuse in L2) and the per-CTA tile
+// counts within a few tiles of each other.  n_runs == ntiles gives the
+// plain strided order t = c, c + G, ...
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+struct TCur {
+    uint32_t t, hi, i;  // current tile, end of the current run, run index
+};
+// first tile of run i: runs [0, run_rem) have run_q + 1 tiles, the rest run_q
+// (host-computed quotient / remainder: no division on the device)
+__device__ __forceinline__ uint32_t run_lo(const Args &a, uint32_t i) { return i * a.run_q + min(i, a.run_rem); }
+__device__ __forceinline__ void tcur_skip(const Args &a, TCur &c) {
+    while (c.t >= c.hi) {  // past the run's end (or an empty run): the CTA's next run
+        c.i += gridDim.x;
+        if (c.i >= a.n_runs) { c.t = kNoTile; return; }
+        c.t = run_lo(a, c.i);
+        c.hi = run_lo(a, c.i + 1);
+    }
+}
+__device__ __forceinline__ TCur tcur_first(const Args &a) {
+    TCur c;
+    c.i = blockIdx.x;
+    if (c.i >= a.n_runs) { c.t = kNoTile; c.hi = 0; return c; }
+    c.t = run_lo(a, c.i);
+    c.hi = run_lo(a, c.i + 1);
+    tcur_skip(a, c);
+    return c;
+}
+__device__ __forceinline__ void tcur_next(const Args &a, TCur &c) {
+    ++c.t;
+    tcur_skip(a, c);
+}
+
+// Two consecutive tiles of a CTA whose B operands are identical (same seed
+// words, N pair, K extent and row count): the second reuses the first one's B
+// chunks in shared memory instead of regenerating them.  Only when the tile's
+// chunks fit in B_SLOTS - 1 slots, so the next set's first chunk can be built
+// while the current set is still in use.
+__device__ __forceinline__ bool same_b(const Tile &x, const Tile &y) {
+    return x.nchunks <= (uint32_t)(B_SLOTS - 1) && x.seed == y.seed && x.n0 == y.n0 && x.nchunks == y.nchunks &&
+           x.k128 == y.k128 && x.r == y.r;
 }
 
 // Store the masked parity words of one epilogue thread (its block b, rows
@@ -356,18 +404,22 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         // packed mode: both N tiles into one of two alternating column sets; one
         // elected lane runs the whole loop (no per-stage warp reconvergence)
         if (elect_one()) {
-            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            uint32_t as = 0, aph = 0, it = 0;
+            uint32_t gb = 0;        // B chunks of the sets before the current one
+            bool first_set = true;  // the current tile starts a B set (its chunks must be waited for)
 #ifdef QRNG_GEMM_TIMELINE
             uint32_t tl_i = 0;
 #endif
             // the next tile's geometry is looked up while the current tile's first
             // stage is in the tensor pipe (measured: the lookup cost ~400 cycles of
             // pipe idle per tile when done at the tile boundary)
+            TCur c = tcur_first(a), nc = c;
             Tile nti{};
-            if (blockIdx.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, blockIdx.x, cur);
-            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            if (c.t != kNoTile) nti = tile_info<GROUPED>(a, seed_s, c.t, cur);
+            for (; c.t != kNoTile; c = nc, ++it) {
                 TL_T(tl_tile);
                 const Tile ti = nti;
+                bool last_set = true;  // the next tile needs other B chunks: release ours
                 const uint32_t r = it & 1, acc = tmem + ACC_COL0 + r * BN;
                 const uint32_t idesc0 = idesc_mxf4(BM, ti.ntc == 1 ? (int)ti.nlast : BN), idesc1 = idesc_mxf4(BM, (int)ti.nlast);
                 TL_T(tl_info);
@@ -376,8 +428,8 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                 TL_T(tl_acc);
                 for (uint32_t ks = 0; ks < ti.kst; ++ks) {
                     TL_T(tl0);
-                    const uint32_t kin = ks % SPC;
-                    if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
+                    const uint32_t kin = ks % SPC, bc = gb + ks / SPC, bs = bc % B_SLOTS, bph = (bc / B_SLOTS) & 1;
+                    if (kin == 0 && first_set) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
                     TL_T(tlb);
                     mbar_wait(&a_full[as], aph);
                     tc_fence_after();
@@ -396,8 +448,15 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                             mma_mxf4_ss(acc, adesc, bdesc + BN, idesc1, tmem + SF_COL, tmem + SF2_COL, true);  // + BN/8 cm
                     }
                     mma_commit(&a_empty[as]);
-                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
-                    if (ks == 0 && t + gridDim.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, t + gridDim.x, cur);
+                    if (ks == 0) {
+                        nc = c;
+                        tcur_next(a, nc);
+                        if (nc.t != kNoTile) {
+                            nti = tile_info<GROUPED>(a, seed_s, nc.t, cur);
+                            last_set = !same_b(ti, nti);
+                        }
+                    }
+                    if (last_set && (kin == SPC - 1 || ks == ti.kst - 1)) mma_commit(&b_empty[bs]);
                     TL_T(tl2);
                     TL_REC(tl_i, ((unsigned long long)it << 8) | ks, ks ? tl0 : tl_tile, ks ? tl0 : tl_info,
                            ks ? tl0 : tl_acc, tlb, tl1, tl2);
@@ -405,10 +464,9 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                     ++tl_i;
 #endif
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
-                    if (kin == SPC - 1 || ks == ti.kst - 1) {
-                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
-                    }
                 }
+                if (last_set) gb += ti.nchunks;
+                first_set = last_set;
                 mma_commit(&acc_full[r]);
             }
         }
@@ -417,11 +475,15 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         // one column set per N tile; N tile 1 of each tile is deferred DEFER
         // stages behind N tile 0; one elected lane runs the loop
         if (elect_one()) {
-            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            uint32_t as = 0, aph = 0, it = 0;
+            uint32_t gb = 0;        // B chunks of the sets before the current one (as above)
+            bool first_set = true;
+            TCur c = tcur_first(a), nc = c;
             Tile nti{};  // next tile's geometry, looked up during the current tile (as above)
-            if (blockIdx.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, blockIdx.x, cur);
-            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            if (c.t != kNoTile) nti = tile_info<GROUPED>(a, seed_s, c.t, cur);
+            for (; c.t != kNoTile; c = nc, ++it) {
                 const Tile ti = nti;
+                bool last_set = true;
                 const uint32_t idesc_full = idesc_mxf4(BM, BN);
                 const uint32_t idesc_last = idesc_mxf4(BM, (int)ti.nlast);
                 const uint32_t ph = (it & 1) ^ 1;
@@ -433,8 +495,8 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                 uint32_t dslot[DEFER];
                 uint32_t cb0 = 0;
                 for (uint32_t ks = 0; ks < ti.kst; ++ks) {
-                    const uint32_t kin = ks % SPC;
-                    if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
+                    const uint32_t kin = ks % SPC, bc = gb + ks / SPC, bs = bc % B_SLOTS, bph = (bc / B_SLOTS) & 1;
+                    if (kin == 0 && first_set) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
                     mbar_wait(&a_full[as], aph);
                     tc_fence_after();
                     const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
@@ -468,14 +530,20 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                                         tmem + SF_COL + 8, (ks | kk) != 0);
                     }
                     if (nt1_on) mma_commit(&a_empty[as]);
-                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
-                    if (ks == 0 && t + gridDim.x < ntiles) nti = tile_info<GROUPED>(a, seed_s, t + gridDim.x, cur);
+                    if (ks == 0) {
+                        nc = c;
+                        tcur_next(a, nc);
+                        if (nc.t != kNoTile) {
+                            nti = tile_info<GROUPED>(a, seed_s, nc.t, cur);
+                            last_set = !same_b(ti, nti);
+                        }
+                    }
+                    if (last_set && (kin == SPC - 1 || ks == ti.kst - 1)) mma_commit(&b_empty[bs]);
                     if (!nt1_on) dslot[ks] = as;
                     if (++as == A_STAGES) { as = 0; aph ^= 1; }
-                    if (kin == SPC - 1 || ks == ti.kst - 1) {
-                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
-                    }
                 }
+                if (last_set) gb += ti.nchunks;
+                first_set = last_set;
                 mma_commit(&acc_full[0]);
             }
         }
@@ -484,13 +552,19 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         // B generators: core matrix tau of chunk (n0, k0): row r' holds seed bits
         // s[n0 + k0 + 8 tau + r' + c], c = 0..31, as E2M1 0/1.
         const int tb = (warp - W_BGEN0) * 32 + lane;
-        uint32_t bs = 0, bph = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+        uint32_t gb = 0;  // B chunks generated so far (ring position)
+        Tile pti{};
+        bool have_prev = false;
+        for (TCur c = tcur_first(a); c.t != kNoTile; tcur_next(a, c)) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, c.t, cur);
+            const bool reuse = have_prev && same_b(pti, ti);
+            pti = ti;
+            have_prev = true;
+            if (reuse) continue;  // the MMA issuer reads the previous tile's chunks again
             // core-matrix rows the MMAs of this tile read (K chunk + the N rows in use)
             const int ncm = KC / 8 + (int)(((ti.ntc - 1) * BN + ti.nlast) / 8) - 1;
-            for (uint32_t c = 0; c < ti.nchunks; ++c) {
-                const uint32_t base = ti.n0 + c * KC;
+            for (uint32_t ch = 0; ch < ti.nchunks; ++ch, ++gb) {
+                const uint32_t base = ti.n0 + ch * KC, bs = gb % B_SLOTS, bph = (gb / B_SLOTS) & 1;
                 mbar_wait(&b_empty[bs], bph ^ 1);
                 uint8_t *cb = chunks + bs * CHUNK_BYTES;
                 for (int r = tb; r < ncm * 8; r += N_BGEN * 32) {
@@ -504,7 +578,6 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&b_full[bs]);
-                if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
             }
         }
     } else if (warp >= W_XFORM0 && warp < W_XFORM0 + N_XFORM) {
@@ -513,15 +586,16 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         // ring of input chunks runs continuously across tiles.
         const uint32_t row = (uint32_t)(warp - W_XFORM0) * 32 + lane;
         uint32_t lcur = 0;                      // leaf cursor of the load side
-        uint32_t lt = blockIdx.x, lks = 0;      // load cursor (tile, K stage)
+        TCur lc = tcur_first(a);  // load cursor (tile, K stage)
+        uint32_t lks = 0;
         Tile lti{};
-        if (lt < ntiles) lti = tile_info<GROUPED>(a, seed_s, lt, lcur);
+        if (lc.t != kNoTile) lti = tile_info<GROUPED>(a, seed_s, lc.t, lcur);
         auto step1 = [&]() {
-            if (lt >= ntiles) return;
+            if (lc.t == kNoTile) return;
             if (++lks == lti.kst) {
                 lks = 0;
-                lt += gridDim.x;
-                if (lt < ntiles) lti = tile_info<GROUPED>(a, seed_s, lt, lcur);
+                tcur_next(a, lc);
+                if (lc.t != kNoTile) lti = tile_info<GROUPED>(a, seed_s, lc.t, lcur);
             }
         };
         // Branch-free prefetch: always load from a valid address (clamped block,
@@ -533,7 +607,7 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         auto load = [&](bool &v, uint32_t hf) -> uint4 {
             const uint64_t b = (uint64_t)lti.mt * BM + row;
             const int32_t ci = (int32_t)lti.k128 - 1 - (int32_t)(KS128 * lks + hf);
-            v = lt < ntiles && b < a.n_blocks && ci >= 0;
+            v = lc.t != kNoTile && b < a.n_blocks && ci >= 0;
             const uint64_t bc = b < a.n_blocks ? b : a.n_blocks - 1;
             return __ldg(reinterpret_cast<const uint4 *>(lti.xb + bc * lti.xs) + (ci >= 0 ? ci : 0));
         };
@@ -541,7 +615,7 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         bool ok[PF], vd[PF][KS128];
 #pragma unroll
         for (int j = 0; j < PF; ++j) {
-            ok[j] = lt < ntiles;
+            ok[j] = lc.t != kNoTile;
 #pragma unroll
             for (int hf = 0; hf < KS128; ++hf) pf[j][hf] = load(vd[j][hf], hf);
             step1();
@@ -556,7 +630,7 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                     uint4 cur4[KS128];
 #pragma unroll
                     for (int hf = 0; hf < KS128; ++hf) cur4[hf] = vd[j][hf] ? pf[j][hf] : make_uint4(0, 0, 0, 0);
-                    ok[j] = lt < ntiles;
+                    ok[j] = lc.t != kNoTile;
 #pragma unroll
                     for (int hf = 0; hf < KS128; ++hf) pf[j][hf] = load(vd[j][hf], hf);
                     step1();
@@ -592,8 +666,8 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         const uint32_t col_lo = h ? GC0 : 0u, col_n = h ? (uint32_t)BN - GC0 : GC0;
         const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + col_lo;
         uint32_t it = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+        for (TCur c = tcur_first(a); c.t != kNoTile; tcur_next(a, c), ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, c.t, cur);
             const uint32_t r = it & 1;
             mbar_wait(&acc_full[r], (it >> 1) & 1);
             tc_fence_after();
@@ -644,8 +718,8 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         const uint32_t col_lo = h ? GC0 : 0u, col_n = h ? (uint32_t)BN - GC0 : GC0;
         const uint32_t quad = tmem + (((uint32_t)(warp & 3) * 32) << 16) + ACC_COL0 + col_lo;
         uint32_t it = 0;
-        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const Tile ti = tile_info<GROUPED>(a, seed_s, t, cur);
+        for (TCur c = tcur_first(a); c.t != kNoTile; tcur_next(a, c), ++it) {
+            const Tile ti = tile_info<GROUPED>(a, seed_s, c.t, cur);
             mbar_wait(&acc_full[0], it & 1);
             tc_fence_after();
             const uint64_t b = (uint64_t)ti.mt * BM + row;
@@ -828,6 +902,33 @@ void plan_free(Plan &pl) {
     pl = Plan{};
 }
 
+// Tile runs of a launch (work distribution above).  Packed Karatsuba launches
+// (leaf K <= 2048: two B chunks, reusable) take about QRNG_GEMM_RUNLEN
+// (default 32) tiles per run; the others keep the strided order.  Measured
+// (tools/runs_ab.sh, tools/runs_ab2.sh; kernel time, strided -> runs):
+// config 2 leaves 165 -> 156 us, config 3 1098 -> 1025 us, 2^17 6.63 -> 6.12
+// ms; runs of 3-7 tiles regenerate B too often (config 2 189 us at 3.5),
+// runs of 100+ tiles spread the CTAs over the whole input (A re-reads miss
+// L2: 2^13 leaves 1.24 ms at 221 vs 1.18 at 28); plain dense n = 1024 403
+// -> 412 us and 2^18 leaves (K = 4096, no reuse) 13.44 -> 13.56 ms, hence
+// strided there.  QRNG_GEMM_RUNS = runs per CTA overrides (0 = strided).
+static uint32_t tile_runs(uint32_t ntiles, unsigned grid, bool reuse_b) {
+    static const int per_cta = [] {
+        const char *e = getenv("QRNG_GEMM_RUNS");
+        return (e && *e) ? atoi(e) : -1;
+    }();
+    static const int run_len = [] {
+        const char *e = getenv("QRNG_GEMM_RUNLEN");
+        const int v = (e && *e) ? atoi(e) : 32;
+        return v > 0 ? v : 32;
+    }();
+    if (per_cta == 0 || (per_cta < 0 && !reuse_b)) return ntiles;
+    uint64_t k = per_cta > 0 ? (uint64_t)per_cta : ((uint64_t)ntiles + (uint64_t)grid * run_len / 2) / ((uint64_t)grid * run_len);
+    if (k < 1) k = 1;
+    const uint64_t r = (uint64_t)grid * k;
+    return r < ntiles ? (uint32_t)r : ntiles;
+}
+
 template <bool GROUPED, bool PACKED = false, int NBG = 3>
 static qrng_status launch_nbg(const Args &a, cudaStream_t s) {
     if ((uint64_t)a.n_mtiles * a.n_npairs > 0xFFFFFFFFull) {
@@ -844,12 +945,16 @@ static qrng_status launch_nbg(const Args &a, cudaStream_t s) {
     }
     const uint32_t ntiles = a.n_mtiles * a.n_npairs;
     const unsigned grid = (unsigned)(ntiles < (uint32_t)sms ? ntiles : (uint32_t)sms);
+    Args b = a;
+    b.n_runs = tile_runs(ntiles, grid, GROUPED && PACKED);
+    b.run_q = ntiles / b.n_runs;
+    b.run_rem = ntiles % b.n_runs;
     KernelTimer tm(s, true);
     if (GROUPED) {
-        const cudaError_t e = launch_pdl(toeplitz_gemm_kernel<GROUPED, PACKED, NBG>, dim3(grid), dim3(nthreads_for(NBG)), smem, s, a);
+        const cudaError_t e = launch_pdl(toeplitz_gemm_kernel<GROUPED, PACKED, NBG>, dim3(grid), dim3(nthreads_for(NBG)), smem, s, b);
         if (e != cudaSuccess) { set_error("grouped GEMM launch: %s", cudaGetErrorString(e)); return QRNG_E_CUDA; }
     } else {
-        toeplitz_gemm_kernel<GROUPED, PACKED, NBG><<<grid, nthreads_for(NBG), smem, s>>>(a);
+        toeplitz_gemm_kernel<GROUPED, PACKED, NBG><<<grid, nthreads_for(NBG), smem, s>>>(b);
     }
     tm.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
@@ -858,7 +963,8 @@ static qrng_status launch_nbg(const Args &a, cudaStream_t s) {
 
 template <bool GROUPED, bool PACKED = false>
 static qrng_status launch(const Args &a, cudaStream_t s) {
-    if constexpr (GROUPED) {
+    if constexpr (GROUPED && PACKED) {
+        // (the deferred-mode kernel with 4 B generators spills: 2^18 leaves 12.9 -> 14.0 ms)
         if (a.n_leaves > 64) return launch_nbg<GROUPED, PACKED, 4>(a, s);
     }
     return launch_nbg<GROUPED, PACKED, 3>(a, s);
