@@ -331,10 +331,12 @@ QRNG_API qrng_status qrng_debug_umma_probe(const uint8_t *d_A, const uint8_t *d_
                                            int N, int K, cudaStream_t stream);
 QRNG_API void        qrng_debug_kernel_timing(int enable);
 /* PROFILING ONLY: the MMA-issue timeline of CTA 0 of the last packed-mode
- * tcgen05 launches (gemm_tc.cu "MMA-issue timeline"): h_out receives 4096
+ * tcgen05 launches (gemm_tc.cu "MMA-issue timeline"): h_out receives 6144
  * uint64 = 512 stages x {tile << 8 | stage, clock64 at the stage's start
  * (stage 0: the tile's start), after the tile lookup, after the accumulator
- * wait, after the B wait, after the A wait, after issue + commits, 0};
+ * wait, after the B wait, after the A wait, after issue + commits, 0}, then
+ * 256 CTAs x {globaltimer ns at entry, first A stage ready, last MMA commit,
+ * exit; tile count, 0, 0, 0};
  * E_UNSUPPORTED unless the library was built with -DQRNG_GEMM_TIMELINE.
  * reset != 0 clears the record. */
 QRNG_API qrng_status qrng_debug_gemm_trace(uint64_t *h_out, int reset);

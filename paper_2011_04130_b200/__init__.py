@@ -246,8 +246,10 @@ def karatsuba_plan(n: int, m: int, max_depth: int) -> KaratsubaPlan:
 
 def gemm_trace(reset: bool = True) -> np.ndarray:
     """PROFILING ONLY (-DQRNG_GEMM_TIMELINE builds): the MMA-issue timeline,
-    512 x (tag, t_start, t_info, t_acc, t_b, t_a, t_issued, 0)."""
-    c = np.zeros(4096, np.uint64)
+    512 x (tag, t_start, t_info, t_acc, t_b, t_a, t_issued, 0), then one row
+    per CTA (< 256): globaltimer ns at entry, first A stage ready, last MMA
+    commit, exit, then the CTA's tile count."""
+    c = np.zeros(8 * 768, np.uint64)
     _check(load_library().qrng_debug_gemm_trace(c.ctypes.data, 1 if reset else 0))
     return c.reshape(-1, 8)
 

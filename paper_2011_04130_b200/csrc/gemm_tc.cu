@@ -113,10 +113,20 @@ static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile
 // ---- optional MMA-issue timeline (profiling builds: -DQRNG_GEMM_TIMELINE) ----------
 // The elected MMA lane of CTA 0 records, per stage, clock64 before its waits,
 // after its waits and after its issue + commits (tag = tile << 8 | stage);
-// read back with qrng_debug_gemm_trace.  Compiled out of the product build.
+// read back with qrng_debug_gemm_trace.  Row 512 + c holds, for CTA c < 256,
+// globaltimer ns at kernel entry, when the first A stage is ready, after the
+// last MMA commit and at exit, then its tile count (packed mode).
+// Compiled out of the product build.
 #ifdef QRNG_GEMM_TIMELINE
-constexpr int kTimelineStages = 512;
-__device__ unsigned long long g_timeline[8 * kTimelineStages];
+constexpr int kTimelineStages = 512, kTimelineCtaRows = 256;
+__device__ unsigned long long g_timeline[8 * (kTimelineStages + kTimelineCtaRows)];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL_CTA(k)                                                                               \
+    if (blockIdx.x < kTimelineCtaRows) g_timeline[8 * kTimelineStages + 8 * blockIdx.x + (k)] = gtimer()
 #define TL_T(v) const unsigned long long v = clock64()
 #define TL_REC(idx, tag, a, b, c, d, e, f)                                                     \
     if (blockIdx.x == 0 && (idx) < kTimelineStages) {                                         \
@@ -124,6 +134,7 @@ __device__ unsigned long long g_timeline[8 * kTimelineStages];
         g_[0] = (tag); g_[1] = (a); g_[2] = (b); g_[3] = (c); g_[4] = (d); g_[5] = (e); g_[6] = (f); \
     }
 #else
+#define TL_CTA(k)
 #define TL_T(v)
 #define TL_REC(idx, tag, a, b, c, d, e, f)
 #endif
@@ -330,6 +341,7 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + ACC_EMPTY);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) TL_CTA(0);
     if (GROUPED) {
         for (uint32_t i = threadIdx.x; i < a.n_leaves; i += NTHREADS) {
             const Leaf &L = a.leaves[i];
@@ -434,6 +446,9 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                     mbar_wait(&a_full[as], aph);
                     tc_fence_after();
                     TL_T(tl1);
+#ifdef QRNG_GEMM_TIMELINE
+                    if (it == 0 && ks == 0) TL_CTA(1);
+#endif
                     // descriptors of the stage's first MMA; the others differ only in the
                     // start-address field (addr >> 4, no carry: shared memory < 256 KB)
                     const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + as * A_STAGE_BYTES), 128, A_SBO);
@@ -469,6 +484,10 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
                 first_set = last_set;
                 mma_commit(&acc_full[r]);
             }
+            TL_CTA(2);
+#ifdef QRNG_GEMM_TIMELINE
+            if (blockIdx.x < kTimelineCtaRows) g_timeline[8 * kTimelineStages + 8 * blockIdx.x + 4] = it;
+#endif
         }
         __syncwarp();
     } else if (warp == W_MMA) {
@@ -763,6 +782,7 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TL_CTA(3);
     if (warp == W_MMA) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
@@ -776,7 +796,7 @@ qrng_status timeline(uint64_t *h_out, int reset) {
     QRNG_CUDA_TRY(cudaDeviceSynchronize());
     QRNG_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_timeline, sizeof(g_timeline)));
     if (reset) {
-        static unsigned long long z[8 * kTimelineStages] = {};
+        static unsigned long long z[8 * (kTimelineStages + kTimelineCtaRows)] = {};
         QRNG_CUDA_TRY(cudaMemcpyToSymbol(g_timeline, z, sizeof z));
     }
     return QRNG_OK;
@@ -963,6 +983,9 @@ static qrng_status launch_nbg(const Args &a, cudaStream_t s) {
 
 template <bool GROUPED, bool PACKED = false>
 static qrng_status launch(const Args &a, cudaStream_t s) {
+#ifdef QRNG_GEMM_NBG_FORCE  // A/B builds: one B-generator count for every launch
+    return launch_nbg<GROUPED, PACKED, QRNG_GEMM_NBG_FORCE>(a, s);
+#endif
     if constexpr (GROUPED && PACKED) {
         // (the deferred-mode kernel with 4 B generators spills: 2^18 leaves 12.9 -> 14.0 ms)
         if (a.n_leaves > 64) return launch_nbg<GROUPED, PACKED, 4>(a, s);

@@ -29,7 +29,9 @@ with q.Plan(w.n, w.m, seed) as pl:
     q.gemm_trace(reset=True)
     pl.extract(raw, w.n_blocks)
     torch.cuda.synchronize()
-    tl = q.gemm_trace(reset=False).astype(np.int64)
+    tr = q.gemm_trace(reset=False).astype(np.int64)
+tl, cta = tr[:512], tr[512:]
+cta = cta[cta[:, 0] != 0]
 tl = tl[tl[:, 1] != 0]
 tag, ts, ti_, ta, tb, tA, tI = (tl[:, k] for k in range(7))
 tile, stage = tag >> 8, tag & 255
@@ -43,4 +45,21 @@ out = {"workload": w.name, "stages": int(len(tl)), "span_cycles": int(span), "cy
        "other": {"b_wait": float((tb - ts)[~s0].mean()), "a_wait": float((tA - tb)[~s0].mean()),
                  "issue": float((tI - tA)[~s0].mean())},
        "gap_between_stages": float(gap[1:].mean())}
+if len(cta):
+    # per-CTA phases (globaltimer ns, relative to the earliest CTA entry)
+    t0 = cta[:, 0].min()
+    out["cta_ns"] = {"ctas": int(len(cta)), "entry_spread": int(cta[:, 0].max() - t0),
+                     "first_a_ready": [int(np.median(cta[:, 1] - cta[:, 0])), int((cta[:, 1] - cta[:, 0]).max())],
+                     "mma_loop": [int(np.median(cta[:, 2] - cta[:, 1])), int((cta[:, 2] - cta[:, 1]).min()),
+                                  int((cta[:, 2] - cta[:, 1]).max())],
+                     "drain_to_exit": [int(np.median(cta[:, 3] - cta[:, 2])), int((cta[:, 3] - cta[:, 2]).max())],
+                     "last_mma_end": int(cta[:, 2].max() - t0), "first_exit": int(cta[:, 3].min() - t0),
+                     "last_exit": int(cta[:, 3].max() - t0),
+                     "tiles_min_max": [int(cta[:, 4].min()), int(cta[:, 4].max())]}
+    loop = cta[:, 2] - cta[:, 1]
+    for k in np.unique(cta[:, 4]):  # loop time by tile count: static imbalance vs per-SM speed
+        sel = cta[:, 4] == k
+        out["cta_ns"][f"loop_us_at_{int(k)}_tiles"] = [int(sel.sum()), round(float(loop[sel].min()) / 1e3, 1),
+                                                      round(float(np.median(loop[sel])) / 1e3, 1),
+                                                      round(float(loop[sel].max()) / 1e3, 1)]
 print(json.dumps(out))
