@@ -115,7 +115,7 @@ static_assert(kTileRows == NT * BN, "leaf tables assume NT*BN rows per work tile
 // after its waits and after its issue + commits (tag = tile << 8 | stage);
 // read back with qrng_debug_gemm_trace.  Row 512 + c holds, for CTA c < 256,
 // globaltimer ns at kernel entry, when the first A stage is ready, after the
-// last MMA commit and at exit, then its tile count (packed mode).
+// last MMA commit and at exit, then its tile count and SM id (packed mode).
 // Compiled out of the product build.
 #ifdef QRNG_GEMM_TIMELINE
 constexpr int kTimelineStages = 512, kTimelineCtaRows = 256;
@@ -486,7 +486,12 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
             }
             TL_CTA(2);
 #ifdef QRNG_GEMM_TIMELINE
-            if (blockIdx.x < kTimelineCtaRows) g_timeline[8 * kTimelineStages + 8 * blockIdx.x + 4] = it;
+            if (blockIdx.x < kTimelineCtaRows) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                g_timeline[8 * kTimelineStages + 8 * blockIdx.x + 4] = it;
+                g_timeline[8 * kTimelineStages + 8 * blockIdx.x + 5] = smid;
+            }
 #endif
         }
         __syncwarp();

@@ -17,6 +17,7 @@ import paper_2011_04130_b200 as q
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--per-cta", action="store_true", help="also print (cta, sm, tiles, loop us) for every CTA")
 a = ap.parse_args()
 q.load_library()
 w = S.CONFIGS[a.config] if a.config in S.CONFIGS else S.sweep_workload(a.config)
@@ -63,3 +64,7 @@ if len(cta):
                                                       round(float(np.median(loop[sel])) / 1e3, 1),
                                                       round(float(loop[sel].max()) / 1e3, 1)]
 print(json.dumps(out))
+if a.per_cta and len(cta):
+    for c in range(len(cta)):
+        print("cta", c, "sm", int(cta[c, 5]), "tiles", int(cta[c, 4]), "entry_us", round((cta[c, 0] - cta[:, 0].min()) / 1e3, 2),
+              "loop_us", round((cta[c, 2] - cta[c, 1]) / 1e3, 1))
