@@ -1270,7 +1270,10 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
         // deeper trees (more generations, longer X rows) want more, smaller CTAs:
         // measured (tools/qbuf_ab.sh) 296 CTAs best at depth 2, 1184 at depth 6
         const uint64_t div = (uint64_t)QRNG_QBUF_DIV << (H.depth >= 6 ? 2 : H.depth >= 4 ? 1 : 0);
-        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(32, n_blocks / div));
+#ifndef QRNG_QBUF_MAXBPC
+#define QRNG_QBUF_MAXBPC 32
+#endif
+        const uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(QRNG_QBUF_MAXBPC, n_blocks / div));
         KernelTimer tq(s, true, 1);
         SeedJob sj{};
         sj.q_ctas = (uint32_t)((n_blocks + bpc - 1) / bpc);
