@@ -625,7 +625,7 @@ struct qrng_stream {
     } slot[8];
     uint64_t *d_counts = nullptr;
     qrng_status err = QRNG_OK;
-    char errmsg[256] = "";
+    char errmsg[512] = "";
 };
 
 static void stream_release(qrng_stream *st) {

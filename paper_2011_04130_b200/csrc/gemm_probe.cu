@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128, 1) umma_probe_kernel(const uint8_t *A, co
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     uint32_t *slot = reinterpret_cast<uint32_t *>(smem + 8);
     uint8_t *cm = smem + 1024;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int warp = threadIdx.x >> 5, tid = threadIdx.x;
     const int ncm = K / 8 + N / 8 - 1;
     for (int r = tid; r < ncm * 8; r += 128) {
         int tau = r >> 3, rr = r & 7;

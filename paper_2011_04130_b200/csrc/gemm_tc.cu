@@ -405,7 +405,6 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t ntiles = a.n_mtiles * a.n_npairs;  // n_npairs: total over leaves in grouped mode
     uint32_t cur = 0;                                 // leaf cursor of this role
     if (GROUPED) {
         pdl_release();  // the combine kernel may be scheduled as CTAs finish
@@ -495,9 +494,12 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
 #endif
         }
         __syncwarp();
-    } else if (warp == W_MMA) {
-        // one column set per N tile; N tile 1 of each tile is deferred DEFER
-        // stages behind N tile 0; one elected lane runs the loop
+    } else if (!GROUPED && warp == W_MMA) {
+        // plain launches: one column set per N tile; N tile 1 of each tile is
+        // deferred DEFER stages behind N tile 0; one elected lane runs the loop,
+        // with the packed loop's one-tile lookahead and B reuse (consecutive
+        // strided tiles often share their N pair: dense n = 1024 2,547 vs 2,447
+        // Gbit/s with the grouped loop below)
         if (elect_one()) {
             uint32_t as = 0, aph = 0, it = 0;
             uint32_t gb = 0;        // B chunks of the sets before the current one (as above)
@@ -572,6 +574,73 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
             }
         }
         __syncwarp();
+    } else if (warp == W_MMA) {
+        // grouped launches with K > 2048 leaves: one column set per N tile; N
+        // tile 1 of each tile is deferred DEFER stages behind N tile 0; one
+        // elected lane runs the loop; no lookahead and no B reuse (four chunks
+        // per tile: nothing to reuse; measured 2^18 leaves 68.1 -> 70.0 Gbit/s
+        // against the plain launches' loop)
+        if (elect_one()) {
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0, it = 0;
+            for (TCur c = tcur_first(a); c.t != kNoTile; tcur_next(a, c), ++it) {
+                const Tile ti = tile_info<GROUPED>(a, seed_s, c.t, cur);
+                const uint32_t idesc_full = idesc_mxf4(BM, BN);
+                const uint32_t idesc_last = idesc_mxf4(BM, (int)ti.nlast);
+                const uint32_t ph = (it & 1) ^ 1;
+                mbar_wait(&acc_empty[0], ph);
+                const bool defer = ti.ntc == 2 && ti.kst > (uint32_t)DEFER;
+                if (!defer) mbar_wait(&acc_empty[1], ph);
+                tc_fence_after();
+                bool nt1_on = !defer;
+                uint32_t dslot[DEFER];
+                uint32_t cb0 = 0;
+                for (uint32_t ks = 0; ks < ti.kst; ++ks) {
+                    const uint32_t kin = ks % SPC;
+                    if (kin == 0) { mbar_wait(&b_full[bs], bph); tc_fence_after(); }
+                    mbar_wait(&a_full[as], aph);
+                    tc_fence_after();
+                    const uint32_t cbase = smem_u32(chunks + bs * CHUNK_BYTES);
+                    if (ks == 0) cb0 = cbase;
+                    if (!nt1_on && ks == (uint32_t)DEFER) {
+                        // N tile 1 drained: its MMAs for the held stages, then release them
+                        mbar_wait(&acc_empty[1], ph);
+                        tc_fence_after();
+#pragma unroll
+                        for (int d = 0; d < DEFER; ++d) {
+                            const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + dslot[d] * A_STAGE_BYTES), 128, A_SBO);
+                            const uint64_t bdesc0 = desc_kmajor(cb0 + (d * KS / 8 + BN / 8) * 128, 512, 128);
+#pragma unroll
+                            for (uint32_t kk = 0; kk < KS / 64; ++kk)
+                                mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc0 + kk * 16, bdesc0 + kk * 64, idesc_last,
+                                            tmem + SF_COL, tmem + SF_COL + 8, (d | kk) != 0);
+                            mma_commit(&a_empty[dslot[d]]);
+                        }
+                        nt1_on = true;
+                    }
+                    // first MMA's descriptors; the others add to the start-address field
+                    const uint64_t adesc0 = desc_kmajor(smem_u32(a_ring + as * A_STAGE_BYTES), 128, A_SBO);
+                    const uint64_t bdesc0 = desc_kmajor(cbase + (kin * KS / 8) * 128, 512, 128);
+#pragma unroll
+                    for (uint32_t kk = 0; kk < KS / 64; ++kk) {
+                        const uint64_t adesc = adesc0 + kk * 16, bdesc = bdesc0 + kk * 64;
+                        mma_mxf4_ss(tmem + ACC_COL0, adesc, bdesc, ti.ntc == 1 ? idesc_last : idesc_full,
+                                    tmem + SF_COL, tmem + SF_COL + 8, (ks | kk) != 0);
+                        if (nt1_on && ti.ntc == 2)
+                            mma_mxf4_ss(tmem + ACC_COL0 + BN, adesc, bdesc + BN, idesc_last, tmem + SF_COL,
+                                        tmem + SF_COL + 8, (ks | kk) != 0);
+                    }
+                    if (nt1_on) mma_commit(&a_empty[as]);
+                    if (kin == SPC - 1 || ks == ti.kst - 1) mma_commit(&b_empty[bs]);
+                    if (!nt1_on) dslot[ks] = as;
+                    if (++as == A_STAGES) { as = 0; aph ^= 1; }
+                    if (kin == SPC - 1 || ks == ti.kst - 1) {
+                        if (++bs == B_SLOTS) { bs = 0; bph ^= 1; }
+                    }
+                }
+                mma_commit(&acc_full[0]);
+            }
+        }
+        __syncwarp();
     } else if (warp >= W_BGEN0 && warp < W_BGEN0 + N_BGEN) {
         // B generators: core matrix tau of chunk (n0, k0): row r' holds seed bits
         // s[n0 + k0 + 8 tau + r' + c], c = 0..31, as E2M1 0/1.
@@ -581,7 +650,7 @@ __global__ void __launch_bounds__(nthreads_for(NBG), 1) toeplitz_gemm_kernel(Arg
         bool have_prev = false;
         for (TCur c = tcur_first(a); c.t != kNoTile; tcur_next(a, c)) {
             const Tile ti = tile_info<GROUPED>(a, seed_s, c.t, cur);
-            const bool reuse = have_prev && same_b(pti, ti);
+            const bool reuse = (PACKED || !GROUPED) && have_prev && same_b(pti, ti);  // (as the MMA loops)
             pti = ti;
             have_prev = true;
             if (reuse) continue;  // the MMA issuer reads the previous tile's chunks again

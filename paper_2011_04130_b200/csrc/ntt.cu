@@ -250,10 +250,11 @@ struct Level {
     __device__ static __forceinline__ void load(uint32_t (&x)[N1], int u, uint32_t *data,
                                                 const FusedArgs &a, uint64_t b0, int nb) {
         if (LV == 0 && MODE != FUSED) {  // segment already in shared memory
+{
+    const int pb = pbase(u);
 #pragma unroll
-            { const int pb = pbase(u);
-#pragma unroll
-            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
+    for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
+}
         } else if (LV == 0 && STRIDE >= 32) {
             // the warp holds u = u0..u0+31 (u0 % 32 == 0): for each q it needs one
             // 32-bit raw word (idx = q*STRIDE + u0 .. +31).  Lane q fetches word q.
@@ -288,10 +289,11 @@ struct Level {
                 x[q] = v;
             }
         } else {
+{
+    const int pb = pbase(u);
 #pragma unroll
-            { const int pb = pbase(u);
-#pragma unroll
-            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
+    for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
+}
         }
     }
 
@@ -309,7 +311,7 @@ struct Level {
     __device__ static __forceinline__ void emit(uint32_t (&x)[N1], int u, uint32_t *stage,
                                                 const FusedArgs &a, uint64_t b0, int nb,
                                                 uint64_t wfirst) {
-        if (STRIDE >= 32) {
+        if constexpr (STRIDE >= 32) {
             // lanes hold 32 consecutive t for every q: one ballot per q gives a
             // 32-bit output word; lane q keeps word q and ORs it into the stage.
             const int lane = threadIdx.x & 31, u0 = u & ~31;
@@ -340,25 +342,25 @@ struct Level {
                     }
                 }
             }
-            return;
-        }
+        } else {
 #pragma unroll
-        for (int q = 0; q < N1; ++q) {
-            const uint32_t t = (uint32_t)(q * STRIDE + u);
-            int64_t i = (int64_t)t - (int64_t)(a.len - 1);
-            if (i >= 0 && i < (int64_t)a.m) {
-                uint32_t z = x[q] >= P ? x[q] - P : x[q];  // canonical residue
-                if (a.xor_tail) {
-                    z ^= raw_bit(a.raw, b0, a.n, t + 1);
-                    if (PACK && nb > 1) z ^= raw_bit(a.raw, b0 + 1, a.n, t + 1) << a.shift;
-                }
-                if (z & 1u) {
-                    uint64_t g = b0 * a.m + (uint64_t)i;
-                    atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
-                }
-                if (PACK && nb > 1 && ((z >> a.shift) & 1u)) {
-                    uint64_t g = (b0 + 1) * a.m + (uint64_t)i;
-                    atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
+            for (int q = 0; q < N1; ++q) {
+                const uint32_t t = (uint32_t)(q * STRIDE + u);
+                int64_t i = (int64_t)t - (int64_t)(a.len - 1);
+                if (i >= 0 && i < (int64_t)a.m) {
+                    uint32_t z = x[q] >= P ? x[q] - P : x[q];  // canonical residue
+                    if (a.xor_tail) {
+                        z ^= raw_bit(a.raw, b0, a.n, t + 1);
+                        if (PACK && nb > 1) z ^= raw_bit(a.raw, b0 + 1, a.n, t + 1) << a.shift;
+                    }
+                    if (z & 1u) {
+                        uint64_t g = b0 * a.m + (uint64_t)i;
+                        atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
+                    }
+                    if (PACK && nb > 1 && ((z >> a.shift) & 1u)) {
+                        uint64_t g = (b0 + 1) * a.m + (uint64_t)i;
+                        atomicOr(&stage[(g >> 5) - wfirst], 0x80000000u >> (g & 31));
+                    }
                 }
             }
         }
@@ -376,10 +378,11 @@ struct Level {
             if (!LAST) {
                 const int n2 = u % STRIDE;
                 if (n2) twiddle<R, F>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
+                {
+                    const int pb = pbase(u);
 #pragma unroll
-                { const int pb = pbase(u);
-#pragma unroll
-                for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q]; }
+                    for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q];
+                }
             } else if (MODE == SEGFWD) {
                 uint32_t *dst = const_cast<uint32_t *>(a.shat) + (size_t)u * N1;
 #pragma unroll
@@ -398,10 +401,9 @@ struct Level {
                 dft_inv<R, F>(x);
                 if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
                 else {
+                    const int pb = pbase(u);
 #pragma unroll
-                    { const int pb = pbase(u);
-#pragma unroll
-                for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q]; }
+                    for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q];
                 }
             }
         }
@@ -415,19 +417,21 @@ struct Level {
             const int u = (int)threadIdx.x + it * T;
             if (NSUB % T != 0 && u >= NSUB) break;
             uint32_t x[N1];
+{
+    const int pb = pbase(u);
 #pragma unroll
-            { const int pb = pbase(u);
-#pragma unroll
-            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)]; }
+    for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
+}
             const int n2 = u % STRIDE;
             if (n2) twiddle<R, F>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
             dft_inv<R, F>(x);
             if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
             else {
+                {
+                    const int pb = pbase(u);
 #pragma unroll
-                { const int pb = pbase(u);
-#pragma unroll
-                for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q]; }
+                    for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q];
+                }
             }
         }
         __syncthreads();
@@ -476,10 +480,11 @@ __global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
     FusedArgs b = a;
     b.shat = a.shat + seg * NS;
     run_levels<LOGS, 0, false, MODE, F>(data, nullptr, b, 0, 1, 0);
-    if (MODE == SEGFWD) return;
-    for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4)
-        *reinterpret_cast<uint4 *>(src + i) =
-            make_uint4(data[pidx(i)], data[pidx(i + 1)], data[pidx(i + 2)], data[pidx(i + 3)]);
+    if constexpr (MODE != SEGFWD) {
+        for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4)
+            *reinterpret_cast<uint4 *>(src + i) =
+                make_uint4(data[pidx(i)], data[pidx(i + 1)], data[pidx(i + 2)], data[pidx(i + 3)]);
+    }
 }
 
 struct PassArgs {
@@ -831,13 +836,6 @@ static qrng_status launch_segments(const FusedArgs &a, uint32_t *ws, int logP, u
     t.stop();
     QRNG_CUDA_TRY(cudaGetLastError());
     return QRNG_OK;
-}
-
-// Workspace words per multi-pass batch (L2-sized batches keep the passes on chip).
-static uint64_t batch_blocks(int logP, uint64_t n_blocks) {
-    uint64_t cap = (1ull << 24) >> logP;
-    if (cap < 1) cap = 1;
-    return cap < n_blocks ? cap : n_blocks;
 }
 
 template <int F>
