@@ -166,6 +166,9 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+PATH_NAMES = {1: "gemm", 2: "ntt", 3: "bits"}
+
+
 def algorithmic_work(q, path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False,
                      macs_per_block: int = 0):
     """Roofline numerators, per step of the main kernel(s)."""
@@ -173,6 +176,9 @@ def algorithmic_work(q, path: int, w: S.Workload, n_blocks: int, pack: bool, mod
         # tensor-core ops (E2M1 or int8): 2 x the leaf MACs of the Karatsuba
         # decomposition (= 2 m n per block for the dense product, depth 0)
         return 2.0 * (macs_per_block or w.m * w.n) * n_blocks, "tensor", "TOPS"
+    if path == q.PATH_BITS:
+        # the CUDA-core product: m n bit-MACs (AND + XOR) per block
+        return float(w.m) * w.n * n_blocks, "alu", "Tbit-MAC/s"
     L = (w.n - 1) if modified else (w.n + w.m - 1)
     P = 1 << max(5, math.ceil(math.log2(L)))
     transforms = (n_blocks + 1) // 2 if pack else n_blocks
@@ -198,6 +204,15 @@ def ntt_two_blocks(w: S.Workload, modified: bool) -> bool:
     L = (w.n - 1) if modified else (w.n + w.m - 1)
     k = n_len.bit_length()
     return L <= (1 << 15) and n_len * ((1 << k) + 1) < 998244353
+
+
+def bits_peak_tmacs(pk):
+    # the CUDA-core product's bound: bits.cu's unrolled loop issues 2 LDS.32
+    # (seed window word, block word), 1 SHF, 1 LOP3 + 1.25 of loop overhead per
+    # 32 bit-MACs per lane; the two shared-memory loads (one wavefront each: the
+    # lanes read at most a few distinct words) at 1 per clock per SM bind before
+    # the issue slots: 32 lanes x 32 MACs / 2 clocks per SM, 148 SMs, max SM clock
+    return 148 * pk.get("sm_max_mhz", 1965.0) * 1e6 * 32 * 32 / 2 / 1e12
 
 
 def alu_peak_gbfly(pk):
@@ -406,9 +421,12 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    oneshot_path = q.last_path()  # the product path the one-shot step ran (small batches: CUDA cores)
     with q.Plan(w.n, w.m, seed, modified=modified) as pl:
         path = pl.path
         pinfo = pl.info()
+    if oneshot_path == q.PATH_BITS:
+        path = q.PATH_BITS
     pack = ntt_two_blocks(w, modified)
 
     def timed_pass(kernel_events):
@@ -508,13 +526,14 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
         "ms_per_step_max_rank0": max(per_step),
         "steady_state": steady, "roofline": roof, "parity": parity, "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "dtype": "u8 bits; int32 mod-p NTT" if path == q.PATH_NTT else (
+        "dtype": "u8 bits; int32 mod-p NTT" if path == q.PATH_NTT else
+                 "u8 bits; 32-bit AND / XOR / popcount on the CUDA cores" if path == q.PATH_BITS else (
             "u8 bits; E2M1 0/1 x E2M1 -> fp32 tensor core (kind::mxf4, unit scales, exact)"
             if q.gemm_operand_bits() == 4 else "u8 bits; int8 x int8 -> int32 tensor core"),
         "config": {"workload": w.name, "n": w.n, "m": w.m, "blocks_total": B_total,
                    "blocks_per_gpu": w.n_blocks if scaling == "weak" else f"~{w.n_blocks / W:g}",
                    "blocks_rank0": B, "seed_bits": w.n if modified else w.seed_bits,
-                   "raw_bits_total": B_total * w.n, "path": {1: "gemm", 2: "ntt"}[path],
+                   "raw_bits_total": B_total * w.n, "path": PATH_NAMES[path],
                    "two_blocks_per_transform": bool(pack and path == q.PATH_NTT),
                    "karatsuba_depth": pinfo["karatsuba_depth"] if path == q.PATH_GEMM else None,
                    "karatsuba_leaves": pinfo["leaves"] if path == q.PATH_GEMM else None,
@@ -615,6 +634,12 @@ def roofline(q, args, w, B, path, pack, modified, pinfo, kern_ms, kern_n, ms_tot
         roof["ops_per_step"] = work
         roof["dense_ops_per_step"] = 2.0 * w.m * w.n * B  # the O(mn) product without Karatsuba
         roof["dense_equivalent_frac"] = roof["dense_ops_per_step"] / per_step_s / 1e12 / peak
+    elif path == q.PATH_BITS:
+        achieved = work / per_step_s / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": bits_peak_tmacs(pk), "unit": unit,
+                "peak_kind": "derived shared-memory load bound of bits.cu's loop (2 LDS.32 per 32 bit-MACs "
+                             "per lane, 1 LDS per clock per SM, 148 SMs at the max SM clock)",
+                "note": "a small batch: latency-bound (launch, seed staging, one pass), not issue-bound"}
     else:
         # multi-pass batches overlap on two streams: the summed per-launch
         # times then exceed the step, so the butterflies are divided by the
@@ -631,7 +656,7 @@ def roofline(q, args, w, B, path, pack, modified, pinfo, kern_ms, kern_n, ms_tot
         roof["pass_rate_peak"] = q.butterfly_rate(with_twiddles=True) / 1e9
         roof["frac_of_pass_rate"] = achieved / roof["pass_rate_peak"]
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"], roof["traffic_source"] = ncu_traffic(w.name, {1: "gemm", 2: "ntt"}[path])
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(w.name, PATH_NAMES[path])
     roof["kernel_ms_per_step"] = kern_ms / args.steps  # summed per-launch device times
     roof["kernel_launches_per_step"] = kern_n / args.steps
     roof["kernel_share_of_step"] = (kern_ms / args.steps) / (ms_total_kt / args.steps)
@@ -870,7 +895,7 @@ def run_ours(args):
     import paper_2011_04130_b200 as q
     q.load_library()
     if args.path != "auto":
-        q.set_debug_path({"gemm": q.PATH_GEMM, "ntt": q.PATH_NTT}[args.path])
+        q.set_debug_path({"gemm": q.PATH_GEMM, "ntt": q.PATH_NTT, "bits": q.PATH_BITS}[args.path])
     q.set_karatsuba(args.karatsuba)
     head = measure(q, ctx, args, args.config, headline=True,
                    cpu_budget=0 if args.no_cpu_baseline else args.cpu_budget)
@@ -1015,7 +1040,7 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="multi-GPU partition (default: weak for configs 1-4, strong for config 5)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--path", choices=["auto", "gemm", "ntt"], default="auto")
+    ap.add_argument("--path", choices=["auto", "gemm", "ntt", "bits"], default="auto")
     ap.add_argument("--variant", choices=["standard", "modified"], default="standard",
                     help="modified = [T | I_m] with an n-bit seed (PAPER.md:253-267, NEXT-1)")
     ap.add_argument("--karatsuba", type=int, default=-1,

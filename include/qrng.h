@@ -50,7 +50,12 @@ typedef enum {
 } qrng_status;
 
 /* Extraction path.  AUTO picks by n (crossover measured on B200). */
-typedef enum { QRNG_PATH_AUTO = 0, QRNG_PATH_GEMM = 1, QRNG_PATH_NTT = 2 } qrng_path;
+/* QRNG_PATH_BITS: the product on the CUDA cores, one lane per output bit
+ * (parity of popcount(seed window AND reversed block), bits.cu) -- what AUTO
+ * runs for small batches of a dense-GEMM shape (n m n_blocks up to 6e8 bit-MACs
+ * at n <= 1024, 6e8 + 2.7e8 log2(n/1024) above: where the tensor-core kernel
+ * is latency-bound); n % 32 == 0. */
+typedef enum { QRNG_PATH_AUTO = 0, QRNG_PATH_GEMM = 1, QRNG_PATH_NTT = 2, QRNG_PATH_BITS = 3 } qrng_path;
 
 /* Ideal ADC model: Gaussian N(mu, sigma^2) discretised on bins [k-1/2, k+1/2),
  * edge bins absorbing the tails (reading A10).  sigma > 0. */
@@ -233,11 +238,17 @@ QRNG_API qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uin
 QRNG_API qrng_status qrng_modified_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_blocks,
                                                           uint64_t n, uint64_t m, const uint8_t *d_seed,
                                                           uint8_t *d_out, cudaStream_t stream);
-/* Path the plan runs (QRNG_PATH_GEMM or QRNG_PATH_NTT); -1 for NULL. */
+/* Path the plan runs (QRNG_PATH_GEMM, QRNG_PATH_NTT or a forced
+ * QRNG_PATH_BITS); -1 for NULL.  An AUTO plan with QRNG_PATH_GEMM and no
+ * Karatsuba tree runs small batches (see QRNG_PATH_BITS) on the CUDA cores;
+ * qrng_debug_last_path tells which ran. */
 QRNG_API int         qrng_plan_path(const qrng_plan *plan);
+/* BENCH / TEST ONLY: product path of the most recent extraction in this
+ * process (QRNG_PATH_*), -1 before the first. */
+QRNG_API int         qrng_debug_last_path(void);
 
 /* How a plan computes its product (for benchmarks and tests).
- *   path                 QRNG_PATH_GEMM or QRNG_PATH_NTT
+ *   path                 QRNG_PATH_GEMM, QRNG_PATH_NTT or QRNG_PATH_BITS
  *   karatsuba_depth      GEMM path: depth of the GF(2) Karatsuba decomposition
  *                        (0 = one dense product); see qrng_debug_set_karatsuba
  *   leaves               GEMM path: Toeplitz products the tensor cores run
@@ -262,8 +273,10 @@ QRNG_API const char *qrng_last_error(void);
 QRNG_API const char *qrng_version(void);
 
 /* TEST ONLY: force the path of plans created afterwards on this process
- * (QRNG_PATH_AUTO restores the measured crossover).  Used to cross-check the
- * two independent GPU paths and to measure the crossover; not a backend switch. */
+ * (QRNG_PATH_AUTO restores the measured crossover; QRNG_PATH_BITS needs
+ * n % 32 == 0 and a seed of at most ~1.6e6 bits, else E_UNSUPPORTED).  Used to
+ * cross-check the independent GPU paths and to measure the crossovers; not a
+ * backend switch. */
 QRNG_API void        qrng_debug_set_path(int path);
 
 /* TEST / BENCH ONLY: depth of the GF(2) Karatsuba decomposition used by GEMM-path

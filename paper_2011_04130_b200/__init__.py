@@ -23,14 +23,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QRNG_LIB_PATH") or os.path.join(_HERE, "libqrng.so")
 
 QRNG_OK, QRNG_E_INVALID, QRNG_E_UNSUPPORTED, QRNG_E_NO_OUTPUT, QRNG_E_CUDA, QRNG_E_NOMEM = range(6)
-PATH_AUTO, PATH_GEMM, PATH_NTT = 0, 1, 2
+PATH_AUTO, PATH_GEMM, PATH_NTT, PATH_BITS = 0, 1, 2, 3
 STATUS_NAMES = {0: "QRNG_OK", 1: "QRNG_E_INVALID", 2: "QRNG_E_UNSUPPORTED", 3: "QRNG_E_NO_OUTPUT",
                 4: "QRNG_E_CUDA", 5: "QRNG_E_NOMEM"}
 
 # Every symbol include/qrng.h declares (checked by tests/test_abi.py).
 EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_toeplitz_extract", "qrng_toeplitz_extract_async", "qrng_toeplitz_extract_host",
-           "qrng_plan_create", "qrng_plan_extract", "qrng_plan_destroy", "qrng_plan_path",
+           "qrng_plan_create", "qrng_plan_extract", "qrng_plan_destroy", "qrng_plan_path", "qrng_debug_last_path",
            "qrng_plan_create_modified", "qrng_modified_toeplitz_extract_async",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_modified_toeplitz_extract_async": ([vp, u64, u64, u64, vp, vp, vp], i32),
         "qrng_plan_destroy": ([vp], None),
         "qrng_plan_path": ([vp], i32),
+        "qrng_debug_last_path": ([], i32),
         "qrng_last_error": ([], ctypes.c_char_p),
         "qrng_version": ([], ctypes.c_char_p),
         "qrng_debug_set_path": ([i32], None),
@@ -206,7 +207,7 @@ def last_error() -> str:
 
 
 def set_debug_path(path: int) -> None:
-    """TEST ONLY: force QRNG_PATH_GEMM / QRNG_PATH_NTT for plans created afterwards."""
+    """TEST ONLY: force QRNG_PATH_GEMM / QRNG_PATH_NTT / QRNG_PATH_BITS for plans created afterwards."""
     load_library().qrng_debug_set_path(int(path))
 
 
@@ -252,6 +253,11 @@ def gemm_trace(reset: bool = True) -> np.ndarray:
     c = np.zeros(8 * 768, np.uint64)
     _check(load_library().qrng_debug_gemm_trace(c.ctypes.data, 1 if reset else 0))
     return c.reshape(-1, 8)
+
+
+def last_path() -> int:
+    """BENCH/TEST ONLY: product path (PATH_*) of the most recent extraction."""
+    return int(load_library().qrng_debug_last_path())
 
 
 def launch_count() -> int:

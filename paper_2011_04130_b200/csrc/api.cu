@@ -114,6 +114,22 @@ void KernelTimer::stop() {
 // Measured GEMM/NTT crossover in n; GEMM for n <= this.
 static uint64_t g_gemm_max_n = 1ull << 18;  // profiles/sweep_r1u.jsonl (E2M1 operands): Karatsuba GEMM 68.5 vs NTT 48.5 Gbit/s at 2^18, 40.6 vs 47.5 at 2^19
 static std::atomic<int> g_debug_path{QRNG_PATH_AUTO};
+static std::atomic<int> g_last_path{-1};  // product path of the most recent extraction (bench labels)
+// Small batches on the CUDA cores (bits.cu) instead of the dense tcgen05 kernel
+// when an AUTO plan's batch has at most bits_max_macs(n) bit-MACs (n m n_blocks).
+// Measured (tools/bits_crossover.py, one-shot device time, L2 flushed): the
+// CUDA-core kernel takes ~8 us + 8.4 ns per 1e6 bit-MACs whatever n; the
+// tcgen05 kernel's small-batch floor grows with n (13.3 / 15.4 / 17.4 us at
+// n = 1024 / 2048 / 4096), so the crossover is 6e8 / 8.8e8 / 1.1e9 bit-MACs:
+// 6e8 + 2.7e8 log2(n / 1024), at least 6e8.  QRNG_BITS_MAX_MACS overrides.
+static double bits_max_macs(uint64_t n) {
+    static const double v = [] {
+        const char *e = getenv("QRNG_BITS_MAX_MACS");
+        return (e && *e) ? atof(e) : -1.0;
+    }();
+    if (v >= 0) return v;
+    return n <= 1024 ? 6.0e8 : 6.0e8 + 2.7e8 * std::log2((double)n / 1024.0);
+}
 // Karatsuba depth over the GEMM path: -1 = the planner's cost model, 0 = plain
 // GEMM kernel, d > 0 = split whenever allowed down to depth d (tests).
 static std::atomic<int> g_kara_depth{-1};
@@ -176,6 +192,7 @@ using namespace qrng;
 struct qrng_plan {
     uint64_t n = 0, m = 0;
     int path = QRNG_PATH_NTT;
+    bool auto_path = false;  // chosen by the scheduler (not forced): small batches may run on the CUDA cores
     bool kara_on = false;  // GEMM path through the Karatsuba decomposition
     bool modified = false;  // modified Toeplitz [T | I_m] (n-bit seed)
     const uint8_t *direct_seed = nullptr;  // one-shot dense GEMM: the caller's seed, read by the kernel itself
@@ -267,6 +284,7 @@ double qrng_debug_kernel_time_split(double *aux_ms, uint64_t *launches, uint64_t
 double qrng_debug_kernel_time_ms(uint64_t *launches) { return qrng_debug_kernel_time_split(nullptr, launches, nullptr); }
 
 int qrng_plan_path(const qrng_plan *plan) { return plan ? plan->path : -1; }
+int qrng_debug_last_path(void) { return g_last_path.load(); }
 
 void qrng_debug_set_karatsuba(int max_depth) { g_kara_depth.store(max_depth < -1 ? -1 : max_depth); }
 
@@ -299,6 +317,14 @@ static qrng_status resolve_path(uint64_t n, uint64_t m, int *path, bool *kara_on
     int want = g_debug_path.load();
     const bool automatic = want == QRNG_PATH_AUTO;
     *kara_on = false;
+    if (want == QRNG_PATH_BITS) {
+        if (!bits::supported(n, m)) {
+            set_error("CUDA-core path does not support n=%llu, m=%llu", (unsigned long long)n, (unsigned long long)m);
+            return QRNG_E_UNSUPPORTED;
+        }
+        *path = want;
+        return QRNG_OK;
+    }
     if (automatic) want = (n % 128 == 0 && n <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
     if (want == QRNG_PATH_GEMM) *kara_on = kara::choose(n, m, g_kara_depth.load());
     // AUTO: a shape the planner leaves undecomposed (small m at large n) that the
@@ -340,8 +366,10 @@ static qrng_status plan_create(uint64_t n, uint64_t m, const uint8_t *d_seed, cu
     p->m = m;
     p->kara_on = kara_on;
     p->path = want;
+    p->auto_path = g_debug_path.load() == QRNG_PATH_AUTO;
     const int kd = g_kara_depth.load();
-    st = (want == QRNG_PATH_NTT) ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
+    st = (want == QRNG_PATH_NTT)    ? ntt::plan_init(p->ntt, n, m, d_seed, 0, false, stream)
+         : (want == QRNG_PATH_BITS) ? bits::plan_init(p->gemm, n, m, d_seed, stream)
          : p->kara_on            ? kara::plan_init(p->kara, n, m, kd, d_seed, stream, oneshot)
                                  : gemm::plan_init(p->gemm, n, m, d_seed, stream);
     if (st != QRNG_OK) { plan_release(p, stream, true); return st; }
@@ -364,6 +392,10 @@ qrng_status qrng_plan_create_modified(uint64_t n, uint64_t m, const uint8_t *d_s
     if (n - 1 > (1ull << ntt::kMaxLogP)) { set_error("n - 1 exceeds 2^23"); return QRNG_E_UNSUPPORTED; }
     if (!d_seed || !aligned16(d_seed)) { set_error("d_seed is NULL or not 16-byte aligned"); return QRNG_E_INVALID; }
     int want = g_debug_path.load();
+    if (want == QRNG_PATH_BITS) {
+        set_error("modified Toeplitz: no CUDA-core path (QRNG_PATH_BITS)");
+        return QRNG_E_UNSUPPORTED;
+    }
     const uint64_t kprod = (n - m + 127) / 128 * 128;  // GEMM product length (n - m rounded up to 128)
     if (want == QRNG_PATH_AUTO) want = (gemm::modified_supported(n, m) && kprod <= g_gemm_max_n) ? QRNG_PATH_GEMM : QRNG_PATH_NTT;
     if (want == QRNG_PATH_GEMM && !gemm::modified_supported(n, m)) {
@@ -430,10 +462,19 @@ qrng_status qrng_plan_extract(const qrng_plan *plan, const uint8_t *d_raw_bits, 
         if (e != cudaSuccess) { set_error("cudaMallocAsync: %s", cudaGetErrorString(e)); return QRNG_E_NOMEM; }
         QRNG_CUDA_TRY(cudaMemsetAsync(o.tail, 0, 4, stream));
     }
-    // the Karatsuba pack kernel writes every output word once; the other
-    // epilogues OR the words they share with a neighbouring tile / CTA
-    if (!(plan->path == QRNG_PATH_GEMM && plan->kara_on)) QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
-    qrng_status st = (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
+    // small batches of a dense AUTO plan run on the CUDA cores (latency-bound on
+    // the tensor cores; bits.cu)
+    const bool use_bits = plan->path == QRNG_PATH_BITS ||
+                          (plan->auto_path && plan->path == QRNG_PATH_GEMM && !plan->kara_on && !plan->modified &&
+                           bits::supported(n, m) && (double)n * (double)m * (double)n_blocks <= bits_max_macs(n));
+    g_last_path.store(use_bits ? QRNG_PATH_BITS : plan->path);
+    // the Karatsuba pack and CUDA-core kernels write every output word once; the
+    // other epilogues OR the words they share with a neighbouring tile / CTA
+    if (!use_bits && !(plan->path == QRNG_PATH_GEMM && plan->kara_on))
+        QRNG_CUDA_TRY(cudaMemsetAsync(d_out, 0, out_bytes, stream));
+    qrng_status st = use_bits ? bits::extract(plan->direct_seed ? nullptr : plan->gemm.seed_words, plan->direct_seed,
+                                              d_raw_bits, n_blocks, n, m, o, stream)
+                     : (plan->path == QRNG_PATH_NTT) ? ntt::extract(plan->ntt, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->kara_on ? kara::extract(plan->kara, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->modified ? gemm::extract_modified(plan->gemm, d_raw_bits, n_blocks, n, m, o, stream)
                      : plan->direct_seed ? gemm::extract_direct(plan->direct_seed, d_raw_bits, n_blocks, n, m, o, stream)
@@ -463,14 +504,16 @@ qrng_status qrng_toeplitz_extract_async(const uint8_t *d_raw_bits, uint64_t n_bl
     int path = 0;
     bool kara_on = false;
     if ((st = resolve_path(n, m, &path, &kara_on)) != QRNG_OK) return st;
-    if (path == QRNG_PATH_GEMM && !kara_on) {
-        // dense tensor-core product: no plan buffers or seed kernel; the GEMM
-        // kernel forms the seed words from d_seed in its prologue (small batches
-        // are latency-bound: this removes an allocation, a launch and a free)
+    if ((path == QRNG_PATH_GEMM && !kara_on) || path == QRNG_PATH_BITS) {
+        // dense product (tensor cores, or the CUDA cores for a small batch): no
+        // plan buffers or seed kernel; the kernel forms the seed words from d_seed
+        // in its prologue (small batches are latency-bound: this removes an
+        // allocation, a launch and a free)
         qrng_plan direct;
         direct.n = n;
         direct.m = m;
-        direct.path = QRNG_PATH_GEMM;
+        direct.path = path;
+        direct.auto_path = g_debug_path.load() == QRNG_PATH_AUTO;
         direct.direct_seed = d_seed;
         return qrng_plan_extract(&direct, d_raw_bits, n_blocks, d_out, stream);
     }

@@ -206,6 +206,18 @@ qrng_status mxf4_probe(const uint8_t *A, const uint8_t *h, float *D, int N, int 
 qrng_status mma_rate(int form, int iters, int n, uint64_t *macs, cudaStream_t s);
 }  // namespace gemm
 
+// The product on the CUDA cores for small batches (bits.cu): one lane per
+// output bit, popcount parity of the seed window AND the reversed block.
+namespace bits {
+bool supported(uint64_t n, uint64_t m);
+// seed words (logical big-endian, zero past n + m - 1) into pl.seed_words
+qrng_status plan_init(gemm::Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, cudaStream_t s);
+// seed from d_seed_words (a plan's) or, if null, straight from the caller's bytes;
+// every output word is written once (no pre-zeroed output needed)
+qrng_status extract(const uint32_t *d_seed_words, const uint8_t *d_seed_bytes, const uint8_t *d_raw,
+                    uint64_t n_blocks, uint64_t n, uint64_t m, const OutStream &out, cudaStream_t s);
+}  // namespace bits
+
 // Karatsuba decomposition over the GEMM path (karatsuba.cu).
 namespace kara {
 struct Tables;  // device-resident leaf / term / combine tables, cached per (n, m, depth)

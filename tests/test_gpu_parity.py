@@ -48,11 +48,11 @@ def assert_same(got, ref, m):
                              f"(block {bad[0] // m}, i {bad[0] % m})")
 
 
-PATHS = ["ntt", "gemm"]
+PATHS = ["ntt", "gemm", "bits"]  # bits: the CUDA-core product AUTO uses for small batches
 
 
 def path_id(q, name):
-    return {"ntt": q.PATH_NTT, "gemm": q.PATH_GEMM}[name]
+    return {"ntt": q.PATH_NTT, "gemm": q.PATH_GEMM, "bits": q.PATH_BITS}[name]
 
 
 SMALL_CASES = [

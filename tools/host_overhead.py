@@ -1,10 +1,11 @@
 #!/usr/bin/env python
-"""Host-side cost per C-ABI call (enqueue time without synchronisation) vs the wall time per call, one-shot and plan-reused, config 2."""
+"""Host-side cost per C-ABI call (enqueue time without synchronisation) vs the wall time per call, one-shot and plan-reused
+(python tools/host_overhead.py [CONFIG], default config 2)."""
 import time, torch, sys
 sys.path.insert(0, '/root/repo')
 import qrng_synth as S, paper_2011_04130_b200 as q
 q.load_library()
-w = S.CONFIGS[2]
+w = S.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 raw_np, seed_np = S.workload_inputs(w)
 raw, seed = torch.from_numpy(raw_np).cuda(), torch.from_numpy(seed_np).cuda()
 out = torch.empty(q.out_bytes(w.n_blocks, w.m), dtype=torch.uint8, device="cuda")
