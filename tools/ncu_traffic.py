@@ -13,12 +13,12 @@ tag, reps = sys.argv[1], sys.argv[2:]
 out = {}
 for rep in reps:
     name = os.path.basename(rep)[len(tag) + 1:-len(".ncu-rep")]  # e.g. gemm_cfg2, ntt_segment_cfg5_n2^19
-    m = re.match(r"(gemm|ntt_segment|ntt_pass)_(cfg\d+|next4)(?:_(n2\^\d+))?$", name)
+    m = re.match(r"(gemm|bits|ntt_segment|ntt_pass)_(cfg\d+|next4)(?:_(n2\^\d+))?$", name)
     if not m:
         continue
     kind, cfg, pt = m.groups()
     wl = f"cfg5_{pt}" if pt else WORKLOAD[cfg]
-    path = "gemm" if kind == "gemm" else "ntt"
+    path = kind if kind in ("gemm", "bits") else "ntt"
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(txt.splitlines()))
     h, u, v = r[0], r[1], r[2]  # names, units, values

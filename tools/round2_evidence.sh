@@ -21,7 +21,7 @@ cap() {  # name config kernel-regex [source]
   echo "$1 rc=$?"
 }
 cap gemm_cfg2 2 toeplitz_gemm_kernel src
-cap gemm_cfg1 1 toeplitz_gemm_kernel
+cap bits_cfg1 1 bits_kernel
 cap gemm_cfg3 3 toeplitz_gemm_kernel
 cap ntt_segment_cfg4 4 ntt_segment_kernel
 cap ntt_pass_cfg4 4 ntt_pass_kernel
@@ -37,7 +37,7 @@ for f in gpurun_out/${T}_*.ncu-rep; do echo "== $f"; python tools/ncu_summary.py
 python tools/ncu_traffic.py $T gpurun_out/${T}_*.ncu-rep > gpurun_out/${T}_ncu_traffic.json
 # keep the headline capture (with source) and the NTT segment capture; the rest
 # live on as summaries + traffic (gpurun copies back at most 64 MiB)
-for f in gpurun_out/${T}_*.ncu-rep; do case $f in *gemm_cfg2*|*ntt_segment_cfg4*) ;; *) rm -f "$f";; esac; done
+for f in gpurun_out/${T}_*.ncu-rep; do case $f in *gemm_cfg2*|*ntt_segment_cfg4.*) ;; *) rm -f "$f";; esac; done
 ls -la gpurun_out/
 python - gpurun_out/bench_default_$T.json <<'PY'
 import json, sys
