@@ -951,25 +951,31 @@ __global__ void __launch_bounds__(QRNG_CSR_THREADS) csr_stream_pack_kernel(const
                     off[e] = (uint32_t)e < c ? 4 * Cs[ywords + e * ywords + kk] : 0u;
                     msk[e] = (uint32_t)e < c ? ~0u : 0u;
                 }
-                const uint32_t rstep = sets * y_stride * 4;
-                uint32_t row = ys_sa + set * y_stride * 4;
-                for (uint32_t bl = set; bl < nb; bl += sets, row += rstep) {
+                const uint32_t rstep = sets * y_stride * 4, sstep = sets * m, kk32 = 32 * kk;
+                const bool active = lane != 31 && kk < wpb;  // lane 31 only feeds lane 30
+                // whole group inside the buffer's full words: plain stores, no per-word check
+                const bool fast = (b0 * m + (uint64_t)nb * m + 31) / 32 <= out.full_words;
+                uint32_t *const ow = out.words + wbase;
+                uint32_t row = ys_sa + set * y_stride * 4, s0 = set * m;  // s0: first bit of block bl in the group
+                for (uint32_t bl = set; bl < nb; bl += sets, row += rstep, s0 += sstep) {
                     uint32_t r0 = 0;
 #pragma unroll
                     for (int e = 0; e < KU; ++e) r0 ^= lds32(row + off[e]) & msk[e];
                     for (uint32_t e = KU; e < c; ++e) r0 ^= lds32(row + 4 * Cs[ywords + e * ywords + kk]);
                     const uint32_t r1 = __shfl_down_sync(0xFFFFFFFFu, r0, 1);  // key word kk + 1
-                    if (lane == 31 || kk >= wpb) continue;
-                    const uint32_t s0 = bl * m, s1 = s0 + m, Wf = (s0 + 31) / 32;
-                    const uint32_t W = Wf + kk;  // kk-th word starting inside block bl
-                    if (32 * W >= s1) continue;
-                    uint32_t word = __funnelshift_l(r1, r0, 32 * Wf - s0);
-                    if (32 * W + 32 > s1) {  // tail of block bl, then the head of block bl + 1
-                        const uint32_t len1 = s1 - 32 * W;
+                    if (!active) continue;
+                    // the kk-th output word starting inside block bl begins at key bit i0
+                    const uint32_t sh = (0u - s0) & 31u, i0 = sh + kk32;
+                    if (i0 >= m) continue;  // block bl has fewer words (other blocks may not)
+                    uint32_t word = __funnelshift_l(r1, r0, sh);
+                    if (i0 + 32 > m) {  // tail of block bl, then the head of block bl + 1
+                        const uint32_t len1 = m - i0;
                         word &= ~(0xFFFFFFFFu >> len1);
                         if (bl + 1 < nb) word |= lds32(rs_sa + (bl + 1) * 4) >> len1;
                     }
-                    emit_word(out, wbase + W, word, true);
+                    const uint32_t W = ((s0 + 31) >> 5) + kk;
+                    if (fast) ow[W] = bswap32(word);
+                    else emit_word(out, wbase + W, word, true);
                 }
             }
             __syncthreads();  // this buffer's rows and the heads are no longer read

@@ -1,5 +1,5 @@
 # The GEMM / NTT kernels of an earlier commit against HEAD, on the same box:
-#   bash tools/hist_ab.sh [COMMIT]      (default cbd8577, the round-2 state before the tile-run work)
+#   [CFGS="2 13 14"] bash tools/hist_ab.sh [COMMIT]   (default cbd8577, the round-2 state before the tile-run work)
 # libqrng_<commit>.so is built from `git archive` of that commit's sources (needs
 # the git metadata: build it here, it travels with the snapshot), loaded via QRNG_LIB_PATH.
 C=${1:-cbd8577}
@@ -14,6 +14,6 @@ if [ ! -f $L ]; then
   [ -z "$GRAFT_REPO_ROOT" ] && { echo "built $L; run this script on the GPU box now"; exit 0; }
 fi
 python -m paper_2011_04130_b200.build > /dev/null || exit 1
-for i in 1 2; do for lib in libqrng_$C.so libqrng.so; do for c in 18 10 1 2 3 4; do
+for i in 1 2; do for lib in libqrng_$C.so libqrng.so; do for c in ${CFGS:-18 10 1 2 3 4}; do
   QRNG_LIB_PATH=$PWD/paper_2011_04130_b200/$lib python bench.py --config $c --configs none --no-e2e --no-cpu-baseline > gpurun_out/h.json 2>/dev/null; python tools/line.py "$lib cfg$c" < gpurun_out/h.json
 done; done; done
