@@ -250,11 +250,9 @@ struct Level {
     __device__ static __forceinline__ void load(uint32_t (&x)[N1], int u, uint32_t *data,
                                                 const FusedArgs &a, uint64_t b0, int nb) {
         if (LV == 0 && MODE != FUSED) {  // segment already in shared memory
-{
-    const int pb = pbase(u);
+            const int pb = pbase(u);
 #pragma unroll
-    for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
-}
+            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
         } else if (LV == 0 && STRIDE >= 32) {
             // the warp holds u = u0..u0+31 (u0 % 32 == 0): for each q it needs one
             // 32-bit raw word (idx = q*STRIDE + u0 .. +31).  Lane q fetches word q.
@@ -289,11 +287,9 @@ struct Level {
                 x[q] = v;
             }
         } else {
-{
-    const int pb = pbase(u);
+            const int pb = pbase(u);
 #pragma unroll
-    for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
-}
+            for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
         }
     }
 
@@ -417,11 +413,11 @@ struct Level {
             const int u = (int)threadIdx.x + it * T;
             if (NSUB % T != 0 && u >= NSUB) break;
             uint32_t x[N1];
-{
-    const int pb = pbase(u);
+            {
+                const int pb = pbase(u);
 #pragma unroll
-    for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
-}
+                for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
+            }
             const int n2 = u % STRIDE;
             if (n2) twiddle<R, F>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
             dft_inv<R, F>(x);
