@@ -208,7 +208,7 @@ static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
         if (async) cudaFreeAsync(ptr, s);
         else cudaFree(ptr);
     };
-    fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.work);
+    fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.l1tw); fr(p->ntt.work);
     fr(p->gemm.seed_words);
     fr(p->kara.seeds);
     delete p;

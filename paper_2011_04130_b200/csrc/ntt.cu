@@ -180,6 +180,20 @@ __device__ __forceinline__ void twiddle(uint32_t (&x)[1 << R], uint32_t tauM) {
     }
 }
 
+// Level-1 twiddles of the 2^15-word segment kernel from shared memory: tab[k * 32 +
+// n2] = (tau^k, floor(tau^k 2^32 / p)) for the sub-DFT with n2 = u % 32 (= the
+// lane: conflict-free 8-byte loads), a 3-instruction Shoup product per element
+// instead of the Montgomery power chain (2 products per element).
+template <int R, int F = 0>
+__device__ __forceinline__ void twiddle_l1(uint32_t (&x)[1 << R], const uint2 *col) {
+    constexpr int N = 1 << R;
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+        const uint2 t = col[k * 32];
+        x[brev(k, R)] = shoup<F>(x[brev(k, R)], t.x, t.y);
+    }
+}
+
 // ---- pass schedule ---------------------------------------------------------
 __host__ __device__ constexpr int np_of(int logP) { return (logP + 4) / 5; }
 __host__ __device__ constexpr int radix_of(int logP, int lv) {
@@ -210,6 +224,7 @@ struct FusedArgs {
     uint32_t scaleM;          // forward-only mode: P^-1 * 2^64 mod p
     uint32_t len;             // raw bits used per block (n, or n - m for the modified Toeplitz)
     uint32_t xor_tail;        // modified Toeplitz: output t also XORs raw bit t + 1 of its block
+    const uint2 *l1tw;        // SEG mode, 2^15-word segments: level-1 Shoup twiddles [dir][k][n2] (or null)
 };
 
 // Level modes: FUSED = one CTA owns a whole transform (bits in, parity bits
@@ -373,7 +388,15 @@ struct Level {
             dft_fwd<R, F>(x);
             if (!LAST) {
                 const int n2 = u % STRIDE;
-                if (n2) twiddle<R, F>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
+                if constexpr (MODE == SEG && LOGP == 15 && LV == 1 && N1 == 32 && STRIDE == 32) {
+                    // stage = the shared-memory level-1 table in SEG mode (null: chains)
+                    if (n2) {
+                        if (stage) twiddle_l1<R, F>(x, reinterpret_cast<const uint2 *>(stage) + n2);
+                        else twiddle<R, F>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
+                    }
+                } else {
+                    if (n2) twiddle<R, F>(x, __ldg(a.tw + ((uint32_t)(n2 << S) << a.tw_shift)));
+                }
                 {
                     const int pb = pbase(u);
 #pragma unroll
@@ -419,7 +442,14 @@ struct Level {
                 for (int q = 0; q < N1; ++q) x[q] = data[pb + poff(q)];
             }
             const int n2 = u % STRIDE;
-            if (n2) twiddle<R, F>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
+            if constexpr (MODE == SEG && LOGP == 15 && LV == 1 && N1 == 32 && STRIDE == 32) {
+                if (n2) {
+                    if (stage) twiddle_l1<R, F>(x, reinterpret_cast<const uint2 *>(stage) + 1024 + n2);
+                    else twiddle<R, F>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
+                }
+            } else {
+                if (n2) twiddle<R, F>(x, __ldg(a.itw + ((uint32_t)(n2 << S) << a.tw_shift)));
+            }
             dft_inv<R, F>(x);
             if (LV == 0 && MODE == FUSED) emit(x, u, stage, a, b0, nb, wfirst);
             else {
@@ -465,6 +495,13 @@ __global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
     uint32_t *data = smem;
     const uint64_t seg = blockIdx.x;
     uint32_t *src = ws + ((uint64_t)blockIdx.y << logP) + seg * NS;
+    // SEG mode: the level-1 twiddle table (2 x 32 x 32 Shoup pairs) after the data
+    uint32_t *tab = nullptr;
+    if (MODE == SEG && LOGS == 15 && a.l1tw) {
+        uint2 *t2 = reinterpret_cast<uint2 *>(smem + pidx(NS));
+        for (int i = threadIdx.x; i < 2048; i += blockDim.x) t2[i] = __ldg(a.l1tw + i);
+        tab = reinterpret_cast<uint32_t *>(t2);
+    }
     for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4) {
         const uint4 v = *reinterpret_cast<const uint4 *>(src + i);
         data[pidx(i)] = v.x;
@@ -475,7 +512,7 @@ __global__ void __launch_bounds__(threads_of(LOGS), 1024 / threads_of(LOGS))
     __syncthreads();
     FusedArgs b = a;
     b.shat = a.shat + seg * NS;
-    run_levels<LOGS, 0, false, MODE, F>(data, nullptr, b, 0, 1, 0);
+    run_levels<LOGS, 0, false, MODE, F>(data, tab, b, 0, 1, 0);
     if constexpr (MODE != SEGFWD) {
         for (int i = threadIdx.x * 4; i < NS; i += blockDim.x * 4)
             *reinterpret_cast<uint4 *>(src + i) =
@@ -627,6 +664,20 @@ __global__ void twiddle_table_kernel(uint32_t *tw, uint32_t *itw, uint32_t Pn, u
         b = mont<F>(b, iwM);
         b = b >= P ? b - P : b;
     }
+}
+
+// The segment kernel's level-1 twiddles (2^15-word segments): l1[dir][k][n2] =
+// (w, floor(w 2^32 / p)), w = w_P^(+-(k n2 2^5) << tw_shift), from the Montgomery tables.
+template <int F = 0>
+__global__ void l1tw_kernel(uint2 *out, const uint32_t *tw, const uint32_t *itw, uint32_t tw_shift, uint32_t Pmask) {
+    constexpr uint32_t P = Fld<F>::P;
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= 2048) return;
+    const uint32_t dir = idx >> 10, k = (idx >> 5) & 31, n2 = idx & 31;
+    const uint32_t e = ((k * n2) << 5 << tw_shift) & Pmask;
+    uint32_t w = mont<F>((dir ? itw : tw)[e], 1u);  // out of Montgomery form, in (0, 2p)
+    w = w >= P ? w - P : w;
+    out[idx] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / P));
 }
 
 // Seed spectrum, fused single-CTA version (P <= 2^15): forward passes only.
@@ -821,7 +872,7 @@ static qrng_status launch_pass(int R, const PassArgs &a, uint64_t nb, cudaStream
 template <int MODE, int F = 0, int LOGS = kSegLog>
 static qrng_status launch_segments(const FusedArgs &a, uint32_t *ws, int logP, uint64_t nb, cudaStream_t s,
                                    bool timed) {
-    const size_t smem = ((size_t)(1 << LOGS) + (1 << LOGS) / 32) * 4;
+    const size_t smem = ((size_t)(1 << LOGS) + (1 << LOGS) / 32) * 4 + ((MODE == SEG && LOGS == 15) ? 2048 * 8 : 0);
     {
         const qrng_status st = allow_max_smem(reinterpret_cast<const void *>(ntt_segment_kernel<LOGS, MODE, F>));
         if (st != QRNG_OK) return st;
@@ -874,6 +925,14 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
         twiddle_table_kernel<0><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
                                                                                        (uint32_t)w, (uint32_t)iw);
     QRNG_CUDA_TRY(cudaGetLastError());
+    if (logP > kMaxFusedLogP && kSegLog == 15) {  // the segment kernel's level-1 twiddles
+        QRNG_CUDA_TRY(cudaMallocAsync(&pl.l1tw, 2048 * sizeof(uint2), s));
+        count_launch();
+        const uint32_t shift = (uint32_t)(logP - kSegLog), mask = (uint32_t)(Pn - 1);
+        if (pl.field) l1tw_kernel<1><<<8, 256, 0, s>>>(pl.l1tw, pl.tw, pl.itw, shift, mask);
+        else l1tw_kernel<0><<<8, 256, 0, s>>>(pl.l1tw, pl.tw, pl.itw, shift, mask);
+        QRNG_CUDA_TRY(cudaGetLastError());
+    }
     count_launch();
     seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_bit_offset, seed_words,
                                                                       nwords);
@@ -943,6 +1002,7 @@ void plan_free(Plan &pl) {
     if (pl.shat) cudaFree(pl.shat);
     if (pl.tw) cudaFree(pl.tw);
     if (pl.itw) cudaFree(pl.itw);
+    if (pl.l1tw) cudaFree(pl.l1tw);
     if (pl.work) cudaFree(pl.work);
     pl = Plan{};
 }
@@ -994,6 +1054,11 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
     fa.tw = pl.tw;
     fa.itw = pl.itw;
     fa.tw_shift = (uint32_t)(logP - kSegLog);
+    static const bool use_l1 = [] {  // QRNG_NTT_L1TW=0: the Montgomery chains at level 1 (A/B)
+        const char *e = getenv("QRNG_NTT_L1TW");
+        return !(e && *e && atoi(e) == 0);
+    }();
+    fa.l1tw = use_l1 ? pl.l1tw : nullptr;
     qrng_status st = QRNG_OK;
     for (uint64_t b0 = 0, it = 0; b0 < n_blocks && st == QRNG_OK; b0 += bb, ++it) {
         const uint64_t nb = (n_blocks - b0) < bb ? (n_blocks - b0) : bb;

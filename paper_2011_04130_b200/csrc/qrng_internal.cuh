@@ -117,6 +117,7 @@ struct Plan {
     uint32_t *shat = nullptr;    // P words: NTT(seed) * P^-1 * 2^32 mod p, DIF order
     uint32_t *tw = nullptr;      // P words: w_P^e * 2^32 mod p
     uint32_t *itw = nullptr;     // P words: w_P^-e * 2^32 mod p
+    uint2 *l1tw = nullptr;       // multi-pass: the segment kernel's level-1 twiddles in Shoup form (ntt.cu)
     uint32_t *work = nullptr;    // multipass scratch (not used by the fused kernel)
     size_t work_words = 0;
 };
