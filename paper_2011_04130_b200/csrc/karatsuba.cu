@@ -43,13 +43,17 @@ namespace kara {
 #endif
 constexpr uint32_t kMinLeafW = 128;   // narrowest leaf the planner creates (one K stage)
 #ifndef QRNG_KARA_MAXLEAVES
-#define QRNG_KARA_MAXLEAVES 1024  // the leaf table is staged in the GEMM kernel's shared memory (32 B per leaf)
+// the leaf table is staged in the GEMM kernel's shared memory (32 B per leaf):
+// 2,187 leaves (3^7) = 70 KB next to the B ring and A stages (~200 KB in all)
+#define QRNG_KARA_MAXLEAVES 2187
 #endif
 constexpr int kMaxLeaves = QRNG_KARA_MAXLEAVES;
 constexpr int kMaxDepth = 10;
 // auto mode: deeper trees spill the leaf parities out of L2 (measured: depth 6
-// loses at n = 2^16, wins at 2^17)
-static int auto_max_depth(uint64_t n) { return n >= (1u << 17) ? 6 : 5; }
+// loses at n = 2^16, wins at 2^17).  At n >= 2^18 depth 7 (the
+// 2048-wide packed leaves, with B reuse across tile runs): 2^18 69.8 -> 77.3
+// Gbit/s (tools/kara_d7_ab.sh)
+static int auto_max_depth(uint64_t n) { return n >= (1u << 18) ? 7 : n >= (1u << 17) ? 6 : 5; }
 
 // ---- planner (host only; no CUDA calls) ------------------------------------
 // Cost model in units of (output row x K) for one M tile of 128 blocks on the
