@@ -390,12 +390,17 @@ struct Tables {
     uint32_t *csr = nullptr;       // device: root word -> Y-row words (counts, then column-major entries)
     uint32_t csr_words = 0;
     uint32_t csr_kmax = 0;         // most entries of one key word
+    // the same flattened tree as runs Z[dst, dst + len) ^= Y[src, src + len),
+    // in batches of runs with disjoint dst ranges (see csr_run_key_kernel)
+    uint4 *runs = nullptr;         // device: {dst, src, len, 0}, batch-major
+    uint32_t *run_ptr = nullptr;   // device: first run of each batch (+ end)
+    uint32_t n_batches = 0, n_runs = 0;
     std::vector<gemm::Leaf> hleaves;
     uint32_t max_leaf_w = 0;       // widest leaf (K) -- the packed-accumulator kernel takes w <= 2048
     ~Tables() {
         // the last owner is the cache or a plan; cudaFree waits for the work that reads them
         for (void *ptr : {(void *)leaves, (void *)terms, (void *)qbufs, (void *)qgen_dev, (void *)inner,
-                          (void *)levels, (void *)unit_node, (void *)csr})
+                          (void *)levels, (void *)unit_node, (void *)csr, (void *)runs, (void *)run_ptr})
             if (ptr) cudaFree(ptr);
     }
 };
@@ -496,6 +501,47 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, std::shared
         t->csr_kmax = kmax;
         if (e == cudaSuccess) e = cudaMalloc(&t->csr, cm.size() * 4);
         if (e == cudaSuccess) e = cudaMemcpy(t->csr, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice);
+        // runs: key word j takes Y word j + d for the entries of each offset d;
+        // maximal stretches of consecutive j with the same d are one run.
+        // Batches: interval partitioning by dst (runs sorted by dst, each into
+        // the first batch that ended before it starts), so runs of one batch
+        // never write the same key word; the batch count is the deepest overlap
+        // (kmax).
+        std::map<int64_t, std::vector<uint32_t>> by_d;
+        for (uint32_t j = 0; j < yw; ++j)
+            for (uint32_t q = H.comb_ptr[j]; q < H.comb_ptr[j + 1]; ++q) by_d[(int64_t)H.comb_idx[q] - j].push_back(j);
+        std::vector<std::array<uint32_t, 3>> rr;  // {dst, src, len}
+        for (const auto &kv : by_d) {
+            const std::vector<uint32_t> &js = kv.second;
+            for (size_t i = 0; i < js.size();) {
+                size_t k = i + 1;
+                while (k < js.size() && js[k] == js[k - 1] + 1) ++k;
+                rr.push_back({js[i], (uint32_t)((int64_t)js[i] + kv.first), (uint32_t)(k - i)});
+                i = k;
+            }
+        }
+        std::sort(rr.begin(), rr.end());
+        std::vector<uint32_t> bend;                      // end of each batch's last run
+        std::vector<std::vector<std::array<uint32_t, 3>>> bat;
+        for (const auto &r : rr) {
+            size_t bi = 0;
+            while (bi < bend.size() && bend[bi] > r[0]) ++bi;
+            if (bi == bend.size()) { bend.push_back(0); bat.emplace_back(); }
+            bend[bi] = r[0] + r[2];
+            bat[bi].push_back(r);
+        }
+        std::vector<uint4> hr;
+        std::vector<uint32_t> hp{0};
+        for (const auto &b : bat) {
+            for (const auto &r : b) hr.push_back(make_uint4(r[0], r[1], r[2], 0));
+            hp.push_back((uint32_t)hr.size());
+        }
+        t->n_batches = (uint32_t)bat.size();
+        t->n_runs = (uint32_t)hr.size();
+        if (e == cudaSuccess) e = cudaMalloc(&t->runs, hr.size() * sizeof(uint4) + 16);
+        if (e == cudaSuccess) e = cudaMalloc(&t->run_ptr, hp.size() * 4);
+        if (e == cudaSuccess && !hr.empty()) e = cudaMemcpy(t->runs, hr.data(), hr.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(t->run_ptr, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess && !H.unit_node.empty())
         e = cudaMemcpy(t->unit_node, H.unit_node.data(), H.unit_node.size() * 4, cudaMemcpyHostToDevice);
@@ -1162,6 +1208,37 @@ __global__ void __launch_bounds__(512) csr_stage_key_kernel(const uint32_t *__re
     }
 }
 
+// Phase (1) from runs, for rows too long to stage: one CTA per block, the key
+// row Z in shared memory; batch by batch (runs of a batch write disjoint key
+// words) every warp XORs whole runs Y[src, src + len) into Z[dst, dst + len) --
+// consecutive lanes read and write consecutive words, no per-word index, no
+// atomics -- with one barrier per batch; the leaf-parity row is read through
+// L1 / L2.  (A staged variant that first copies the row into shared memory lost
+// to csr_stage_key_kernel; see the dispatch.)
+__global__ void __launch_bounds__(512) csr_run_key_kernel(const uint4 *__restrict__ runs,
+                                                          const uint32_t *__restrict__ run_ptr, uint32_t n_batches,
+                                                          const uint32_t *__restrict__ yws, uint32_t y_stride,
+                                                          uint32_t ywords, uint32_t *__restrict__ zws,
+                                                          uint32_t z_stride) {
+    extern __shared__ uint4 sm4[];
+    const uint32_t zw4 = (ywords + 3) / 4;
+    uint32_t *Z = reinterpret_cast<uint32_t *>(sm4);
+    const uint64_t b = blockIdx.x;
+    const uint32_t *yrow = yws + b * y_stride;
+    for (uint32_t i = threadIdx.x; i < zw4; i += blockDim.x) sm4[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (uint32_t bt = 0; bt < n_batches; ++bt) {
+        const uint32_t r1 = __ldg(run_ptr + bt + 1);
+        for (uint32_t r = __ldg(run_ptr + bt) + warp; r < r1; r += nwarps) {
+            const uint4 R = __ldg(runs + r);
+            for (uint32_t i = lane; i < R.z; i += 32) Z[R.x + i] ^= __ldg(yrow + R.y + i);
+        }
+        __syncthreads();
+    }
+    for (uint32_t j = threadIdx.x; j < ywords; j += blockDim.x) zws[b * z_stride + j] = Z[j];
+}
+
 __global__ void __launch_bounds__(256) zpack_kernel(const uint32_t *__restrict__ zws, uint32_t z_stride,
                                                     uint64_t n_blocks, uint32_t m, uint64_t m_magic, OutStream out) {
     const uint32_t ywords = (m + 31) / 32;
@@ -1361,11 +1438,25 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
                 return e ? atoi(e) != 0 : true;
             }();
             const size_t ysmem = (size_t)H.y_stride * 4;
+            static const bool use_runs = [] {  // QRNG_CSR_RUNS=0: the CSR key kernels (A/B)
+                const char *e = getenv("QRNG_CSR_RUNS");
+                return !(e && *e && atoi(e) == 0);
+            }();
+            const size_t zsmem = (size_t)((ywords + 3) / 4) * 16;
             KernelTimer tc(s, true, 1);
+            // rows that fit in shared memory: the staged CSR kernel (a runs form
+            // with the row staged in shared memory measured slower: config 3 218 -> 195,
+            // 2^17 140 -> 106 Gbit/s -- a barrier per batch of ~2 runs per warp);
+            // longer rows: the runs kernel reading the row through L1 / L2
+            // instead of the CSR gather (2^18 77.4 -> 83.2; tools/csr_runs_ab.sh)
             if (staged && ysmem <= 200 * 1024 && H.y_stride % 4 == 0) {
                 if (ysmem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_stage_key_kernel));
                 csr_stage_key_kernel<<<(unsigned)n_blocks, 512, ysmem, s>>>(t->csr, yws, H.y_stride, ywords, kz,
                                                                             z_stride);
+            } else if (use_runs && t->n_runs && zsmem <= 200 * 1024) {
+                if (zsmem > 48 * 1024) allow_max_smem(reinterpret_cast<const void *>(csr_run_key_kernel));
+                csr_run_key_kernel<<<(unsigned)n_blocks, 512, zsmem, s>>>(
+                    t->runs, t->run_ptr, t->n_batches, yws, H.y_stride, ywords, kz, z_stride);
             } else {
                 csr_key_kernel<<<(unsigned)(w1 < cap ? w1 : cap), 256, 0, s>>>(t->csr, yws, H.y_stride, n_blocks,
                                                                               ywords, kz, z_stride);
