@@ -17,6 +17,7 @@
 // ~2e8 bit-MACs -- under a microsecond of ALU issue.  The crossover is by
 // measurement (api.cu).
 #include <algorithm>
+#include <cstdlib>
 #include "qrng_internal.cuh"
 
 namespace qrng {
@@ -153,14 +154,20 @@ qrng_status extract(const uint32_t *d_seed_words, const uint8_t *d_seed_bytes, c
     QRNG_CUDA_TRY(cudaGetDevice(&dev));
     QRNG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint64_t total_words = (n_blocks * m + 31) / 32;
-    // output words per CTA: two per warp while that gives at most 8 CTAs per SM
-    // (latency-bound sizes: many CTAs, each one memory round trip), more per CTA
-    // beyond; capped so the touched block rows fit in ~40 KB
+    // output words per CTA: one per warp while that gives at most 8 CTAs per SM
+    // (latency-bound sizes: many CTAs, each one memory round trip; measured at
+    // config 1, plan reused: 1 / 2 / 4 / 8 / 16 words per warp 30.5 / 28.9 /
+    // 25.3 / 21.8 / 16.3 Gbit/s), more per CTA beyond; capped so the touched
+    // block rows fit in ~40 KB
     if (n_blocks * m >= (1ull << 32)) {
         set_error("CUDA-core path: n_blocks * m >= 2^32");
         return QRNG_E_UNSUPPORTED;
     }
-    uint64_t wpc = std::max<uint64_t>(2 * kWarps, (total_words + (uint64_t)sms * 8 - 1) / ((uint64_t)sms * 8));
+    static const int wpw_env = [] {  // QRNG_BITS_WPW: minimum output words per warp (A/B)
+        const char *e = getenv("QRNG_BITS_WPW");
+        return (e && *e) ? std::max(1, atoi(e)) : 1;
+    }();
+    uint64_t wpc = std::max<uint64_t>((uint64_t)wpw_env * kWarps, (total_words + (uint64_t)sms * 8 - 1) / ((uint64_t)sms * 8));
     const uint64_t max_rows = std::max<uint64_t>(2, (40u * 1024u) / (nw * 4u));
     wpc = std::min<uint64_t>(wpc, std::max<uint64_t>(1, (max_rows - 1) * m / 32));
     const uint64_t ctas = (total_words + wpc - 1) / wpc;
