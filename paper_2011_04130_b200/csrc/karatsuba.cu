@@ -26,7 +26,10 @@
 // (C4).  Exactness: every step is a GF(2) identity and each leaf is exact
 // int32 accumulation followed by & 1.
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <array>
 #include <list>
 #include <map>
@@ -397,6 +400,8 @@ struct Tables {
     uint32_t n_batches = 0, n_runs = 0;
     std::vector<gemm::Leaf> hleaves;
     uint32_t max_leaf_w = 0;       // widest leaf (K) -- the packed-accumulator kernel takes w <= 2048
+    int qs_ns = 0;                 // slices of the one-pass Q-buffer form (0: trees it does not cover)
+    struct QSliceHost { uint32_t n_ent = 0, lsu = 0; uint32_t ent[80] = {}; } qs;  // = QSlice (defined with the kernels)
     ~Tables() {
         // the last owner is the cache or a plan; cudaFree waits for the work that reads them
         for (void *ptr : {(void *)leaves, (void *)terms, (void *)qbufs, (void *)qgen_dev, (void *)inner,
@@ -448,6 +453,45 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, std::shared
         }
     }
     t->qgen.push_back((uint32_t)hq.size());
+    // one-pass form (qslice_kernel): each Q buffer as the XOR of raw windows
+    // x[o, o + h) (symmetric difference of the parent's expansion shifted to
+    // x0 and x1), cut into chunks of the narrowest Q width s
+    if (!H.qbufs.empty()) {
+        uint32_t s = UINT32_MAX;
+        for (const auto &Q : H.qbufs) s = std::min(s, Q.h);
+        const uint64_t ns = n / s;
+        std::vector<std::vector<uint32_t>> ex(H.qbufs.size());  // sorted raw offsets (bits)
+        std::vector<std::array<uint32_t, 2>> ent;
+        bool ok = s % 128 == 0 && n % s == 0 && ns <= 16;
+        for (size_t qi = 0; ok && qi < H.qbufs.size(); ++qi) {
+            const QBuf &Q = H.qbufs[qi];
+            const std::vector<uint32_t> par = Q.src < 0 ? std::vector<uint32_t>{0} : ex[Q.src];
+            std::map<uint32_t, int> cnt;
+            for (uint32_t o : par) { cnt[o + Q.src_off] ^= 1; cnt[o + Q.src_off + Q.h] ^= 1; }
+            for (const auto &kv : cnt)
+                if (kv.second) ex[qi].push_back(kv.first);
+            for (uint32_t c = 0; ok && c < Q.h / s; ++c) {
+                uint32_t mask = 0;
+                for (uint32_t o : ex[qi]) {
+                    const uint64_t bit = o + (uint64_t)c * s;
+                    if (bit % s || bit / s >= ns) { ok = false; break; }
+                    mask ^= 1u << (bit / s);
+                }
+                const uint32_t dunit = (Q.dst + c * s / 32) / 4;
+                if (dunit >= 65536 || (Q.dst + c * s / 32) % 4) ok = false;
+                ent.push_back({mask, dunit});
+            }
+        }
+        if (ok && ent.size() <= 80) {
+            t->qs_ns = (int)ns;
+            t->qs.n_ent = (uint32_t)ent.size();
+            uint32_t su = s / 128, lsu = 0;
+            while ((1u << lsu) < su) ++lsu;
+            t->qs.lsu = lsu;
+            for (size_t i = 0; i < ent.size(); ++i) t->qs.ent[i] = ent[i][0] | (ent[i][1] << 16);
+            if ((1u << lsu) != su) t->qs_ns = 0;
+        }
+    }
     for (const auto &L : H.leaves) {
         gemm::Leaf g{};
         g.w = L.w;
@@ -675,6 +719,48 @@ __global__ void __launch_bounds__(512) qbuf_kernel(const uint4 *units, const uin
             for (int u = 0; u < U; ++u)
                 if (dst[u]) *dst[u] = make_uint4(a[u].x ^ c[u].x, a[u].y ^ c[u].y, a[u].z ^ c[u].z, a[u].w ^ c[u].w);
         }
+    }
+}
+
+// All Q buffers of shallow trees in one pass, no generation barrier (round 2).
+// Every Q buffer of width h is an XOR of windows x[o, o + h) of the raw block
+// with o a multiple of h (the node inputs sit at multiples of their width), so
+// with s = the narrowest Q width each s-bit chunk of a Q buffer is the XOR of
+// a fixed set of the block's NS = n / s aligned s-bit slices.  Thread (block,
+// unit j of a slice) loads unit j of every slice once (NS 16-byte loads, all in
+// flight) and writes unit j of every Q chunk from registers; the host lists
+// each chunk as {slice mask, destination unit in the X row}.
+constexpr int kQSliceMaxEnt = 80;  // Q chunks at NS = 16: (3^4 - 2^4) = 65
+struct QSlice {
+    uint32_t n_ent, lsu;           // chunks; log2 of 16-byte units per slice
+    uint32_t ent[kQSliceMaxEnt];   // slice mask (bits 0..15) | destination unit (bits 16..31)
+};
+
+template <int NS>
+__global__ void __launch_bounds__(256) qslice_kernel(const __grid_constant__ QSlice qs, const uint4 *raw,
+                                                     uint64_t n_blocks, uint4 *xws, uint32_t x_stride, SeedJob sj) {
+    pdl_release();  // the grouped GEMM may be scheduled as CTAs finish
+    if (blockIdx.x >= sj.q_ctas) {  // leaf-seed CTAs (one-shot calls)
+        for (uint32_t l = blockIdx.x - sj.q_ctas; l < sj.n_leaves; l += gridDim.x - sj.q_ctas)
+            leaf_seed_words(sj.leaves[l], sj.terms, sj.seed, sj.L, sj.seeds, threadIdx.x, blockDim.x);
+        return;
+    }
+    const uint64_t item = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t b = item >> qs.lsu;
+    if (b >= n_blocks) return;
+    const uint32_t su = 1u << qs.lsu, j = (uint32_t)item & (su - 1);
+    const uint4 *src = raw + b * (NS * su) + j;
+    uint4 v[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) v[i] = __ldcs(src + i * su);  // read once: streaming
+    uint4 *dst = xws + b * (x_stride / 4) + j;
+    for (uint32_t e = 0; e < qs.n_ent; ++e) {
+        const uint32_t en = qs.ent[e];
+        uint4 a = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+            if ((en >> i) & 1u) a = make_uint4(a.x ^ v[i].x, a.y ^ v[i].y, a.z ^ v[i].z, a.w ^ v[i].w);
+        dst[en >> 16] = a;
     }
 }
 
@@ -1374,9 +1460,31 @@ static qrng_status extract_chunk(const Plan &pl, const uint8_t *d_raw, uint64_t 
             sj.n_leaves = (uint32_t)t->hleaves.size();
             seed_ctas = std::min<uint32_t>(sj.n_leaves, 64);
         }
-        qbuf_kernel<QRNG_QBUF_U><<<sj.q_ctas + seed_ctas, 512, 0, s>>>(
-            t->qbufs, t->qgen_dev, (uint32_t)t->qgen.size() - 1, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
-            (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc, sj);
+        // one-pass slice form where the tree allows it (QRNG_QSLICE=0: the generation kernel, A/B)
+        static const bool qslice_on = [] {
+            const char *e = getenv("QRNG_QSLICE");
+            return !(e && *e && atoi(e) == 0);
+        }();
+        if (qslice_on && t->qs_ns) {
+            static_assert(sizeof(QSlice) == sizeof(t->qs), "QSlice host/device layout");
+            QSlice qs;
+            memcpy(&qs, &t->qs, sizeof(qs));
+            const uint64_t items = n_blocks << qs.lsu;
+            sj.q_ctas = (uint32_t)((items + 255) / 256);
+            const uint4 *r4 = reinterpret_cast<const uint4 *>(d_raw);
+            uint4 *x4 = reinterpret_cast<uint4 *>(xws);
+            const dim3 grid(sj.q_ctas + seed_ctas);
+            switch (t->qs_ns) {
+                case 2: qslice_kernel<2><<<grid, 256, 0, s>>>(qs, r4, n_blocks, x4, H.x_stride, sj); break;
+                case 4: qslice_kernel<4><<<grid, 256, 0, s>>>(qs, r4, n_blocks, x4, H.x_stride, sj); break;
+                case 8: qslice_kernel<8><<<grid, 256, 0, s>>>(qs, r4, n_blocks, x4, H.x_stride, sj); break;
+                default: qslice_kernel<16><<<grid, 256, 0, s>>>(qs, r4, n_blocks, x4, H.x_stride, sj); break;
+            }
+        } else {
+            qbuf_kernel<QRNG_QBUF_U><<<sj.q_ctas + seed_ctas, 512, 0, s>>>(
+                t->qbufs, t->qgen_dev, (uint32_t)t->qgen.size() - 1, reinterpret_cast<const uint4 *>(d_raw), n_blocks,
+                (uint32_t)n, reinterpret_cast<uint4 *>(xws), H.x_stride, bpc, sj);
+        }
         tq.stop();
         if (cudaGetLastError() != cudaSuccess) { set_error("qbuf_kernel launch failed"); st = QRNG_E_CUDA; }
     }
