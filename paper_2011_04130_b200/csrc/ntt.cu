@@ -532,8 +532,11 @@ struct PassArgs {
 };
 enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4, PASS_INV_EMIT_XOR = 5 };
 
+#ifndef QRNG_NTT_EMIT_SKIP
+#define QRNG_NTT_EMIT_SKIP 1  // 0: every q through the window test (A/B)
+#endif
 template <int R, int MODE, int F = 0>
-__global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(256, (QRNG_NTT_EMIT_SKIP && R >= 6 && MODE >= PASS_INV_EMIT) ? 3 : 1) ntt_pass_kernel(PassArgs a) {
     constexpr int N1 = 1 << R;
     constexpr uint32_t P = Fld<F>::P;
     const uint32_t logseg = a.logP - a.S, logstride = logseg - R;
@@ -585,16 +588,26 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
     // PASS_INV_EMIT[_XOR] (level 0): element q is z_t with t = q*STRIDE + u
     const int lane = threadIdx.x & 31;
     const uint32_t u0 = u & ~31u;
+    // the warp's t = q*STRIDE + u0..u0+31 meet the key window [len-1, len-1+m)
+    // only for q in [q_lo, q_hi] (a third of the q at config 4): the others
+    // skip the canonical residue, window test and ballot (warp-uniform)
+    const int64_t w_lo = (int64_t)(a.len - 1), w_hi = w_lo + (int64_t)a.m;  // [w_lo, w_hi)
+    const int64_t ql = (w_lo - (int64_t)(u0 + 31) + (int64_t)STRIDE - 1) / (int64_t)STRIDE;
+    const int64_t qh = (w_hi - 1 - (int64_t)u0) / (int64_t)STRIDE;
+    const int q_lo = ql < 0 ? 0 : (int)ql;
+    const int q_hi = qh > N1 - 1 ? N1 - 1 : (int)qh;
     uint32_t mine = 0;
 #pragma unroll
     for (int q = 0; q < N1; ++q) {
-        const uint32_t t = (uint32_t)q * STRIDE + u;
-        const int64_t i = (int64_t)t - (int64_t)(a.len - 1);
-        const bool valid = i >= 0 && i < (int64_t)a.m;
-        uint32_t z = x[q] >= P ? x[q] - P : x[q];
-        if (MODE == PASS_INV_EMIT_XOR && valid) z ^= raw_bit(a.bits, a.b0 + bb, a.n, t + 1);  // identity block
-        const uint32_t bal = __ballot_sync(0xffffffffu, valid && (z & 1u));
-        if (lane == (q & 31)) mine = bal;
+        if (!QRNG_NTT_EMIT_SKIP || (q >= q_lo && q <= q_hi)) {
+            const uint32_t t = (uint32_t)q * STRIDE + u;
+            const int64_t i = (int64_t)t - (int64_t)(a.len - 1);
+            const bool valid = i >= 0 && i < (int64_t)a.m;
+            uint32_t z = x[q] >= P ? x[q] - P : x[q];
+            if (MODE == PASS_INV_EMIT_XOR && valid) z ^= raw_bit(a.bits, a.b0 + bb, a.n, t + 1);  // identity block
+            const uint32_t bal = __ballot_sync(0xffffffffu, valid && (z & 1u));
+            if (lane == (q & 31)) mine = bal;
+        }
         if ((q & 31) == 31 || q == N1 - 1) {
             const int qb = q & ~31;
             if (lane <= (q & 31) && mine) {
@@ -607,6 +620,7 @@ __global__ void __launch_bounds__(256) ntt_pass_kernel(PassArgs a) {
                 if (hi) emit_word(a.out, (uint64_t)W0, hi, false);
                 if (lo) emit_word(a.out, (uint64_t)(W0 + 1), lo, false);
             }
+            mine = 0;  // a skipped q of the next group leaves its lane's word empty
         }
     }
 }
