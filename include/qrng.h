@@ -303,6 +303,19 @@ QRNG_API void        qrng_debug_set_karatsuba(int max_depth);
 QRNG_API qrng_status qrng_debug_karatsuba_plan(uint64_t n, uint64_t m, int max_depth, uint32_t *leaf_rw,
                                                uint32_t leaf_cap, uint32_t *terms, uint32_t term_cap,
                                                uint32_t *comb, uint32_t comb_cap, uint32_t *counts);
+/* TEST ONLY (no GPU needed): the one-pass Q-buffer form of the same plan
+ * (karatsuba.cu qslice_kernel).  Every Q buffer (x0 ^ x1 of a Karatsuba node,
+ * stored in a block's X row of info[3] 32-bit words) is cut into chunks of
+ * s = n / info[0] bits; chunk e is written at 16-byte unit ent[e] >> 16 of the
+ * X row as the XOR of the block's aligned s-bit slices i (x[i s, (i+1) s))
+ * with bit i of ent[e] & 0xFFFF set.  info = {slices (0: the tree is not
+ * covered and ent is empty), log2(s / 128), chunks, X-row words, leaves};
+ * leaf_x[2l..2l+1] = {input is the X row (1) or the raw block (0), word offset
+ * of leaf l's input window}, leaves in qrng_debug_karatsuba_plan's order.
+ * Buffers too small (ent_cap < chunks, leaf_cap < leaves): sizes only.
+ * Errors: E_INVALID for a NULL info, E_UNSUPPORTED as above. */
+QRNG_API qrng_status qrng_debug_qslice_plan(uint64_t n, uint64_t m, int max_depth, uint32_t *ent, uint32_t ent_cap,
+                                            uint32_t *leaf_x, uint32_t leaf_cap, uint32_t *info);
 
 /* BENCH / TEST ONLY instrumentation.
  * qrng_debug_launch_count: number of kernels this library has launched in the

@@ -35,7 +35,7 @@ EXPORTS = ["qrng_minentropy", "qrng_hist256_async", "qrng_entropy_from_counts",
            "qrng_last_error", "qrng_version", "qrng_debug_set_path", "qrng_debug_launch_count",
            "qrng_debug_kernel_timing", "qrng_debug_kernel_time_ms", "qrng_debug_umma_probe",
            "qrng_debug_butterfly_rate", "qrng_debug_pass_rate", "qrng_debug_mxf4_probe", "qrng_debug_gemm_operand_bits", "qrng_debug_set_karatsuba", "qrng_plan_info",
-           "qrng_debug_karatsuba_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
+           "qrng_debug_karatsuba_plan", "qrng_debug_qslice_plan", "qrng_debug_gemm_trace", "qrng_stream_create", "qrng_stream_submit",
            "qrng_stream_synchronize", "qrng_stream_counts", "qrng_stream_destroy", "qrng_debug_kernel_time_split",
            "qrng_debug_mma_rate", "qrng_dist_plan_create", "qrng_dist_exchange_words", "qrng_dist_local",
            "qrng_dist_finish", "qrng_dist_plan_destroy"]
@@ -133,6 +133,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "qrng_stream_destroy": ([vp], None),
         "qrng_plan_info": ([vp, vp], i32),
         "qrng_debug_karatsuba_plan": ([u64, u64, i32, vp, u32, vp, u32, vp, u32, vp], i32),
+        "qrng_debug_qslice_plan": ([u64, u64, i32, vp, u32, vp, u32, vp], i32),
         "qrng_dist_plan_create": ([u64, u64, vp, u32, u32, vp, ctypes.POINTER(vp)], i32),
         "qrng_dist_exchange_words": ([vp], u64),
         "qrng_dist_local": ([vp, vp, vp, vp], i32),
@@ -243,6 +244,19 @@ def karatsuba_plan(n: int, m: int, max_depth: int) -> KaratsubaPlan:
         r, w, off, t0, ns, ni = (int(v) for v in leaf[6 * l:6 * l + 6])
         leaves.append((r, w, off, [int(v) for v in terms[t0:t0 + ns]], [int(v) for v in terms[t0 + ns:t0 + ns + ni]]))
     return KaratsubaPlan(depth, leaves, comb[:words + 1].copy(), comb[words + 1:].copy())
+
+
+def qslice_plan(n: int, m: int, max_depth: int):
+    """TEST ONLY (no GPU): the one-pass Q-buffer chunk list of the plan for (n, m)
+    (qrng_debug_qslice_plan): (slices, log2(s/128), chunks[], X-row words, leaf_x[l] = (src, word))."""
+    lib = load_library()
+    info = (ctypes.c_uint32 * 5)()
+    _check(lib.qrng_debug_qslice_plan(n, m, max_depth, None, 0, None, 0, info))
+    ns, lsu, ne, xw, nl = (int(v) for v in info)
+    ent = np.zeros(max(ne, 1), np.uint32)
+    lx = np.zeros(2 * max(nl, 1), np.uint32)
+    _check(lib.qrng_debug_qslice_plan(n, m, max_depth, ent.ctypes.data, ne, lx.ctypes.data, nl, info))
+    return ns, lsu, [int(v) for v in ent[:ne]], xw, [(int(lx[2 * l]), int(lx[2 * l + 1])) for l in range(nl)]
 
 
 def gemm_trace(reset: bool = True) -> np.ndarray:

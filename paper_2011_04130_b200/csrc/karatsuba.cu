@@ -379,6 +379,54 @@ static bool plan_host_depth(uint64_t n, uint64_t m, int depth, bool forced, Host
     return true;
 }
 
+// One-pass Q-buffer form (qslice_kernel): each Q buffer as the XOR of raw
+// windows x[o, o + h) (symmetric difference of the parent's expansion shifted
+// to x0 and x1), cut into chunks of the narrowest Q width s; chunk = {mask of
+// the block's n / s aligned s-bit slices, destination 16-byte unit in the X
+// row}.  Returns n / s, or 0 when the tree has no Q buffers or needs more than
+// 16 slices / 80 chunks (the generation kernel then forms them).
+struct QSliceHost {
+    uint32_t n_ent = 0, lsu = 0;  // chunks; log2 of 16-byte units per slice
+    uint32_t ent[80] = {};        // slice mask (bits 0..15) | destination unit (bits 16..31)
+};
+static int qslice_host(const HostTables &H, uint64_t n, QSliceHost &qs) {
+    qs = QSliceHost{};
+    if (H.qbufs.empty()) return 0;
+    uint32_t s = UINT32_MAX;
+    for (const auto &Q : H.qbufs) s = std::min(s, Q.h);
+    if (s % 128 || n % s || n / s > 16) return 0;
+    const uint64_t ns = n / s;
+    std::vector<std::vector<uint32_t>> ex(H.qbufs.size());  // sorted raw offsets (bits)
+    std::vector<std::array<uint32_t, 2>> ent;
+    for (size_t qi = 0; qi < H.qbufs.size(); ++qi) {
+        const QBuf &Q = H.qbufs[qi];
+        const std::vector<uint32_t> par = Q.src < 0 ? std::vector<uint32_t>{0} : ex[Q.src];
+        std::map<uint32_t, int> cnt;
+        for (uint32_t o : par) { cnt[o + Q.src_off] ^= 1; cnt[o + Q.src_off + Q.h] ^= 1; }
+        for (const auto &kv : cnt)
+            if (kv.second) ex[qi].push_back(kv.first);
+        for (uint32_t c = 0; c < Q.h / s; ++c) {
+            uint32_t mask = 0;
+            for (uint32_t o : ex[qi]) {
+                const uint64_t bit = o + (uint64_t)c * s;
+                if (bit % s || bit / s >= ns) return 0;
+                mask ^= 1u << (bit / s);
+            }
+            const uint32_t dw = Q.dst + c * s / 32;  // destination word in the X row
+            if (dw % 4 || dw / 4 >= 65536) return 0;
+            ent.push_back({mask, dw / 4});
+        }
+    }
+    if (ent.size() > 80) return 0;
+    uint32_t lsu = 0;
+    while ((1u << lsu) < s / 128) ++lsu;
+    if ((1u << lsu) != s / 128) return 0;
+    qs.n_ent = (uint32_t)ent.size();
+    qs.lsu = lsu;
+    for (size_t i = 0; i < ent.size(); ++i) qs.ent[i] = ent[i][0] | (ent[i][1] << 16);
+    return (int)ns;
+}
+
 // ---- device tables (cached per device and (n, m, depth)) ------------------
 struct Tables {
     HostTables host;
@@ -401,7 +449,7 @@ struct Tables {
     std::vector<gemm::Leaf> hleaves;
     uint32_t max_leaf_w = 0;       // widest leaf (K) -- the packed-accumulator kernel takes w <= 2048
     int qs_ns = 0;                 // slices of the one-pass Q-buffer form (0: trees it does not cover)
-    struct QSliceHost { uint32_t n_ent = 0, lsu = 0; uint32_t ent[80] = {}; } qs;  // = QSlice (defined with the kernels)
+    QSliceHost qs;                 // its chunk list (= QSlice, defined with the kernels)
     ~Tables() {
         // the last owner is the cache or a plan; cudaFree waits for the work that reads them
         for (void *ptr : {(void *)leaves, (void *)terms, (void *)qbufs, (void *)qgen_dev, (void *)inner,
@@ -453,45 +501,7 @@ static qrng_status get_tables(uint64_t n, uint64_t m, int max_depth, std::shared
         }
     }
     t->qgen.push_back((uint32_t)hq.size());
-    // one-pass form (qslice_kernel): each Q buffer as the XOR of raw windows
-    // x[o, o + h) (symmetric difference of the parent's expansion shifted to
-    // x0 and x1), cut into chunks of the narrowest Q width s
-    if (!H.qbufs.empty()) {
-        uint32_t s = UINT32_MAX;
-        for (const auto &Q : H.qbufs) s = std::min(s, Q.h);
-        const uint64_t ns = n / s;
-        std::vector<std::vector<uint32_t>> ex(H.qbufs.size());  // sorted raw offsets (bits)
-        std::vector<std::array<uint32_t, 2>> ent;
-        bool ok = s % 128 == 0 && n % s == 0 && ns <= 16;
-        for (size_t qi = 0; ok && qi < H.qbufs.size(); ++qi) {
-            const QBuf &Q = H.qbufs[qi];
-            const std::vector<uint32_t> par = Q.src < 0 ? std::vector<uint32_t>{0} : ex[Q.src];
-            std::map<uint32_t, int> cnt;
-            for (uint32_t o : par) { cnt[o + Q.src_off] ^= 1; cnt[o + Q.src_off + Q.h] ^= 1; }
-            for (const auto &kv : cnt)
-                if (kv.second) ex[qi].push_back(kv.first);
-            for (uint32_t c = 0; ok && c < Q.h / s; ++c) {
-                uint32_t mask = 0;
-                for (uint32_t o : ex[qi]) {
-                    const uint64_t bit = o + (uint64_t)c * s;
-                    if (bit % s || bit / s >= ns) { ok = false; break; }
-                    mask ^= 1u << (bit / s);
-                }
-                const uint32_t dunit = (Q.dst + c * s / 32) / 4;
-                if (dunit >= 65536 || (Q.dst + c * s / 32) % 4) ok = false;
-                ent.push_back({mask, dunit});
-            }
-        }
-        if (ok && ent.size() <= 80) {
-            t->qs_ns = (int)ns;
-            t->qs.n_ent = (uint32_t)ent.size();
-            uint32_t su = s / 128, lsu = 0;
-            while ((1u << lsu) < su) ++lsu;
-            t->qs.lsu = lsu;
-            for (size_t i = 0; i < ent.size(); ++i) t->qs.ent[i] = ent[i][0] | (ent[i][1] << 16);
-            if ((1u << lsu) != su) t->qs_ns = 0;
-        }
-    }
+    t->qs_ns = qslice_host(H, n, t->qs);  // one-pass Q-buffer form (qslice_kernel)
     for (const auto &L : H.leaves) {
         gemm::Leaf g{};
         g.w = L.w;
@@ -1698,5 +1708,30 @@ extern "C" qrng_status qrng_debug_karatsuba_plan(uint64_t n, uint64_t m, int max
     }
     for (size_t j = 0; j < T.comb_ptr.size(); ++j) comb[j] = T.comb_ptr[j];
     for (size_t j = 0; j < T.comb_idx.size(); ++j) comb[T.comb_ptr.size() + j] = T.comb_idx[j];
+    return QRNG_OK;
+}
+
+// TEST ONLY: the one-pass Q-buffer chunk list and each leaf's input location
+// (no GPU needed).  See include/qrng.h (qrng_debug_qslice_plan).
+extern "C" qrng_status qrng_debug_qslice_plan(uint64_t n, uint64_t m, int max_depth, uint32_t *ent, uint32_t ent_cap,
+                                              uint32_t *leaf_x, uint32_t leaf_cap, uint32_t *info) {
+    using namespace qrng;
+    using namespace qrng::kara;
+    HostTables T;
+    if (!info) { set_error("info is NULL"); return QRNG_E_INVALID; }
+    if (!plan_host(n, m, max_depth, T)) { set_error("no decomposition"); return QRNG_E_UNSUPPORTED; }
+    QSliceHost qs;
+    info[0] = (uint32_t)qslice_host(T, n, qs);
+    info[1] = qs.lsu;
+    info[2] = qs.n_ent;
+    info[3] = T.x_stride;
+    info[4] = (uint32_t)T.leaves.size();
+    if (!ent || !leaf_x || ent_cap < qs.n_ent || leaf_cap < T.leaves.size()) return QRNG_OK;  // sizes only
+    for (uint32_t e = 0; e < qs.n_ent; ++e) ent[e] = qs.ent[e];
+    for (size_t l = 0; l < T.leaves.size(); ++l) {
+        const auto &L = T.leaves[l];
+        leaf_x[2 * l] = L.src < 0 ? 0u : 1u;
+        leaf_x[2 * l + 1] = L.src < 0 ? L.src_off / 32 : T.qbufs[L.src].dst + L.src_off / 32;
+    }
     return QRNG_OK;
 }
