@@ -170,7 +170,7 @@ PATH_NAMES = {1: "gemm", 2: "ntt", 3: "bits"}
 
 
 def algorithmic_work(q, path: int, w: S.Workload, n_blocks: int, pack: bool, modified: bool = False,
-                     macs_per_block: int = 0):
+                     macs_per_block: int = 0, blocks_per_transform: int = 0, primes: int = 1):
     """Roofline numerators, per step of the main kernel(s)."""
     if path == q.PATH_GEMM:
         # tensor-core ops (E2M1 or int8): 2 x the leaf MACs of the Karatsuba
@@ -181,8 +181,13 @@ def algorithmic_work(q, path: int, w: S.Workload, n_blocks: int, pack: bool, mod
         return float(w.m) * w.n * n_blocks, "alu", "Tbit-MAC/s"
     L = (w.n - 1) if modified else (w.n + w.m - 1)
     P = 1 << max(5, math.ceil(math.log2(L)))
-    transforms = (n_blocks + 1) // 2 if pack else n_blocks
-    bfly = transforms * (P * math.log2(P) + P)  # fwd + inv radix-2 butterflies (P/2 log P each) + P products
+    if blocks_per_transform:  # the plan says: groups of blocks_per_transform blocks, `primes` transforms each
+        transforms = -(-n_blocks // blocks_per_transform) * max(1, primes)
+    else:
+        transforms = (n_blocks + 1) // 2 if pack else n_blocks
+    # fwd + inv radix-2 butterflies (P/2 log P each) + P products per transform
+    # (the packed three-prime form: 3 transforms per 4 blocks, CRT not counted)
+    bfly = transforms * (P * math.log2(P) + P)
     return bfly, "alu", "Gbutterfly/s"
 
 
@@ -535,6 +540,8 @@ def measure(q, ctx: Ctx, args, cfg: int, *, headline: bool, cpu_budget: float):
                    "blocks_rank0": B, "seed_bits": w.n if modified else w.seed_bits,
                    "raw_bits_total": B_total * w.n, "path": PATH_NAMES[path],
                    "two_blocks_per_transform": bool(pack and path == q.PATH_NTT),
+                   "blocks_per_transform": pinfo["blocks_per_transform"] if path == q.PATH_NTT else None,
+                   "ntt_primes": pinfo["primes"] if path == q.PATH_NTT else None,
                    "karatsuba_depth": pinfo["karatsuba_depth"] if path == q.PATH_GEMM else None,
                    "karatsuba_leaves": pinfo["leaves"] if path == q.PATH_GEMM else None,
                    "ntt_log2_transform": pinfo["log2_transform"] if path == q.PATH_NTT else None,
@@ -607,7 +614,8 @@ def measure_e2e(q, ctx, args, w, B, raw_np, seed, bits_all, flush, stream):
 
 def roofline(q, args, w, B, path, pack, modified, pinfo, kern_ms, kern_n, ms_total_kt, aux_ms, aux_n):
     pk, pk_kind = peaks()
-    work, bound, unit = algorithmic_work(q, path, w, B, pack, modified, pinfo["macs_per_block"])
+    work, bound, unit = algorithmic_work(q, path, w, B, pack, modified, pinfo["macs_per_block"],
+                                         pinfo.get("blocks_per_transform", 0), pinfo.get("primes", 1))
     if not kern_n:
         return None
     # the path's extraction kernel(s) of one step (GEMM and fused NTT: one

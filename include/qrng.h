@@ -255,13 +255,17 @@ QRNG_API int         qrng_debug_last_path(void);
  *   macs_per_block       GEMM path: int8 multiply-accumulates per block over all
  *                        leaves (n*m for the dense product)
  *   log2_transform       NTT path: log2 of the cyclic length P
- *   blocks_per_transform NTT path: 2 when two blocks share one transform
+ *   blocks_per_transform NTT path: blocks that share one transform (2: two
+ *                        blocks as x1 + 2^k x2, P <= 2^15; G = 4: the packed
+ *                        three-prime form, multi-pass sizes with n < 2^21)
+ *   primes               NTT path: transforms per direction for each group of
+ *                        blocks_per_transform blocks (3 in the packed form)
  *   x_words, y_words     Karatsuba: 32-bit workspace words per block of the
  *                        combined inputs (Q buffers) and of the leaf parities
  * Errors: E_INVALID for NULL arguments. */
 typedef struct {
     int32_t path, karatsuba_depth, leaves, log2_transform;
-    int32_t blocks_per_transform, reserved;
+    int32_t blocks_per_transform, primes;
     uint64_t macs_per_block;
     uint32_t x_words, y_words;
 } qrng_plan_info_t;

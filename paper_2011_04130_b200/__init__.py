@@ -54,7 +54,7 @@ class _Gauss(ctypes.Structure):
 class _PlanInfo(ctypes.Structure):
     _fields_ = [("path", ctypes.c_int32), ("karatsuba_depth", ctypes.c_int32), ("leaves", ctypes.c_int32),
                 ("log2_transform", ctypes.c_int32), ("blocks_per_transform", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("macs_per_block", ctypes.c_uint64),
+                ("primes", ctypes.c_int32), ("macs_per_block", ctypes.c_uint64),
                 ("x_words", ctypes.c_uint32), ("y_words", ctypes.c_uint32)]
 
 

@@ -209,6 +209,7 @@ static void plan_release(qrng_plan *p, cudaStream_t s, bool async) {
         else cudaFree(ptr);
     };
     fr(p->ntt.shat); fr(p->ntt.tw); fr(p->ntt.itw); fr(p->ntt.l1tw); fr(p->ntt.work);
+    for (int f = 0; f < 3; ++f) { fr(p->ntt.shat3[f]); fr(p->ntt.tw3[f]); fr(p->ntt.itw3[f]); fr(p->ntt.l1tw3[f]); }
     fr(p->gemm.seed_words);
     fr(p->kara.seeds);
     delete p;
@@ -294,7 +295,8 @@ qrng_status qrng_plan_info(const qrng_plan *plan, qrng_plan_info_t *info) {
     info->path = plan->path;
     if (plan->path == QRNG_PATH_NTT) {
         info->log2_transform = plan->ntt.logP;
-        info->blocks_per_transform = plan->ntt.pack_shift ? 2 : 1;
+        info->blocks_per_transform = plan->ntt.crt ? plan->ntt.crt : plan->ntt.pack_shift ? 2 : 1;
+        info->primes = plan->ntt.crt ? 3 : 1;
     } else if (plan->kara_on) {
         int d = 0, l = 0;
         uint64_t macs = 0;

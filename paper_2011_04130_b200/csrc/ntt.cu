@@ -38,7 +38,11 @@ namespace ntt {
 template <int F> struct Fld;
 template <> struct Fld<0> { static constexpr uint32_t P = kP, PINV = 3296722945u; static constexpr int LOG2 = 23; };
 template <> struct Fld<1> { static constexpr uint32_t P = kP2, PINV = 3825205249u; static constexpr int LOG2 = 26; };
-static_assert(Fld<0>::P * Fld<0>::PINV == 1u && Fld<1>::P * Fld<1>::PINV == 1u, "PINV = p^-1 mod 2^32");
+//   F = 2: p =   5 * 2^25 + 1 = 167772161 -- third prime of the packed
+//          three-prime form (kP kP2 kP3 > 2^86; primitive root 3)
+template <> struct Fld<2> { static constexpr uint32_t P = kP3, PINV = 4127195137u; static constexpr int LOG2 = 25; };
+static_assert(Fld<0>::P * Fld<0>::PINV == 1u && Fld<1>::P * Fld<1>::PINV == 1u && Fld<2>::P * Fld<2>::PINV == 1u,
+              "PINV = p^-1 mod 2^32");
 static_assert(4ull * Fld<0>::P < (1ull << 32) && 4ull * Fld<1>::P < (1ull << 32), "lazy [0, 4p) sums fit 32 bits");
 constexpr uint32_t P = kP;  // the single-GPU prime (fused kernels, plans of ntt.cu's host code)
 
@@ -71,7 +75,7 @@ constexpr RootTab make_roots(uint64_t p) {
     }
     return t;
 }
-__constant__ RootTab c_roots[2] = {make_roots(Fld<0>::P), make_roots(Fld<1>::P)};
+__constant__ RootTab c_roots[3] = {make_roots(Fld<0>::P), make_roots(Fld<1>::P), make_roots(Fld<2>::P)};
 
 // ---- modular arithmetic on lazy residues in [0, 2p) ------------------------
 template <int F = 0>
@@ -529,14 +533,57 @@ struct PassArgs {
     uint32_t logP, S;         // this pass works on segments of 2^(logP - S) words
     OutStream out;
     uint32_t xor_tail;        // modified Toeplitz: output t also XORs raw bit t + 1 of its block
+    // PASS_FWD_PACK (packed three-prime form): transform b of the batch holds
+    // blocks (b0 + b) G + g, g < G, as sum_g cg[g] x_g (cg[g] = 2^(k g) mod p)
+    uint32_t G;
+    uint32_t cg[4];
+    uint64_t n_blocks;
+    // PASS_INV_CRT: the first two primes' z_t (natural order, same layout as ws)
+    const uint32_t *crt0, *crt1;
+    uint32_t crt_k;
 };
-enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4, PASS_INV_EMIT_XOR = 5 };
+enum { PASS_FWD_BITS = 0, PASS_FWD_SEED = 1, PASS_FWD = 2, PASS_INV = 3, PASS_INV_EMIT = 4, PASS_INV_EMIT_XOR = 5,
+       PASS_FWD_PACK = 6, PASS_INV_CRT = 8 };
+
+// ---- packed three-prime form: CRT and key bits ------------------------------
+// Garner constants for (p0, p1, p2) = (kP, kP2, kP3); Shoup companions
+// floor(c 2^32 / p) so every product is a 3-instruction Shoup multiply.
+struct Crt {
+    static constexpr uint64_t p0 = kP, p1 = kP2, p2 = kP3;
+    static constexpr uint32_t c1 = (uint32_t)powmod_p(p0 % p1, p1 - 2, p1);  // p0^-1 mod p1
+    static constexpr uint32_t c1p = (uint32_t)(((uint64_t)c1 << 32) / p1);
+    static constexpr uint32_t one2p = (uint32_t)((1ull << 32) / p2);         // reduces r0 mod p2
+    static constexpr uint32_t p0m2 = (uint32_t)(p0 % p2);
+    static constexpr uint32_t p0m2p = (uint32_t)(((uint64_t)p0m2 << 32) / p2);
+    static constexpr uint32_t c2 = (uint32_t)powmod_p(p0 % p2 * (p1 % p2) % p2, p2 - 2, p2);  // (p0 p1)^-1 mod p2
+    static constexpr uint32_t c2p = (uint32_t)(((uint64_t)c2 << 32) / p2);
+    static constexpr uint64_t p01 = p0 * p1;
+};
+constexpr int kCrtQ = 32;  // window q per warp staged in shared memory by PASS_INV_CRT (8 warps: 64 KB)
+__device__ __forceinline__ uint32_t shoup_p(uint32_t a, uint32_t w, uint32_t wp, uint32_t p) {
+    return a * w - __umulhi(a, wp) * p;  // a w mod p in [0, 2p)
+}
 
 #ifndef QRNG_NTT_EMIT_SKIP
 #define QRNG_NTT_EMIT_SKIP 1  // 0: every q through the window test (A/B)
 #endif
+// Radix-64 passes: ptxas otherwise spends 214-254 registers (one 256-thread
+// CTA per SM); 3 CTAs per SM (85 registers) where that costs at most a few
+// bytes of spill, 2 (128 registers) for the forms that spill at 3
+#ifndef QRNG_NTT_PASS_BOUND
+#define QRNG_NTT_PASS_BOUND 1  // 0: no bound on the radix-64 passes except the emit pass (A/B)
+#endif
+__host__ __device__ constexpr int ntt_pass_min_ctas(int R, int MODE) {
+    return R < 6 ? 1
+           : (MODE == 4 || MODE == 5) ? (QRNG_NTT_EMIT_SKIP ? 3 : 1)  // PASS_INV_EMIT[_XOR]
+           : !QRNG_NTT_PASS_BOUND ? 1
+           : (MODE == 6 || MODE == 8) ? 3                             // PASS_FWD_PACK, PASS_INV_CRT
+           : MODE == 2 ? 1                                            // PASS_FWD spills even at 2
+           : 2;
+}
 template <int R, int MODE, int F = 0>
-__global__ void __launch_bounds__(256, (QRNG_NTT_EMIT_SKIP && R >= 6 && MODE >= PASS_INV_EMIT) ? 3 : 1) ntt_pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(256, ntt_pass_min_ctas(R, MODE))
+    ntt_pass_kernel(PassArgs a) {
     constexpr int N1 = 1 << R;
     constexpr uint32_t P = Fld<F>::P;
     const uint32_t logseg = a.logP - a.S, logstride = logseg - R;
@@ -545,6 +592,33 @@ __global__ void __launch_bounds__(256, (QRNG_NTT_EMIT_SKIP && R >= 6 && MODE >= 
     const uint32_t seg = u >> logstride, n2 = u & ((1u << logstride) - 1);
     const uint32_t STRIDE = 1u << logstride;
     uint32_t *base = a.ws + (bb << a.logP) + ((uint64_t)seg << logseg) + n2;
+    // PASS_INV_CRT: the first two primes' z_t of the warp's window q (up to
+    // kCrtQ of them) are copied into shared memory by cp.async while the
+    // transform runs, so the CRT loop finds them there (a load per q inside
+    // that loop exposes its latency once per q)
+    extern __shared__ uint32_t crt_sm[];
+    int crt_qlo = 0, crt_nq = 0;
+    if constexpr (MODE == PASS_INV_CRT) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t u0 = u & ~31u;
+        const int64_t w_lo = (int64_t)(a.len - 1), w_hi = w_lo + (int64_t)a.m;
+        const int64_t ql = (w_lo - (int64_t)(u0 + 31) + (int64_t)STRIDE - 1) / (int64_t)STRIDE;
+        const int64_t qh = (w_hi - 1 - (int64_t)u0) / (int64_t)STRIDE;
+        crt_qlo = ql < 0 ? 0 : (int)ql;
+        const int qhi = qh > N1 - 1 ? N1 - 1 : (int)qh;
+        crt_nq = qhi >= crt_qlo ? min(qhi - crt_qlo + 1, kCrtQ) : 0;
+        const uint64_t off0 = (bb << a.logP) + u;
+        uint32_t *d0 = crt_sm + (warp * 2 * kCrtQ) * 32 + lane;
+        for (int j = 0; j < crt_nq; ++j) {
+            const uint64_t off = off0 + (uint64_t)(crt_qlo + j) * STRIDE;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(d0 + j * 32)),
+                         "l"(a.crt0 + off) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(d0 + (kCrtQ + j) * 32)),
+                         "l"(a.crt1 + off) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     uint32_t x[N1];
     if (MODE == PASS_FWD_BITS || MODE == PASS_FWD_SEED) {
         // level 0, STRIDE >= 32: lanes hold 32 consecutive idx = q*STRIDE + u
@@ -567,11 +641,46 @@ __global__ void __launch_bounds__(256, (QRNG_NTT_EMIT_SKIP && R >= 6 && MODE >= 
         }
 #pragma unroll
         for (int q = 0; q < N1; ++q) x[q] = (__shfl_sync(0xffffffffu, w[q >> 5], q & 31) >> (31 - lane)) & 1u;
+    } else if (MODE == PASS_FWD_PACK) {
+        // as PASS_FWD_BITS for each of the G <= 4 blocks of the group, combined
+        // as sum_g cg[g] bit_g (< 4p, reduced to [0, 2p)); blocks past the
+        // stream contribute nothing
+        const int lane = threadIdx.x & 31;
+        const uint32_t u0 = u & ~31u;
+        constexpr int NG = (N1 + 31) / 32;
+        // block by block, so only one block's words are live next to x[]
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint64_t blk = (a.b0 + bb) * a.G + (uint64_t)g;
+            const bool have = (uint32_t)g < a.G && blk < a.n_blocks;
+            const uint32_t *src = a.bits + blk * (a.n >> 5);
+            uint32_t w[NG];
+#pragma unroll
+            for (int gg = 0; gg < NG; ++gg) {
+                w[gg] = 0;
+                const uint32_t myidx = (uint32_t)(lane + 32 * gg) * STRIDE + u0;
+                if (have && lane + 32 * gg < N1 && myidx < a.len) {
+                    uint32_t v = bswap32(__ldg(src + (myidx >> 5)));
+                    const uint32_t rem = a.len - myidx;
+                    if (rem < 32) v &= 0xFFFFFFFFu << (32 - rem);
+                    w[gg] = v;
+                }
+            }
+            const uint32_t c = a.cg[g];
+#pragma unroll
+            for (int q = 0; q < N1; ++q) {
+                const uint32_t bit = (__shfl_sync(0xffffffffu, w[q >> 5], q & 31) >> (31 - lane)) & 1u;
+                if (g == 0) x[q] = bit;  // cg[0] = 1
+                else x[q] += bit ? c : 0u;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < N1; ++q) x[q] = red2<F>(x[q]);  // < 1 + 3 (p - 1) < 4p -> [0, 2p)
     } else {
 #pragma unroll
         for (int q = 0; q < N1; ++q) x[q] = base[(size_t)q * STRIDE];
     }
-    if (MODE <= PASS_FWD) {
+    if (MODE <= PASS_FWD || MODE == PASS_FWD_PACK) {
         dft_fwd<R, F>(x);
         if (n2) twiddle<R, F>(x, __ldg(a.tw + ((uint64_t)n2 << a.S)));
 #pragma unroll
@@ -585,7 +694,7 @@ __global__ void __launch_bounds__(256, (QRNG_NTT_EMIT_SKIP && R >= 6 && MODE >= 
         for (int q = 0; q < N1; ++q) base[(size_t)q * STRIDE] = x[q];
         return;
     }
-    // PASS_INV_EMIT[_XOR] (level 0): element q is z_t with t = q*STRIDE + u
+    // level 0 from here: element q is z_t with t = q*STRIDE + u
     const int lane = threadIdx.x & 31;
     const uint32_t u0 = u & ~31u;
     // the warp's t = q*STRIDE + u0..u0+31 meet the key window [len-1, len-1+m)
@@ -596,6 +705,72 @@ __global__ void __launch_bounds__(256, (QRNG_NTT_EMIT_SKIP && R >= 6 && MODE >= 
     const int64_t qh = (w_hi - 1 - (int64_t)u0) / (int64_t)STRIDE;
     const int q_lo = ql < 0 ? 0 : (int)ql;
     const int q_hi = qh > N1 - 1 ? N1 - 1 : (int)qh;
+    if constexpr (MODE == PASS_INV_CRT) {
+        // packed form, third prime: with the first two primes' z_t, the CRT
+        // value v mod 2^64 (Garner; v < kP kP2 kP3 exactly) holds block g's
+        // window sum in bits [k g, k g + k): key bit = bit k g.  Lane (q & 31)
+        // keeps the G ballots of its q; every 32 q each lane ORs its words in.
+        using C = Crt;
+        const uint64_t off0 = (bb << a.logP) + u;
+        const uint32_t *s0 = crt_sm + ((threadIdx.x >> 5) * 2 * kCrtQ) * 32 + lane;
+        asm volatile("cp.async.wait_all;" ::: "memory");  // this lane's own copies
+        uint32_t mine4[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < N1; ++q) {
+            if (q >= q_lo && q <= q_hi) {
+                const uint32_t t = (uint32_t)q * STRIDE + u;
+                const int64_t i = (int64_t)t - (int64_t)(a.len - 1);
+                const bool valid = i >= 0 && i < (int64_t)a.m;
+                uint64_t v = 0;
+                if (valid) {
+                    const int j = q - crt_qlo;
+                    uint32_t r0 = j < crt_nq ? s0[j * 32] : __ldcs(a.crt0 + off0 + (size_t)q * STRIDE);
+                    uint32_t r1 = j < crt_nq ? s0[(kCrtQ + j) * 32] : __ldcs(a.crt1 + off0 + (size_t)q * STRIDE);
+                    uint32_t r2 = x[q];
+                    r0 = r0 >= (uint32_t)C::p0 ? r0 - (uint32_t)C::p0 : r0;
+                    r1 = r1 >= (uint32_t)C::p1 ? r1 - (uint32_t)C::p1 : r1;
+                    r2 = r2 >= (uint32_t)C::p2 ? r2 - (uint32_t)C::p2 : r2;
+                    uint32_t r0m1 = r0 >= (uint32_t)C::p1 ? r0 - (uint32_t)C::p1 : r0;  // r0 < p0 < 3 p1
+                    r0m1 = r0m1 >= (uint32_t)C::p1 ? r0m1 - (uint32_t)C::p1 : r0m1;
+                    uint32_t y1 = shoup_p(r1 + (uint32_t)C::p1 - r0m1, C::c1, C::c1p, (uint32_t)C::p1);
+                    y1 = y1 >= (uint32_t)C::p1 ? y1 - (uint32_t)C::p1 : y1;
+                    const uint32_t r0m2 = shoup_p(r0, 1u, C::one2p, (uint32_t)C::p2);     // [0, 2 p2)
+                    const uint32_t q02 = shoup_p(y1, C::p0m2, C::p0m2p, (uint32_t)C::p2);  // p0 y1 mod p2
+                    uint32_t y2 = shoup_p(r2 + 4u * (uint32_t)C::p2 - r0m2 - q02, C::c2, C::c2p, (uint32_t)C::p2);
+                    y2 = y2 >= (uint32_t)C::p2 ? y2 - (uint32_t)C::p2 : y2;
+                    v = (uint64_t)r0 + C::p0 * (uint64_t)y1 + C::p01 * (uint64_t)y2;  // mod 2^64
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, valid && ((v >> (a.crt_k * g)) & 1u));
+                    if (lane == (q & 31)) mine4[g] = bal;
+                }
+            }
+            if ((q & 31) == 31 || q == N1 - 1) {
+                const int qb = q & ~31;
+                if (lane <= (q & 31)) {
+                    const int64_t i0 = (int64_t)(qb + lane) * STRIDE + u0 - (int64_t)(a.len - 1);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const uint64_t blk = (a.b0 + bb) * a.G + (uint64_t)g;
+                        if (mine4[g] && (uint32_t)g < a.G && blk < a.n_blocks) {
+                            const int64_t Gb = (int64_t)(blk * a.m) + i0;
+                            const uint32_t V = __brev(mine4[g]);
+                            const int64_t W0 = Gb >= 0 ? (Gb >> 5) : -((31 - Gb) >> 5);
+                            const int o = (int)(Gb - W0 * 32);
+                            const uint32_t hi = V >> o, lo = o ? (V << (32 - o)) : 0u;
+                            if (hi) emit_word(a.out, (uint64_t)W0, hi, false);
+                            if (lo) emit_word(a.out, (uint64_t)(W0 + 1), lo, false);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) mine4[g] = 0;  // a skipped q of the next group leaves its words empty
+            }
+        }
+        return;
+    }
+    // PASS_INV_EMIT[_XOR]
     uint32_t mine = 0;
 #pragma unroll
     for (int q = 0; q < N1; ++q) {
@@ -869,9 +1044,20 @@ template <int MODE, int F = 0>
 static qrng_status launch_pass(int R, const PassArgs &a, uint64_t nb, cudaStream_t s, bool timed) {
     const uint64_t nsub = 1ull << (a.logP - R);
     dim3 grid((unsigned)(nsub / 256), (unsigned)nb);
+    const size_t smem = MODE == PASS_INV_CRT ? (size_t)8 * 2 * kCrtQ * 32 * 4 : 0;
+    if (smem) {
+        qrng_status st = QRNG_OK;
+        switch (R) {
+#define X(RR) case RR: st = allow_max_smem(reinterpret_cast<const void *>(ntt_pass_kernel<RR, MODE, F>)); break;
+            X(1) X(2) X(3) X(4) X(5) X(6)
+#undef X
+            default: break;
+        }
+        if (st != QRNG_OK) return st;
+    }
     KernelTimer t(s, timed);
     switch (R) {
-#define X(RR) case RR: ntt_pass_kernel<RR, MODE, F><<<grid, 256, 0, s>>>(a); break;
+#define X(RR) case RR: ntt_pass_kernel<RR, MODE, F><<<grid, 256, smem, s>>>(a); break;
         X(1) X(2) X(3) X(4) X(5) X(6)
 #undef X
         default:
@@ -899,9 +1085,80 @@ static qrng_status launch_segments(const FusedArgs &a, uint32_t *ws, int logP, u
     return QRNG_OK;
 }
 
+// per-prime tables of a plan: seed spectrum and twiddles
+struct FieldTabs {
+    uint32_t **shat, **tw, **itw;
+    uint2 **l1tw;
+};
+
 template <int F>
-static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
+static qrng_status seed_multipass(const FieldTabs &ft, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
                                   int logP, uint32_t scaleM, cudaStream_t s);
+
+// twiddle tables, level-1 table and seed spectrum of field F for P = 2^logP
+template <int F>
+static qrng_status init_field(const FieldTabs &ft, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
+                              int logP, cudaStream_t s) {
+    const uint64_t Pf = Fld<F>::P, Pn = 1ull << logP;
+    QRNG_CUDA_TRY(cudaMallocAsync(ft.shat, Pn * 4, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(ft.tw, Pn * 4, s));
+    QRNG_CUDA_TRY(cudaMallocAsync(ft.itw, Pn * 4, s));
+    const uint64_t w = powmod_p(3, (Pf - 1) >> logP, Pf), iw = powmod_p(w, Pf - 2, Pf);
+    count_launch();
+    twiddle_table_kernel<F><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(*ft.tw, *ft.itw, (uint32_t)Pn,
+                                                                                   (uint32_t)w, (uint32_t)iw);
+    QRNG_CUDA_TRY(cudaGetLastError());
+    if (logP > kMaxFusedLogP && kSegLog == 15) {  // the segment kernel's level-1 twiddles
+        QRNG_CUDA_TRY(cudaMallocAsync(ft.l1tw, 2048 * sizeof(uint2), s));
+        count_launch();
+        const uint32_t shift = (uint32_t)(logP - kSegLog), mask = (uint32_t)(Pn - 1);
+        l1tw_kernel<F><<<8, 256, 0, s>>>(*ft.l1tw, *ft.tw, *ft.itw, shift, mask);
+        QRNG_CUDA_TRY(cudaGetLastError());
+    }
+    // scale = P^-1 * 2^64 mod p, so mont(v, scale) = v * P^-1 * 2^32 (Montgomery form for the pointwise product)
+    const uint64_t pinvP = powmod_p(Pn % Pf, Pf - 2, Pf);
+    const uint64_t r2 = (uint64_t)(((unsigned __int128)1 << 64) % Pf);
+    const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * r2 % Pf);
+    if (logP > kMaxFusedLogP) return seed_multipass<F>(ft, seed_words, n, m, L, logP, scaleM, s);
+    if constexpr (F == 0) {
+        switch (logP) {
+#define X(LP) case LP: return launch_seed<LP>(seed_words, (uint32_t)L, *ft.tw, *ft.shat, scaleM, s);
+            QRNG_LOGP_CASES(X)
+#undef X
+            default: break;
+        }
+    }
+    set_error("NTT plan: no transform for P = 2^%d", logP);
+    return QRNG_E_UNSUPPORTED;
+}
+
+// Packed three-prime form: G blocks per transform as v = sum_g 2^(k g) x_g,
+// k = bit length of n (every window sum c_g <= n < 2^k, so the convolution of v
+// with the seed holds each c_g in its own k-bit field), transformed modulo
+// each of kP, kP2, kP3 and recombined by CRT (M = kP kP2 kP3 > 2^86 > max v).
+// Pays when G >= 4 (4 blocks for 3 transforms per direction): n < 2^21 with
+// (G - 1) k <= 63 (the key bits 0, k, 2k, 3k are read from v mod 2^64).
+// Multi-pass sizes only (P > 2^15, P <= 2^23); QRNG_NTT_CRT=0 disables it.
+int choose_crt(uint64_t n, int logP, bool xor_tail, uint32_t *k_out) {
+    static const bool on = [] {
+        const char *e = getenv("QRNG_NTT_CRT");
+        return !(e && *e && atoi(e) == 0);
+    }();
+    if (!on || xor_tail || logP <= kMaxFusedLogP || logP > kMaxLogP) return 0;
+    uint32_t k = 0;
+    while ((1ull << k) <= n) ++k;  // 2^k > n
+    const long double M = (long double)kP * kP2 * kP3;
+    int G = 1;
+    while (G < 4 && (uint64_t)G * k <= 63) {
+        long double vmax = 0;  // n * sum_{g <= G} 2^(k g)
+        for (int g = 0; g <= G; ++g) vmax += ldexpl((long double)n, (int)(k * g));
+        if (vmax >= M * 0.999L) break;
+        ++G;
+    }
+    if (G < 4) return 0;
+    *k_out = k;
+    return G;
+}
 
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t seed_bit_offset,
                       bool xor_tail, cudaStream_t s) {
@@ -920,52 +1177,26 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
         set_error("NTT path: L = %llu exceeds 2^26", (unsigned long long)L);
         return QRNG_E_UNSUPPORTED;
     }
-    const uint64_t Pf = pl.field ? (uint64_t)kP2 : (uint64_t)kP;
     pl.logP = logP;
     pl.pack_shift = logP <= kMaxFusedLogP ? choose_pack_shift(n, logP) : 0;  // window sums <= n
-    const uint64_t Pn = 1ull << logP;
+    pl.crt = choose_crt(n, logP, xor_tail, &pl.crt_k);
     const uint64_t nwords = (L + 31) / 32 + 1;
     uint32_t *seed_words = nullptr;
-    QRNG_CUDA_TRY(cudaMallocAsync(&pl.shat, Pn * 4, s));
-    QRNG_CUDA_TRY(cudaMallocAsync(&pl.tw, Pn * 4, s));
-    QRNG_CUDA_TRY(cudaMallocAsync(&pl.itw, Pn * 4, s));
     QRNG_CUDA_TRY(cudaMallocAsync(&seed_words, nwords * 4, s));
-    const uint64_t w = powmod_p(3, (Pf - 1) >> logP, Pf), iw = powmod_p(w, Pf - 2, Pf);
-    count_launch();
-    if (pl.field)
-        twiddle_table_kernel<1><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
-                                                                                       (uint32_t)w, (uint32_t)iw);
-    else
-        twiddle_table_kernel<0><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(pl.tw, pl.itw, (uint32_t)Pn,
-                                                                                       (uint32_t)w, (uint32_t)iw);
-    QRNG_CUDA_TRY(cudaGetLastError());
-    if (logP > kMaxFusedLogP && kSegLog == 15) {  // the segment kernel's level-1 twiddles
-        QRNG_CUDA_TRY(cudaMallocAsync(&pl.l1tw, 2048 * sizeof(uint2), s));
-        count_launch();
-        const uint32_t shift = (uint32_t)(logP - kSegLog), mask = (uint32_t)(Pn - 1);
-        if (pl.field) l1tw_kernel<1><<<8, 256, 0, s>>>(pl.l1tw, pl.tw, pl.itw, shift, mask);
-        else l1tw_kernel<0><<<8, 256, 0, s>>>(pl.l1tw, pl.tw, pl.itw, shift, mask);
-        QRNG_CUDA_TRY(cudaGetLastError());
-    }
     count_launch();
     seed_words_kernel<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(d_seed, L, seed_bit_offset, seed_words,
                                                                       nwords);
     QRNG_CUDA_TRY(cudaGetLastError());
-    // scale = P^-1 * 2^64 mod p, so mont(v, scale) = v * P^-1 * 2^32 (Montgomery form for the pointwise product)
-    const uint64_t pinvP = powmod_p(Pn % Pf, Pf - 2, Pf);
-    const uint64_t r2 = (uint64_t)(((unsigned __int128)1 << 64) % Pf);
-    const uint32_t scaleM = (uint32_t)((unsigned __int128)pinvP * r2 % Pf);
-    qrng_status st = QRNG_E_UNSUPPORTED;
-    if (logP <= kMaxFusedLogP) {
-        switch (logP) {
-#define X(LP) case LP: st = launch_seed<LP>(seed_words, (uint32_t)L, pl.tw, pl.shat, scaleM, s); break;
-            QRNG_LOGP_CASES(X)
-#undef X
-            default: break;
-        }
+    qrng_status st;
+    if (pl.crt) {
+        st = init_field<0>(FieldTabs{&pl.shat3[0], &pl.tw3[0], &pl.itw3[0], &pl.l1tw3[0]}, seed_words, n, m, L, logP, s);
+        if (st == QRNG_OK)
+            st = init_field<1>(FieldTabs{&pl.shat3[1], &pl.tw3[1], &pl.itw3[1], &pl.l1tw3[1]}, seed_words, n, m, L, logP, s);
+        if (st == QRNG_OK)
+            st = init_field<2>(FieldTabs{&pl.shat3[2], &pl.tw3[2], &pl.itw3[2], &pl.l1tw3[2]}, seed_words, n, m, L, logP, s);
     } else {
-        st = pl.field ? seed_multipass<1>(pl, seed_words, n, m, L, logP, scaleM, s)
-                      : seed_multipass<0>(pl, seed_words, n, m, L, logP, scaleM, s);
+        const FieldTabs ft{&pl.shat, &pl.tw, &pl.itw, &pl.l1tw};
+        st = pl.field ? init_field<1>(ft, seed_words, n, m, L, logP, s) : init_field<0>(ft, seed_words, n, m, L, logP, s);
     }
     cudaFreeAsync(seed_words, s);
     return st;
@@ -973,7 +1204,7 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
 
 // seed spectrum through the multi-pass decomposition, forward only
 template <int F>
-static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
+static qrng_status seed_multipass(const FieldTabs &ft, const uint32_t *seed_words, uint64_t n, uint64_t m, uint64_t L,
                                   int logP, uint32_t scaleM, cudaStream_t s) {
     const uint64_t Pn = 1ull << logP;
     qrng_status st = QRNG_OK;
@@ -989,8 +1220,8 @@ static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, ui
         pa.m = (uint32_t)m;
         pa.len = (uint32_t)L;
         pa.ws = ws;
-        pa.tw = pl.tw;
-        pa.itw = pl.itw;
+        pa.tw = *ft.tw;
+        pa.itw = *ft.itw;
         pa.logP = (uint32_t)logP;
         pa.S = 0;
         st = launch_pass<PASS_FWD_SEED, F>(r[0], pa, 1, s, false);
@@ -1000,9 +1231,9 @@ static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, ui
         }
         if (st == QRNG_OK) {
             FusedArgs fa{};
-            fa.shat = pl.shat;
-            fa.tw = pl.tw;
-            fa.itw = pl.itw;
+            fa.shat = *ft.shat;
+            fa.tw = *ft.tw;
+            fa.itw = *ft.itw;
             fa.tw_shift = (uint32_t)(logP - kSegLog);
             fa.scaleM = scaleM;
             st = launch_segments<SEGFWD, F>(fa, ws, logP, 1, s, false);
@@ -1013,11 +1244,11 @@ static qrng_status seed_multipass(const Plan &pl, const uint32_t *seed_words, ui
 }
 
 void plan_free(Plan &pl) {
-    if (pl.shat) cudaFree(pl.shat);
-    if (pl.tw) cudaFree(pl.tw);
-    if (pl.itw) cudaFree(pl.itw);
-    if (pl.l1tw) cudaFree(pl.l1tw);
-    if (pl.work) cudaFree(pl.work);
+    for (void *ptr : {(void *)pl.shat, (void *)pl.tw, (void *)pl.itw, (void *)pl.l1tw, (void *)pl.work})
+        if (ptr) cudaFree(ptr);
+    for (int f = 0; f < 3; ++f)
+        for (void *ptr : {(void *)pl.shat3[f], (void *)pl.tw3[f], (void *)pl.itw3[f], (void *)pl.l1tw3[f]})
+            if (ptr) cudaFree(ptr);
     pl = Plan{};
 }
 
@@ -1106,8 +1337,111 @@ static qrng_status extract_multipass(const Plan &pl, const uint8_t *d_raw, uint6
     return st;
 }
 
+// Packed three-prime form: per batch of groups (G blocks each), for each prime
+// the forward passes (the first forming the packed input), segments and
+// inverse passes down to natural order in that prime's workspace, then the CRT
+// kernel.  Batches alternate between two streams as in extract_multipass.
+template <int F>
+static qrng_status crt_prime(const Plan &pl, PassArgs pa, FusedArgs fa, int logP, uint64_t nb, cudaStream_t s) {
+    int r[2];
+    const int np = global_radices(logP, r);
+    const uint64_t Pf = Fld<F>::P;
+    for (int g = 0; g < 4; ++g) pa.cg[g] = (uint32_t)powmod_p(2, (uint64_t)pl.crt_k * g, Pf);
+    pa.tw = pl.tw3[F];
+    pa.itw = pl.itw3[F];
+    fa.shat = pl.shat3[F];
+    fa.tw = pl.tw3[F];
+    fa.itw = pl.itw3[F];
+    fa.l1tw = pl.l1tw3[F];
+    pa.S = 0;
+    qrng_status st = launch_pass<PASS_FWD_PACK, F>(r[0], pa, nb, s, true);
+    if (st == QRNG_OK && np == 2) {
+        pa.S = (uint32_t)r[0];
+        st = launch_pass<PASS_FWD, F>(r[1], pa, nb, s, true);
+    }
+    if (st == QRNG_OK) st = launch_segments<SEG, F>(fa, pa.ws, logP, nb, s, true);
+    if (st == QRNG_OK && np == 2) {
+        pa.S = (uint32_t)r[0];
+        st = launch_pass<PASS_INV, F>(r[1], pa, nb, s, true);
+    }
+    if (st == QRNG_OK) {  // natural order: z_t (F < 2), or CRT + key bits (F = 2)
+        pa.S = 0;
+        // (storing only the window's q spills at any launch bound for radix 64)
+        if constexpr (F < 2) st = launch_pass<PASS_INV, F>(r[0], pa, nb, s, true);
+        else st = launch_pass<PASS_INV_CRT, F>(r[0], pa, nb, s, true);
+    }
+    return st;
+}
+
+static qrng_status extract_crt(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
+                               const OutStream &out, cudaStream_t s) {
+    const int logP = pl.logP;
+    const uint64_t G = (uint64_t)pl.crt, groups = (n_blocks + G - 1) / G;
+    static const int kBatchLog = [] {  // as extract_multipass: workspace words per batch (all three primes)
+        const char *e = getenv("QRNG_NTT_BATCH_LOG");
+        const int v = e ? atoi(e) : 0;
+        return v >= 18 && v <= 27 ? v : 26;
+    }();
+    // groups per batch: a 2^28-word budget over the three primes (4 GB in all
+    // on two streams at most) -- the 2^26 of the one-prime form would leave
+    // the segment launches a few waves long, and their tails cost ~15%
+    uint64_t bb = ((1ull << (kBatchLog + 2)) >> logP) / 3;
+    if (bb < 1) bb = 1;
+    if (bb > groups) bb = groups;
+    const bool two = groups > bb;
+    cudaStream_t s2 = s;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (two) {
+        qrng_status st2 = side_stream(&s2, &fork, &join);
+        if (st2 != QRNG_OK) return st2;
+    }
+    const uint64_t wsw = bb << logP;  // words per prime per batch
+    uint32_t *wsb[2] = {nullptr, nullptr};
+    QRNG_CUDA_TRY(cudaMallocAsync(&wsb[0], 3 * wsw * 4, s));
+    if (two) {
+        QRNG_CUDA_TRY(cudaMallocAsync(&wsb[1], 3 * wsw * 4, s));
+        QRNG_CUDA_TRY(cudaEventRecord(fork, s));
+        QRNG_CUDA_TRY(cudaStreamWaitEvent(s2, fork, 0));
+    }
+    PassArgs pa{};
+    pa.bits = reinterpret_cast<const uint32_t *>(d_raw);
+    pa.n = (uint32_t)n;
+    pa.m = (uint32_t)m;
+    pa.len = pl.len;
+    pa.logP = (uint32_t)logP;
+    pa.out = out;
+    pa.G = (uint32_t)G;
+    pa.n_blocks = n_blocks;
+    pa.crt_k = pl.crt_k;
+    FusedArgs fa{};
+    fa.tw_shift = (uint32_t)(logP - kSegLog);
+    qrng_status st = QRNG_OK;
+    for (uint64_t g0 = 0, it = 0; g0 < groups && st == QRNG_OK; g0 += bb, ++it) {
+        const uint64_t nb = (groups - g0) < bb ? (groups - g0) : bb;
+        const cudaStream_t sb = (it & 1) ? s2 : s;
+        uint32_t *ws = wsb[it & 1];
+        pa.b0 = g0;
+        pa.ws = ws;
+        st = crt_prime<0>(pl, pa, fa, logP, nb, sb);
+        pa.ws = ws + wsw;
+        if (st == QRNG_OK) st = crt_prime<1>(pl, pa, fa, logP, nb, sb);
+        pa.ws = ws + 2 * wsw;
+        pa.crt0 = ws;
+        pa.crt1 = ws + wsw;
+        if (st == QRNG_OK) st = crt_prime<2>(pl, pa, fa, logP, nb, sb);
+    }
+    if (two) {
+        cudaEventRecord(join, s2);
+        cudaStreamWaitEvent(s, join, 0);
+        cudaFreeAsync(wsb[1], s);
+    }
+    cudaFreeAsync(wsb[0], s);
+    return st;
+}
+
 qrng_status extract(const Plan &pl, const uint8_t *d_raw, uint64_t n_blocks, uint64_t n, uint64_t m,
                     const OutStream &out, cudaStream_t s) {
+    if (pl.crt) return extract_crt(pl, d_raw, n_blocks, n, m, out, s);
     if (pl.logP > kMaxFusedLogP)
         return pl.field ? extract_multipass<1>(pl, d_raw, n_blocks, n, m, out, s)
                         : extract_multipass<0>(pl, d_raw, n_blocks, n, m, out, s);

@@ -104,6 +104,7 @@ __device__ __forceinline__ void emit_word(const OutStream &o, uint64_t W, uint32
 namespace ntt {
 constexpr uint32_t kP = 998244353u;
 constexpr uint32_t kP2 = 469762049u;  // 7 * 2^26 + 1: the distributed (NEXT-4) transforms, P up to 2^26
+constexpr uint32_t kP3 = 167772161u;  // 5 * 2^25 + 1: third prime of the packed three-prime form
 constexpr int kMaxLogP = 23;
 constexpr int kMaxLogP2 = 26;
 constexpr int kMaxFusedLogP = 15;  // one CTA holds the whole transform in smem
@@ -120,6 +121,13 @@ struct Plan {
     uint2 *l1tw = nullptr;       // multi-pass: the segment kernel's level-1 twiddles in Shoup form (ntt.cu)
     uint32_t *work = nullptr;    // multipass scratch (not used by the fused kernel)
     size_t work_words = 0;
+    // packed three-prime form (multi-pass, n < 2^21): crt blocks share one
+    // transform per prime as sum_g 2^(crt_k g) x_g; the key bits come back by
+    // CRT (ntt.cu "Packed three-prime form").  0: one block per transform.
+    int crt = 0;
+    uint32_t crt_k = 0;
+    uint32_t *shat3[3] = {}, *tw3[3] = {}, *itw3[3] = {};  // per prime kP, kP2, kP3
+    uint2 *l1tw3[3] = {};
 };
 qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, uint32_t seed_bit_offset,
                       bool xor_tail, cudaStream_t s);
