@@ -574,7 +574,8 @@ __device__ __forceinline__ uint32_t shoup_p(uint32_t a, uint32_t w, uint32_t wp,
 #define QRNG_NTT_PASS_BOUND 1  // 0: no bound on the radix-64 passes except the emit pass (A/B)
 #endif
 __host__ __device__ constexpr int ntt_pass_min_ctas(int R, int MODE) {
-    return R < 6 ? 1
+    return (R == 5 && MODE == 6 && QRNG_NTT_PASS_BOUND) ? 3             // PASS_FWD_PACK at radix 32: 145 -> 85
+           : R < 6 ? 1
            : (MODE == 4 || MODE == 5) ? (QRNG_NTT_EMIT_SKIP ? 3 : 1)  // PASS_INV_EMIT[_XOR]
            : !QRNG_NTT_PASS_BOUND ? 1
            : (MODE == 6 || MODE == 8) ? 3                             // PASS_FWD_PACK, PASS_INV_CRT
@@ -835,17 +836,30 @@ __device__ uint32_t powmod_d(uint64_t b, uint64_t e) {
 }
 
 // tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P (Montgomery
-// form).  Each thread owns 64 consecutive exponents: one modular power for the
-// first, then a Montgomery chain (mont(x * R, w * R) = x w R), canonicalised.
+// form).  Each thread owns kTwChain consecutive exponents: the first power by
+// Montgomery square-and-multiply, then a Montgomery chain (mont(x * R, w * R) =
+// x w R), canonicalised.  (Round 2: 16-long chains and a Montgomery power
+// instead of 64 and a 64-bit-modulo power -- the table build was 29 us at
+// P = 2^21, once per prime of a one-shot plan.)
+constexpr uint32_t kTwChain = 16;
 template <int F = 0>
 __global__ void twiddle_table_kernel(uint32_t *tw, uint32_t *itw, uint32_t Pn, uint32_t w, uint32_t iw) {
     constexpr uint32_t P = Fld<F>::P;
-    const uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) * 64u;
+    const uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) * kTwChain;
     if (e0 >= Pn) return;
     const uint32_t wM = (uint32_t)(((uint64_t)w << 32) % P), iwM = (uint32_t)(((uint64_t)iw << 32) % P);
-    uint32_t a = (uint32_t)(((uint64_t)powmod_d<F>(w, e0) << 32) % P);
-    uint32_t b = (uint32_t)(((uint64_t)powmod_d<F>(iw, e0) << 32) % P);
-    for (uint32_t k = 0; k < 64 && e0 + k < Pn; ++k) {
+    uint32_t a = (uint32_t)((1ull << 32) % P), b = a;  // 1 in Montgomery form
+    {
+        uint32_t sa = wM, sb = iwM;
+        for (uint32_t e = e0; e; e >>= 1) {  // square-and-multiply, lazy residues in (0, 2p)
+            if (e & 1) { a = mont<F>(a, sa); b = mont<F>(b, sb); }
+            sa = mont<F>(sa, sa);
+            sb = mont<F>(sb, sb);
+        }
+        a = a >= P ? a - P : a;
+        b = b >= P ? b - P : b;
+    }
+    for (uint32_t k = 0; k < kTwChain && e0 + k < Pn; ++k) {
         tw[e0 + k] = a;
         itw[e0 + k] = b;
         a = mont<F>(a, wM);
@@ -1105,7 +1119,7 @@ static qrng_status init_field(const FieldTabs &ft, const uint32_t *seed_words, u
     QRNG_CUDA_TRY(cudaMallocAsync(ft.itw, Pn * 4, s));
     const uint64_t w = powmod_p(3, (Pf - 1) >> logP, Pf), iw = powmod_p(w, Pf - 2, Pf);
     count_launch();
-    twiddle_table_kernel<F><<<(unsigned)(((Pn + 63) / 64 + 127) / 128), 128, 0, s>>>(*ft.tw, *ft.itw, (uint32_t)Pn,
+    twiddle_table_kernel<F><<<(unsigned)(((Pn + kTwChain - 1) / kTwChain + 127) / 128), 128, 0, s>>>(*ft.tw, *ft.itw, (uint32_t)Pn,
                                                                                    (uint32_t)w, (uint32_t)iw);
     QRNG_CUDA_TRY(cudaGetLastError());
     if (logP > kMaxFusedLogP && kSegLog == 15) {  // the segment kernel's level-1 twiddles
@@ -1671,7 +1685,7 @@ qrng_status dist_plan_init(DistPlan &pl, uint64_t n, uint64_t m, const uint8_t *
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.tw, bytes, s));
     QRNG_CUDA_TRY(cudaMallocAsync(&pl.itw, bytes, s));
     count_launch();
-    twiddle_table_kernel<1><<<(unsigned)(((pl.N2 + 63) / 64 + 127) / 128), 128, 0, s>>>(
+    twiddle_table_kernel<1><<<(unsigned)(((pl.N2 + kTwChain - 1) / kTwChain + 127) / 128), 128, 0, s>>>(
         pl.tw, pl.itw, pl.N2, (uint32_t)wN2, (uint32_t)powmod_p(wN2, Pp - 2, Pp));
     QRNG_CUDA_TRY(cudaGetLastError());
     if (rank != 0) {  // twist tables w_P^(+-n2 r), Montgomery form
@@ -1679,7 +1693,7 @@ qrng_status dist_plan_init(DistPlan &pl, uint64_t n, uint64_t m, const uint8_t *
         QRNG_CUDA_TRY(cudaMallocAsync(&pl.itwr, bytes, s));
         const uint64_t wr = powmod_p(wP, rank, Pp);
         count_launch();
-        twiddle_table_kernel<1><<<(unsigned)(((pl.N2 + 63) / 64 + 127) / 128), 128, 0, s>>>(
+        twiddle_table_kernel<1><<<(unsigned)(((pl.N2 + kTwChain - 1) / kTwChain + 127) / 128), 128, 0, s>>>(
             pl.twr, pl.itwr, pl.N2, (uint32_t)wr, (uint32_t)powmod_p(wr, Pp - 2, Pp));
         QRNG_CUDA_TRY(cudaGetLastError());
     }
