@@ -1203,11 +1203,22 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
     QRNG_CUDA_TRY(cudaGetLastError());
     qrng_status st;
     if (pl.crt) {
-        st = init_field<0>(FieldTabs{&pl.shat3[0], &pl.tw3[0], &pl.itw3[0], &pl.l1tw3[0]}, seed_words, n, m, L, logP, s);
-        if (st == QRNG_OK)
-            st = init_field<1>(FieldTabs{&pl.shat3[1], &pl.tw3[1], &pl.itw3[1], &pl.l1tw3[1]}, seed_words, n, m, L, logP, s);
-        if (st == QRNG_OK)
-            st = init_field<2>(FieldTabs{&pl.shat3[2], &pl.tw3[2], &pl.itw3[2], &pl.l1tw3[2]}, seed_words, n, m, L, logP, s);
+        // the second prime's tables on the side stream, next to the other two
+        // (each prime's chain is a few small launches: the two streams fill the SMs)
+        cudaStream_t s2;
+        cudaEvent_t fork, join;
+        st = side_stream(&s2, &fork, &join);
+        if (st != QRNG_OK) return st;
+        QRNG_CUDA_TRY(cudaEventRecord(fork, s));
+        QRNG_CUDA_TRY(cudaStreamWaitEvent(s2, fork, 0));
+        st = init_field<1>(FieldTabs{&pl.shat3[1], &pl.tw3[1], &pl.itw3[1], &pl.l1tw3[1]}, seed_words, n, m, L, logP, s2);
+        const qrng_status st0 =
+            init_field<0>(FieldTabs{&pl.shat3[0], &pl.tw3[0], &pl.itw3[0], &pl.l1tw3[0]}, seed_words, n, m, L, logP, s);
+        const qrng_status st2 = st0 != QRNG_OK ? st0 :
+            init_field<2>(FieldTabs{&pl.shat3[2], &pl.tw3[2], &pl.itw3[2], &pl.l1tw3[2]}, seed_words, n, m, L, logP, s);
+        cudaEventRecord(join, s2);  // always joined: seed_words is freed on s below
+        cudaStreamWaitEvent(s, join, 0);
+        if (st == QRNG_OK) st = st2;
     } else {
         const FieldTabs ft{&pl.shat, &pl.tw, &pl.itw, &pl.l1tw};
         st = pl.field ? init_field<1>(ft, seed_words, n, m, L, logP, s) : init_field<0>(ft, seed_words, n, m, L, logP, s);
