@@ -15,24 +15,24 @@ timeout 900 python bench.py --gpus 2 --configs cfg4a,cfg5_n2^16,next4_n2^24 --no
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/${T}_launches_bench_cfg2.csv python bench.py --steps 3 --warmup 3 --configs none \
     --no-e2e --no-cpu-baseline --no-parity > /dev/null 2>&1
-cap() {  # name config kernel-regex [source]
-  ncu --set full --clock-control none ${4:+--import-source on} -k regex:$3 -s 1 -c 1 -o gpurun_out/${T}_$1 \
+cap() {  # name config kernel-regex (on the demangled name, so template arguments can select) [source]
+  ncu --set full --clock-control none ${4:+--import-source on} --kernel-name-base demangled -k "regex:$3" -s 1 -c 1 -o gpurun_out/${T}_$1 \
       python tools/one_extract.py --config $2 --reps 2 > gpurun_out/${T}_$1.log 2>&1
   echo "$1 rc=$?"
 }
-cap gemm_cfg2 2 toeplitz_gemm_kernel src
+cap gemm_cfg2 2 'toeplitz_gemm_kernel' src
 cap bits_cfg1 1 bits_kernel
 cap gemm_cfg3 3 toeplitz_gemm_kernel
-cap ntt_segment_cfg4 4 ntt_segment_kernel
-cap ntt_pass_cfg4 4 ntt_pass_kernel
+cap ntt_segment_cfg4 4 'ntt_segment_kernel<15, 1,'
+cap ntt_pass_cfg4 4 'ntt_pass_kernel<6, 8,'
 cap gemm_cfg5_n2^10 10 toeplitz_gemm_kernel
-cap ntt_segment_cfg5_n2^19 19 ntt_segment_kernel
-cap ntt_segment_cfg5_n2^22 22 ntt_segment_kernel
+cap ntt_segment_cfg5_n2^19 19 'ntt_segment_kernel<15, 1,'
+cap ntt_segment_cfg5_n2^22 22 'ntt_segment_kernel<15, 1,'
 cap gemm_cfg5_n2^13 13 toeplitz_gemm_kernel
 cap gemm_cfg5_n2^16 16 toeplitz_gemm_kernel
 cap gemm_cfg5_n2^18 18 toeplitz_gemm_kernel
-cap ntt_segment_cfg41 41 ntt_segment_kernel
-cap ntt_segment_next4 124 ntt_segment_kernel
+cap ntt_segment_cfg41 41 'ntt_segment_kernel<15, 1,'
+cap ntt_segment_next4 124 'ntt_segment_kernel<15, 1,'
 for f in gpurun_out/${T}_*.ncu-rep; do echo "== $f"; python tools/ncu_summary.py $f; done > gpurun_out/${T}_ncu_summaries.txt 2>&1
 python tools/ncu_traffic.py $T gpurun_out/${T}_*.ncu-rep > gpurun_out/${T}_ncu_traffic.json
 # keep the headline capture (with source) and the NTT segment capture; the rest
