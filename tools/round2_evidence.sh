@@ -23,16 +23,16 @@ cap() {  # name config kernel-regex (on the demangled name, so template argument
 cap gemm_cfg2 2 'toeplitz_gemm_kernel' src
 cap bits_cfg1 1 bits_kernel
 cap gemm_cfg3 3 toeplitz_gemm_kernel
-cap ntt_segment_cfg4 4 'ntt_segment_kernel<15, 1,'
-cap ntt_pass_cfg4 4 'ntt_pass_kernel<6, 8,'
+cap ntt_segment_cfg4 4 'ntt_segment_kernel<.int.15, .int.1,'
+cap ntt_pass_cfg4 4 'ntt_pass_kernel<.int.6, .int.8,'
 cap gemm_cfg5_n2^10 10 toeplitz_gemm_kernel
-cap ntt_segment_cfg5_n2^19 19 'ntt_segment_kernel<15, 1,'
-cap ntt_segment_cfg5_n2^22 22 'ntt_segment_kernel<15, 1,'
+cap ntt_segment_cfg5_n2^19 19 'ntt_segment_kernel<.int.15, .int.1,'
+cap ntt_segment_cfg5_n2^22 22 'ntt_segment_kernel<.int.15, .int.1,'
 cap gemm_cfg5_n2^13 13 toeplitz_gemm_kernel
 cap gemm_cfg5_n2^16 16 toeplitz_gemm_kernel
 cap gemm_cfg5_n2^18 18 toeplitz_gemm_kernel
-cap ntt_segment_cfg41 41 'ntt_segment_kernel<15, 1,'
-cap ntt_segment_next4 124 'ntt_segment_kernel<15, 1,'
+cap ntt_segment_cfg41 41 'ntt_segment_kernel<.int.15, .int.1,'
+cap ntt_segment_next4 124 'ntt_segment_kernel<.int.15, .int.1,'
 for f in gpurun_out/${T}_*.ncu-rep; do echo "== $f"; python tools/ncu_summary.py $f; done > gpurun_out/${T}_ncu_summaries.txt 2>&1
 python tools/ncu_traffic.py $T gpurun_out/${T}_*.ncu-rep > gpurun_out/${T}_ncu_traffic.json
 # keep the headline capture (with source) and the NTT segment capture; the rest
