@@ -22,6 +22,11 @@
 // n (2^k + 1) < p keeps both convolutions exact and separable: parity of c1
 // is bit 0, parity of c2 is bit k).  Values are kept lazily in [0, 2p); the
 // final residue is made canonical before its parity is taken.
+// Larger P run as global radix passes around 2^15-word segment kernels; for
+// n < 2^21 four blocks share each transform as sum_g 2^(k g) x_g modulo three
+// primes, and the window sums come back by CRT ("Packed three-prime form",
+// DESIGN.md 6.3).
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -822,18 +827,6 @@ __global__ void __launch_bounds__(threads_of(LOGP), 1024 / threads_of(LOGP)) ntt
 }
 
 // ---- plan preparation kernels ----------------------------------------------
-template <int F = 0>
-__device__ uint32_t powmod_d(uint64_t b, uint64_t e) {
-    constexpr uint64_t PP = Fld<F>::P;
-    uint64_t r = 1;
-    b %= PP;
-    while (e) {
-        if (e & 1) r = r * b % PP;
-        b = b * b % PP;
-        e >>= 1;
-    }
-    return (uint32_t)r;
-}
 
 // tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P (Montgomery
 // form).  Each thread owns kTwChain consecutive exponents: the first power by
