@@ -748,7 +748,11 @@ __global__ void __launch_bounds__(256, ntt_pass_min_ctas(R, MODE))
                 }
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    const uint32_t bal = __ballot_sync(0xffffffffu, valid && ((v >> (a.crt_k * g)) & 1u));
+                    uint32_t bit = (uint32_t)(v >> (a.crt_k * g)) & 1u;
+                    const uint64_t blk = (a.b0 + bb) * a.G + (uint64_t)g;
+                    if (a.xor_tail && valid && (uint32_t)g < a.G && blk < a.n_blocks)
+                        bit ^= raw_bit(a.bits, blk, a.n, t + 1);  // identity block of [T | I_m]
+                    const uint32_t bal = __ballot_sync(0xffffffffu, valid && bit);
                     if (lane == (q & 31)) mine4[g] = bal;
                 }
             }
@@ -1145,13 +1149,15 @@ static qrng_status init_field(const FieldTabs &ft, const uint32_t *seed_words, u
 // each of kP, kP2, kP3 and recombined by CRT (M = kP kP2 kP3 > 2^86 > max v).
 // Pays when G >= 4 (4 blocks for 3 transforms per direction): n < 2^21 with
 // (G - 1) k <= 63 (the key bits 0, k, 2k, 3k are read from v mod 2^64).
-// Multi-pass sizes only (P > 2^15, P <= 2^23); QRNG_NTT_CRT=0 disables it.
-int choose_crt(uint64_t n, int logP, bool xor_tail, uint32_t *k_out) {
+// Multi-pass sizes from P = 2^17 to 2^23; QRNG_NTT_CRT=0 disables it.
+int choose_crt(uint64_t n, int logP, bool /*xor_tail: the CRT pass XORs the identity block too*/, uint32_t *k_out) {
     static const bool on = [] {
         const char *e = getenv("QRNG_NTT_CRT");
         return !(e && *e && atoi(e) == 0);
     }();
-    if (!on || xor_tail || logP <= kMaxFusedLogP || logP > kMaxLogP) return 0;
+    // P = 2^16 (one global pass of radix 2, 2 segments): measured slower packed
+    // (modified config 3: 78.1 -> 72.1 Gbit/s), so from P = 2^17
+    if (!on || logP < kMaxFusedLogP + 2 || logP > kMaxLogP) return 0;
     uint32_t k = 0;
     while ((1ull << k) <= n) ++k;  // 2^k > n
     const long double M = (long double)kP * kP2 * kP3;
@@ -1431,6 +1437,7 @@ static qrng_status extract_crt(const Plan &pl, const uint8_t *d_raw, uint64_t n_
     pa.G = (uint32_t)G;
     pa.n_blocks = n_blocks;
     pa.crt_k = pl.crt_k;
+    pa.xor_tail = pl.xor_tail ? 1u : 0u;  // modified Toeplitz: the CRT pass XORs raw bit t + 1
     FusedArgs fa{};
     fa.tw_shift = (uint32_t)(logP - kSegLog);
     qrng_status st = QRNG_OK;

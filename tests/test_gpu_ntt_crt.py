@@ -43,7 +43,7 @@ def plan_form(q, n, m, seed):
 
 
 @pytest.mark.parametrize("n,m,B", [(65536, 45875, 1), (65536, 45875, 3), (65536, 45875, 5), (65536, 45875, 8),
-                                   (40960, 30001, 7), (65536, 1, 6), (65536, 65535 - 32, 9), (131072, 90000, 4)])
+                                   (40960, 30001, 7), (98304, 1, 6), (65536, 65535 - 32, 9), (131072, 90000, 4)])
 def test_packed_form_whole_blocks(q, oracle_mod, n, m, B):
     rng = np.random.default_rng(n + 3 * m + B)
     raw = rng.integers(0, 256, B * n // 8, dtype=np.uint8)
@@ -90,6 +90,34 @@ def test_packed_form_config4_sampled(q, oracle_mod):
     blocks = np.repeat(np.arange(B, dtype=np.uint64), rows.size)
     ref = oracle_mod.extract_rows(raw, blocks, np.tile(rows, B), w.n, w.m, seed)
     assert np.array_equal(got[blocks.astype(int), np.tile(rows, B).astype(int)], ref)
+
+
+@pytest.mark.parametrize("n,m,B", [(131072, 50000, 5), (1 << 20, 734003, 2)])
+def test_packed_form_modified_toeplitz(q, oracle_mod, n, m, B):
+    # [T | I_m] (reading A24): the product of the first n - m bits, then the
+    # CRT pass XORs raw bit t + 1 of each block of the group; every block's
+    # first / last rows and 300 random rows against the oracle's row form
+    rng = np.random.default_rng(n + m)
+    raw = rng.integers(0, 256, B * n // 8, dtype=np.uint8)
+    seed = rng.integers(0, 256, n // 8, dtype=np.uint8)
+    with q.Plan(n, m, dev(seed), modified=True) as pl:
+        info = pl.info()
+        got = pl.extract(dev(raw), B).cpu().numpy()
+    assert info["path"] == q.PATH_NTT and (info["blocks_per_transform"], info["primes"]) == (4, 3), info
+    bits = np.unpackbits(got)[:B * m].reshape(B, m)
+    rows = np.concatenate([[0, 1, m - 2, m - 1], rng.integers(0, m, 300)]).astype(np.uint64)
+    bl = np.repeat(np.arange(B, dtype=np.uint64), rows.size)
+    rw = np.tile(rows, B)
+    ref = oracle_mod.modified_rows(raw, bl, rw, n, m, seed)
+    assert np.array_equal(bits[bl.astype(int), rw.astype(int)], ref)
+
+
+def test_small_transform_keeps_one_prime(q):
+    # P = 2^16 measured slower packed: one block per transform
+    n, m = 65536, 1
+    seed = np.random.default_rng(6).integers(0, 256, (n + m - 1 + 7) // 8, dtype=np.uint8)
+    info = plan_form(q, n, m, seed)
+    assert info["log2_transform"] == 16 and info["blocks_per_transform"] == 1, info
 
 
 def test_one_prime_form_above_2_20(q, oracle_mod):
