@@ -1202,22 +1202,41 @@ qrng_status plan_init(Plan &pl, uint64_t n, uint64_t m, const uint8_t *d_seed, u
     QRNG_CUDA_TRY(cudaGetLastError());
     qrng_status st;
     if (pl.crt) {
-        // the second prime's tables on the side stream, next to the other two
-        // (each prime's chain is a few small launches: the two streams fill the SMs)
-        cudaStream_t s2;
+        // the three primes' tables on three streams (the caller's, the side
+        // stream and a third of this thread's): each chain is a few small
+        // launches (a seed-spectrum segment launch is P / 2^15 CTAs), so they
+        // fill the SMs together
+        cudaStream_t s2, s3;
         cudaEvent_t fork, join;
         st = side_stream(&s2, &fork, &join);
         if (st != QRNG_OK) return st;
+        static thread_local cudaStream_t t3 = nullptr;
+        static thread_local cudaEvent_t j3 = nullptr;
+        static thread_local int t3dev = -1;
+        int dev = 0;
+        QRNG_CUDA_TRY(cudaGetDevice(&dev));
+        if (t3dev != dev) {  // (a stream per device and thread, as side_stream)
+            if (t3) { cudaStreamDestroy(t3); cudaEventDestroy(j3); }
+            t3 = nullptr;
+            QRNG_CUDA_TRY(cudaStreamCreateWithFlags(&t3, cudaStreamNonBlocking));
+            QRNG_CUDA_TRY(cudaEventCreateWithFlags(&j3, cudaEventDisableTiming));
+            t3dev = dev;
+        }
+        s3 = t3;
         QRNG_CUDA_TRY(cudaEventRecord(fork, s));
         QRNG_CUDA_TRY(cudaStreamWaitEvent(s2, fork, 0));
+        QRNG_CUDA_TRY(cudaStreamWaitEvent(s3, fork, 0));
         st = init_field<1>(FieldTabs{&pl.shat3[1], &pl.tw3[1], &pl.itw3[1], &pl.l1tw3[1]}, seed_words, n, m, L, logP, s2);
+        const qrng_status st2 =
+            init_field<2>(FieldTabs{&pl.shat3[2], &pl.tw3[2], &pl.itw3[2], &pl.l1tw3[2]}, seed_words, n, m, L, logP, s3);
         const qrng_status st0 =
             init_field<0>(FieldTabs{&pl.shat3[0], &pl.tw3[0], &pl.itw3[0], &pl.l1tw3[0]}, seed_words, n, m, L, logP, s);
-        const qrng_status st2 = st0 != QRNG_OK ? st0 :
-            init_field<2>(FieldTabs{&pl.shat3[2], &pl.tw3[2], &pl.itw3[2], &pl.l1tw3[2]}, seed_words, n, m, L, logP, s);
         cudaEventRecord(join, s2);  // always joined: seed_words is freed on s below
         cudaStreamWaitEvent(s, join, 0);
+        cudaEventRecord(j3, s3);
+        cudaStreamWaitEvent(s, j3, 0);
         if (st == QRNG_OK) st = st2;
+        if (st == QRNG_OK) st = st0;
     } else {
         const FieldTabs ft{&pl.shat, &pl.tw, &pl.itw, &pl.l1tw};
         st = pl.field ? init_field<1>(ft, seed_words, n, m, L, logP, s) : init_field<0>(ft, seed_words, n, m, L, logP, s);
