@@ -663,6 +663,11 @@ def roofline(q, args, w, B, path, pack, modified, pinfo, kern_ms, kern_n, ms_tot
                 "peak_derived_issue_bound": alu_peak_gbfly(pk)}
         roof["pass_rate_peak"] = q.butterfly_rate(with_twiddles=True) / 1e9
         roof["frac_of_pass_rate"] = achieved / roof["pass_rate_peak"]
+        bpt, primes = pinfo.get("blocks_per_transform", 1), pinfo.get("primes", 1)
+        if primes > 1:  # packed three-prime form: the same time credited with one transform per block
+            roof["one_block_per_transform_equivalent_frac"] = achieved * bpt / primes / peak
+            roof["work_note"] = (f"{primes} transforms per {bpt} blocks (packed three-prime form); "
+                                 "butterflies counted as run, the CRT not counted")
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"], roof["traffic_source"] = ncu_traffic(w.name, PATH_NAMES[path])
     roof["kernel_ms_per_step"] = kern_ms / args.steps  # summed per-launch device times
