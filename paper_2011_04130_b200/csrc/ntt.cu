@@ -575,6 +575,9 @@ __device__ __forceinline__ uint32_t shoup_p(uint32_t a, uint32_t w, uint32_t wp,
 // Radix-64 passes: ptxas otherwise spends 214-254 registers (one 256-thread
 // CTA per SM); 3 CTAs per SM (85 registers) where that costs at most a few
 // bytes of spill, 2 (128 registers) for the forms that spill at 3
+#ifndef QRNG_NTT_CRT_CTAS
+#define QRNG_NTT_CRT_CTAS 3  // CTAs per SM of the CRT pass (80 registers, 24 B of spill at radix 64)
+#endif
 #ifndef QRNG_NTT_PASS_BOUND
 #define QRNG_NTT_PASS_BOUND 1  // 0: no bound on the radix-64 passes except the emit pass (A/B)
 #endif
@@ -583,7 +586,8 @@ __host__ __device__ constexpr int ntt_pass_min_ctas(int R, int MODE) {
            : R < 6 ? 1
            : (MODE == 4 || MODE == 5) ? (QRNG_NTT_EMIT_SKIP ? 3 : 1)  // PASS_INV_EMIT[_XOR]
            : !QRNG_NTT_PASS_BOUND ? 1
-           : (MODE == 6 || MODE == 8) ? 3                             // PASS_FWD_PACK, PASS_INV_CRT
+           : MODE == 6 ? 3                                            // PASS_FWD_PACK
+           : MODE == 8 ? QRNG_NTT_CRT_CTAS                            // PASS_INV_CRT
            : MODE == 2 ? 1                                            // PASS_FWD spills even at 2
            : 2;
 }
