@@ -837,35 +837,42 @@ __global__ void __launch_bounds__(threads_of(LOGP), 1024 / threads_of(LOGP)) ntt
 // ---- plan preparation kernels ----------------------------------------------
 
 // tw[e] = w^e * 2^32 mod p, itw[e] = w^-e * 2^32 mod p for e < P (Montgomery
-// form).  Each thread owns kTwChain consecutive exponents: the first power by
-// Montgomery square-and-multiply, then a Montgomery chain (mont(x * R, w * R) =
-// x w R), canonicalised.  (Round 2: 16-long chains and a Montgomery power
-// instead of 64 and a 64-bit-modulo power -- the table build was 29 us at
-// P = 2^21, once per prime of a one-shot plan.)
-constexpr uint32_t kTwChain = 16;
+// form): per thread a first power by Montgomery square-and-multiply, then a
+// Montgomery chain (mont(x * R, w * R) = x w R), canonicalised.  (Round 2:
+// ~16 exponents per thread and Montgomery powers instead of 64 and a
+// 64-bit-modulo power -- the table build was 29 us at P = 2^21, once per
+// prime of a one-shot plan.)
+constexpr uint32_t kTwChain = 64;  // exponents per thread (the per-thread start powers dominate at 16)
+// x^e in Montgomery form (xM = x 2^32 mod p), canonical
+template <int F>
+__device__ __forceinline__ uint32_t mont_pow(uint32_t xM, uint32_t e) {
+    constexpr uint32_t P = Fld<F>::P;
+    uint32_t r = (uint32_t)((1ull << 32) % P);  // 1 in Montgomery form
+    for (; e; e >>= 1) {  // square-and-multiply, lazy residues in (0, 2p)
+        if (e & 1) r = mont<F>(r, xM);
+        xM = mont<F>(xM, xM);
+    }
+    return r >= P ? r - P : r;
+}
+// Thread t of T takes exponents t, t + T, t + 2T, ... (kTwChain of
+// them), so every store instruction of a warp writes 32 consecutive words
+// (with chains of consecutive exponents per thread the warp's stores were 64
+// bytes apart: 329 us for the two 128 MB tables at P = 2^25).
 template <int F = 0>
 __global__ void twiddle_table_kernel(uint32_t *tw, uint32_t *itw, uint32_t Pn, uint32_t w, uint32_t iw) {
     constexpr uint32_t P = Fld<F>::P;
-    const uint32_t e0 = (blockIdx.x * blockDim.x + threadIdx.x) * kTwChain;
+    const uint32_t T = gridDim.x * blockDim.x;
+    const uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x;
     if (e0 >= Pn) return;
     const uint32_t wM = (uint32_t)(((uint64_t)w << 32) % P), iwM = (uint32_t)(((uint64_t)iw << 32) % P);
-    uint32_t a = (uint32_t)((1ull << 32) % P), b = a;  // 1 in Montgomery form
-    {
-        uint32_t sa = wM, sb = iwM;
-        for (uint32_t e = e0; e; e >>= 1) {  // square-and-multiply, lazy residues in (0, 2p)
-            if (e & 1) { a = mont<F>(a, sa); b = mont<F>(b, sb); }
-            sa = mont<F>(sa, sa);
-            sb = mont<F>(sb, sb);
-        }
+    uint32_t a = mont_pow<F>(wM, e0), b = mont_pow<F>(iwM, e0);
+    const uint32_t sa = mont_pow<F>(wM, T), sb = mont_pow<F>(iwM, T);  // w^T, w^-T
+    for (uint32_t e = e0; e < Pn; e += T) {
+        tw[e] = a;
+        itw[e] = b;
+        a = mont<F>(a, sa);
         a = a >= P ? a - P : a;
-        b = b >= P ? b - P : b;
-    }
-    for (uint32_t k = 0; k < kTwChain && e0 + k < Pn; ++k) {
-        tw[e0 + k] = a;
-        itw[e0 + k] = b;
-        a = mont<F>(a, wM);
-        a = a >= P ? a - P : a;
-        b = mont<F>(b, iwM);
+        b = mont<F>(b, sb);
         b = b >= P ? b - P : b;
     }
 }
