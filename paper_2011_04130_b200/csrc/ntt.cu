@@ -413,8 +413,16 @@ struct Level {
                 }
             } else if (MODE == SEGFWD) {
                 uint32_t *dst = const_cast<uint32_t *>(a.shat) + (size_t)u * N1;
+                if constexpr (N1 % 4 == 0) {  // 16-byte stores (the spectrum row of sub-DFT u is contiguous)
 #pragma unroll
-                for (int q = 0; q < N1; ++q) dst[q] = mont<F>(x[q], a.scaleM);  // * P^-1 * 2^32
+                    for (int q4 = 0; q4 < N1 / 4; ++q4)
+                        reinterpret_cast<uint4 *>(dst)[q4] =
+                            make_uint4(mont<F>(x[4 * q4], a.scaleM), mont<F>(x[4 * q4 + 1], a.scaleM),
+                                       mont<F>(x[4 * q4 + 2], a.scaleM), mont<F>(x[4 * q4 + 3], a.scaleM));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < N1; ++q) dst[q] = mont<F>(x[q], a.scaleM);  // * P^-1 * 2^32
+                }
             } else {
                 // pointwise product with the seed spectrum (DIF order: position u*N1+q)
                 const uint4 *sh = reinterpret_cast<const uint4 *>(a.shat + (size_t)u * N1);
