@@ -248,6 +248,19 @@ __device__ __forceinline__ uint32_t raw_bit(const uint32_t *raw, uint64_t b, uin
     return (bswap32(w) >> (31 - (idx & 31))) & 1u;
 }
 
+// Seed spectrum layout: element (sub-DFT u, register q) of a transform's (or
+// segment's) last level.  Interleaved (default): the four-word group q / 4 of
+// consecutive u is contiguous, so the pointwise product's 16-byte loads (and
+// the spectrum's stores) of a warp are consecutive; QRNG_NTT_SHAT_ILV=0: row u
+// contiguous (the round-1 layout, for A/B).
+#ifndef QRNG_NTT_SHAT_ILV
+#define QRNG_NTT_SHAT_ILV 1
+#endif
+template <int N1, int NSUB>
+__device__ __forceinline__ size_t shat4_idx(int u, int q4) {  // uint4 index of words 4 q4 .. 4 q4 + 3
+    return QRNG_NTT_SHAT_ILV ? (size_t)q4 * NSUB + u : (size_t)u * (N1 / 4) + q4;
+}
+
 template <int LOGP, int LV, bool PACK, int MODE = FUSED, int F = 0>
 struct Level {
     static constexpr uint32_t P = Fld<F>::P;
@@ -412,23 +425,19 @@ struct Level {
                     for (int q = 0; q < N1; ++q) data[pb + poff(q)] = x[q];
                 }
             } else if (MODE == SEGFWD) {
-                uint32_t *dst = const_cast<uint32_t *>(a.shat) + (size_t)u * N1;
-                if constexpr (N1 % 4 == 0) {  // 16-byte stores (the spectrum row of sub-DFT u is contiguous)
+                static_assert(N1 % 4 == 0, "last level radix >= 4");
+                uint4 *dst4 = reinterpret_cast<uint4 *>(const_cast<uint32_t *>(a.shat));
 #pragma unroll
-                    for (int q4 = 0; q4 < N1 / 4; ++q4)
-                        reinterpret_cast<uint4 *>(dst)[q4] =
-                            make_uint4(mont<F>(x[4 * q4], a.scaleM), mont<F>(x[4 * q4 + 1], a.scaleM),
-                                       mont<F>(x[4 * q4 + 2], a.scaleM), mont<F>(x[4 * q4 + 3], a.scaleM));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < N1; ++q) dst[q] = mont<F>(x[q], a.scaleM);  // * P^-1 * 2^32
-                }
+                for (int q4 = 0; q4 < N1 / 4; ++q4)  // * P^-1 * 2^32, 16-byte stores
+                    dst4[shat4_idx<N1, NSUB>(u, q4)] =
+                        make_uint4(mont<F>(x[4 * q4], a.scaleM), mont<F>(x[4 * q4 + 1], a.scaleM),
+                                   mont<F>(x[4 * q4 + 2], a.scaleM), mont<F>(x[4 * q4 + 3], a.scaleM));
             } else {
-                // pointwise product with the seed spectrum (DIF order: position u*N1+q)
-                const uint4 *sh = reinterpret_cast<const uint4 *>(a.shat + (size_t)u * N1);
+                // pointwise product with the seed spectrum (DIF order: sub-DFT u, register q)
+                const uint4 *sh = reinterpret_cast<const uint4 *>(a.shat);
 #pragma unroll
                 for (int q4 = 0; q4 < N1 / 4; ++q4) {
-                    uint4 s4 = __ldg(sh + q4);
+                    uint4 s4 = __ldg(sh + shat4_idx<N1, NSUB>(u, q4));
                     x[4 * q4 + 0] = mont<F>(x[4 * q4 + 0], s4.x);
                     x[4 * q4 + 1] = mont<F>(x[4 * q4 + 1], s4.y);
                     x[4 * q4 + 2] = mont<F>(x[4 * q4 + 2], s4.z);
@@ -926,8 +935,12 @@ __device__ __forceinline__ void seed_levels(uint32_t *data, const uint32_t *seed
 #pragma unroll
             for (int q = 0; q < N1; ++q) data[pidx(seg * NSEG + q * STRIDE + n2)] = x[q];
         } else {
+            static_assert(N1 % 4 == 0, "last level radix >= 4");
 #pragma unroll
-            for (int q = 0; q < N1; ++q) shat[u * N1 + q] = mont(x[q], scaleM);  // * P^-1 * 2^32
+            for (int q4 = 0; q4 < N1 / 4; ++q4)  // * P^-1 * 2^32
+                reinterpret_cast<uint4 *>(shat)[shat4_idx<N1, NSUB>(u, q4)] =
+                    make_uint4(mont(x[4 * q4], scaleM), mont(x[4 * q4 + 1], scaleM), mont(x[4 * q4 + 2], scaleM),
+                               mont(x[4 * q4 + 3], scaleM));
         }
     }
     __syncthreads();
